@@ -1,0 +1,214 @@
+/*
+ * p3.h — C ABI of the B200-native P3 (Priority-based Parameter Propagation) sync path.
+ *
+ * This is the drop-in boundary. Every entry point replaces one call site of the
+ * reference's Python API (`/root/reference/pkg/src/p3sync`); the citation above each
+ * declaration names the reference interface (file:line) it stands in for.
+ *
+ * Conventions
+ *   - Return codes mirror the reference CLI exit codes (cli.py:49-52):
+ *       P3_OK 0, P3_EUSAGE 1 (ValueError / PlanError / ProfileError),
+ *       P3_EPROTOCOL 2 (ProtocolError), P3_ETIMEOUT 3 (DeadlockError), P3_ECUDA 4.
+ *   - Plain pointers and sizes only. `stream` arguments are CUstream / cudaStream_t
+ *     handles passed as void* (NULL = legacy default stream).
+ *   - Host arrays are owned by the caller. Device pointers are borrowed. A p3_ctx_t owns
+ *     its device arenas (parameters, receive slots, flags, trace) and frees them in
+ *     p3_ctx_destroy.
+ *   - Hot calls (p3_layer_ready, p3_wait_layer, p3_iteration_begin, p3_gradgen_layer)
+ *     are asynchronous and stream-ordered; none of them synchronises the host.
+ *   - The library has no CPU fallback: every compute entry point runs sm_100a code and
+ *     returns P3_ECUDA when no device is available.
+ */
+#ifndef P3_H_
+#define P3_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define P3_OK 0
+#define P3_EUSAGE 1
+#define P3_EPROTOCOL 2
+#define P3_ETIMEOUT 3
+#define P3_ECUDA 4
+
+/* Plan modes: plan.py:53-54 (P3_MODE / BASELINE_MODE). */
+#define P3_PLAN_P3 0
+#define P3_PLAN_BASELINE 1
+
+/* Queue disciplines: FrameQueue(priority_mode=True/False), queues.py:28-39. */
+#define P3_SCHED_PRIORITY 0
+#define P3_SCHED_FIFO 1
+
+/* Maximum ranks (workers == servers) in one NVSwitch domain handled by one context. */
+#define P3_MAX_RANKS 16
+
+/* Trace events (the Frame msg types that cross the link, proto.py:26-32). */
+#define P3_EV_PUSH 0  /* worker popped a slice and stored it into the owner's slot */
+#define P3_EV_BCAST 1 /* owner reduced + updated a slice and broadcast it */
+
+/* One row of a SlicePlan (plan.py:30-45: SliceKey + Slice). */
+typedef struct p3_slice {
+  uint32_t layer;    /* SliceKey.layer_index */
+  uint32_t slice;    /* SliceKey.slice_index */
+  uint64_t offset;   /* Slice.offset (elements into the layer) */
+  uint64_t length;   /* Slice.length (elements) */
+  uint32_t priority; /* Slice.priority (== layer index) */
+  uint32_t server;   /* Slice.server (owner rank) */
+} p3_slice_t;
+
+/* One device trace record; the wire header fields of proto.py:20-21 minus the codec. */
+typedef struct p3_trace_rec {
+  uint64_t t_ns;      /* %globaltimer at the event */
+  uint32_t iteration; /* Frame.iteration */
+  uint32_t layer;     /* Frame.layer_index (== priority) */
+  uint32_t slice;     /* Frame.slice_index */
+  uint16_t rank;      /* Frame.worker_rank (pusher for PUSH, owner for BCAST) */
+  uint16_t event;     /* P3_EV_* */
+} p3_trace_rec_t;
+
+/* ---------------------------------------------------------------- planning (host) */
+
+/* make_p3_plan, plan.py:94-119 (greedy max_slice chunks, remainder last, server =
+ * running counter % num_servers, priority = layer index). Rows are written in
+ * (layer, slice) order. With out == NULL only *n_out is computed. */
+int p3_plan_p3(const uint64_t* param_counts, uint32_t n_layers, uint32_t num_servers,
+               uint64_t max_slice, p3_slice_t* out, uint64_t cap, uint64_t* n_out);
+
+/* make_baseline_plan, plan.py:122-164 (small layer -> splitmix64_stream(seed, L) % N,
+ * layer >= big_threshold -> N equal parts, remainder on the last part). */
+int p3_plan_baseline(const uint64_t* param_counts, uint32_t n_layers, uint32_t num_servers,
+                     uint64_t big_threshold, uint64_t rng_seed, p3_slice_t* out,
+                     uint64_t cap, uint64_t* n_out);
+
+/* splitmix64_stream, hashing.py:32-35. */
+uint64_t p3_splitmix64_stream(uint64_t seed, uint64_t index);
+
+/* fnv1a64 over `nbytes` bytes with chaining seed `h`, hashing.py:79-83. */
+uint64_t p3_fnv1a64(const void* data, uint64_t nbytes, uint64_t h);
+
+/* ------------------------------------------------------- standalone device kernels */
+
+/* gradient_block, hashing.py:55-63: out_dev[i] = gradient_value(seed, it, layer,
+ * start + i) for i < count, bit-exact, written by the K1 gradgen kernel. */
+int p3_gradient_block(uint64_t seed, uint64_t iteration, uint64_t layer, uint64_t start,
+                      uint64_t count, float* out_dev, void* stream);
+
+/* ShardState.aggregate_and_update, server.py:55-68, for one slice:
+ *   acc = 0; for r in 0..num_workers-1 (ascending): acc += grads[r]; g = acc / N;
+ *   params -= lr * g            (IEEE fp32, no contraction; bit-exact)
+ * grads_dev is a HOST array of num_workers device pointers (rank order).
+ * momentum_dev may be NULL (plain SGD, the reference); otherwise
+ *   v = momentum * v + g; params -= lr * v   (extension, not in the reference). */
+int p3_shard_update(float* params_dev, const float* const* grads_dev, uint32_t num_workers,
+                    uint64_t n, float lr, float momentum, float* momentum_dev, void* stream);
+
+/* Device-side sleep for `duration_us` (TrainingWorker._emulate, worker.py:299-310). */
+int p3_emulate_compute(uint64_t duration_us, void* stream);
+
+/* ---------------------------------------------------- scripted device priority queue */
+
+/* The device slice queue driven one operation at a time (FrameQueue, queues.py:20-75).
+ * Used for tick-replay parity against the reference simulator; the same __device__ pop
+ * routine runs inside the persistent comm kernel. */
+typedef struct p3_queue p3_queue_t;
+int p3_queue_create(const uint32_t* layer_nslices, uint32_t n_layers, uint32_t sched,
+                    p3_queue_t** out);
+/* FrameQueue.put_batch of all slices of `layer` (queues.py:44-50): atomic. */
+int p3_queue_put_layer(p3_queue_t* q, uint32_t layer, uint32_t iteration);
+/* FrameQueue.poll (queues.py:52-62) without blocking: returns P3_OK and the popped
+ * (layer, slice), or P3_ETIMEOUT when nothing is queued. */
+int p3_queue_poll(p3_queue_t* q, uint32_t* layer, uint32_t* slice);
+int p3_queue_destroy(p3_queue_t* q);
+
+/* --------------------------------------------------------------- sync context (K3) */
+
+typedef struct p3_ctx p3_ctx_t;
+
+typedef struct p3_config {
+  uint32_t world;                      /* N workers == N servers (cli.py:81-82) */
+  uint32_t n_local;                    /* ranks hosted by this process (1, or N when
+                                          emulating all ranks on one GPU) */
+  uint32_t local_ranks[P3_MAX_RANKS];  /* which ranks */
+  uint32_t n_layers;
+  const uint64_t* layer_counts;        /* LayerSpec.param_count per layer */
+  uint64_t max_slice;                  /* make_p3_plan max_slice (plan.py:22) */
+  uint32_t plan_mode;                  /* P3_PLAN_P3 (baseline plan: future) */
+  uint32_t sched;                      /* P3_SCHED_PRIORITY (p3) or P3_SCHED_FIFO */
+  float lr;                            /* RunConfig.lr (cli.py:69) */
+  float momentum;                      /* 0 == the reference's plain SGD */
+  uint32_t comm_ctas;                  /* CTAs of the persistent comm kernel */
+  uint32_t comm_threads;               /* threads per comm CTA (multiple of 32) */
+  double timeout_s;                    /* device spin deadline (deadlock_timeout) */
+  uint32_t trace_cap;                  /* trace records per local rank (0 = off) */
+  uint32_t emulate_grads;              /* allocate a gradient arena for gradgen mode */
+} p3_config_t;
+
+/* Builds the plan, allocates per-local-rank arenas (parameters W zero-initialised like
+ * worker.py:72 / server.py:112-115, receive slots R, flags) and uploads plan tables. */
+int p3_ctx_create(const p3_config_t* cfg, p3_ctx_t** out);
+int p3_ctx_destroy(p3_ctx_t* ctx);
+
+/* Multi-process bootstrap: the IPC handle of a local rank's arena (P3_IPC_BYTES bytes),
+ * and opening every rank's handle (world * P3_IPC_BYTES bytes, rank order; entries of
+ * local ranks are ignored). Replaces the TCP connect/HELLO of worker.py:136-148. */
+#define P3_IPC_BYTES 64
+int p3_ctx_ipc_handle(p3_ctx_t* ctx, uint32_t local_idx, void* out);
+int p3_ctx_open_peers(p3_ctx_t* ctx, const void* handles);
+
+/* Device pointer of local rank's parameter replica and each layer's element offset in
+ * it (layers are 16-byte aligned). TrainingWorker.params, worker.py:72. */
+int p3_ctx_params(p3_ctx_t* ctx, uint32_t local_idx, float** params_dev);
+int p3_ctx_layer_offset(p3_ctx_t* ctx, uint32_t layer, uint64_t* elem_offset);
+/* Device pointer of the local rank's gradient arena (emulate_grads only). */
+int p3_ctx_grads(p3_ctx_t* ctx, uint32_t local_idx, float** grads_dev);
+
+/* Launch iteration k's persistent comm kernel on `comm_stream` (K3: worker pop/push +
+ * server reduce/update/broadcast for all local ranks). Replaces the _priority_sender /
+ * _fifo_sender threads (worker.py:184-198) and ServerEngine._consumer (server.py:208-249). */
+int p3_iteration_begin(p3_ctx_t* ctx, uint64_t iteration, void* comm_stream);
+
+/* TrainingWorker.enqueue_layer (worker.py:173-182): publish all slices of `layer` for
+ * `iteration` atomically (one release store after the gradient pointer). `grad_dev` is
+ * the layer's fp32 gradient (param_count elements); NULL = the context's gradient arena. */
+int p3_layer_ready(p3_ctx_t* ctx, uint32_t local_idx, uint32_t layer, uint64_t iteration,
+                   const float* grad_dev, void* stream);
+
+/* K1 emulate mode: fill the gradient arena for `layer` with GradGen(seed) values
+ * (TrainingWorker._materialize, worker.py:166-171). The reference pushes the same seed
+ * from every rank (worker.py:71); callers wanting rank-distinct gradients pass a
+ * per-rank seed. */
+int p3_gradgen_layer(p3_ctx_t* ctx, uint32_t local_idx, uint64_t seed, uint64_t iteration,
+                     uint32_t layer, void* stream);
+
+/* TrainingWorker._wait_layer (worker.py:277-285): make `stream` wait until `layer` holds
+ * the parameters for forward pass `iteration` (flags[layer] >= iteration). A stream
+ * memory wait: no SM is occupied. */
+int p3_wait_layer(p3_ctx_t* ctx, uint32_t local_idx, uint32_t layer, uint64_t iteration,
+                  void* stream);
+
+/* TrainingWorker._wait_all (worker.py:287-289) + error check: block the host until the
+ * comm kernels finished and every local layer reached `iteration`, or timeout. */
+int p3_sync_all(p3_ctx_t* ctx, uint64_t iteration, double timeout_s);
+
+/* Transmission sequence (trace) of a local rank, in device append order. */
+int p3_trace_read(p3_ctx_t* ctx, uint32_t local_idx, p3_trace_rec_t* out, uint64_t cap,
+                  uint64_t* n_out);
+int p3_trace_clear(p3_ctx_t* ctx);
+
+/* NetCounters.totals (metrics.py:31-45): NVLink/HBM payload bytes in / out. */
+int p3_counters(p3_ctx_t* ctx, uint32_t local_idx, uint64_t* bytes_in, uint64_t* bytes_out);
+
+/* Diagnostics of the last failing call on this context (thread-local when ctx == NULL). */
+const char* p3_last_error(p3_ctx_t* ctx);
+
+/* Device attributes the runtime depends on (stream memory ops, SM count). */
+int p3_device_info(int* sm_count, int* stream_memops, int* cc_major, int* cc_minor);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* P3_H_ */

@@ -1,0 +1,708 @@
+// Sync context: plan tables on the device, per-rank arenas, IPC bootstrap, stream memory
+// operations for layer publication (enqueue_layer) and forward gating (_wait_layer), and
+// the per-iteration launch of the comm kernel.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "p3_internal.h"
+
+namespace p3 {
+
+static thread_local std::string g_thread_error;
+void set_thread_error(const std::string& msg) { g_thread_error = msg; }
+
+// ------------------------------------------------------------ driver entry points
+
+typedef CUresult (*PFN_wait32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+typedef CUresult (*PFN_write32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+typedef CUresult (*PFN_write64)(CUstream, CUdeviceptr, cuuint64_t, unsigned int);
+typedef CUresult (*PFN_attr)(int*, CUdevice_attribute, CUdevice);
+
+struct Driver {
+  PFN_wait32 wait32 = nullptr;
+  PFN_write32 write32 = nullptr;
+  PFN_write64 write64 = nullptr;
+  PFN_attr attr = nullptr;
+  bool ok = false;
+  bool has64 = false;
+};
+
+static Driver& driver() {
+  static Driver d;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void* fp = nullptr;
+    bool ok = true;
+    ok &= cudaGetDriverEntryPointByVersion("cuStreamWaitValue32", &fp, 12000, cudaEnableDefault, &q) ==
+              cudaSuccess && q == cudaDriverEntryPointSuccess;
+    d.wait32 = (PFN_wait32)fp;
+    ok &= cudaGetDriverEntryPointByVersion("cuStreamWriteValue32", &fp, 12000, cudaEnableDefault, &q) ==
+              cudaSuccess && q == cudaDriverEntryPointSuccess;
+    d.write32 = (PFN_write32)fp;
+    ok &= cudaGetDriverEntryPointByVersion("cuStreamWriteValue64", &fp, 12000, cudaEnableDefault, &q) ==
+              cudaSuccess && q == cudaDriverEntryPointSuccess;
+    d.write64 = (PFN_write64)fp;
+    ok &= cudaGetDriverEntryPointByVersion("cuDeviceGetAttribute", &fp, 12000, cudaEnableDefault, &q) ==
+              cudaSuccess && q == cudaDriverEntryPointSuccess;
+    d.attr = (PFN_attr)fp;
+    d.ok = ok;
+    if (ok) {
+      int dev = 0, v = 0;
+      cudaGetDevice(&dev);
+      if (d.attr(&v, CU_DEVICE_ATTRIBUTE_CAN_USE_64_BIT_STREAM_MEM_OPS, dev) == CUDA_SUCCESS) d.has64 = v != 0;
+    }
+  });
+  return d;
+}
+
+static inline uint64_t align_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
+
+}  // namespace p3
+
+using namespace p3;
+
+// Peer-visible arena of one rank: W | R | arrivals | hint | done (256-byte aligned parts).
+struct PeerLayout {
+  uint64_t w, r, arrivals, hint, done, bytes;
+};
+
+// Local arena of one rank. The per-iteration part (cursor | srv_lo | srv_taken | it) is
+// contiguous so one memset resets it before each launch.
+struct LocalLayout {
+  uint64_t ready, fifo_key, gptr, claim, iter_begin, cursor, srv_lo, srv_taken, it, iter_end, V, bytes,
+      trace_n, trace, total;
+};
+
+struct p3_ctx {
+  p3_config_t cfg;
+  std::vector<uint64_t> counts;
+  std::vector<p3_slice_t> plan;
+  uint32_t L = 0, S = 0, N = 0;
+  std::vector<uint64_t> layer_woff;
+  std::vector<uint32_t> layer_nslices, layer_first;
+  std::vector<uint32_t> own_total;
+  std::vector<uint64_t> own_stride;
+  std::vector<uint64_t> bcast_in_bytes;  // per rank: broadcast payload received per iteration
+  uint64_t w_elems = 0;
+  int device = 0;
+
+  void* d_plan = nullptr;
+  PlanDev plan_dev{};
+  PeersDev peers{};
+  LocalDev loc[P3_MAX_LOCAL]{};
+  PeerLayout peer_layout[P3_MAX_RANKS]{};
+  LocalLayout local_layout{};
+  void* peer_arena[P3_MAX_LOCAL]{};
+  void* local_arena[P3_MAX_LOCAL]{};
+  float* grads[P3_MAX_LOCAL]{};
+  void* opened[P3_MAX_RANKS]{};
+  uint32_t* d_err = nullptr;
+  uint32_t fifo_seq[P3_MAX_LOCAL]{};
+  cudaEvent_t comm_done = nullptr;
+  cudaStream_t poll_stream = nullptr;
+  bool comm_pending = false;
+  uint64_t synced_iterations = 0;
+  std::string err;
+};
+
+namespace {
+
+int fail(p3_ctx* c, int code, const std::string& msg) {
+  if (c) c->err = msg;
+  set_thread_error(msg);
+  return code;
+}
+
+int cuda_fail(p3_ctx* c, cudaError_t e, const char* what) {
+  return fail(c, P3_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+#define CK(call)                                           \
+  do {                                                     \
+    cudaError_t e_ = (call);                               \
+    if (e_ != cudaSuccess) return cuda_fail(c, e_, #call); \
+  } while (0)
+
+PeerLayout peer_layout_of(const p3_ctx* c, uint32_t rank) {
+  PeerLayout p;
+  uint64_t o = 0;
+  p.w = o;
+  o = align_up(o + c->w_elems * 4, 256);
+  p.r = o;
+  o = align_up(o + (uint64_t)c->N * c->own_stride[rank] * 4, 256);
+  p.arrivals = o;
+  o = align_up(o + (uint64_t)c->S * 4, 256);
+  p.hint = o;
+  o = align_up(o + (uint64_t)c->L * 4, 256);
+  p.done = o;
+  o = align_up(o + (uint64_t)c->L * 4, 256);
+  p.bytes = o;
+  return p;
+}
+
+LocalLayout local_layout_of(const p3_ctx* c, uint64_t v_elems) {
+  LocalLayout q;
+  uint64_t o = 0;
+  auto take = [&](uint64_t& field, uint64_t bytes) {
+    field = o;
+    o = align_up(o + bytes, 256);
+  };
+  take(q.ready, c->L * 4ull);
+  take(q.fifo_key, c->L * 4ull);
+  take(q.gptr, c->L * 8ull);
+  take(q.claim, c->S * 4ull);
+  q.iter_begin = o;
+  take(q.cursor, c->L * 4ull);
+  take(q.srv_lo, c->L * 4ull);
+  take(q.srv_taken, c->L * 4ull);
+  take(q.it, sizeof(IterState));
+  q.iter_end = o;
+  take(q.V, v_elems * 4);
+  take(q.bytes, 16);
+  take(q.trace_n, 8);
+  take(q.trace, (uint64_t)c->cfg.trace_cap * sizeof(p3_trace_rec_t));
+  q.total = o;
+  return q;
+}
+
+void set_peer_pointers(p3_ctx* c, uint32_t rank, char* base) {
+  const PeerLayout& p = c->peer_layout[rank];
+  c->peers.W[rank] = reinterpret_cast<float*>(base + p.w);
+  c->peers.R[rank] = reinterpret_cast<float*>(base + p.r);
+  c->peers.arrivals[rank] = reinterpret_cast<uint32_t*>(base + p.arrivals);
+  c->peers.hint[rank] = reinterpret_cast<uint32_t*>(base + p.hint);
+  c->peers.done[rank] = reinterpret_cast<uint32_t*>(base + p.done);
+}
+
+int check_local(p3_ctx* c, uint32_t li) {
+  if (!c) return fail(nullptr, P3_EUSAGE, "null context");
+  if (li >= c->cfg.n_local) return fail(c, P3_EUSAGE, "local rank index out of range");
+  return P3_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* p3_last_error(p3_ctx_t* ctx) { return ctx ? ctx->err.c_str() : g_thread_error.c_str(); }
+
+int p3_device_info(int* sm_count, int* stream_memops, int* cc_major, int* cc_minor) {
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess || n == 0) {
+    set_thread_error(std::string("no CUDA device: ") + cudaGetErrorString(e));
+    return P3_ECUDA;
+  }
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (sm_count) cudaDeviceGetAttribute(sm_count, cudaDevAttrMultiProcessorCount, dev);
+  if (cc_major) cudaDeviceGetAttribute(cc_major, cudaDevAttrComputeCapabilityMajor, dev);
+  if (cc_minor) cudaDeviceGetAttribute(cc_minor, cudaDevAttrComputeCapabilityMinor, dev);
+  Driver& d = driver();
+  if (stream_memops) *stream_memops = d.ok ? (d.has64 ? 2 : 1) : 0;
+  return P3_OK;
+}
+
+int p3_ctx_create(const p3_config_t* cfg, p3_ctx_t** out) {
+  p3_ctx* c = nullptr;
+  if (!cfg || !out) return fail(nullptr, P3_EUSAGE, "null argument");
+  if (cfg->world < 1 || cfg->world > P3_MAX_RANKS) return fail(nullptr, P3_EUSAGE, "world must be in [1, 16]");
+  if (cfg->n_local < 1 || cfg->n_local > cfg->world) return fail(nullptr, P3_EUSAGE, "bad n_local");
+  if (cfg->n_layers < 1 || !cfg->layer_counts) return fail(nullptr, P3_EUSAGE, "profile needs at least one layer");
+  if (cfg->plan_mode != P3_PLAN_P3) return fail(nullptr, P3_EUSAGE, "only the p3 plan runs on the comm kernel");
+  if (cfg->comm_threads < 32 || cfg->comm_threads > 1024 || cfg->comm_threads % 32)
+    return fail(nullptr, P3_EUSAGE, "comm_threads must be a multiple of 32 in [32, 1024]");
+  if (cfg->comm_ctas < 1) return fail(nullptr, P3_EUSAGE, "comm_ctas must be >= 1");
+  for (uint32_t i = 0; i < cfg->n_local; ++i)
+    if (cfg->local_ranks[i] >= cfg->world) return fail(nullptr, P3_EUSAGE, "local rank out of range");
+  if (!driver().ok) return fail(nullptr, P3_ECUDA, "CUDA driver stream memory operations unavailable");
+
+  c = new p3_ctx();
+  c->cfg = *cfg;
+  c->counts.assign(cfg->layer_counts, cfg->layer_counts + cfg->n_layers);
+  c->cfg.layer_counts = c->counts.data();
+  c->L = cfg->n_layers;
+  c->N = cfg->world;
+  std::string perr;
+  int rc = build_p3_plan(c->counts.data(), c->L, c->N, cfg->max_slice, &c->plan, &perr);
+  if (rc != P3_OK) {
+    delete c;
+    return fail(nullptr, rc, perr);
+  }
+  if (c->plan.size() >= 0x7fffffffull) {
+    delete c;
+    return fail(nullptr, P3_EUSAGE, "too many slices");
+  }
+  c->S = (uint32_t)c->plan.size();
+  cudaGetDevice(&c->device);
+
+  // ---- host-side plan tables
+  const uint32_t L = c->L, S = c->S, N = c->N;
+  c->layer_woff.resize(L);
+  c->layer_nslices.assign(L, 0);
+  c->layer_first.assign(L, 0);
+  uint64_t w = 0;
+  for (uint32_t l = 0; l < L; ++l) {
+    c->layer_woff[l] = w;
+    w = align_up(w + c->counts[l], 64);  // 256-byte aligned layer starts
+  }
+  c->w_elems = w;
+  std::vector<uint64_t> slice_off(S), slice_slot(S);
+  std::vector<uint32_t> slice_len(S), slice_layer(S), slice_owner(S);
+  std::vector<uint32_t> own_list;
+  std::vector<uint32_t> own_lfirst((size_t)N * L, 0), own_lcount((size_t)N * L, 0);
+  c->own_total.assign(N, 0);
+  c->own_stride.assign(N, 0);
+  c->bcast_in_bytes.assign(N, 0);
+  for (uint32_t g = 0; g < S; ++g) {
+    const p3_slice_t& r = c->plan[g];
+    if (r.slice == 0) c->layer_first[r.layer] = g;
+    c->layer_nslices[r.layer]++;
+    slice_off[g] = r.offset;
+    slice_len[g] = (uint32_t)r.length;
+    slice_layer[g] = r.layer;
+    slice_owner[g] = r.server;
+    if (r.length >= 0xffffffffull) {
+      delete c;
+      return fail(nullptr, P3_EUSAGE, "max_slice too large");
+    }
+  }
+  own_list.reserve(S);
+  for (uint32_t o = 0; o < N; ++o) {
+    uint64_t slot = 0;
+    for (uint32_t l = 0; l < L; ++l) {
+      own_lfirst[(size_t)o * L + l] = (uint32_t)own_list.size();
+      for (uint32_t s = 0; s < c->layer_nslices[l]; ++s) {
+        const uint32_t g = c->layer_first[l] + s;
+        if (slice_owner[g] != o) continue;
+        own_list.push_back(g);
+        own_lcount[(size_t)o * L + l]++;
+        slice_slot[g] = slot;
+        slot = align_up(slot + slice_len[g], 64);
+      }
+    }
+    c->own_stride[o] = std::max<uint64_t>(slot, 64);
+  }
+  {
+    std::vector<uint32_t> tot(N, 0);
+    for (uint32_t g = 0; g < S; ++g) tot[slice_owner[g]]++;
+    c->own_total = tot;
+    for (uint32_t r = 0; r < N; ++r)
+      for (uint32_t g = 0; g < S; ++g)
+        if (slice_owner[g] != r) c->bcast_in_bytes[r] += 4ull * slice_len[g];
+  }
+
+  // ---- device plan tables: one allocation
+  std::vector<char> blob;
+  auto put = [&](const void* src, size_t bytes) -> size_t {
+    size_t off = align_up(blob.size(), 256);
+    blob.resize(off + std::max<size_t>(bytes, 4));
+    if (bytes) std::memcpy(blob.data() + off, src, bytes);
+    return off;
+  };
+  const size_t o_lns = put(c->layer_nslices.data(), L * 4ull);
+  const size_t o_lf = put(c->layer_first.data(), L * 4ull);
+  const size_t o_lw = put(c->layer_woff.data(), L * 8ull);
+  const size_t o_so = put(slice_off.data(), S * 8ull);
+  const size_t o_sl = put(slice_len.data(), S * 4ull);
+  const size_t o_sly = put(slice_layer.data(), S * 4ull);
+  const size_t o_sow = put(slice_owner.data(), S * 4ull);
+  const size_t o_ss = put(slice_slot.data(), S * 8ull);
+  const size_t o_ol = put(own_list.data(), own_list.size() * 4ull);
+  const size_t o_olf = put(own_lfirst.data(), own_lfirst.size() * 4ull);
+  const size_t o_olc = put(own_lcount.data(), own_lcount.size() * 4ull);
+  const size_t o_ot = put(c->own_total.data(), N * 4ull);
+  const size_t o_ost = put(c->own_stride.data(), N * 8ull);
+  cudaError_t e = cudaMalloc(&c->d_plan, blob.size());
+  if (e == cudaSuccess) e = cudaMemcpy(c->d_plan, blob.data(), blob.size(), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMalloc(&c->d_err, 256);
+  if (e == cudaSuccess) e = cudaMemset(c->d_err, 0, 256);
+  if (e != cudaSuccess) {
+    int r2 = cuda_fail(c, e, "plan upload");
+    p3_ctx_destroy(c);
+    return r2;
+  }
+  char* pb = static_cast<char*>(c->d_plan);
+  PlanDev& P = c->plan_dev;
+  P.n_layers = L;
+  P.total_slices = S;
+  P.world = N;
+  P.layer_nslices = reinterpret_cast<const uint32_t*>(pb + o_lns);
+  P.layer_first = reinterpret_cast<const uint32_t*>(pb + o_lf);
+  P.layer_woff = reinterpret_cast<const uint64_t*>(pb + o_lw);
+  P.slice_off = reinterpret_cast<const uint64_t*>(pb + o_so);
+  P.slice_len = reinterpret_cast<const uint32_t*>(pb + o_sl);
+  P.slice_layer = reinterpret_cast<const uint32_t*>(pb + o_sly);
+  P.slice_owner = reinterpret_cast<const uint32_t*>(pb + o_sow);
+  P.slice_slot = reinterpret_cast<const uint64_t*>(pb + o_ss);
+  P.own_list = reinterpret_cast<const uint32_t*>(pb + o_ol);
+  P.own_lfirst = reinterpret_cast<const uint32_t*>(pb + o_olf);
+  P.own_lcount = reinterpret_cast<const uint32_t*>(pb + o_olc);
+  P.own_total = reinterpret_cast<const uint32_t*>(pb + o_ot);
+  P.own_stride = reinterpret_cast<const uint64_t*>(pb + o_ost);
+
+  // ---- per-rank arenas
+  for (uint32_t r = 0; r < N; ++r) c->peer_layout[r] = peer_layout_of(c, r);
+  for (uint32_t i = 0; i < cfg->n_local; ++i) {
+    const uint32_t rank = cfg->local_ranks[i];
+    const PeerLayout& pl = c->peer_layout[rank];
+    e = cudaMalloc(&c->peer_arena[i], pl.bytes);
+    if (e == cudaSuccess) e = cudaMemset(c->peer_arena[i], 0, pl.bytes);
+    const uint64_t v_elems = cfg->momentum != 0.f ? c->own_stride[rank] : 0;
+    LocalLayout ll = local_layout_of(c, v_elems);
+    c->local_layout = ll;
+    if (e == cudaSuccess) e = cudaMalloc(&c->local_arena[i], ll.total);
+    if (e == cudaSuccess) e = cudaMemset(c->local_arena[i], 0, ll.total);
+    if (e == cudaSuccess && cfg->emulate_grads) {
+      e = cudaMalloc(&c->grads[i], std::max<uint64_t>(c->w_elems, 4) * 4);
+      if (e == cudaSuccess) e = cudaMemset(c->grads[i], 0, std::max<uint64_t>(c->w_elems, 4) * 4);
+    }
+    if (e != cudaSuccess) {
+      int r2 = cuda_fail(c, e, "arena allocation");
+      p3_ctx_destroy(c);
+      return r2;
+    }
+    set_peer_pointers(c, rank, static_cast<char*>(c->peer_arena[i]));
+    char* lb = static_cast<char*>(c->local_arena[i]);
+    LocalDev& D = c->loc[i];
+    D.rank = rank;
+    D.trace_cap = cfg->trace_cap;
+    D.ready = reinterpret_cast<uint32_t*>(lb + ll.ready);
+    D.fifo_key = reinterpret_cast<uint32_t*>(lb + ll.fifo_key);
+    D.gptr = reinterpret_cast<uint64_t*>(lb + ll.gptr);
+    D.claim = reinterpret_cast<uint32_t*>(lb + ll.claim);
+    D.cursor = reinterpret_cast<uint32_t*>(lb + ll.cursor);
+    D.srv_lo = reinterpret_cast<uint32_t*>(lb + ll.srv_lo);
+    D.srv_taken = reinterpret_cast<uint32_t*>(lb + ll.srv_taken);
+    D.it = reinterpret_cast<IterState*>(lb + ll.it);
+    D.V = v_elems ? reinterpret_cast<float*>(lb + ll.V) : nullptr;
+    D.bytes = reinterpret_cast<unsigned long long*>(lb + ll.bytes);
+    D.trace_n = reinterpret_cast<unsigned long long*>(lb + ll.trace_n);
+    D.trace = reinterpret_cast<p3_trace_rec_t*>(lb + ll.trace);
+  }
+  e = cudaEventCreateWithFlags(&c->comm_done, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->poll_stream, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) {
+    int r2 = cuda_fail(c, e, "context init");
+    p3_ctx_destroy(c);
+    return r2;
+  }
+  *out = c;
+  return P3_OK;
+}
+
+int p3_ctx_destroy(p3_ctx_t* c) {
+  if (!c) return P3_OK;
+  cudaDeviceSynchronize();
+  for (uint32_t r = 0; r < P3_MAX_RANKS; ++r)
+    if (c->opened[r]) cudaIpcCloseMemHandle(c->opened[r]);
+  for (uint32_t i = 0; i < P3_MAX_LOCAL; ++i) {
+    if (c->peer_arena[i]) cudaFree(c->peer_arena[i]);
+    if (c->local_arena[i]) cudaFree(c->local_arena[i]);
+    if (c->grads[i]) cudaFree(c->grads[i]);
+  }
+  if (c->d_plan) cudaFree(c->d_plan);
+  if (c->d_err) cudaFree(c->d_err);
+  if (c->comm_done) cudaEventDestroy(c->comm_done);
+  if (c->poll_stream) cudaStreamDestroy(c->poll_stream);
+  delete c;
+  return P3_OK;
+}
+
+int p3_ctx_ipc_handle(p3_ctx_t* c, uint32_t li, void* out) {
+  int rc = check_local(c, li);
+  if (rc) return rc;
+  static_assert(sizeof(cudaIpcMemHandle_t) <= P3_IPC_BYTES, "ipc handle size");
+  cudaIpcMemHandle_t h;
+  CK(cudaIpcGetMemHandle(&h, c->peer_arena[li]));
+  std::memset(out, 0, P3_IPC_BYTES);
+  std::memcpy(out, &h, sizeof(h));
+  return P3_OK;
+}
+
+int p3_ctx_open_peers(p3_ctx_t* c, const void* handles) {
+  if (!c || !handles) return fail(c, P3_EUSAGE, "null argument");
+  const char* hb = static_cast<const char*>(handles);
+  for (uint32_t r = 0; r < c->N; ++r) {
+    bool local = false;
+    for (uint32_t i = 0; i < c->cfg.n_local; ++i) local |= c->cfg.local_ranks[i] == r;
+    if (local || c->opened[r]) continue;
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, hb + (size_t)r * P3_IPC_BYTES, sizeof(h));
+    void* p = nullptr;
+    CK(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+    c->opened[r] = p;
+    set_peer_pointers(c, r, static_cast<char*>(p));
+  }
+  return P3_OK;
+}
+
+int p3_ctx_params(p3_ctx_t* c, uint32_t li, float** params) {
+  int rc = check_local(c, li);
+  if (rc) return rc;
+  *params = c->peers.W[c->cfg.local_ranks[li]];
+  return P3_OK;
+}
+
+int p3_ctx_grads(p3_ctx_t* c, uint32_t li, float** grads) {
+  int rc = check_local(c, li);
+  if (rc) return rc;
+  if (!c->grads[li]) return fail(c, P3_EUSAGE, "context has no gradient arena (emulate_grads = 0)");
+  *grads = c->grads[li];
+  return P3_OK;
+}
+
+int p3_ctx_layer_offset(p3_ctx_t* c, uint32_t layer, uint64_t* off) {
+  if (!c || layer >= c->L) return fail(c, P3_EUSAGE, "layer out of range");
+  *off = c->layer_woff[layer];
+  return P3_OK;
+}
+
+int p3_iteration_begin(p3_ctx_t* c, uint64_t k, void* stream) {
+  if (!c) return fail(nullptr, P3_EUSAGE, "null context");
+  if (k >= 0x3fffffffull) return fail(c, P3_EUSAGE, "iteration out of range");
+  cudaStream_t s = (cudaStream_t)stream;
+  const LocalLayout& ll = c->local_layout;
+  for (uint32_t i = 0; i < c->cfg.n_local; ++i)
+    CK(cudaMemsetAsync(static_cast<char*>(c->local_arena[i]) + ll.iter_begin, 0, ll.iter_end - ll.iter_begin, s));
+  CommArgs a;
+  std::memset(&a, 0, sizeof(a));
+  a.plan = c->plan_dev;
+  a.peers = c->peers;
+  for (uint32_t i = 0; i < c->cfg.n_local; ++i) a.loc[i] = c->loc[i];
+  a.n_local = c->cfg.n_local;
+  a.k = (uint32_t)k;
+  a.sched = c->cfg.sched;
+  a.lr = c->cfg.lr;
+  a.momentum = c->cfg.momentum;
+  a.timeout_ns = (unsigned long long)(c->cfg.timeout_s * 1e9);
+  a.err = c->d_err;
+  for (uint32_t r = 0; r < c->N; ++r)
+    if (!a.peers.W[r]) return fail(c, P3_EUSAGE, "peer arenas not opened (call p3_ctx_open_peers)");
+  if (launch_comm(a, c->cfg.comm_ctas, c->cfg.comm_threads, stream) != P3_OK)
+    return cuda_fail(c, cudaGetLastError(), "comm kernel launch");
+  CK(cudaEventRecord(c->comm_done, s));
+  c->comm_pending = true;
+  return P3_OK;
+}
+
+int p3_layer_ready(p3_ctx_t* c, uint32_t li, uint32_t layer, uint64_t k, const float* grad, void* stream) {
+  int rc = check_local(c, li);
+  if (rc) return rc;
+  if (layer >= c->L) return fail(c, P3_EUSAGE, "layer out of range");
+  if (!grad) {
+    if (!c->grads[li]) return fail(c, P3_EUSAGE, "no gradient pointer and no gradient arena");
+    grad = c->grads[li] + c->layer_woff[layer];
+  }
+  Driver& d = driver();
+  const LocalDev& D = c->loc[li];
+  CUstream s = (CUstream)stream;
+  CUresult r = d.write32(s, (CUdeviceptr)(D.fifo_key + layer), c->fifo_seq[li]++, 0);
+  const uint64_t gp = (uint64_t)(uintptr_t)grad;
+  if (r == CUDA_SUCCESS) {
+    if (d.has64) {
+      r = d.write64(s, (CUdeviceptr)(D.gptr + layer), gp, 0);
+    } else {
+      r = d.write32(s, (CUdeviceptr)(D.gptr + layer), (cuuint32_t)(gp & 0xffffffffu), 0);
+      if (r == CUDA_SUCCESS) r = d.write32(s, (CUdeviceptr)(D.gptr + layer) + 4, (cuuint32_t)(gp >> 32), 0);
+    }
+  }
+  if (r == CUDA_SUCCESS) r = d.write32(s, (CUdeviceptr)(D.ready + layer), (cuuint32_t)(k + 1), 0);
+  if (r != CUDA_SUCCESS) return fail(c, P3_ECUDA, "cuStreamWriteValue failed (code " + std::to_string(r) + ")");
+  return P3_OK;
+}
+
+int p3_gradgen_layer(p3_ctx_t* c, uint32_t li, uint64_t seed, uint64_t k, uint32_t layer, void* stream) {
+  int rc = check_local(c, li);
+  if (rc) return rc;
+  if (layer >= c->L) return fail(c, P3_EUSAGE, "layer out of range");
+  if (!c->grads[li]) return fail(c, P3_EUSAGE, "context has no gradient arena (emulate_grads = 0)");
+  if (launch_gradgen(seed, k, layer, 0, c->counts[layer], c->grads[li] + c->layer_woff[layer], stream) != P3_OK)
+    return cuda_fail(c, cudaGetLastError(), "gradgen launch");
+  return P3_OK;
+}
+
+int p3_wait_layer(p3_ctx_t* c, uint32_t li, uint32_t layer, uint64_t k, void* stream) {
+  int rc = check_local(c, li);
+  if (rc) return rc;
+  if (layer >= c->L) return fail(c, P3_EUSAGE, "layer out of range");
+  if (k == 0) return P3_OK;  // forward pass 0 reads the initial parameters
+  const uint32_t target = (uint32_t)(k * c->layer_nslices[layer]);
+  uint32_t* flag = c->peers.done[c->cfg.local_ranks[li]] + layer;
+  CUresult r = driver().wait32((CUstream)stream, (CUdeviceptr)flag, target, CU_STREAM_WAIT_VALUE_GEQ);
+  if (r != CUDA_SUCCESS) return fail(c, P3_ECUDA, "cuStreamWaitValue32 failed (code " + std::to_string(r) + ")");
+  return P3_OK;
+}
+
+int p3_sync_all(p3_ctx_t* c, uint64_t k, double timeout_s) {
+  if (!c) return fail(nullptr, P3_EUSAGE, "null context");
+  const auto t0 = std::chrono::steady_clock::now();
+  auto elapsed = [&] { return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count(); };
+  if (c->comm_pending) {
+    for (;;) {
+      cudaError_t q = cudaEventQuery(c->comm_done);
+      if (q == cudaSuccess) break;
+      if (q != cudaErrorNotReady) return cuda_fail(c, q, "comm kernel");
+      if (elapsed() > timeout_s) return fail(c, P3_ETIMEOUT, "comm kernel did not finish before the timeout");
+      std::this_thread::sleep_for(std::chrono::microseconds(200));
+    }
+    c->comm_pending = false;
+  }
+  uint32_t err = 0;
+  CK(cudaMemcpyAsync(&err, c->d_err, 4, cudaMemcpyDeviceToHost, c->poll_stream));
+  CK(cudaStreamSynchronize(c->poll_stream));
+  if (err) return fail(c, (int)err, "comm kernel reported a stall (timeout waiting for peers or gradients)");
+  std::vector<uint32_t> done(c->L);
+  for (uint32_t i = 0; i < c->cfg.n_local; ++i) {
+    const uint32_t rank = c->cfg.local_ranks[i];
+    for (;;) {
+      CK(cudaMemcpyAsync(done.data(), c->peers.done[rank], c->L * 4ull, cudaMemcpyDeviceToHost, c->poll_stream));
+      CK(cudaStreamSynchronize(c->poll_stream));
+      std::vector<uint32_t> unmet;
+      for (uint32_t l = 0; l < c->L; ++l)
+        if ((int32_t)(done[l] - (uint32_t)(k * c->layer_nslices[l])) < 0) unmet.push_back(l);
+      if (unmet.empty()) break;
+      if (elapsed() > timeout_s) {
+        std::string m = "rank " + std::to_string(rank) + " stalled waiting for iteration-" + std::to_string(k) +
+                        " parameters; unmet layers [";
+        for (size_t j = 0; j < unmet.size() && j < 16; ++j) m += (j ? "," : "") + std::to_string(unmet[j]);
+        return fail(c, P3_ETIMEOUT, m + (unmet.size() > 16 ? ",...]" : "]"));
+      }
+      std::this_thread::sleep_for(std::chrono::microseconds(200));
+    }
+  }
+  if (k > c->synced_iterations) c->synced_iterations = k;
+  return P3_OK;
+}
+
+int p3_trace_read(p3_ctx_t* c, uint32_t li, p3_trace_rec_t* out, uint64_t cap, uint64_t* n_out) {
+  int rc = check_local(c, li);
+  if (rc) return rc;
+  unsigned long long n = 0;
+  CK(cudaMemcpyAsync(&n, c->loc[li].trace_n, 8, cudaMemcpyDeviceToHost, c->poll_stream));
+  CK(cudaStreamSynchronize(c->poll_stream));
+  n = std::min<unsigned long long>(n, c->cfg.trace_cap);
+  if (n_out) *n_out = n;
+  if (out && n) {
+    if (cap < n) return fail(c, P3_EUSAGE, "trace buffer too small");
+    CK(cudaMemcpyAsync(out, c->loc[li].trace, n * sizeof(p3_trace_rec_t), cudaMemcpyDeviceToHost, c->poll_stream));
+    CK(cudaStreamSynchronize(c->poll_stream));
+  }
+  return P3_OK;
+}
+
+int p3_trace_clear(p3_ctx_t* c) {
+  if (!c) return fail(nullptr, P3_EUSAGE, "null context");
+  for (uint32_t i = 0; i < c->cfg.n_local; ++i) CK(cudaMemsetAsync(c->loc[i].trace_n, 0, 8, c->poll_stream));
+  CK(cudaStreamSynchronize(c->poll_stream));
+  return P3_OK;
+}
+
+int p3_counters(p3_ctx_t* c, uint32_t li, uint64_t* bytes_in, uint64_t* bytes_out) {
+  int rc = check_local(c, li);
+  if (rc) return rc;
+  unsigned long long b[2] = {0, 0};
+  CK(cudaMemcpyAsync(b, c->loc[li].bytes, 16, cudaMemcpyDeviceToHost, c->poll_stream));
+  CK(cudaStreamSynchronize(c->poll_stream));
+  // broadcasts land by remote stores; their byte count follows from the plan per synced iteration
+  if (bytes_in) *bytes_in = b[0] + c->bcast_in_bytes[c->cfg.local_ranks[li]] * c->synced_iterations;
+  if (bytes_out) *bytes_out = b[1];
+  return P3_OK;
+}
+
+// ------------------------------------------------------------ scripted device queue
+
+struct p3_queue {
+  uint32_t L = 0, sched = 0, tag = 0, seq = 0;
+  std::vector<uint32_t> nslices;
+  char* d = nullptr;  // nslices | first | ready | fifo_key | cursor | result
+  uint32_t *d_nslices, *d_first, *d_ready, *d_fifo, *d_cursor, *d_result;
+  cudaStream_t s = nullptr;
+};
+
+int p3_queue_create(const uint32_t* layer_nslices, uint32_t n_layers, uint32_t sched, p3_queue_t** out) {
+  p3_ctx* c = nullptr;
+  if (!layer_nslices || !out || n_layers == 0) return fail(nullptr, P3_EUSAGE, "bad queue arguments");
+  if (sched > P3_SCHED_FIFO) return fail(nullptr, P3_EUSAGE, "bad queue discipline");
+  p3_queue* q = new p3_queue();
+  q->L = n_layers;
+  q->sched = sched;
+  q->nslices.assign(layer_nslices, layer_nslices + n_layers);
+  std::vector<uint32_t> first(n_layers);
+  uint64_t f = 0;
+  for (uint32_t l = 0; l < n_layers; ++l) {
+    first[l] = (uint32_t)f;
+    f += layer_nslices[l];
+  }
+  const size_t stride = align_up(n_layers * 4ull, 256);
+  cudaError_t e = cudaMalloc(&q->d, stride * 6);
+  if (e == cudaSuccess) e = cudaMemset(q->d, 0, stride * 6);
+  q->d_nslices = reinterpret_cast<uint32_t*>(q->d);
+  q->d_first = reinterpret_cast<uint32_t*>(q->d + stride);
+  q->d_ready = reinterpret_cast<uint32_t*>(q->d + 2 * stride);
+  q->d_fifo = reinterpret_cast<uint32_t*>(q->d + 3 * stride);
+  q->d_cursor = reinterpret_cast<uint32_t*>(q->d + 4 * stride);
+  q->d_result = reinterpret_cast<uint32_t*>(q->d + 5 * stride);
+  if (e == cudaSuccess) e = cudaMemcpy(q->d_nslices, layer_nslices, n_layers * 4ull, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(q->d_first, first.data(), n_layers * 4ull, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&q->s, cudaStreamNonBlocking);
+  if (e != cudaSuccess) {
+    p3_queue_destroy(q);
+    return cuda_fail(c, e, "queue init");
+  }
+  *out = q;
+  return P3_OK;
+}
+
+int p3_queue_put_layer(p3_queue_t* q, uint32_t layer, uint32_t iteration) {
+  p3_ctx* c = nullptr;
+  if (!q || layer >= q->L) return fail(nullptr, P3_EUSAGE, "layer out of range");
+  const uint32_t tag = iteration + 1, zero = 0, key = q->seq++;
+  CK(cudaMemcpyAsync(q->d_cursor + layer, &zero, 4, cudaMemcpyHostToDevice, q->s));
+  CK(cudaMemcpyAsync(q->d_fifo + layer, &key, 4, cudaMemcpyHostToDevice, q->s));
+  CK(cudaMemcpyAsync(q->d_ready + layer, &tag, 4, cudaMemcpyHostToDevice, q->s));
+  CK(cudaStreamSynchronize(q->s));
+  q->tag = std::max(q->tag, tag);
+  return P3_OK;
+}
+
+int p3_queue_poll(p3_queue_t* q, uint32_t* layer, uint32_t* slice) {
+  p3_ctx* c = nullptr;
+  if (!q) return fail(nullptr, P3_EUSAGE, "null queue");
+  if (q->tag == 0) return P3_ETIMEOUT;
+  if (launch_queue_pop(q->d_nslices, q->d_first, q->d_ready, q->d_fifo, q->d_cursor, q->L, q->sched, q->tag,
+                       q->d_result, q->s) != P3_OK)
+    return cuda_fail(c, cudaGetLastError(), "queue pop launch");
+  uint32_t g = 0;
+  CK(cudaMemcpyAsync(&g, q->d_result, 4, cudaMemcpyDeviceToHost, q->s));
+  CK(cudaStreamSynchronize(q->s));
+  if (g == 0xffffffffu) return P3_ETIMEOUT;
+  // global slice id -> (layer, slice)
+  uint32_t l = 0;
+  uint64_t f = 0;
+  while (l < q->L && f + q->nslices[l] <= g) f += q->nslices[l++];
+  *layer = l;
+  *slice = (uint32_t)(g - f);
+  return P3_OK;
+}
+
+int p3_queue_destroy(p3_queue_t* q) {
+  if (!q) return P3_OK;
+  if (q->s) cudaStreamSynchronize(q->s);
+  if (q->d) cudaFree(q->d);
+  if (q->s) cudaStreamDestroy(q->s);
+  delete q;
+  return P3_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,103 @@
+// Internal declarations shared by the host planner, the kernels and the context.
+#pragma once
+
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/p3.h"
+
+#define P3_MAX_LOCAL P3_MAX_RANKS
+
+namespace p3 {
+
+uint64_t splitmix64_mix(uint64_t z);
+int build_p3_plan(const uint64_t* counts, uint32_t n_layers, uint32_t servers, uint64_t max_slice,
+                  std::vector<p3_slice_t>* out, std::string* err);
+int build_baseline_plan(const uint64_t* counts, uint32_t n_layers, uint32_t servers,
+                        uint64_t big_threshold, uint64_t rng_seed, std::vector<p3_slice_t>* out,
+                        std::string* err);
+void set_thread_error(const std::string& msg);
+
+// ---------------------------------------------------------------- device-side views
+
+// Read-only plan tables (one copy per GPU). Global slice id g enumerates the plan in
+// (layer, slice) order, i.e. in priority order.
+struct PlanDev {
+  uint32_t n_layers;
+  uint32_t total_slices;
+  uint32_t world;
+  uint32_t pad_;
+  const uint32_t* layer_nslices;  // [L]
+  const uint32_t* layer_first;    // [L] first global slice id of the layer
+  const uint64_t* layer_woff;     // [L] element offset of the layer in W / G arenas
+  const uint64_t* slice_off;      // [S] element offset inside the layer
+  const uint32_t* slice_len;      // [S]
+  const uint32_t* slice_layer;    // [S]
+  const uint32_t* slice_owner;    // [S]
+  const uint64_t* slice_slot;     // [S] element offset in the owner's per-pusher R block
+  const uint32_t* own_list;       // [S] slice ids grouped by owner, plan order inside
+  const uint32_t* own_lfirst;     // [world*L] index into own_list of (owner, layer)
+  const uint32_t* own_lcount;     // [world*L] owned slices of (owner, layer)
+  const uint32_t* own_total;      // [world] owned slices per owner
+  const uint64_t* own_stride;     // [world] R block stride (padded owned elements)
+};
+
+// Peer-visible state of every rank (pointers valid in this process: local or IPC-mapped).
+struct PeersDev {
+  float* W[P3_MAX_RANKS];          // parameter replica
+  float* R[P3_MAX_RANKS];          // receive slots [world][own_stride]
+  uint32_t* arrivals[P3_MAX_RANKS];  // [S] pushes received per owned slice (monotone)
+  uint32_t* hint[P3_MAX_RANKS];      // [L] owned slices completed per layer (monotone)
+  uint32_t* done[P3_MAX_RANKS];      // [L] slices of a layer broadcast into W (monotone)
+};
+
+// Per-iteration scratch of one local rank; zeroed before each comm launch.
+struct IterState {
+  uint32_t pushed;   // worker slices claimed
+  uint32_t reduced;  // owned slices claimed
+  uint32_t pad_[2];
+};
+
+// Local-only state of one rank hosted in this process.
+struct LocalDev {
+  uint32_t rank;
+  uint32_t trace_cap;
+  uint32_t* ready;      // [L] iteration tag k+1 once the layer's gradient is published
+  uint32_t* fifo_key;   // [L] publish sequence (FIFO discipline)
+  uint64_t* gptr;       // [L] gradient pointer of the layer
+  uint32_t* claim;      // [S] server claim tag (monotone: k -> k+1)
+  uint32_t* cursor;     // [L] worker claim cursor (per iteration)
+  uint32_t* srv_lo;     // [L] server scan watermark (per iteration)
+  uint32_t* srv_taken;  // [L] owned slices claimed (per iteration)
+  IterState* it;        // per iteration
+  float* V;             // momentum of owned elements [own_stride] (may be null)
+  unsigned long long* bytes;  // [2] in, out
+  unsigned long long* trace_n;
+  p3_trace_rec_t* trace;
+};
+
+struct CommArgs {
+  PlanDev plan;
+  PeersDev peers;
+  LocalDev loc[P3_MAX_LOCAL];
+  uint32_t n_local;
+  uint32_t k;  // iteration
+  uint32_t sched;
+  float lr;
+  float momentum;
+  uint32_t pad_;
+  unsigned long long timeout_ns;
+  uint32_t* err;  // device error word (P3_* code)
+};
+
+// Launchers (p3_kernels.cu)
+int launch_comm(const CommArgs& a, uint32_t ctas, uint32_t threads, void* stream);
+int launch_gradgen(uint64_t seed, uint64_t iteration, uint64_t layer, uint64_t start, uint64_t count,
+                   float* out, void* stream);
+int launch_queue_pop(const uint32_t* nslices, const uint32_t* first, const uint32_t* ready,
+                     const uint32_t* fifo_key, uint32_t* cursor, uint32_t n_layers, uint32_t sched,
+                     uint32_t tag, uint32_t* result, void* stream);
+
+}  // namespace p3

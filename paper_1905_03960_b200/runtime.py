@@ -1,0 +1,319 @@
+"""Device runtime of the P3 sync path: the sync context and the emulated training worker.
+
+``SyncContext`` wraps one ``p3_ctx_t`` (csrc/p3_ctx.cu): the plan tables on the GPU, the
+per-rank parameter replica ``W`` (peer-writable), the receive slots ``R``, the flags, and
+the per-iteration launch of the persistent comm kernel (K3). It hosts either one rank
+(one process per GPU, peers opened through CUDA IPC) or all ranks of a world on one GPU
+(single-launch emulation for tests).
+
+``TrainingWorker`` mirrors ``p3sync.worker.TrainingWorker`` (reference
+``pkg/src/p3sync/worker.py:64-392``) in emulate mode: per-layer forward gating
+(_wait_layer), sleep-emulated fwd/bwd compute on the device, synthetic GradGen gradients
+(K1) and atomic per-layer publication (enqueue_layer), with the comm kernel doing the
+priority send, the owner-side aggregate/update and the broadcast.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from .hashing import FNV_OFFSET, fnv1a64
+from .model import ModelProfile
+from .plan import BASELINE_MODE, P3_MODE, DEFAULT_MAX_SLICE, SliceKey, make_p3_plan
+
+
+class _DeviceArray:
+    """Zero-copy __cuda_array_interface__ view so torch can alias libp3-owned memory."""
+
+    def __init__(self, ptr: int, n: int, owner) -> None:
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<f4", "data": (ptr, False), "version": 2}
+        self._owner = owner
+
+
+@dataclass
+class TraceEvent:
+    t_ns: int
+    iteration: int
+    layer: int
+    slice: int
+    rank: int
+    event: int  # _lib.P3_EV_PUSH / P3_EV_BCAST
+
+
+class SyncContext:
+    """One p3 sync context (see include/p3.h, p3_ctx_create)."""
+
+    def __init__(
+        self,
+        layer_counts: list[int],
+        world: int,
+        local_ranks: list[int],
+        max_slice: int = DEFAULT_MAX_SLICE,
+        lr: float = 0.1,
+        momentum: float = 0.0,
+        priority_mode: bool = True,
+        comm_ctas: int = 16,
+        comm_threads: int = 512,
+        timeout_s: float = 60.0,
+        trace_cap: int = 0,
+        emulate_grads: bool = False,
+    ) -> None:
+        import torch
+
+        torch.cuda.init()
+        self.lib = _lib.load()
+        self.layer_counts = [int(c) for c in layer_counts]
+        self.world = world
+        self.local_ranks = list(local_ranks)
+        self.max_slice = max_slice
+        self.lr = lr
+        self.trace_cap = trace_cap
+        self.timeout_s = timeout_s
+        cfg = _lib.Config()
+        cfg.world = world
+        cfg.n_local = len(self.local_ranks)
+        for i, r in enumerate(self.local_ranks):
+            cfg.local_ranks[i] = r
+        cfg.n_layers = len(self.layer_counts)
+        self._counts = _lib.u64_array(self.layer_counts)
+        cfg.layer_counts = ctypes.cast(self._counts, ctypes.POINTER(ctypes.c_uint64))
+        cfg.max_slice = max_slice
+        cfg.plan_mode = _lib.P3_PLAN_P3
+        cfg.sched = _lib.P3_SCHED_PRIORITY if priority_mode else _lib.P3_SCHED_FIFO
+        cfg.lr = lr
+        cfg.momentum = momentum
+        cfg.comm_ctas = comm_ctas
+        cfg.comm_threads = comm_threads
+        cfg.timeout_s = timeout_s
+        cfg.trace_cap = trace_cap
+        cfg.emulate_grads = 1 if emulate_grads else 0
+        h = ctypes.c_void_p()
+        _lib.check(self.lib.p3_ctx_create(ctypes.byref(cfg), ctypes.byref(h)), what="p3_ctx_create")
+        self._h = h
+        self.layer_offsets = []
+        off = ctypes.c_uint64()
+        for l in range(len(self.layer_counts)):
+            self._check(self.lib.p3_ctx_layer_offset(self._h, l, ctypes.byref(off)), "p3_ctx_layer_offset")
+            self.layer_offsets.append(int(off.value))
+        self.arena_elems = self.layer_offsets[-1] + self.layer_counts[-1]
+        self.slices_per_layer = [(c + max_slice - 1) // max_slice for c in self.layer_counts]
+
+    # ------------------------------------------------------------------ plumbing
+    def _check(self, rc: int, what: str) -> None:
+        _lib.check(rc, self._h, what)
+
+    @property
+    def handle(self):
+        return self._h
+
+    def _ptr(self, fn, li: int) -> int:
+        p = ctypes.c_void_p()
+        self._check(fn(self._h, li, ctypes.byref(p)), fn.__name__)
+        return int(p.value)
+
+    def params_arena(self, li: int = 0):
+        """torch float32 view over the whole parameter replica W of local rank ``li``."""
+        import torch
+
+        return torch.as_tensor(_DeviceArray(self._ptr(self.lib.p3_ctx_params, li), self.arena_elems, self), device="cuda")
+
+    def grads_arena(self, li: int = 0):
+        import torch
+
+        return torch.as_tensor(_DeviceArray(self._ptr(self.lib.p3_ctx_grads, li), self.arena_elems, self), device="cuda")
+
+    def layer_params(self, li: int, layer: int):
+        off = self.layer_offsets[layer]
+        return self.params_arena(li)[off : off + self.layer_counts[layer]]
+
+    def ipc_handle(self, li: int = 0) -> bytes:
+        buf = ctypes.create_string_buffer(_lib.P3_IPC_BYTES)
+        self._check(self.lib.p3_ctx_ipc_handle(self._h, li, buf), "p3_ctx_ipc_handle")
+        return buf.raw
+
+    def open_peers(self, handles: list[bytes]) -> None:
+        blob = b"".join(h.ljust(_lib.P3_IPC_BYTES, b"\0") for h in handles)
+        buf = ctypes.create_string_buffer(blob, len(blob))
+        self._check(self.lib.p3_ctx_open_peers(self._h, buf), "p3_ctx_open_peers")
+
+    # ------------------------------------------------------------------ hot calls
+    def iteration_begin(self, k: int, stream=None) -> None:
+        self._check(self.lib.p3_iteration_begin(self._h, k, _lib.stream_handle(stream)), "p3_iteration_begin")
+
+    def layer_ready(self, li: int, layer: int, k: int, grad=None, stream=None) -> None:
+        ptr = grad.data_ptr() if grad is not None else None
+        self._check(self.lib.p3_layer_ready(self._h, li, layer, k, ptr, _lib.stream_handle(stream)), "p3_layer_ready")
+
+    def gradgen_layer(self, li: int, seed: int, k: int, layer: int, stream=None) -> None:
+        self._check(
+            self.lib.p3_gradgen_layer(self._h, li, seed & 0xFFFFFFFFFFFFFFFF, k, layer, _lib.stream_handle(stream)),
+            "p3_gradgen_layer",
+        )
+
+    def wait_layer(self, li: int, layer: int, k: int, stream=None) -> None:
+        self._check(self.lib.p3_wait_layer(self._h, li, layer, k, _lib.stream_handle(stream)), "p3_wait_layer")
+
+    def sync_all(self, k: int, timeout_s: float | None = None) -> None:
+        self._check(self.lib.p3_sync_all(self._h, k, self.timeout_s if timeout_s is None else timeout_s), "p3_sync_all")
+
+    # ------------------------------------------------------------------ outputs
+    def trace(self, li: int = 0) -> list[TraceEvent]:
+        n = ctypes.c_uint64()
+        self._check(self.lib.p3_trace_read(self._h, li, None, 0, ctypes.byref(n)), "p3_trace_read")
+        if n.value == 0:
+            return []
+        recs = (_lib.TraceRec * n.value)()
+        self._check(self.lib.p3_trace_read(self._h, li, recs, n.value, ctypes.byref(n)), "p3_trace_read")
+        return [TraceEvent(r.t_ns, r.iteration, r.layer, r.slice, r.rank, r.event) for r in recs[: n.value]]
+
+    def clear_trace(self) -> None:
+        self._check(self.lib.p3_trace_clear(self._h), "p3_trace_clear")
+
+    def counters(self, li: int = 0) -> tuple[int, int]:
+        a, b = ctypes.c_uint64(), ctypes.c_uint64()
+        self._check(self.lib.p3_counters(self._h, li, ctypes.byref(a), ctypes.byref(b)), "p3_counters")
+        return int(a.value), int(b.value)
+
+    def params_numpy(self, li: int = 0) -> list[np.ndarray]:
+        flat = self.params_arena(li).cpu().numpy()
+        return [flat[o : o + c].copy() for o, c in zip(self.layer_offsets, self.layer_counts)]
+
+    def params_digest(self, li: int = 0) -> int:
+        """params_digest (worker.py:372-376): chained FNV-1a over fp32 LE layer bytes."""
+        h = FNV_OFFSET
+        for vec in self.params_numpy(li):
+            h = fnv1a64(vec.astype("<f4").tobytes(), h)
+        return h
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            self.lib.p3_ctx_destroy(self._h)
+            self._h = None
+
+    def __del__(self):  # pragma: no cover - best effort
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+@dataclass
+class WorkerConfig:
+    """Worker settings (worker.py:25-36); ``servers`` is replaced by the world size."""
+
+    rank: int
+    mode: str
+    world: int
+    iterations: int
+    lr: float = 0.1
+    batch_size: int = 32
+    max_slice: int = DEFAULT_MAX_SLICE
+    deadlock_timeout: float = 60.0
+    emulate_compute: bool = True
+    comm_ctas: int = 16
+    comm_threads: int = 512
+    trace_cap: int = 0
+    rank_distinct_grads: bool = False
+
+
+def rank_seed(seed: int, rank: int, distinct: bool) -> int:
+    """GradGen seed of a rank: the reference's seed for every rank (worker.py:71), or a
+    splitmix-salted seed per rank when distinct gradients are requested."""
+    if not distinct or rank == 0:
+        return seed
+    from .hashing import splitmix64_stream
+
+    return seed ^ splitmix64_stream(0x5EED, rank)
+
+
+class TrainingWorker:
+    """Emulate-mode worker(s) on one GPU; ``ranks`` > 1 emulates a whole world in one process.
+
+    ``run_iteration`` issues, per hosted rank and on that rank's compute stream:
+    forward: ``_wait_layer`` gate (stream memory wait) + device sleep per layer;
+    backward: device sleep, K1 gradient generation and ``enqueue_layer`` per layer in
+    reverse order (worker.py:312-325). The comm kernel for the iteration is launched first
+    on the comm stream.
+    """
+
+    def __init__(self, config: WorkerConfig, profile: ModelProfile, ranks: list[int] | None = None, ctx: SyncContext | None = None) -> None:
+        import torch
+
+        if config.mode not in (P3_MODE, "fifo"):
+            raise ValueError(f"emulate worker runs the p3 (priority) or fifo discipline, not {config.mode!r}")
+        self.cfg = config
+        self.profile = profile
+        self.ranks = list(ranks) if ranks is not None else [config.rank]
+        self.plan = make_p3_plan(profile, config.world, config.max_slice)
+        self.ctx = ctx or SyncContext(
+            profile.param_counts(),
+            config.world,
+            self.ranks,
+            max_slice=config.max_slice,
+            lr=config.lr,
+            priority_mode=config.mode == P3_MODE,
+            comm_ctas=config.comm_ctas,
+            comm_threads=config.comm_threads,
+            timeout_s=config.deadlock_timeout,
+            trace_cap=config.trace_cap,
+            emulate_grads=True,
+        )
+        self.comm_stream = torch.cuda.Stream()
+        self.streams = [torch.cuda.Stream() for _ in self.ranks]
+        self.iterations_done = 0
+        self.iter_events: list = []
+
+    def run_iteration(self, k: int) -> None:
+        import torch
+
+        lib = self.ctx.lib
+        ctx = self.ctx
+        ctx.iteration_begin(k, self.comm_stream)
+        for li, rank in enumerate(self.ranks):
+            s = self.streams[li]
+            sh = _lib.stream_handle(s)
+            seed = rank_seed(self.profile.seed, rank, self.cfg.rank_distinct_grads)
+            for layer in self.profile.layers:
+                ctx._check(lib.p3_wait_layer(ctx.handle, li, layer.index, k, sh), "p3_wait_layer")
+                if self.cfg.emulate_compute and layer.fwd_time:
+                    _lib.check(lib.p3_emulate_compute(layer.fwd_time, sh), what="p3_emulate_compute")
+            if li == 0:
+                ev = torch.cuda.Event(enable_timing=True)
+                ev.record(s)
+                self.iter_events.append(ev)
+            for layer in reversed(self.profile.layers):
+                if self.cfg.emulate_compute and layer.bwd_time:
+                    _lib.check(lib.p3_emulate_compute(layer.bwd_time, sh), what="p3_emulate_compute")
+                ctx._check(lib.p3_gradgen_layer(ctx.handle, li, seed & 0xFFFFFFFFFFFFFFFF, k, layer.index, sh), "p3_gradgen_layer")
+                ctx._check(lib.p3_layer_ready(ctx.handle, li, layer.index, k, None, sh), "p3_layer_ready")
+        self.iterations_done = k + 1
+
+    def run(self) -> None:
+        for k in range(self.cfg.iterations):
+            self.run_iteration(k)
+        self.wait_all(self.cfg.iterations)
+
+    def wait_all(self, iteration: int) -> None:
+        self.ctx.sync_all(iteration, self.cfg.deadlock_timeout)
+        import torch
+
+        for s in self.streams:
+            s.synchronize()
+
+    def params(self, li: int = 0) -> list[np.ndarray]:
+        return self.ctx.params_numpy(li)
+
+    def params_digest(self, li: int = 0) -> int:
+        return self.ctx.params_digest(li)
+
+    def transmission_sequence(self, li: int = 0, iteration: int | None = None) -> list[SliceKey]:
+        ev = [e for e in self.ctx.trace(li) if e.event == _lib.P3_EV_PUSH and (iteration is None or e.iteration == iteration)]
+        return [SliceKey(e.layer, e.slice) for e in ev]
+
+    def close(self) -> None:
+        self.ctx.close()
