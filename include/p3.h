@@ -202,6 +202,13 @@ int p3_trace_clear(p3_ctx_t* ctx);
 /* NetCounters.totals (metrics.py:31-45): NVLink/HBM payload bytes in / out. */
 int p3_counters(p3_ctx_t* ctx, uint32_t local_idx, uint64_t* bytes_in, uint64_t* bytes_out);
 
+/* Diagnostics snapshot of a local rank (deadlock dumps, worker.py:291-297): 5 arrays of
+ * n_layers u32 — ready tag, claim cursor, server claims, completed-hint, done counter —
+ * followed by the 4 per-iteration counters. Copied on a private stream (never blocks on
+ * the compute or comm streams). */
+int p3_debug_snapshot(p3_ctx_t* ctx, uint32_t local_idx, uint32_t* out, uint64_t cap,
+                      uint64_t* n_out);
+
 /* Diagnostics of the last failing call on this context (thread-local when ctx == NULL). */
 const char* p3_last_error(p3_ctx_t* ctx);
 

@@ -105,6 +105,7 @@ SIGNATURES = {
     "p3_trace_read": (ctypes.c_int, [_P, _U32, ctypes.POINTER(TraceRec), _U64, _PU64]),
     "p3_trace_clear": (ctypes.c_int, [_P]),
     "p3_counters": (ctypes.c_int, [_P, _U32, _PU64, _PU64]),
+    "p3_debug_snapshot": (ctypes.c_int, [_P, _U32, _PU32, _U64, _PU64]),
     "p3_last_error": (ctypes.c_char_p, [_P]),
     "p3_device_info": (ctypes.c_int, [ctypes.POINTER(ctypes.c_int)] * 4),
 }

@@ -225,6 +225,7 @@ int p3_ctx_create(const p3_config_t* cfg, p3_ctx_t** out) {
   for (uint32_t i = 0; i < cfg->n_local; ++i)
     if (cfg->local_ranks[i] >= cfg->world) return fail(nullptr, P3_EUSAGE, "local rank out of range");
   if (!driver().ok) return fail(nullptr, P3_ECUDA, "CUDA driver stream memory operations unavailable");
+  if (preload_kernels() != P3_OK) return fail(nullptr, P3_ECUDA, "loading the sm_100a kernels failed");
 
   c = new p3_ctx();
   c->cfg = *cfg;
@@ -558,10 +559,25 @@ int p3_sync_all(p3_ctx_t* c, uint64_t k, double timeout_s) {
     }
     c->comm_pending = false;
   }
-  uint32_t err = 0;
-  CK(cudaMemcpyAsync(&err, c->d_err, 4, cudaMemcpyDeviceToHost, c->poll_stream));
+  uint32_t ew[64] = {0};
+  CK(cudaMemcpyAsync(ew, c->d_err, sizeof(ew), cudaMemcpyDeviceToHost, c->poll_stream));
   CK(cudaStreamSynchronize(c->poll_stream));
-  if (err) return fail(c, (int)err, "comm kernel reported a stall (timeout waiting for peers or gradients)");
+  if (ew[0]) {
+    std::string m = "comm kernel of iteration " + std::to_string(ew[1]) +
+                    " stalled (timeout waiting for peers or gradients);";
+    for (uint32_t i = 0; i < c->cfg.n_local; ++i) {
+      std::vector<uint32_t> ready(c->L);
+      cudaMemcpyAsync(ready.data(), c->loc[i].ready, c->L * 4ull, cudaMemcpyDeviceToHost, c->poll_stream);
+      cudaStreamSynchronize(c->poll_stream);
+      uint32_t nready = 0;
+      for (uint32_t l = 0; l < c->L; ++l) nready += ready[l] > ew[1];
+      m += " rank " + std::to_string(c->cfg.local_ranks[i]) + ": pushed " + std::to_string(ew[2 + 2 * i]) + "/" +
+           std::to_string(c->S) + " reduced " + std::to_string(ew[3 + 2 * i]) + "/" +
+           std::to_string(c->own_total[c->cfg.local_ranks[i]]) + " ready layers " + std::to_string(nready) + "/" +
+           std::to_string(c->L) + ";";
+    }
+    return fail(c, (int)ew[0], m);
+  }
   std::vector<uint32_t> done(c->L);
   for (uint32_t i = 0; i < c->cfg.n_local; ++i) {
     const uint32_t rank = c->cfg.local_ranks[i];
@@ -620,6 +636,23 @@ int p3_counters(p3_ctx_t* c, uint32_t li, uint64_t* bytes_in, uint64_t* bytes_ou
   return P3_OK;
 }
 
+int p3_debug_snapshot(p3_ctx_t* c, uint32_t li, uint32_t* out, uint64_t cap, uint64_t* n_out) {
+  int rc = check_local(c, li);
+  if (rc) return rc;
+  const uint64_t n = 5ull * c->L + 4;
+  if (n_out) *n_out = n;
+  if (!out) return P3_OK;
+  if (cap < n) return fail(c, P3_EUSAGE, "snapshot buffer too small");
+  const LocalDev& D = c->loc[li];
+  const uint32_t rank = c->cfg.local_ranks[li];
+  const uint32_t* src[5] = {D.ready, D.cursor, D.srv_taken, c->peers.hint[rank], c->peers.done[rank]};
+  for (int a = 0; a < 5; ++a)
+    CK(cudaMemcpyAsync(out + (uint64_t)a * c->L, src[a], c->L * 4ull, cudaMemcpyDeviceToHost, c->poll_stream));
+  CK(cudaMemcpyAsync(out + 5ull * c->L, D.it, 16, cudaMemcpyDeviceToHost, c->poll_stream));
+  CK(cudaStreamSynchronize(c->poll_stream));
+  return P3_OK;
+}
+
 // ------------------------------------------------------------ scripted device queue
 
 struct p3_queue {
@@ -634,6 +667,7 @@ int p3_queue_create(const uint32_t* layer_nslices, uint32_t n_layers, uint32_t s
   p3_ctx* c = nullptr;
   if (!layer_nslices || !out || n_layers == 0) return fail(nullptr, P3_EUSAGE, "bad queue arguments");
   if (sched > P3_SCHED_FIFO) return fail(nullptr, P3_EUSAGE, "bad queue discipline");
+  if (preload_kernels() != P3_OK) return fail(nullptr, P3_ECUDA, "loading the sm_100a kernels failed");
   p3_queue* q = new p3_queue();
   q->L = n_layers;
   q->sched = sched;

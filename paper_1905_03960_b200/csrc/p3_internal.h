@@ -93,6 +93,7 @@ struct CommArgs {
 };
 
 // Launchers (p3_kernels.cu)
+int preload_kernels();
 int launch_comm(const CommArgs& a, uint32_t ctas, uint32_t threads, void* stream);
 int launch_gradgen(uint64_t seed, uint64_t iteration, uint64_t layer, uint64_t start, uint64_t count,
                    float* out, void* stream);

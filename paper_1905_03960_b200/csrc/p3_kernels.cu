@@ -564,8 +564,13 @@ __global__ void __launch_bounds__(1024) k_comm(const __grid_constant__ CommArgs 
         } else if (globaltimer() - t0 > a.timeout_ns) {
           job = 3;
           if (lane == 0 && atomicCAS(a.err, 0u, (uint32_t)P3_ETIMEOUT) == 0u) {
-            // release every forward gate of the local ranks so the compute streams drain;
-            // the host reports the timeout from p3_sync_all
+            // diagnostics for the host (p3_sync_all), then release every forward gate of the
+            // local ranks so the compute streams drain
+            a.err[1] = a.k;
+            for (uint32_t t = 0; t < a.n_local; ++t) {
+              a.err[2 + 2 * t] = ld_relaxed_gpu(&a.loc[t].it->pushed);
+              a.err[3 + 2 * t] = ld_relaxed_gpu(&a.loc[t].it->reduced);
+            }
             for (uint32_t t = 0; t < a.n_local; ++t)
               for (uint32_t l = 0; l < a.plan.n_layers; ++l)
                 atomicAdd(a.peers.done[a.loc[t].rank] + l, 0x40000000u);
@@ -586,6 +591,19 @@ __global__ void __launch_bounds__(1024) k_comm(const __grid_constant__ CommArgs 
     else if (job == 2) do_push(a, a.loc[s_li], s_g, &s_push);
     __syncthreads();
   }
+}
+
+// With lazy module loading (CUDA_MODULE_LOADING=LAZY, the CUDA 12 default) the first launch
+// of a kernel loads it, and loading waits for the kernels already running on the device.
+// A persistent comm kernel waits for work of the compute streams, so every kernel those
+// streams may launch must be loaded before the comm kernel starts: query them all here.
+int preload_kernels() {
+  cudaFuncAttributes fa;
+  const void* fns[] = {(const void*)k_comm, (const void*)k_gradgen, (const void*)k_sleep,
+                       (const void*)k_shard_update, (const void*)k_queue_pop};
+  for (const void* f : fns)
+    if (cudaFuncGetAttributes(&fa, f) != cudaSuccess) return P3_ECUDA;
+  return P3_OK;
 }
 
 int launch_comm(const CommArgs& a, uint32_t ctas, uint32_t threads, void* stream) {

@@ -171,6 +171,18 @@ class SyncContext:
         self._check(self.lib.p3_trace_read(self._h, li, recs, n.value, ctypes.byref(n)), "p3_trace_read")
         return [TraceEvent(r.t_ns, r.iteration, r.layer, r.slice, r.rank, r.event) for r in recs[: n.value]]
 
+    def debug_snapshot(self, li: int = 0) -> dict:
+        n = ctypes.c_uint64()
+        self._check(self.lib.p3_debug_snapshot(self._h, li, None, 0, ctypes.byref(n)), "p3_debug_snapshot")
+        buf = (ctypes.c_uint32 * n.value)()
+        self._check(self.lib.p3_debug_snapshot(self._h, li, buf, n.value, ctypes.byref(n)), "p3_debug_snapshot")
+        L = len(self.layer_counts)
+        arr = list(buf)
+        names = ("ready", "cursor", "srv_taken", "hint", "done")
+        out = {nm: arr[i * L : (i + 1) * L] for i, nm in enumerate(names)}
+        out["pushed"], out["reduced"] = arr[5 * L], arr[5 * L + 1]
+        return out
+
     def clear_trace(self) -> None:
         self._check(self.lib.p3_trace_clear(self._h), "p3_trace_clear")
 
