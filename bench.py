@@ -1,0 +1,376 @@
+#!/usr/bin/env python
+"""Benchmark of the P3 sync path on B200 (BASELINE.json metric: samples/s of P3 vs
+layer-wise sync; slice-sync GB/s; roofline fraction).
+
+One step = one data-parallel training iteration of the named model on synthetic input:
+forward (each layer gated on its synced parameters), backward (each layer's gradient
+published by a hook), and the sliced, priority-scheduled reduce + SGD + broadcast done by
+the persistent comm kernel, overlapped with compute. Launch:
+
+    python bench.py [--gpus 1] [--steps K] [--warmup W]
+    python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 bench.py --gpus N
+    python bench.py --impl reference   # the reference P3 path on host cores (oracle port)
+
+Rank 0 prints ONE JSON line.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+from pathlib import Path
+
+os.environ.setdefault("CUDA_MODULE_LOADING", "EAGER")
+REPO = Path(__file__).resolve().parent
+sys.path.insert(0, str(REPO))
+
+METRIC = "samples/sec (P3 sliced priority sync, data-parallel training step)"
+DEFAULT_BATCH = {"resnet50": 256, "vgg19": 128, "seq2seq": 128}
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--model", choices=["resnet50", "vgg19", "seq2seq"], default="resnet50")
+    ap.add_argument("--batch", type=int, default=0, help="per-GPU batch (default per model)")
+    ap.add_argument("--max-slice", type=int, default=50_000)
+    ap.add_argument("--comm-ctas", type=int, default=16)
+    ap.add_argument("--lr", type=float, default=0.01)
+    ap.add_argument("--skip-layerwise", action="store_true")
+    ap.add_argument("--skip-cpu", action="store_true")
+    ap.add_argument("--sync-reps", type=int, default=10)
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------------------- helpers
+
+
+class ClockSampler:
+    FIELDS = ("clocks.sm", "clocks.max.sm", "clocks_event_reasons.hw_slowdown",
+              "clocks_event_reasons.hw_thermal_slowdown", "clocks_event_reasons.sw_thermal_slowdown",
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index: int) -> None:
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        try:
+            self.p = subprocess.Popen(
+                ["nvidia-smi", "-i", str(device_index), f"--query-gpu={','.join(self.FIELDS)}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=self.f, stderr=subprocess.DEVNULL)
+        except OSError:
+            self.p = None
+
+    def stop(self) -> dict:
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        self.p.wait()
+        self.f.seek(0)
+        rows = [r.split(", ") for r in self.f.read().strip().splitlines() if r.strip()]
+        os.unlink(self.f.name)
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if len(r) > 2 + i and r[2 + i].strip() == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+def dist_setup(args):
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return world, rank, local
+
+
+def max_over_ranks(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([x], device="cuda", dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(world: int) -> None:
+    import torch
+
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+    torch.cuda.synchronize()
+
+
+def build(args, rank):
+    import torch
+
+    from paper_1905_03960_b200.torch_models import build_model
+
+    torch.manual_seed(1234)
+    m = build_model(args.model).cuda()
+    if args.model in ("resnet50", "vgg19"):
+        m = m.to(memory_format=torch.channels_last)
+    return m
+
+
+def time_training(args, world, rank, ddp, x, y, steps, warmup, e2e=None):
+    """Device time of `steps` training steps (max over ranks), after `warmup` steps."""
+    import torch
+
+    from paper_1905_03960_b200.torch_models import loss_fn
+
+    def step(i):
+        if e2e is None:
+            loss = loss_fn(args.model, ddp, x, y)
+            loss.backward()
+            return loss
+        xh, yh, lh = e2e
+        xd = xh.to("cuda", non_blocking=True)
+        yd = yh.to("cuda", non_blocking=True)
+        loss = loss_fn(args.model, ddp, xd, yd)
+        loss.backward()
+        lh[i % len(lh)].copy_(loss.detach(), non_blocking=True)
+        return loss
+
+    for i in range(warmup):
+        step(i)
+    ddp.synchronize()
+    barrier(world)
+    clocks = ClockSampler(torch.cuda.current_device()) if rank == 0 else None
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for i in range(steps):
+        step(i)
+    ddp.synchronize()
+    e.record()
+    torch.cuda.synchronize()
+    ms = s.elapsed_time(e)
+    ck = clocks.stop() if clocks else None
+    return max_over_ranks(ms, world), ck
+
+
+# ----------------------------------------------------------------------------- arms
+
+
+def sync_only_roofline(args, world, rank, counts):
+    """Slice-sync kernel alone: every layer's gradient already in HBM and published, the
+    comm kernel (K3 + K4) launched over the whole GPU. Returns per-launch device ms."""
+    import torch
+
+    from paper_1905_03960_b200 import _lib
+    from paper_1905_03960_b200.runtime import SyncContext
+
+    props = torch.cuda.get_device_properties(0)
+    ctas = 2 * props.multi_processor_count
+    ctx = SyncContext(counts, world, [rank], max_slice=args.max_slice, lr=args.lr, comm_ctas=ctas,
+                      comm_threads=512, timeout_s=60.0, emulate_grads=True)
+    if world > 1:
+        import torch.distributed as dist
+
+        hs = [None] * world
+        dist.all_gather_object(hs, ctx.ipc_handle(0))
+        ctx.open_peers(hs)
+    stream = torch.cuda.Stream()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")  # > 126 MB L2
+    for l in range(len(counts)):
+        ctx.gradgen_layer(0, 7, 0, l, stream)
+    stream.synchronize()
+    times = []
+    reps = args.sync_reps
+    for k in range(reps + 2):
+        with torch.cuda.stream(stream):
+            flush.fill_(k & 0xFF)
+        for l in range(len(counts)):
+            ctx.layer_ready(0, l, k, None, stream)
+        stream.synchronize()
+        barrier(world)
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record(stream)
+        ctx.iteration_begin(k, stream)
+        e.record(stream)
+        ctx.sync_all(k + 1, 60.0)
+        stream.synchronize()
+        if k >= 2:
+            times.append(max_over_ranks(s.elapsed_time(e), world))
+    ctx.close()
+    return statistics.mean(times), ctas
+
+
+def cpu_reference(counts, world, batch, steps, warmup, seconds_budget=20.0):
+    """The reference P3 iteration on host cores (oracle port), bounded sample."""
+    sys.path.insert(0, str(REPO / "oracle"))
+    from cpu_p3 import CpuP3
+
+    cpu = CpuP3(counts, world)
+    n_slices = len(cpu.rows)
+    dt, frac = cpu.time_iteration(0, sample_slices=min(n_slices, 32))  # calibrate
+    per_iter = dt / frac
+    sample = n_slices if per_iter * max(steps, 1) < seconds_budget else max(8, int(n_slices * seconds_budget / (per_iter * max(steps, 1))))
+    sample = min(sample, n_slices)
+    for k in range(warmup):
+        cpu.time_iteration(1 + k, sample_slices=min(sample, 16))
+    tot, cov = 0.0, 0.0
+    for k in range(steps):
+        dt, frac = cpu.time_iteration(100 + k, sample_slices=sample)
+        tot += dt
+        cov += frac
+    iter_s = tot / cov  # seconds per full iteration
+    cpu.close()
+    return {
+        "value": batch * world / iter_s,
+        "unit": "samples/sec",
+        "cores": cpu.threads,
+        "kind": "port",
+        "sample": f"{sample} of {n_slices} slices per step (priority pop order), {steps} steps, scaled to a full "
+                  f"iteration; sync path only (GradGen materialise + rank-ordered aggregate + SGD + replica apply), "
+                  f"compute excluded",
+        "seconds_per_iteration": iter_s,
+    }
+
+
+def run_reference(args):
+    from paper_1905_03960_b200.torch_models import real_counts
+
+    world = args.gpus
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    batch = args.batch or DEFAULT_BATCH[args.model]
+    counts = real_counts(args.model)
+    cb = cpu_reference(counts, world, batch, args.steps, args.warmup)
+    ms = 1000.0 * batch * world / cb["value"]
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": cb["value"], "unit": "samples/sec", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic (GradGen gradients)",
+        "config": {"workload": f"{args.model} P3 sync path, {world} ranks, {args.max_slice}-param slices",
+                   "global_batch": batch * world, "max_slice": args.max_slice},
+        "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
+        "e2e": {"value": cb["value"], "unit": "samples/sec", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+def run_ours(args):
+    import torch
+
+    from paper_1905_03960_b200 import _lib
+    from paper_1905_03960_b200.ddp import LayerwiseDataParallel, P3DataParallel
+    from paper_1905_03960_b200.torch_models import real_counts, synthetic_batch
+
+    world, rank, local = dist_setup(args)
+    batch = args.batch or DEFAULT_BATCH[args.model]
+    counts = real_counts(args.model)
+    P = sum(counts)
+    torch.backends.cudnn.benchmark = False
+
+    # --- P3: device-resident inputs
+    model = build(args, rank)
+    ddp = P3DataParallel(model, lr=args.lr, max_slice=args.max_slice, comm_ctas=args.comm_ctas)
+    x, y = synthetic_batch(args.model, batch, seed=1234 + rank)
+    ms, clocks = time_training(args, world, rank, ddp, x, y, args.steps, args.warmup)
+    value = args.steps * batch * world / (ms / 1000.0)
+
+    # --- e2e through the public API: pinned host batch copied in, loss copied out, every step
+    xh, yh = synthetic_batch(args.model, batch, seed=1234 + rank, pinned_host=True)
+    lh = [torch.empty((), dtype=torch.float32).pin_memory() for _ in range(args.steps)]
+    ms_e2e, _ = time_training(args, world, rank, ddp, None, None, args.steps, 1, e2e=(xh, yh, lh))
+    e2e_value = args.steps * batch * world / (ms_e2e / 1000.0)
+    h2d = xh.numel() * xh.element_size() + yh.numel() * yh.element_size()
+    ddp.close()
+    del ddp, model
+    torch.cuda.empty_cache()
+
+    # --- layer-wise baseline (NCCL all-reduce per tensor, FIFO) on the same box
+    layerwise = None
+    if not args.skip_layerwise:
+        model = build(args, rank)
+        lw = LayerwiseDataParallel(model, lr=args.lr)
+        ms_lw, _ = time_training(args, world, rank, lw, x, y, args.steps, args.warmup)
+        layerwise = {"value": args.steps * batch * world / (ms_lw / 1000.0), "ms_per_step": ms_lw / args.steps,
+                     "impl": "per-tensor NCCL all_reduce in backward-hook order + SGD" if world > 1 else
+                             "SGD only (no communication at N=1)"}
+        lw.close()
+        del lw, model
+        torch.cuda.empty_cache()
+
+    # --- slice-sync kernel roofline
+    sync_ms, ctas = sync_only_roofline(args, world, rank, counts)
+    peaks = json.loads((REPO / "MEASURED_PEAKS.json").read_text()) if (REPO / "MEASURED_PEAKS.json").exists() else {}
+    if world == 1:
+        alg = 12 * P  # read G + read W + write W per element (SURVEY §8(d), K4 with N=1)
+        peak = peaks.get("hbm_gbs", 6650.0)
+        roof = {"bound": "hbm", "achieved": alg / (sync_ms * 1e-3) / 1e9, "peak": peak, "unit": "GB/s",
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6.65 TB/s"}
+    else:
+        alg = 2 * (world - 1) / world * P * 4  # NVLink egress per GPU: pushes + broadcasts
+        peak = 770.0
+        roof = {"bound": "nvlink", "achieved": alg / (sync_ms * 1e-3) / 1e9, "peak": peak, "unit": "GB/s",
+                "peak_source": "B200_PROFILING.md measured peer copy 770 GB/s per direction"}
+    roof.update({"frac": roof["achieved"] / peak, "traffic": None, "kernel": "k_comm (K3 push + K4 reduce/SGD/bcast)",
+                 "algorithmic_bytes_per_launch": alg, "launch_ms": sync_ms, "ctas": ctas,
+                 "measured_in": "sync-only phase: all layers' gradients in HBM and published, one launch per "
+                                "iteration over the whole GPU, L2 flushed (256 MB write) between launches"})
+
+    out = None
+    if rank == 0:
+        cpu = None
+        if world == 1 and not args.skip_cpu:
+            cb = cpu_reference(counts, world, batch, 3, 1)
+            cpu = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        out = {
+            "metric": METRIC, "value": value, "unit": "samples/sec", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (random-init weights, N(0,1) bf16 images / uniform labels)",
+            "config": {"workload": f"{args.model} bf16-autocast training, P3 sliced priority sync",
+                       "model": args.model, "per_gpu_batch": batch, "global_batch": batch * world,
+                       "max_slice": args.max_slice, "comm_ctas": args.comm_ctas, "parallelism": f"dp{world}",
+                       "params": P, "tensors": len(counts), "l2": "activations >> 126 MB L2 each step"},
+            "e2e": {"value": e2e_value, "unit": "samples/sec", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 4},
+            "layerwise": layerwise,
+            "p3_vs_layerwise": (value / layerwise["value"]) if layerwise else None,
+            "roofline": roof,
+            "slice_sync": {"ms": sync_ms, "GBps_per_gpu": roof["achieved"], "bound": roof["bound"]},
+            "cpu_baseline": cpu,
+            "clocks": clocks,
+            "gpu_launches": args.steps,
+        }
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

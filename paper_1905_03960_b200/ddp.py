@@ -1,0 +1,248 @@
+"""P3 for real PyTorch models: backward hooks publish layers, forward hooks gate them.
+
+``P3DataParallel`` is the torch-mode driver of the sync path. Every trainable parameter
+tensor is one P3 layer (one KVStore key) whose priority is its forward index
+(registration order). Its storage is moved into the context's peer-writable parameter
+arena ``W`` so the comm kernel's broadcast stores land directly in the tensors the next
+forward reads.
+
+Per iteration k:
+  - root forward pre-hook: the gradients of iteration k-1 are released to the allocator
+    only after the comm stream's current work (record_stream), then the persistent comm
+    kernel for iteration k is launched on a high-priority comm stream;
+  - per-module forward pre-hook: ``p3_wait_layer`` (a stream memory wait, no SM) gates the
+    module on its parameters having been updated by iteration k-1 (worker.py:277-285);
+  - post-accumulate-grad hook: ``p3_layer_ready`` publishes the layer's gradient pointer
+    and iteration tag with stream-ordered writes (enqueue_layer, worker.py:173-182);
+  - end-of-backward callback: publishes layers that got no gradient (zeros) and advances k.
+The optimizer step is fused into the comm kernel (SGD, optional momentum): do not run a
+torch optimizer on these parameters. Iteration 0 runs the comm kernel only after the
+backward pass has executed, so every kernel the step uses is loaded before a persistent
+kernel is resident (lazy module loading would otherwise wait for it).
+
+``LayerwiseDataParallel`` is the baseline the paper compares against (aggressive,
+non-sliced, FIFO layer-wise sync): per-tensor NCCL all-reduce issued in backward-hook
+order, the SGD step applied in the next forward's pre-hook behind the same gates.
+"""
+
+from __future__ import annotations
+
+import torch
+import torch.distributed as dist
+
+from .plan import DEFAULT_MAX_SLICE
+from .runtime import SyncContext
+
+
+def _dist_info() -> tuple[int, int]:
+    if dist.is_available() and dist.is_initialized():
+        return dist.get_world_size(), dist.get_rank()
+    return 1, 0
+
+
+def _param_modules(module: torch.nn.Module, params: list) -> list[tuple[torch.nn.Module, list[int]]]:
+    index = {id(p): i for i, p in enumerate(params)}
+    out = []
+    for m in module.modules():
+        own = [index[id(p)] for p in m._parameters.values() if p is not None and id(p) in index]
+        if own:
+            out.append((m, own))
+    return out
+
+
+class _HookedDataParallel:
+    def __init__(self, module: torch.nn.Module) -> None:
+        self.module = module
+        self.params = [p for p in module.parameters() if p.requires_grad]
+        self.world, self.rank = _dist_info()
+        self.k = 0
+        self._handles = []
+        self._gated: set[int] = set()
+        self._ready: set[int] = set()
+
+    def __call__(self, *args, **kwargs):
+        return self.module(*args, **kwargs)
+
+    def _install(self) -> None:
+        self._handles.append(self.module.register_forward_pre_hook(self._root_pre_hook))
+        for m, layers in _param_modules(self.module, self.params):
+            self._handles.append(m.register_forward_pre_hook(self._make_gate(layers)))
+        for l, p in enumerate(self.params):
+            self._handles.append(p.register_post_accumulate_grad_hook(self._make_ready(l)))
+
+    def _make_gate(self, layers):
+        def hook(mod, inputs):
+            for l in layers:
+                if l not in self._gated:
+                    self._gate(l)
+                    self._gated.add(l)
+
+        return hook
+
+    def _make_ready(self, l):
+        def hook(p):
+            if not self._ready:
+                torch.autograd.Variable._execution_engine.queue_callback(self._end_backward)
+            self._ready.add(l)
+            self._publish(l, p.grad)
+
+        return hook
+
+    def _end_backward(self) -> None:
+        for l, p in enumerate(self.params):
+            if l not in self._ready:  # no gradient this iteration: sync zeros
+                if l not in self._gated:
+                    self._gate(l)
+                    self._gated.add(l)
+                p.grad = torch.zeros_like(p)
+                self._publish(l, p.grad)
+        self._after_backward()
+        self._ready.clear()
+        self._gated.clear()
+        self.k += 1
+
+    def _root_pre_hook(self, mod, inputs):
+        self._begin_iteration()
+
+    def remove_hooks(self) -> None:
+        for h in self._handles:
+            h.remove()
+        self._handles.clear()
+
+
+class P3DataParallel(_HookedDataParallel):
+    """Sliced, priority-scheduled parameter sync of ``module`` on the local GPU."""
+
+    def __init__(
+        self,
+        module: torch.nn.Module,
+        lr: float,
+        momentum: float = 0.0,
+        max_slice: int = DEFAULT_MAX_SLICE,
+        comm_ctas: int = 16,
+        comm_threads: int = 512,
+        timeout_s: float = 120.0,
+        trace_cap: int = 0,
+        priority_mode: bool = True,
+    ) -> None:
+        super().__init__(module)
+        self.lr = lr
+        counts = [p.numel() for p in self.params]
+        self.ctx = SyncContext(
+            counts, self.world, [self.rank], max_slice=max_slice, lr=lr, momentum=momentum,
+            priority_mode=priority_mode, comm_ctas=comm_ctas, comm_threads=comm_threads,
+            timeout_s=timeout_s, trace_cap=trace_cap,
+        )
+        if self.world > 1:
+            handles = [None] * self.world
+            dist.all_gather_object(handles, self.ctx.ipc_handle(0))
+            self.ctx.open_peers(handles)
+        arena = self.ctx.params_arena(0)
+        with torch.no_grad():
+            for l, p in enumerate(self.params):
+                if self.world > 1:
+                    dist.broadcast(p.data, src=0)
+                off = self.ctx.layer_offsets[l]
+                flat = arena[off : off + p.numel()]
+                if p.is_contiguous() or not p.is_non_overlapping_and_dense():
+                    view = flat.view(p.shape)
+                else:  # keep e.g. channels_last weights in their memory order
+                    view = flat.as_strided(p.shape, p.stride())
+                view.copy_(p.data)
+                p.data = view
+        torch.cuda.synchronize()
+        if self.world > 1:
+            dist.barrier()
+        self.comm_stream = torch.cuda.Stream(priority=-1)
+        self._grads: list = []
+        self._launched = -1
+        self._install()
+
+    # -- hooks
+    def _begin_iteration(self) -> None:
+        if self._launched == self.k:
+            return
+        for p in self.params:
+            if p.grad is not None:
+                # the comm kernel of the previous iteration may still read this gradient
+                p.grad.record_stream(self.comm_stream)
+                p.grad = None
+        if self.k > 0:
+            self.ctx.iteration_begin(self.k, self.comm_stream)
+        self._launched = self.k
+
+    def _gate(self, l: int) -> None:
+        self.ctx.wait_layer(0, l, self.k)
+
+    def _publish(self, l: int, grad) -> None:
+        p = self.params[l]
+        if grad.dtype != torch.float32 or grad.stride() != p.stride():
+            grad = _relayout(grad, p)
+            p.grad = grad
+        self.ctx.layer_ready(0, l, self.k, grad)
+
+    def _after_backward(self) -> None:
+        if self.k == 0:
+            # first iteration: start the comm kernel only after the step's kernels ran
+            torch.cuda.current_stream().synchronize()
+            self.comm_stream.wait_stream(torch.cuda.current_stream())
+            self.ctx.iteration_begin(0, self.comm_stream)
+
+    # -- API
+    def synchronize(self, timeout_s: float | None = None) -> None:
+        """Block until every layer holds the parameters of the last finished iteration."""
+        self.ctx.sync_all(self.k, timeout_s)
+        torch.cuda.current_stream().wait_stream(self.comm_stream)
+
+    def close(self) -> None:
+        self.remove_hooks()
+        self.ctx.close()
+
+
+def _relayout(grad: torch.Tensor, p: torch.Tensor) -> torch.Tensor:
+    out = torch.empty_strided(p.shape, p.stride(), dtype=torch.float32, device=p.device)
+    out.copy_(grad)
+    return out
+
+
+class LayerwiseDataParallel(_HookedDataParallel):
+    """Baseline: per-tensor NCCL all-reduce (FIFO in backward order) + SGD before reuse."""
+
+    def __init__(self, module: torch.nn.Module, lr: float) -> None:
+        super().__init__(module)
+        self.lr = lr
+        if self.world > 1:
+            with torch.no_grad():
+                for p in self.params:
+                    dist.broadcast(p.data, src=0)
+        self._work: dict[int, object] = {}
+        self._install()
+
+    def _begin_iteration(self) -> None:
+        pass
+
+    def _publish(self, l: int, grad) -> None:
+        if self.world > 1:
+            self._work[l] = dist.all_reduce(grad, async_op=True)
+
+    def _gate(self, l: int) -> None:
+        p = self.params[l]
+        if p.grad is None:
+            return
+        w = self._work.pop(l, None)
+        if w is not None:
+            w.wait()
+        with torch.no_grad():
+            p.add_(p.grad, alpha=-self.lr / self.world)
+        p.grad = None
+
+    def _after_backward(self) -> None:
+        pass
+
+    def synchronize(self, timeout_s: float | None = None) -> None:
+        for l in range(len(self.params)):
+            self._gate(l)
+        torch.cuda.current_stream().synchronize()
+
+    def close(self) -> None:
+        self.remove_hooks()

@@ -33,6 +33,17 @@ def _torch():
 def build_seq2seq():
     torch, nn = _torch()
 
+    class TiedSoftmax(nn.Module):
+        # output projection sharing the embedding matrix; owns only the softmax bias so the
+        # bias is gated (and prioritised) at its point of use, last in the forward pass
+        def __init__(self, embed) -> None:
+            super().__init__()
+            self.bias = nn.Parameter(torch.zeros(VOCAB))
+            self._embed = [embed]  # not a submodule: the weight stays owned by `embed`
+
+        def forward(self, x):
+            return torch.nn.functional.linear(x, self._embed[0].weight, self.bias)
+
     class Seq2Seq(nn.Module):
         def __init__(self) -> None:
             super().__init__()
@@ -42,7 +53,7 @@ def build_seq2seq():
             self.dec = nn.LSTM(2 * HIDDEN, HIDDEN, num_layers=4, batch_first=True)
             self.att = nn.Linear(HIDDEN, HIDDEN, bias=False)
             self.combine = nn.Linear(2 * HIDDEN, HIDDEN)
-            self.out_bias = nn.Parameter(torch.zeros(VOCAB))
+            self.softmax = TiedSoftmax(self.embed)
 
         def forward(self, src, trg):
             e = self.embed(src)
@@ -53,7 +64,7 @@ def build_seq2seq():
             scores = torch.bmm(self.att(d), h.transpose(1, 2))  # [B, T, S]
             ctx = torch.bmm(torch.softmax(scores, dim=-1), h)
             o = torch.tanh(self.combine(torch.cat([d, ctx], dim=-1)))
-            return torch.nn.functional.linear(o, self.embed.weight, self.out_bias)  # tied softmax
+            return self.softmax(o)
 
     return Seq2Seq()
 
