@@ -26,7 +26,6 @@ import tempfile
 import time
 from pathlib import Path
 
-os.environ.setdefault("CUDA_MODULE_LOADING", "EAGER")
 REPO = Path(__file__).resolve().parent
 sys.path.insert(0, str(REPO))
 
@@ -201,13 +200,14 @@ def sync_only_roofline(args, world, rank, counts):
     for k in range(reps + 2):
         with torch.cuda.stream(stream):
             flush.fill_(k & 0xFF)
-        for l in range(len(counts)):
+        for l in range(len(counts)):  # published before the iteration opens: no DRAIN launches
             ctx.layer_ready(0, l, k, None, stream)
         stream.synchronize()
         barrier(world)
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s.record(stream)
         ctx.iteration_begin(k, stream)
+        ctx.iteration_end(k)  # one FINISH launch does the whole iteration
         e.record(stream)
         ctx.sync_all(k + 1, 60.0)
         stream.synchronize()
@@ -288,8 +288,11 @@ def run_ours(args):
     model = build(args, rank)
     ddp = P3DataParallel(model, lr=args.lr, max_slice=args.max_slice, comm_ctas=args.comm_ctas)
     x, y = synthetic_batch(args.model, batch, seed=1234 + rank)
+    launches0 = ddp.ctx.launches()
     ms, clocks = time_training(args, world, rank, ddp, x, y, args.steps, args.warmup)
     value = args.steps * batch * world / (ms / 1000.0)
+    # comm kernel launches (DRAIN per layer + FINISH per iteration) of the timed steps
+    gpu_launches = (ddp.ctx.launches() - launches0) * args.steps // (args.steps + args.warmup)
 
     # --- e2e through the public API: pinned host batch copied in, loss copied out, every step
     xh, yh = synthetic_batch(args.model, batch, seed=1234 + rank, pinned_host=True)
@@ -354,7 +357,7 @@ def run_ours(args):
             "slice_sync": {"ms": sync_ms, "GBps_per_gpu": roof["achieved"], "bound": roof["bound"]},
             "cpu_baseline": cpu,
             "clocks": clocks,
-            "gpu_launches": args.steps,
+            "gpu_launches": gpu_launches,
         }
         print(json.dumps(out), flush=True)
     if world > 1:

@@ -14,7 +14,7 @@
  *   - Host arrays are owned by the caller. Device pointers are borrowed. A p3_ctx_t owns
  *     its device arenas (parameters, receive slots, flags, trace) and frees them in
  *     p3_ctx_destroy.
- *   - Hot calls (p3_layer_ready, p3_wait_layer, p3_iteration_begin, p3_gradgen_layer)
+ *   - Hot calls (p3_layer_ready, p3_wait_layer, p3_iteration_begin/end, p3_gradgen_layer)
  *     are asynchronous and stream-ordered; none of them synchronises the host.
  *   - The library has no CPU fallback: every compute entry point runs sm_100a code and
  *     returns P3_ECUDA when no device is available.
@@ -166,16 +166,28 @@ int p3_ctx_layer_offset(p3_ctx_t* ctx, uint32_t layer, uint64_t* elem_offset);
 /* Device pointer of the local rank's gradient arena (emulate_grads only). */
 int p3_ctx_grads(p3_ctx_t* ctx, uint32_t local_idx, float** grads_dev);
 
-/* Launch iteration k's persistent comm kernel on `comm_stream` (K3: worker pop/push +
- * server reduce/update/broadcast for all local ranks). Replaces the _priority_sender /
- * _fifo_sender threads (worker.py:184-198) and ServerEngine._consumer (server.py:208-249). */
+/* Open iteration k on `comm_stream`: reset the per-iteration queue state (stream-ordered
+ * after the previous iteration's comm work). The comm kernel (K3: worker pop/push +
+ * server reduce/update/broadcast for all local ranks) replaces the _priority_sender /
+ * _fifo_sender threads (worker.py:184-198) and ServerEngine._consumer (server.py:208-249);
+ * it is launched by p3_layer_ready and p3_iteration_end below. */
 int p3_iteration_begin(p3_ctx_t* ctx, uint64_t iteration, void* comm_stream);
 
 /* TrainingWorker.enqueue_layer (worker.py:173-182): publish all slices of `layer` for
- * `iteration` atomically (one release store after the gradient pointer). `grad_dev` is
- * the layer's fp32 gradient (param_count elements); NULL = the context's gradient arena. */
+ * `iteration` atomically with stream-ordered writes on `stream` (gradient pointer, then
+ * the iteration tag). `grad_dev` is the layer's fp32 gradient (param_count elements);
+ * NULL = the context's gradient arena. When an iteration is open, the comm stream then
+ * waits for this point of `stream` and launches the comm kernel in DRAIN mode: it pops
+ * the most urgent published slices (including layers published while it runs: slice-
+ * granular preemption), reduces owned slices whose pushes are complete, and exits once
+ * nothing is poppable — it never spins on compute that has not been published. */
 int p3_layer_ready(p3_ctx_t* ctx, uint32_t local_idx, uint32_t layer, uint64_t iteration,
                    const float* grad_dev, void* stream);
+
+/* End of iteration k's backward for every local rank: launch the comm kernel in FINISH
+ * mode on the comm stream; it exits when every local slice is pushed and every owned
+ * slice reduced and broadcast (waiting only for pushes of peers), or at the deadline. */
+int p3_iteration_end(p3_ctx_t* ctx, uint64_t iteration);
 
 /* K1 emulate mode: fill the gradient arena for `layer` with GradGen(seed) values
  * (TrainingWorker._materialize, worker.py:166-171). The reference pushes the same seed
@@ -198,6 +210,9 @@ int p3_sync_all(p3_ctx_t* ctx, uint64_t iteration, double timeout_s);
 int p3_trace_read(p3_ctx_t* ctx, uint32_t local_idx, p3_trace_rec_t* out, uint64_t cap,
                   uint64_t* n_out);
 int p3_trace_clear(p3_ctx_t* ctx);
+
+/* Comm kernel launches issued by this context so far (DRAIN + FINISH). */
+int p3_comm_launches(p3_ctx_t* ctx, uint64_t* n);
 
 /* NetCounters.totals (metrics.py:31-45): NVLink/HBM payload bytes in / out. */
 int p3_counters(p3_ctx_t* ctx, uint32_t local_idx, uint64_t* bytes_in, uint64_t* bytes_out);

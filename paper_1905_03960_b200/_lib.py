@@ -98,6 +98,8 @@ SIGNATURES = {
     "p3_ctx_layer_offset": (ctypes.c_int, [_P, _U32, _PU64]),
     "p3_ctx_grads": (ctypes.c_int, [_P, _U32, ctypes.POINTER(_P)]),
     "p3_iteration_begin": (ctypes.c_int, [_P, _U64, _P]),
+    "p3_iteration_end": (ctypes.c_int, [_P, _U64]),
+    "p3_comm_launches": (ctypes.c_int, [_P, _PU64]),
     "p3_layer_ready": (ctypes.c_int, [_P, _U32, _U32, _U64, _P, _P]),
     "p3_gradgen_layer": (ctypes.c_int, [_P, _U32, _U64, _U64, _U32, _P]),
     "p3_wait_layer": (ctypes.c_int, [_P, _U32, _U32, _U64, _P]),

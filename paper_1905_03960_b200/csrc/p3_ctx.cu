@@ -108,7 +108,12 @@ struct p3_ctx {
   uint32_t* d_err = nullptr;
   uint32_t fifo_seq[P3_MAX_LOCAL]{};
   cudaEvent_t comm_done = nullptr;
+  cudaEvent_t ready_ev[P3_MAX_LOCAL]{};
   cudaStream_t poll_stream = nullptr;
+  cudaStream_t comm_stream = nullptr;
+  uint64_t open_iter = 0;
+  bool iter_open = false;
+  uint64_t launches = 0;
   bool comm_pending = false;
   uint64_t synced_iterations = 0;
   std::string err;
@@ -391,6 +396,8 @@ int p3_ctx_create(const p3_config_t* cfg, p3_ctx_t** out) {
     D.trace = reinterpret_cast<p3_trace_rec_t*>(lb + ll.trace);
   }
   e = cudaEventCreateWithFlags(&c->comm_done, cudaEventDisableTiming);
+  for (uint32_t i = 0; i < cfg->n_local && e == cudaSuccess; ++i)
+    e = cudaEventCreateWithFlags(&c->ready_ev[i], cudaEventDisableTiming);
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->poll_stream, cudaStreamNonBlocking);
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
   if (e != cudaSuccess) {
@@ -415,6 +422,8 @@ int p3_ctx_destroy(p3_ctx_t* c) {
   if (c->d_plan) cudaFree(c->d_plan);
   if (c->d_err) cudaFree(c->d_err);
   if (c->comm_done) cudaEventDestroy(c->comm_done);
+  for (uint32_t i = 0; i < P3_MAX_LOCAL; ++i)
+    if (c->ready_ev[i]) cudaEventDestroy(c->ready_ev[i]);
   if (c->poll_stream) cudaStreamDestroy(c->poll_stream);
   delete c;
   return P3_OK;
@@ -469,31 +478,48 @@ int p3_ctx_layer_offset(p3_ctx_t* c, uint32_t layer, uint64_t* off) {
   return P3_OK;
 }
 
-int p3_iteration_begin(p3_ctx_t* c, uint64_t k, void* stream) {
-  if (!c) return fail(nullptr, P3_EUSAGE, "null context");
-  if (k >= 0x3fffffffull) return fail(c, P3_EUSAGE, "iteration out of range");
-  cudaStream_t s = (cudaStream_t)stream;
-  const LocalLayout& ll = c->local_layout;
-  for (uint32_t i = 0; i < c->cfg.n_local; ++i)
-    CK(cudaMemsetAsync(static_cast<char*>(c->local_arena[i]) + ll.iter_begin, 0, ll.iter_end - ll.iter_begin, s));
+static CommArgs comm_args(p3_ctx* c, uint32_t mode) {
   CommArgs a;
   std::memset(&a, 0, sizeof(a));
   a.plan = c->plan_dev;
   a.peers = c->peers;
   for (uint32_t i = 0; i < c->cfg.n_local; ++i) a.loc[i] = c->loc[i];
   a.n_local = c->cfg.n_local;
-  a.k = (uint32_t)k;
+  a.mode = mode;
+  a.k = (uint32_t)c->open_iter;
   a.sched = c->cfg.sched;
   a.lr = c->cfg.lr;
   a.momentum = c->cfg.momentum;
   a.timeout_ns = (unsigned long long)(c->cfg.timeout_s * 1e9);
   a.err = c->d_err;
+  return a;
+}
+
+int p3_iteration_begin(p3_ctx_t* c, uint64_t k, void* stream) {
+  if (!c) return fail(nullptr, P3_EUSAGE, "null context");
+  if (k >= 0x3fffffffull) return fail(c, P3_EUSAGE, "iteration out of range");
+  if (c->iter_open) return fail(c, P3_EUSAGE, "previous iteration not ended (p3_iteration_end)");
   for (uint32_t r = 0; r < c->N; ++r)
-    if (!a.peers.W[r]) return fail(c, P3_EUSAGE, "peer arenas not opened (call p3_ctx_open_peers)");
-  if (launch_comm(a, c->cfg.comm_ctas, c->cfg.comm_threads, stream) != P3_OK)
+    if (!c->peers.W[r]) return fail(c, P3_EUSAGE, "peer arenas not opened (call p3_ctx_open_peers)");
+  cudaStream_t s = (cudaStream_t)stream;
+  const LocalLayout& ll = c->local_layout;
+  for (uint32_t i = 0; i < c->cfg.n_local; ++i)
+    CK(cudaMemsetAsync(static_cast<char*>(c->local_arena[i]) + ll.iter_begin, 0, ll.iter_end - ll.iter_begin, s));
+  c->comm_stream = s;
+  c->open_iter = k;
+  c->iter_open = true;
+  return P3_OK;
+}
+
+int p3_iteration_end(p3_ctx_t* c, uint64_t k) {
+  if (!c) return fail(nullptr, P3_EUSAGE, "null context");
+  if (!c->iter_open || c->open_iter != k) return fail(c, P3_EUSAGE, "iteration not open");
+  if (launch_comm(comm_args(c, P3_COMM_FINISH), c->cfg.comm_ctas, c->cfg.comm_threads, c->comm_stream) != P3_OK)
     return cuda_fail(c, cudaGetLastError(), "comm kernel launch");
-  CK(cudaEventRecord(c->comm_done, s));
+  CK(cudaEventRecord(c->comm_done, c->comm_stream));
+  c->launches++;
   c->comm_pending = true;
+  c->iter_open = false;
   return P3_OK;
 }
 
@@ -520,6 +546,14 @@ int p3_layer_ready(p3_ctx_t* c, uint32_t li, uint32_t layer, uint64_t k, const f
   }
   if (r == CUDA_SUCCESS) r = d.write32(s, (CUdeviceptr)(D.ready + layer), (cuuint32_t)(k + 1), 0);
   if (r != CUDA_SUCCESS) return fail(c, P3_ECUDA, "cuStreamWriteValue failed (code " + std::to_string(r) + ")");
+  if (c->iter_open && c->open_iter == k) {
+    // the comm stream follows this publication point, then drains what is published
+    CK(cudaEventRecord(c->ready_ev[li], (cudaStream_t)stream));
+    CK(cudaStreamWaitEvent(c->comm_stream, c->ready_ev[li], 0));
+    if (launch_comm(comm_args(c, P3_COMM_DRAIN), c->cfg.comm_ctas, c->cfg.comm_threads, c->comm_stream) != P3_OK)
+      return cuda_fail(c, cudaGetLastError(), "comm kernel launch");
+    c->launches++;
+  }
   return P3_OK;
 }
 
@@ -621,6 +655,12 @@ int p3_trace_clear(p3_ctx_t* c) {
   if (!c) return fail(nullptr, P3_EUSAGE, "null context");
   for (uint32_t i = 0; i < c->cfg.n_local; ++i) CK(cudaMemsetAsync(c->loc[i].trace_n, 0, 8, c->poll_stream));
   CK(cudaStreamSynchronize(c->poll_stream));
+  return P3_OK;
+}
+
+int p3_comm_launches(p3_ctx_t* c, uint64_t* n) {
+  if (!c || !n) return fail(c, P3_EUSAGE, "null argument");
+  *n = c->launches;
   return P3_OK;
 }
 

@@ -9,6 +9,8 @@
 #include "../../include/p3.h"
 
 #define P3_MAX_LOCAL P3_MAX_RANKS
+#define P3_COMM_DRAIN 0   // exit as soon as nothing is poppable or reducible
+#define P3_COMM_FINISH 1  // exit when the iteration's local work is complete
 
 namespace p3 {
 
@@ -83,11 +85,11 @@ struct CommArgs {
   PeersDev peers;
   LocalDev loc[P3_MAX_LOCAL];
   uint32_t n_local;
+  uint32_t mode;  // P3_COMM_DRAIN or P3_COMM_FINISH
   uint32_t k;  // iteration
   uint32_t sched;
   float lr;
   float momentum;
-  uint32_t pad_;
   unsigned long long timeout_ns;
   uint32_t* err;  // device error word (P3_* code)
 };

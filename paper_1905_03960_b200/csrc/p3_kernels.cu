@@ -517,10 +517,15 @@ __device__ __forceinline__ QueueView queue_of(const CommArgs& a, const LocalDev&
   return q;
 }
 
-// Persistent per-iteration comm kernel. Every CTA loops: warp 0 picks a job (server work
-// first, since a finished slice unblocks the next forward pass; then the most urgent
-// ready slice of the local worker queues), the whole CTA executes it. The kernel ends
-// once every slice of every local rank has been pushed and every owned slice reduced.
+// Comm kernel. Every CTA loops: warp 0 picks a job (server work first, since a finished
+// slice unblocks the next forward pass; then the most urgent ready slice of the local
+// worker queues), the whole CTA executes it. The queue is re-read before every job, so a
+// layer published while the kernel runs preempts less urgent slices at slice granularity.
+// DRAIN launches (one per published layer) exit when no job is available: a kernel that
+// spun on not-yet-published gradients would hold SMs that the compute producing them may
+// need (co-residency-bound library kernels, lazy module loading). The FINISH launch of an
+// iteration ends once every local slice is pushed and every owned slice reduced; it waits
+// only for peers' pushes, never for local compute.
 __global__ void __launch_bounds__(1024) k_comm(const __grid_constant__ CommArgs a) {
   __shared__ uint32_t s_job, s_li, s_g;
   __shared__ PushSmem s_push;
@@ -552,7 +557,9 @@ __global__ void __launch_bounds__(1024) k_comm(const __grid_constant__ CommArgs 
           }
         }
       }
-      if (job == 0) {
+      if (job == 0 && a.mode == P3_COMM_DRAIN) {
+        job = 3;  // nothing published is pending: leave the SMs to compute
+      } else if (job == 0) {
         bool fin = true;
         for (uint32_t t = 0; t < a.n_local; ++t) {
           const LocalDev& L = a.loc[t];

@@ -8,17 +8,17 @@ forward reads.
 
 Per iteration k:
   - root forward pre-hook: the gradients of iteration k-1 are released to the allocator
-    only after the comm stream's current work (record_stream), then the persistent comm
-    kernel for iteration k is launched on a high-priority comm stream;
+    only after the comm stream's current work (record_stream), and iteration k is opened
+    on a high-priority comm stream;
   - per-module forward pre-hook: ``p3_wait_layer`` (a stream memory wait, no SM) gates the
     module on its parameters having been updated by iteration k-1 (worker.py:277-285);
   - post-accumulate-grad hook: ``p3_layer_ready`` publishes the layer's gradient pointer
-    and iteration tag with stream-ordered writes (enqueue_layer, worker.py:173-182);
-  - end-of-backward callback: publishes layers that got no gradient (zeros) and advances k.
+    and iteration tag with stream-ordered writes (enqueue_layer, worker.py:173-182) and
+    queues a DRAIN launch of the comm kernel behind that point;
+  - end-of-backward callback: publishes layers that got no gradient (zeros), queues the
+    iteration's FINISH launch and advances k.
 The optimizer step is fused into the comm kernel (SGD, optional momentum): do not run a
-torch optimizer on these parameters. Iteration 0 runs the comm kernel only after the
-backward pass has executed, so every kernel the step uses is loaded before a persistent
-kernel is resident (lazy module loading would otherwise wait for it).
+torch optimizer on these parameters.
 
 ``LayerwiseDataParallel`` is the baseline the paper compares against (aggressive,
 non-sliced, FIFO layer-wise sync): per-tensor NCCL all-reduce issued in backward-hook
@@ -144,7 +144,7 @@ class P3DataParallel(_HookedDataParallel):
                     dist.broadcast(p.data, src=0)
                 off = self.ctx.layer_offsets[l]
                 flat = arena[off : off + p.numel()]
-                if p.is_contiguous() or not p.is_non_overlapping_and_dense():
+                if p.is_contiguous() or not _dense(p):
                     view = flat.view(p.shape)
                 else:  # keep e.g. channels_last weights in their memory order
                     view = flat.as_strided(p.shape, p.stride())
@@ -167,8 +167,7 @@ class P3DataParallel(_HookedDataParallel):
                 # the comm kernel of the previous iteration may still read this gradient
                 p.grad.record_stream(self.comm_stream)
                 p.grad = None
-        if self.k > 0:
-            self.ctx.iteration_begin(self.k, self.comm_stream)
+        self.ctx.iteration_begin(self.k, self.comm_stream)
         self._launched = self.k
 
     def _gate(self, l: int) -> None:
@@ -182,11 +181,7 @@ class P3DataParallel(_HookedDataParallel):
         self.ctx.layer_ready(0, l, self.k, grad)
 
     def _after_backward(self) -> None:
-        if self.k == 0:
-            # first iteration: start the comm kernel only after the step's kernels ran
-            torch.cuda.current_stream().synchronize()
-            self.comm_stream.wait_stream(torch.cuda.current_stream())
-            self.ctx.iteration_begin(0, self.comm_stream)
+        self.ctx.iteration_end(self.k)
 
     # -- API
     def synchronize(self, timeout_s: float | None = None) -> None:
@@ -197,6 +192,18 @@ class P3DataParallel(_HookedDataParallel):
     def close(self) -> None:
         self.remove_hooks()
         self.ctx.close()
+
+
+def _dense(t: torch.Tensor) -> bool:
+    """Non-overlapping and dense (some permutation of a contiguous layout)."""
+    expect = 1
+    for size, stride in sorted(zip(t.shape, t.stride()), key=lambda d: d[1]):
+        if size == 1:
+            continue
+        if stride != expect:
+            return False
+        expect *= size
+    return True
 
 
 def _relayout(grad: torch.Tensor, p: torch.Tensor) -> torch.Tensor:

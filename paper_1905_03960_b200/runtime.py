@@ -145,6 +145,14 @@ class SyncContext:
     def iteration_begin(self, k: int, stream=None) -> None:
         self._check(self.lib.p3_iteration_begin(self._h, k, _lib.stream_handle(stream)), "p3_iteration_begin")
 
+    def iteration_end(self, k: int) -> None:
+        self._check(self.lib.p3_iteration_end(self._h, k), "p3_iteration_end")
+
+    def launches(self) -> int:
+        n = ctypes.c_uint64()
+        self._check(self.lib.p3_comm_launches(self._h, ctypes.byref(n)), "p3_comm_launches")
+        return int(n.value)
+
     def layer_ready(self, li: int, layer: int, k: int, grad=None, stream=None) -> None:
         ptr = grad.data_ptr() if grad is not None else None
         self._check(self.lib.p3_layer_ready(self._h, li, layer, k, ptr, _lib.stream_handle(stream)), "p3_layer_ready")
@@ -249,8 +257,8 @@ class TrainingWorker:
     ``run_iteration`` issues, per hosted rank and on that rank's compute stream:
     forward: ``_wait_layer`` gate (stream memory wait) + device sleep per layer;
     backward: device sleep, K1 gradient generation and ``enqueue_layer`` per layer in
-    reverse order (worker.py:312-325). The comm kernel for the iteration is launched first
-    on the comm stream.
+    reverse order (worker.py:312-325); each publication is followed on the comm stream by
+    a DRAIN launch of the comm kernel, and the iteration ends with a FINISH launch.
     """
 
     def __init__(self, config: WorkerConfig, profile: ModelProfile, ranks: list[int] | None = None, ctx: SyncContext | None = None) -> None:
@@ -303,6 +311,7 @@ class TrainingWorker:
                     _lib.check(lib.p3_emulate_compute(layer.bwd_time, sh), what="p3_emulate_compute")
                 ctx._check(lib.p3_gradgen_layer(ctx.handle, li, seed & 0xFFFFFFFFFFFFFFFF, k, layer.index, sh), "p3_gradgen_layer")
                 ctx._check(lib.p3_layer_ready(ctx.handle, li, layer.index, k, None, sh), "p3_layer_ready")
+        ctx.iteration_end(k)
         self.iterations_done = k + 1
 
     def run(self) -> None:

@@ -1,10 +1,6 @@
 import json
 import os
 import sys
-
-# A persistent comm kernel waits for work of other streams; lazily loading a kernel while
-# it runs would wait for it (see csrc/p3_kernels.cu preload_kernels). Load eagerly.
-os.environ.setdefault("CUDA_MODULE_LOADING", "EAGER")
 from pathlib import Path
 
 import pytest
