@@ -181,7 +181,7 @@ def sync_only_roofline(args, world, rank, counts):
     from paper_1905_03960_b200.runtime import SyncContext
 
     props = torch.cuda.get_device_properties(0)
-    ctas = 2 * props.multi_processor_count
+    ctas = props.multi_processor_count  # one 512-thread comm CTA per SM (126 registers)
     ctx = SyncContext(counts, world, [rank], max_slice=args.max_slice, lr=args.lr, comm_ctas=ctas,
                       comm_threads=512, timeout_s=60.0, emulate_grads=True)
     if world > 1:

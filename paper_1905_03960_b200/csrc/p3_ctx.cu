@@ -79,7 +79,7 @@ struct PeerLayout {
 // contiguous so one memset resets it before each launch.
 struct LocalLayout {
   uint64_t ready, fifo_key, gptr, claim, iter_begin, cursor, srv_lo, srv_taken, it, iter_end, V, bytes,
-      trace_n, trace, total;
+      trace_n, trace, cta_phase, total;
 };
 
 struct p3_ctx {
@@ -175,6 +175,7 @@ LocalLayout local_layout_of(const p3_ctx* c, uint64_t v_elems) {
   take(q.bytes, 16);
   take(q.trace_n, 8);
   take(q.trace, (uint64_t)c->cfg.trace_cap * sizeof(p3_trace_rec_t));
+  take(q.cta_phase, P3_DBG_CTAS * 4ull);
   q.total = o;
   return q;
 }
@@ -224,8 +225,8 @@ int p3_ctx_create(const p3_config_t* cfg, p3_ctx_t** out) {
   if (cfg->n_local < 1 || cfg->n_local > cfg->world) return fail(nullptr, P3_EUSAGE, "bad n_local");
   if (cfg->n_layers < 1 || !cfg->layer_counts) return fail(nullptr, P3_EUSAGE, "profile needs at least one layer");
   if (cfg->plan_mode != P3_PLAN_P3) return fail(nullptr, P3_EUSAGE, "only the p3 plan runs on the comm kernel");
-  if (cfg->comm_threads < 32 || cfg->comm_threads > 1024 || cfg->comm_threads % 32)
-    return fail(nullptr, P3_EUSAGE, "comm_threads must be a multiple of 32 in [32, 1024]");
+  if (cfg->comm_threads < 32 || cfg->comm_threads > 512 || cfg->comm_threads % 32)
+    return fail(nullptr, P3_EUSAGE, "comm_threads must be a multiple of 32 in [32, 512]");
   if (cfg->comm_ctas < 1) return fail(nullptr, P3_EUSAGE, "comm_ctas must be >= 1");
   for (uint32_t i = 0; i < cfg->n_local; ++i)
     if (cfg->local_ranks[i] >= cfg->world) return fail(nullptr, P3_EUSAGE, "local rank out of range");
@@ -394,6 +395,7 @@ int p3_ctx_create(const p3_config_t* cfg, p3_ctx_t** out) {
     D.bytes = reinterpret_cast<unsigned long long*>(lb + ll.bytes);
     D.trace_n = reinterpret_cast<unsigned long long*>(lb + ll.trace_n);
     D.trace = reinterpret_cast<p3_trace_rec_t*>(lb + ll.trace);
+    D.cta_phase = reinterpret_cast<uint32_t*>(lb + ll.cta_phase);
   }
   e = cudaEventCreateWithFlags(&c->comm_done, cudaEventDisableTiming);
   for (uint32_t i = 0; i < cfg->n_local && e == cudaSuccess; ++i)
@@ -486,6 +488,7 @@ static CommArgs comm_args(p3_ctx* c, uint32_t mode) {
   for (uint32_t i = 0; i < c->cfg.n_local; ++i) a.loc[i] = c->loc[i];
   a.n_local = c->cfg.n_local;
   a.mode = mode;
+  for (uint32_t r = 0; r < c->N; ++r) a.remote |= c->opened[r] != nullptr;
   a.k = (uint32_t)c->open_iter;
   a.sched = c->cfg.sched;
   a.lr = c->cfg.lr;
@@ -679,7 +682,7 @@ int p3_counters(p3_ctx_t* c, uint32_t li, uint64_t* bytes_in, uint64_t* bytes_ou
 int p3_debug_snapshot(p3_ctx_t* c, uint32_t li, uint32_t* out, uint64_t cap, uint64_t* n_out) {
   int rc = check_local(c, li);
   if (rc) return rc;
-  const uint64_t n = 5ull * c->L + 4;
+  const uint64_t n = 5ull * c->L + 4 + P3_DBG_CTAS;
   if (n_out) *n_out = n;
   if (!out) return P3_OK;
   if (cap < n) return fail(c, P3_EUSAGE, "snapshot buffer too small");
@@ -689,6 +692,7 @@ int p3_debug_snapshot(p3_ctx_t* c, uint32_t li, uint32_t* out, uint64_t cap, uin
   for (int a = 0; a < 5; ++a)
     CK(cudaMemcpyAsync(out + (uint64_t)a * c->L, src[a], c->L * 4ull, cudaMemcpyDeviceToHost, c->poll_stream));
   CK(cudaMemcpyAsync(out + 5ull * c->L, D.it, 16, cudaMemcpyDeviceToHost, c->poll_stream));
+  CK(cudaMemcpyAsync(out + 5ull * c->L + 4, D.cta_phase, P3_DBG_CTAS * 4ull, cudaMemcpyDeviceToHost, c->poll_stream));
   CK(cudaStreamSynchronize(c->poll_stream));
   return P3_OK;
 }

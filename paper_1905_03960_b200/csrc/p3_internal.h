@@ -9,6 +9,7 @@
 #include "../../include/p3.h"
 
 #define P3_MAX_LOCAL P3_MAX_RANKS
+#define P3_DBG_CTAS 512
 #define P3_COMM_DRAIN 0   // exit as soon as nothing is poppable or reducible
 #define P3_COMM_FINISH 1  // exit when the iteration's local work is complete
 
@@ -59,7 +60,8 @@ struct PeersDev {
 struct IterState {
   uint32_t pushed;   // worker slices claimed
   uint32_t reduced;  // owned slices claimed
-  uint32_t pad_[2];
+  uint32_t exited;   // CTAs of the FINISH launch that left (diagnostics)
+  uint32_t jobs;     // jobs executed (diagnostics)
 };
 
 // Local-only state of one rank hosted in this process.
@@ -78,6 +80,7 @@ struct LocalDev {
   unsigned long long* bytes;  // [2] in, out
   unsigned long long* trace_n;
   p3_trace_rec_t* trace;
+  uint32_t* cta_phase;  // [P3_DBG_CTAS] last phase of each comm CTA (diagnostics)
 };
 
 struct CommArgs {
@@ -85,7 +88,8 @@ struct CommArgs {
   PeersDev peers;
   LocalDev loc[P3_MAX_LOCAL];
   uint32_t n_local;
-  uint32_t mode;  // P3_COMM_DRAIN or P3_COMM_FINISH
+  uint32_t mode;    // P3_COMM_DRAIN or P3_COMM_FINISH
+  uint32_t remote;  // some peer lives on another GPU: system-scope fences
   uint32_t k;  // iteration
   uint32_t sched;
   float lr;

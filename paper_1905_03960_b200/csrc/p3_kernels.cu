@@ -128,12 +128,10 @@ __device__ __forceinline__ float sgd_step(float p, float gsum, const UpdCoef& c,
   return __fsub_rn(p, __fmul_rn(c.lr, step));
 }
 
-// Sum of NW sources in ascending rank order (starting from +0.0 like np.zeros + ...).
+// fp32 sum of one float4 lane-set in ascending rank order, starting from +0.0 exactly like
+// np.zeros(...) followed by `acc += g_rank` (server.py:60-63).
 template <int NW>
-__device__ __forceinline__ float4 sum_sources(const float* const* src, uint64_t i) {
-  float4 v[NW];
-#pragma unroll
-  for (int q = 0; q < NW; ++q) v[q] = __ldcg(reinterpret_cast<const float4*>(src[q] + i));
+__device__ __forceinline__ float4 sum_in_rank_order(const float4 (&v)[NW]) {
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
   for (int q = 0; q < NW; ++q) {
@@ -151,29 +149,58 @@ __device__ __forceinline__ float sum_sources_scalar(const float* const* src, int
   return acc;
 }
 
-// CTA-wide: params (dst[0..ndst) all receive the update; p_src is the master copy),
-// src[0..nw) gradient sources in rank order, optional momentum v.
-template <int NW>
+__device__ __forceinline__ float4 sgd4(float4 p, const float4& acc, const UpdCoef& c, float4* v) {
+  if (v) {
+    p.x = sgd_step(p.x, acc.x, c, &v->x);
+    p.y = sgd_step(p.y, acc.y, c, &v->y);
+    p.z = sgd_step(p.z, acc.z, c, &v->z);
+    p.w = sgd_step(p.w, acc.w, c, &v->w);
+  } else {
+    p.x = sgd_step(p.x, acc.x, c, nullptr);
+    p.y = sgd_step(p.y, acc.y, c, nullptr);
+    p.z = sgd_step(p.z, acc.z, c, nullptr);
+    p.w = sgd_step(p.w, acc.w, c, nullptr);
+  }
+  return p;
+}
+
+// CTA-wide reduce + update over n4 float4s: dst[0..ndst) all receive the result (dst[0]
+// is also the master copy read as p), src[0..NW) are the gradient sources in rank order,
+// v the optional momentum. U float4 columns per thread are loaded before any arithmetic
+// so each thread keeps (NW + 1) * U independent 16-byte loads in flight.
+template <int NW, int U>
 __device__ void cta_update_vec(const float* p_src, float* const* dst, int ndst, const float* const* src,
                                float* v, uint64_t n4, const UpdCoef& c) {
-  for (uint64_t j = threadIdx.x; j < n4; j += blockDim.x) {
-    const uint64_t i = 4 * j;
-    const float4 acc = sum_sources<NW>(src, i);
-    float4 p = __ldcg(reinterpret_cast<const float4*>(p_src + i));
-    if (v) {
-      float4 vv = __ldcg(reinterpret_cast<const float4*>(v + i));
-      p.x = sgd_step(p.x, acc.x, c, &vv.x);
-      p.y = sgd_step(p.y, acc.y, c, &vv.y);
-      p.z = sgd_step(p.z, acc.z, c, &vv.z);
-      p.w = sgd_step(p.w, acc.w, c, &vv.w);
-      *reinterpret_cast<float4*>(v + i) = vv;
-    } else {
-      p.x = sgd_step(p.x, acc.x, c, nullptr);
-      p.y = sgd_step(p.y, acc.y, c, nullptr);
-      p.z = sgd_step(p.z, acc.z, c, nullptr);
-      p.w = sgd_step(p.w, acc.w, c, nullptr);
+  const uint64_t stride = blockDim.x;
+  uint64_t j = threadIdx.x;
+  for (; j + (U - 1) * stride < n4; j += U * stride) {
+    float4 g[U][NW], p[U], vv[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint64_t i = 4 * (j + u * stride);
+#pragma unroll
+      for (int q = 0; q < NW; ++q) g[u][q] = __ldcg(reinterpret_cast<const float4*>(src[q] + i));
+      p[u] = __ldcg(reinterpret_cast<const float4*>(p_src + i));
+      if (v) vv[u] = __ldcg(reinterpret_cast<const float4*>(v + i));
     }
-    for (int d = 0; d < ndst; ++d) *reinterpret_cast<float4*>(dst[d] + i) = p;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint64_t i = 4 * (j + u * stride);
+      const float4 r = sgd4(p[u], sum_in_rank_order<NW>(g[u]), c, v ? &vv[u] : nullptr);
+      if (v) *reinterpret_cast<float4*>(v + i) = vv[u];
+      for (int d = 0; d < ndst; ++d) *reinterpret_cast<float4*>(dst[d] + i) = r;
+    }
+  }
+  for (; j < n4; j += stride) {
+    const uint64_t i = 4 * j;
+    float4 g1[NW];
+#pragma unroll
+    for (int q = 0; q < NW; ++q) g1[q] = __ldcg(reinterpret_cast<const float4*>(src[q] + i));
+    float4 vv1 = v ? __ldcg(reinterpret_cast<const float4*>(v + i)) : make_float4(0.f, 0.f, 0.f, 0.f);
+    const float4 r = sgd4(__ldcg(reinterpret_cast<const float4*>(p_src + i)), sum_in_rank_order<NW>(g1), c,
+                          v ? &vv1 : nullptr);
+    if (v) *reinterpret_cast<float4*>(v + i) = vv1;
+    for (int d = 0; d < ndst; ++d) *reinterpret_cast<float4*>(dst[d] + i) = r;
   }
 }
 
@@ -184,7 +211,7 @@ __device__ void cta_update_generic(const float* p_src, float* const* dst, int nd
     const uint64_t n4 = n / 4;
     switch (nw) {
 #define P3_CASE(K) \
-  case K: cta_update_vec<K>(p_src, dst, ndst, src, v, n4, c); break;
+  case K: cta_update_vec<K, (K <= 1 ? 4 : K <= 2 ? 2 : 1)>(p_src, dst, ndst, src, v, n4, c); break;
       P3_CASE(1) P3_CASE(2) P3_CASE(3) P3_CASE(4) P3_CASE(5) P3_CASE(6) P3_CASE(7) P3_CASE(8)
 #undef P3_CASE
       default: aligned = false; break;
@@ -287,15 +314,48 @@ struct QueueView {
 };
 
 // Executed by one full warp; returns the popped global slice id or P3_NONE.
-__device__ uint32_t warp_pop(const QueueView& q, uint32_t tag) {
-  const int lane = threadIdx.x & 31;
-  for (;;) {
+// Priority discipline: layers are examined in ascending order 32 at a time (lane i owns
+// layer base+i); each lane first loads the availability of all its layers (independent
+// loads, one memory round trip), then the warp walks the availability ballots in layer
+// order and claims the first slice it wins. A lost race moves on to the next candidate
+// without rescanning. FIFO discipline: arg-min of the publish sequence, then claim.
+__device__ uint32_t warp_pop(const QueueView& q, uint32_t tag, uint32_t* dbg = nullptr) {
+  const uint32_t lane = threadIdx.x & 31;
+  if (q.sched == P3_SCHED_PRIORITY) {
+    for (uint32_t group = 0; group < q.n_layers; group += 32 * 32) {
+      uint32_t bits = 0;  // bit c: layer group + 32*c + lane is poppable
+#pragma unroll 4
+      for (uint32_t c = 0; c < 32; ++c) {
+        const uint32_t l = group + 32 * c + lane;
+        if (l >= q.n_layers) break;
+        const bool ok = (int32_t)(ld_acquire_gpu(q.ready + l) - tag) >= 0 &&
+                        ld_relaxed_gpu(q.cursor + l) < q.nslices[l];
+        bits |= (uint32_t)ok << c;
+      }
+      const uint32_t nchunk = min(32u, (q.n_layers - group + 31) / 32);
+      for (uint32_t c = 0; c < nchunk; ++c) {
+        uint32_t m = __ballot_sync(FULL_MASK, (bits >> c) & 1u);
+        while (m) {
+          const uint32_t j = __ffs(m) - 1;
+          const uint32_t l = group + 32 * c + j;
+          uint32_t s = 0;
+          if (lane == j) s = atomicAdd(q.cursor + l, 1u);
+          s = __shfl_sync(FULL_MASK, s, j);
+          if (s < q.nslices[l]) return q.first[l] + s;
+          m &= m - 1;  // lost the race for the layer's last slice: next candidate
+        }
+      }
+    }
+    return P3_NONE;
+  }
+  for (uint32_t retry = 0;; ++retry) {
+    if (dbg && lane == 0) *(volatile uint32_t*)dbg = (6u << 20) | (retry & 0xfffff);
     uint32_t best_key = P3_NONE, best_l = P3_NONE;
     for (uint32_t l = lane; l < q.n_layers; l += 32) {
       const uint32_t r = ld_acquire_gpu(q.ready + l);
       if ((int32_t)(r - tag) < 0) continue;
       if (ld_relaxed_gpu(q.cursor + l) >= q.nslices[l]) continue;
-      const uint32_t key = q.sched == P3_SCHED_FIFO ? ld_relaxed_gpu(q.fifo_key + l) : l;
+      const uint32_t key = ld_relaxed_gpu(q.fifo_key + l);
       if (key < best_key || (key == best_key && l < best_l)) {
         best_key = key;
         best_l = l;
@@ -337,56 +397,71 @@ int launch_queue_pop(const uint32_t* nslices, const uint32_t* first, const uint3
 // Server role pick (one warp): the lowest layer with a completed, unclaimed owned slice,
 // then the first such slice of that layer (ascending slice index). The inbox of
 // ServerEngine is priority ordered (server.py:118), so the same order is used here.
-__device__ uint32_t warp_server_pick(const CommArgs& a, const LocalDev& L) {
-  const int lane = threadIdx.x & 31;
+__device__ uint32_t warp_server_pick(const CommArgs& a, const LocalDev& L, uint32_t* dbg = nullptr) {
+  const uint32_t lane = threadIdx.x & 31;
   const PlanDev& P = a.plan;
   const uint32_t o = L.rank, nl = P.n_layers, k = a.k;
   const uint32_t* hint = a.peers.hint[o];
   const uint32_t* arrivals = a.peers.arrivals[o];
   const uint32_t* lcount = P.own_lcount + (uint64_t)o * nl;
-  uint32_t best_l = P3_NONE;
-  for (uint32_t l = lane; l < nl; l += 32) {
-    const uint32_t oc = lcount[l];
-    if (!oc) continue;
-    const uint32_t completed = ld_acquire_sys(hint + l) - k * oc;
-    const uint32_t taken = ld_relaxed_gpu(L.srv_taken + l);
-    if ((int32_t)(completed - taken) > 0) {
-      best_l = l;
-      break;  // lanes scan ascending strided layers: the first hit is this lane's minimum
-    }
-  }
-#pragma unroll
-  for (int off = 16; off; off >>= 1) best_l = min(best_l, __shfl_xor_sync(FULL_MASK, best_l, off));
-  if (best_l == P3_NONE) return P3_NONE;
-  const uint32_t l = best_l;
-  const uint32_t lf = P.own_lfirst[(uint64_t)o * nl + l], cnt = lcount[l];
   const uint32_t need = (k + 1) * P.world;
-  for (uint32_t i0 = ld_relaxed_gpu(L.srv_lo + l); i0 < cnt; i0 += 32) {
-    const uint32_t i = i0 + lane;
-    uint32_t g = P3_NONE;
-    bool ok = false, claimed = true;
-    if (i < cnt) {
-      g = P.own_list[lf + i];
-      const uint32_t c = ld_relaxed_gpu(L.claim + g);
-      claimed = c != k;
-      ok = !claimed && (int32_t)(ld_acquire_sys(arrivals + g) - need) >= 0;
+  for (uint32_t group = 0; group < nl; group += 32 * 32) {
+    // candidate layers: an owned slice completed this iteration and not yet claimed
+    uint32_t bits = 0;
+#pragma unroll 4
+    for (uint32_t c = 0; c < 32; ++c) {
+      const uint32_t l = group + 32 * c + lane;
+      if (l >= nl) break;
+      const uint32_t oc = lcount[l];
+      bool ok = false;
+      if (oc) {
+        const uint32_t completed = ld_acquire_sys(hint + l) - k * oc;
+        ok = (int32_t)(completed - ld_relaxed_gpu(L.srv_taken + l)) > 0;
+      }
+      bits |= (uint32_t)ok << c;
     }
-    if (__all_sync(FULL_MASK, claimed) && lane == 0) atomicMax(L.srv_lo + l, i0 + 32);
-    uint32_t m = __ballot_sync(FULL_MASK, ok);
-    while (m) {
-      const int j = __ffs(m) - 1;
-      const uint32_t gj = __shfl_sync(FULL_MASK, g, j);
-      uint32_t won = 0;
-      if (lane == 0) {
-        won = atomicCAS(L.claim + gj, k, k + 1) == k;
-        if (won) {
-          atomicAdd(L.srv_taken + l, 1u);
-          atomicAdd(&L.it->reduced, 1u);
+    const uint32_t nchunk = min(32u, (nl - group + 31) / 32);
+    for (uint32_t c = 0; c < nchunk; ++c) {
+      uint32_t lm = __ballot_sync(FULL_MASK, (bits >> c) & 1u);
+      while (lm) {
+        const uint32_t l = group + 32 * c + (__ffs(lm) - 1);
+        lm &= lm - 1;
+        const uint32_t lf = P.own_lfirst[(uint64_t)o * nl + l], cnt = lcount[l];
+        // lanes are not guaranteed to execute this load together (independent thread
+        // scheduling) and other CTAs move the watermark: take lane 0's value so the trip
+        // count — and every warp-synchronous call inside — is uniform across the warp
+        uint32_t lo = 0;
+        if (lane == 0) lo = ld_relaxed_gpu(L.srv_lo + l);
+        lo = __shfl_sync(FULL_MASK, lo, 0);
+        for (uint32_t i0 = lo; i0 < cnt; i0 += 32) {
+          if (dbg && lane == 0) *(volatile uint32_t*)dbg = (8u << 20) | ((l & 0x3ff) << 10) | (i0 & 0x3ff);
+          const uint32_t i = i0 + lane;
+          uint32_t g = P3_NONE;
+          bool ok = false, claimed = true;
+          if (i < cnt) {
+            g = P.own_list[lf + i];
+            claimed = ld_relaxed_gpu(L.claim + g) != k;
+            ok = !claimed && (int32_t)(ld_acquire_sys(arrivals + g) - need) >= 0;
+          }
+          if (__all_sync(FULL_MASK, claimed) && lane == 0) atomicMax(L.srv_lo + l, i0 + 32);
+          uint32_t m = __ballot_sync(FULL_MASK, ok);
+          while (m) {
+            const int j = __ffs(m) - 1;
+            const uint32_t gj = __shfl_sync(FULL_MASK, g, j);
+            uint32_t won = 0;
+            if (lane == 0) {
+              won = atomicCAS(L.claim + gj, k, k + 1) == k;
+              if (won) {
+                atomicAdd(L.srv_taken + l, 1u);
+                atomicAdd(&L.it->reduced, 1u);
+              }
+            }
+            won = __shfl_sync(FULL_MASK, won, 0);
+            if (won) return gj;
+            m &= m - 1;
+          }
         }
       }
-      won = __shfl_sync(FULL_MASK, won, 0);
-      if (won) return gj;
-      m &= m - 1;
     }
   }
   return P3_NONE;
@@ -409,21 +484,21 @@ __device__ __forceinline__ void trace_append(const LocalDev& L, uint32_t k, uint
 }
 
 __device__ void cta_copy(float* dst, const float* src, uint32_t n) {
+  constexpr int U = 8;  // 8 independent 16-byte loads in flight per thread
   uint32_t done = 0;
   if ((((uintptr_t)dst | (uintptr_t)src) & 15) == 0) {
-    const uint32_t n4 = n / 4;
+    const uint32_t n4 = n / 4, stride = blockDim.x;
     const float4* s4 = reinterpret_cast<const float4*>(src);
     float4* d4 = reinterpret_cast<float4*>(dst);
     uint32_t j = threadIdx.x;
-    for (; j + 3 * blockDim.x < n4; j += 4 * blockDim.x) {  // 4 loads in flight per thread
-      const float4 a0 = __ldcg(s4 + j), a1 = __ldcg(s4 + j + blockDim.x);
-      const float4 a2 = __ldcg(s4 + j + 2 * blockDim.x), a3 = __ldcg(s4 + j + 3 * blockDim.x);
-      d4[j] = a0;
-      d4[j + blockDim.x] = a1;
-      d4[j + 2 * blockDim.x] = a2;
-      d4[j + 3 * blockDim.x] = a3;
+    for (; j + (U - 1) * stride < n4; j += U * stride) {
+      float4 r[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) r[u] = __ldcg(s4 + j + u * stride);
+#pragma unroll
+      for (int u = 0; u < U; ++u) d4[j + u * stride] = r[u];
     }
-    for (; j < n4; j += blockDim.x) d4[j] = __ldcg(s4 + j);
+    for (; j < n4; j += stride) d4[j] = __ldcg(s4 + j);
     done = 4 * n4;
   }
   for (uint32_t i = done + threadIdx.x; i < n; i += blockDim.x) dst[i] = __ldcg(src + i);
@@ -439,21 +514,26 @@ __device__ void do_push(const CommArgs& a, const LocalDev& L, uint32_t g, PushSm
   const PlanDev& P = a.plan;
   const uint32_t r = L.rank, o = P.slice_owner[g], l = P.slice_layer[g];
   const uint32_t len = P.slice_len[g];
+  if (o == r) {
+    // the owner reads its own contribution from the gradient in place: only count it
+    if (threadIdx.x == 0) {
+      (void)ld_acquire_gpu(L.ready + l);  // gradient published -> visible to the reducer
+      const uint32_t old = atom_add_release_sys(a.peers.arrivals[o] + g, 1u);
+      if (old + 1 == (a.k + 1) * P.world) red_add_release_sys(a.peers.hint[o] + l, 1u);
+    }
+    return;
+  }
   if (threadIdx.x == 0) {
     (void)ld_acquire_gpu(L.ready + l);
     sm->src = reinterpret_cast<const float*>(ld_relaxed_gpu64(L.gptr + l)) + P.slice_off[g];
   }
   __syncthreads();
-  if (o != r) {
-    float* dst = a.peers.R[o] + (uint64_t)r * P.own_stride[o] + P.slice_slot[g];
-    cta_copy(dst, sm->src, len);
-  }
+  float* dst = a.peers.R[o] + (uint64_t)r * P.own_stride[o] + P.slice_slot[g];
+  cta_copy(dst, sm->src, len);
   __syncthreads();
   if (threadIdx.x == 0) {
-    if (o != r) {
-      __threadfence_system();
-      atomicAdd(L.bytes + 1, 4ull * len);
-    }
+    if (a.remote) __threadfence_system(); else __threadfence();
+    atomicAdd(L.bytes + 1, 4ull * len);
     const uint32_t old = atom_add_release_sys(a.peers.arrivals[o] + g, 1u);
     if (old + 1 == (a.k + 1) * P.world) red_add_release_sys(a.peers.hint[o] + l, 1u);
   }
@@ -497,7 +577,7 @@ __device__ void do_reduce(const CommArgs& a, const LocalDev& L, uint32_t g, Redu
                      len, sm->aligned != 0, make_coef(N, a.lr, a.momentum));
   __syncthreads();
   if (threadIdx.x == 0) {
-    __threadfence_system();
+    if (a.remote) __threadfence_system(); else __threadfence();
     for (uint32_t q = 0; q < N; ++q) red_add_release_sys(a.peers.done[q] + l, 1u);
     atomicAdd(L.bytes + 0, 4ull * len * (N - 1));  // pushes received
     atomicAdd(L.bytes + 1, 4ull * len * (N - 1));  // broadcasts sent
@@ -526,25 +606,28 @@ __device__ __forceinline__ QueueView queue_of(const CommArgs& a, const LocalDev&
 // need (co-residency-bound library kernels, lazy module loading). The FINISH launch of an
 // iteration ends once every local slice is pushed and every owned slice reduced; it waits
 // only for peers' pushes, never for local compute.
-__global__ void __launch_bounds__(1024) k_comm(const __grid_constant__ CommArgs a) {
+__global__ void __launch_bounds__(512, 1) k_comm(const __grid_constant__ CommArgs a) {
   __shared__ uint32_t s_job, s_li, s_g;
   __shared__ PushSmem s_push;
   __shared__ ReduceSmem s_red;
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint64_t t0 = globaltimer();
   uint32_t backoff = 0;
-  for (;;) {
+  uint32_t* phase = (threadIdx.x == 0 && blockIdx.x < P3_DBG_CTAS) ? a.loc[0].cta_phase + blockIdx.x : nullptr;
+  for (uint32_t iter = 0;; ++iter) {
+    if (phase) *(volatile uint32_t*)phase = (a.k << 24) | (1u << 20) | (iter & 0xfffff);
     if (warp == 0) {
       if (backoff) __nanosleep(backoff);
       uint32_t job = 0, li = 0, g = P3_NONE;
       for (uint32_t t = 0; t < a.n_local && job == 0; ++t) {
         li = (blockIdx.x + t) % a.n_local;
-        g = warp_server_pick(a, a.loc[li]);
+        if (phase) *(volatile uint32_t*)phase = (7u << 20);
+        g = warp_server_pick(a, a.loc[li], phase);
         if (g != P3_NONE) job = 1;
       }
       for (uint32_t t = 0; t < a.n_local && job == 0; ++t) {
         li = (blockIdx.x + t) % a.n_local;
-        g = warp_pop(queue_of(a, a.loc[li]), a.k + 1);
+        g = warp_pop(queue_of(a, a.loc[li]), a.k + 1, phase);
         if (g != P3_NONE) {
           job = 2;
           if (lane == 0) {
@@ -560,15 +643,21 @@ __global__ void __launch_bounds__(1024) k_comm(const __grid_constant__ CommArgs 
       if (job == 0 && a.mode == P3_COMM_DRAIN) {
         job = 3;  // nothing published is pending: leave the SMs to compute
       } else if (job == 0) {
-        bool fin = true;
-        for (uint32_t t = 0; t < a.n_local; ++t) {
-          const LocalDev& L = a.loc[t];
-          fin = fin && ld_relaxed_gpu(&L.it->pushed) >= a.plan.total_slices &&
-                ld_relaxed_gpu(&L.it->reduced) >= a.plan.own_total[L.rank];
+        // decided by lane 0 and broadcast: a per-lane decision could split the warp
+        uint32_t verdict = 0;  // 0 keep waiting, 1 done or failed elsewhere, 2 timed out
+        if (lane == 0) {
+          bool fin = true;
+          for (uint32_t t = 0; t < a.n_local; ++t) {
+            const LocalDev& L = a.loc[t];
+            fin = fin && ld_relaxed_gpu(&L.it->pushed) >= a.plan.total_slices &&
+                  ld_relaxed_gpu(&L.it->reduced) >= a.plan.own_total[L.rank];
+          }
+          verdict = (fin || ld_relaxed_gpu(a.err) != 0) ? 1u : (globaltimer() - t0 > a.timeout_ns ? 2u : 0u);
         }
-        if (fin || ld_relaxed_gpu(a.err) != 0) {
+        verdict = __shfl_sync(FULL_MASK, verdict, 0);
+        if (verdict == 1) {
           job = 3;
-        } else if (globaltimer() - t0 > a.timeout_ns) {
+        } else if (verdict == 2) {
           job = 3;
           if (lane == 0 && atomicCAS(a.err, 0u, (uint32_t)P3_ETIMEOUT) == 0u) {
             // diagnostics for the host (p3_sync_all), then release every forward gate of the
@@ -594,10 +683,14 @@ __global__ void __launch_bounds__(1024) k_comm(const __grid_constant__ CommArgs 
     __syncthreads();
     const uint32_t job = s_job;
     if (job == 3) break;
+    if (phase) *(volatile uint32_t*)phase = (a.k << 24) | ((1u + job) << 20) | (iter & 0xfffff);
     if (job == 1) do_reduce(a, a.loc[s_li], s_g, &s_red);
     else if (job == 2) do_push(a, a.loc[s_li], s_g, &s_push);
+    if (job && threadIdx.x == 0) atomicAdd(&a.loc[0].it->jobs, 1u);
     __syncthreads();
   }
+  if (phase) *(volatile uint32_t*)phase = (a.k << 24) | (5u << 20);
+  if (threadIdx.x == 0 && a.mode == P3_COMM_FINISH) atomicAdd(&a.loc[0].it->exited, 1u);
 }
 
 // With lazy module loading (CUDA_MODULE_LOADING=LAZY, the CUDA 12 default) the first launch

@@ -188,7 +188,8 @@ class SyncContext:
         arr = list(buf)
         names = ("ready", "cursor", "srv_taken", "hint", "done")
         out = {nm: arr[i * L : (i + 1) * L] for i, nm in enumerate(names)}
-        out["pushed"], out["reduced"] = arr[5 * L], arr[5 * L + 1]
+        out["pushed"], out["reduced"], out["exited"], out["jobs"] = arr[5 * L : 5 * L + 4]
+        out["cta_phase"] = arr[5 * L + 4 :]
         return out
 
     def clear_trace(self) -> None:
