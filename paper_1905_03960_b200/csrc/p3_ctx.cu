@@ -225,8 +225,8 @@ int p3_ctx_create(const p3_config_t* cfg, p3_ctx_t** out) {
   if (cfg->n_local < 1 || cfg->n_local > cfg->world) return fail(nullptr, P3_EUSAGE, "bad n_local");
   if (cfg->n_layers < 1 || !cfg->layer_counts) return fail(nullptr, P3_EUSAGE, "profile needs at least one layer");
   if (cfg->plan_mode != P3_PLAN_P3) return fail(nullptr, P3_EUSAGE, "only the p3 plan runs on the comm kernel");
-  if (cfg->comm_threads < 32 || cfg->comm_threads > 512 || cfg->comm_threads % 32)
-    return fail(nullptr, P3_EUSAGE, "comm_threads must be a multiple of 32 in [32, 512]");
+  if (cfg->comm_threads < 64 || cfg->comm_threads > 512 || cfg->comm_threads % 32)
+    return fail(nullptr, P3_EUSAGE, "comm_threads must be a multiple of 32 in [64, 512] (one scheduler warp + movers)");
   if (cfg->comm_ctas < 1) return fail(nullptr, P3_EUSAGE, "comm_ctas must be >= 1");
   for (uint32_t i = 0; i < cfg->n_local; ++i)
     if (cfg->local_ranks[i] >= cfg->world) return fail(nullptr, P3_EUSAGE, "local rank out of range");

@@ -170,9 +170,9 @@ __device__ __forceinline__ float4 sgd4(float4 p, const float4& acc, const UpdCoe
 // so each thread keeps (NW + 1) * U independent 16-byte loads in flight.
 template <int NW, int U>
 __device__ void cta_update_vec(const float* p_src, float* const* dst, int ndst, const float* const* src,
-                               float* v, uint64_t n4, const UpdCoef& c) {
-  const uint64_t stride = blockDim.x;
-  uint64_t j = threadIdx.x;
+                               float* v, uint64_t n4, const UpdCoef& c, uint32_t tid, uint32_t nthr) {
+  const uint64_t stride = nthr;
+  uint64_t j = tid;
   for (; j + (U - 1) * stride < n4; j += U * stride) {
     float4 g[U][NW], p[U], vv[U];
 #pragma unroll
@@ -205,20 +205,21 @@ __device__ void cta_update_vec(const float* p_src, float* const* dst, int ndst, 
 }
 
 __device__ void cta_update_generic(const float* p_src, float* const* dst, int ndst, const float* const* src,
-                                   int nw, float* v, uint64_t n, bool aligned, const UpdCoef& c) {
+                                   int nw, float* v, uint64_t n, bool aligned, const UpdCoef& c, uint32_t tid,
+                                   uint32_t nthr) {
   uint64_t done = 0;
   if (aligned) {
     const uint64_t n4 = n / 4;
     switch (nw) {
 #define P3_CASE(K) \
-  case K: cta_update_vec<K, (K <= 1 ? 4 : K <= 2 ? 2 : 1)>(p_src, dst, ndst, src, v, n4, c); break;
+  case K: cta_update_vec<K, (K <= 1 ? 4 : K <= 2 ? 2 : 1)>(p_src, dst, ndst, src, v, n4, c, tid, nthr); break;
       P3_CASE(1) P3_CASE(2) P3_CASE(3) P3_CASE(4) P3_CASE(5) P3_CASE(6) P3_CASE(7) P3_CASE(8)
 #undef P3_CASE
       default: aligned = false; break;
     }
     if (aligned) done = 4 * n4;
   }
-  for (uint64_t i = done + threadIdx.x; i < n; i += blockDim.x) {
+  for (uint64_t i = done + tid; i < n; i += nthr) {
     const float acc = sum_sources_scalar(src, nw, i);
     float p = __ldcg(p_src + i);
     p = sgd_step(p, acc, c, v ? v + i : nullptr);
@@ -255,7 +256,7 @@ __global__ void __launch_bounds__(256) k_shard_update(float* params, GradPtrs g,
   uintptr_t al = (uintptr_t)(params + lo) | (V ? (uintptr_t)(V + lo) : 0);
   for (uint32_t q = 0; q < nw; ++q) al |= (uintptr_t)(g.p[q] + lo);
   cta_update_generic(params + lo, dst, 1, src, (int)nw, V ? V + lo : nullptr, len, (al & 15) == 0,
-                     make_coef(nw, lr, mu));
+                     make_coef(nw, lr, mu), threadIdx.x, blockDim.x);
 }
 
 }  // namespace p3
@@ -483,106 +484,25 @@ __device__ __forceinline__ void trace_append(const LocalDev& L, uint32_t k, uint
   }
 }
 
-__device__ void cta_copy(float* dst, const float* src, uint32_t n) {
+__device__ void cta_copy(float* dst, const float* src, uint32_t n, uint32_t tid, uint32_t nthr) {
   constexpr int U = 8;  // 8 independent 16-byte loads in flight per thread
   uint32_t done = 0;
   if ((((uintptr_t)dst | (uintptr_t)src) & 15) == 0) {
-    const uint32_t n4 = n / 4, stride = blockDim.x;
+    const uint32_t n4 = n / 4;
     const float4* s4 = reinterpret_cast<const float4*>(src);
     float4* d4 = reinterpret_cast<float4*>(dst);
-    uint32_t j = threadIdx.x;
-    for (; j + (U - 1) * stride < n4; j += U * stride) {
+    uint32_t j = tid;
+    for (; j + (U - 1) * nthr < n4; j += U * nthr) {
       float4 r[U];
 #pragma unroll
-      for (int u = 0; u < U; ++u) r[u] = __ldcg(s4 + j + u * stride);
+      for (int u = 0; u < U; ++u) r[u] = __ldcg(s4 + j + u * nthr);
 #pragma unroll
-      for (int u = 0; u < U; ++u) d4[j + u * stride] = r[u];
+      for (int u = 0; u < U; ++u) d4[j + u * nthr] = r[u];
     }
-    for (; j < n4; j += stride) d4[j] = __ldcg(s4 + j);
+    for (; j < n4; j += nthr) d4[j] = __ldcg(s4 + j);
     done = 4 * n4;
   }
-  for (uint32_t i = done + threadIdx.x; i < n; i += blockDim.x) dst[i] = __ldcg(src + i);
-}
-
-struct PushSmem {
-  const float* src;
-};
-
-// Worker role: store one slice of this rank's gradient into the owner's receive slot
-// over NVLink (or nothing when the owner is local), then count the arrival.
-__device__ void do_push(const CommArgs& a, const LocalDev& L, uint32_t g, PushSmem* sm) {
-  const PlanDev& P = a.plan;
-  const uint32_t r = L.rank, o = P.slice_owner[g], l = P.slice_layer[g];
-  const uint32_t len = P.slice_len[g];
-  if (o == r) {
-    // the owner reads its own contribution from the gradient in place: only count it
-    if (threadIdx.x == 0) {
-      (void)ld_acquire_gpu(L.ready + l);  // gradient published -> visible to the reducer
-      const uint32_t old = atom_add_release_sys(a.peers.arrivals[o] + g, 1u);
-      if (old + 1 == (a.k + 1) * P.world) red_add_release_sys(a.peers.hint[o] + l, 1u);
-    }
-    return;
-  }
-  if (threadIdx.x == 0) {
-    (void)ld_acquire_gpu(L.ready + l);
-    sm->src = reinterpret_cast<const float*>(ld_relaxed_gpu64(L.gptr + l)) + P.slice_off[g];
-  }
-  __syncthreads();
-  float* dst = a.peers.R[o] + (uint64_t)r * P.own_stride[o] + P.slice_slot[g];
-  cta_copy(dst, sm->src, len);
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    if (a.remote) __threadfence_system(); else __threadfence();
-    atomicAdd(L.bytes + 1, 4ull * len);
-    const uint32_t old = atom_add_release_sys(a.peers.arrivals[o] + g, 1u);
-    if (old + 1 == (a.k + 1) * P.world) red_add_release_sys(a.peers.hint[o] + l, 1u);
-  }
-}
-
-struct ReduceSmem {
-  const float* src[P3_MAX_RANKS];
-  float* dst[P3_MAX_RANKS];
-  int aligned;
-};
-
-// Server role: aggregate the N pushes of an owned slice in rank order, apply SGD to the
-// master (the owner's replica), store the result into every replica, bump done[layer].
-__device__ void do_reduce(const CommArgs& a, const LocalDev& L, uint32_t g, ReduceSmem* sm) {
-  const PlanDev& P = a.plan;
-  const uint32_t o = L.rank, l = P.slice_layer[g], N = P.world;
-  const uint32_t len = P.slice_len[g];
-  const uint64_t woff = P.layer_woff[l] + P.slice_off[g];
-  if (threadIdx.x < N) {
-    const uint32_t q = threadIdx.x;
-    if (q == o) {
-      (void)ld_acquire_sys(a.peers.arrivals[o] + g);
-      sm->src[q] = reinterpret_cast<const float*>(ld_relaxed_gpu64(L.gptr + l)) + P.slice_off[g];
-    } else {
-      sm->src[q] = a.peers.R[o] + (uint64_t)q * P.own_stride[o] + P.slice_slot[g];
-    }
-    // the owner's own replica goes first: it is also the master copy read below
-    const uint32_t d = q == o ? 0 : (q < o ? q + 1 : q);
-    sm->dst[d] = a.peers.W[q] + woff;
-  }
-  if (threadIdx.x == 0) (void)ld_acquire_sys(a.peers.arrivals[o] + g);
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    uintptr_t al = 0;
-    for (uint32_t q = 0; q < N; ++q) al |= (uintptr_t)sm->src[q] | (uintptr_t)sm->dst[q];
-    if (L.V) al |= (uintptr_t)(L.V + P.slice_slot[g]);
-    sm->aligned = (al & 15) == 0;
-  }
-  __syncthreads();
-  cta_update_generic(sm->dst[0], sm->dst, (int)N, sm->src, (int)N, L.V ? L.V + P.slice_slot[g] : nullptr,
-                     len, sm->aligned != 0, make_coef(N, a.lr, a.momentum));
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    if (a.remote) __threadfence_system(); else __threadfence();
-    for (uint32_t q = 0; q < N; ++q) red_add_release_sys(a.peers.done[q] + l, 1u);
-    atomicAdd(L.bytes + 0, 4ull * len * (N - 1));  // pushes received
-    atomicAdd(L.bytes + 1, 4ull * len * (N - 1));  // broadcasts sent
-    trace_append(L, a.k, l, g - P.layer_first[l], o, P3_EV_BCAST);
-  }
+  for (uint32_t i = done + tid; i < n; i += nthr) dst[i] = __ldcg(src + i);
 }
 
 __device__ __forceinline__ QueueView queue_of(const CommArgs& a, const LocalDev& L) {
@@ -597,100 +517,230 @@ __device__ __forceinline__ QueueView queue_of(const CommArgs& a, const LocalDev&
   return q;
 }
 
-// Comm kernel. Every CTA loops: warp 0 picks a job (server work first, since a finished
-// slice unblocks the next forward pass; then the most urgent ready slice of the local
-// worker queues), the whole CTA executes it. The queue is re-read before every job, so a
-// layer published while the kernel runs preempts less urgent slices at slice granularity.
-// DRAIN launches (one per published layer) exit when no job is available: a kernel that
-// spun on not-yet-published gradients would hold SMs that the compute producing them may
-// need (co-residency-bound library kernels, lazy module loading). The FINISH launch of an
-// iteration ends once every local slice is pushed and every owned slice reduced; it waits
-// only for peers' pushes, never for local compute.
-__global__ void __launch_bounds__(512, 1) k_comm(const __grid_constant__ CommArgs a) {
-  __shared__ uint32_t s_job, s_li, s_g;
-  __shared__ PushSmem s_push;
-  __shared__ ReduceSmem s_red;
-  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint64_t t0 = globaltimer();
-  uint32_t backoff = 0;
-  uint32_t* phase = (threadIdx.x == 0 && blockIdx.x < P3_DBG_CTAS) ? a.loc[0].cta_phase + blockIdx.x : nullptr;
-  for (uint32_t iter = 0;; ++iter) {
-    if (phase) *(volatile uint32_t*)phase = (a.k << 24) | (1u << 20) | (iter & 0xfffff);
-    if (warp == 0) {
-      if (backoff) __nanosleep(backoff);
-      uint32_t job = 0, li = 0, g = P3_NONE;
-      for (uint32_t t = 0; t < a.n_local && job == 0; ++t) {
-        li = (blockIdx.x + t) % a.n_local;
-        if (phase) *(volatile uint32_t*)phase = (7u << 20);
-        g = warp_server_pick(a, a.loc[li], phase);
-        if (g != P3_NONE) job = 1;
+// One job handed from the scheduler warp to the mover warps of a CTA.
+#define JOB_NONE 0
+#define JOB_REDUCE 1
+#define JOB_PUSH 2
+#define JOB_EXIT 3
+struct Job {
+  uint32_t kind, li, g, layer, slice, rank, len, n, aligned;
+  const float* src[P3_MAX_RANKS];  // PUSH: src[0]; REDUCE: contributions in rank order
+  float* dst[P3_MAX_RANKS];        // PUSH: dst[0]; REDUCE: replicas, dst[0] = owner's master
+  float* v;
+};
+
+// Named barriers (0 is __syncthreads): per job slot b "slot full" (scheduler -> movers) and
+// "slot free" (movers -> scheduler), plus one among the movers.
+#define BAR_FULL(b) (1 + (b))
+#define BAR_EMPTY(b) (3 + (b))
+#define BAR_MOVERS 5
+__device__ __forceinline__ void bar_sync(uint32_t id, uint32_t n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ void bar_arrive(uint32_t id, uint32_t n) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+// Scheduler side of a push. With job == nullptr: if the owner is this rank, its
+// contribution stays in place — count the arrival here and return false (no data to move).
+// With a slot: fill it for the movers, who store the slice into the owner's receive slot
+// over NVLink.
+__device__ bool prepare_push(const CommArgs& a, uint32_t li, uint32_t g, Job* job) {
+  const PlanDev& P = a.plan;
+  const LocalDev& L = a.loc[li];
+  const uint32_t r = L.rank, o = P.slice_owner[g], l = P.slice_layer[g];
+  const uint32_t lane = threadIdx.x & 31;
+  if (!job) {
+    if (lane == 0) {
+      (void)ld_acquire_gpu(L.ready + l);  // the gradient is published: visible from here on
+      trace_append(L, a.k, l, g - P.layer_first[l], r, P3_EV_PUSH);
+      if (o == r) {
+        const uint32_t old = atom_add_release_sys(a.peers.arrivals[o] + g, 1u);
+        if (old + 1 == (a.k + 1) * P.world) red_add_release_sys(a.peers.hint[o] + l, 1u);
       }
-      for (uint32_t t = 0; t < a.n_local && job == 0; ++t) {
+    }
+    __syncwarp();
+    return o != r;
+  }
+  if (lane == 0) {
+    job->kind = JOB_PUSH;
+    job->li = li;
+    job->g = g;
+    job->layer = l;
+    job->rank = o;
+    job->len = P.slice_len[g];
+    job->src[0] = reinterpret_cast<const float*>(ld_relaxed_gpu64(L.gptr + l)) + P.slice_off[g];
+    job->dst[0] = a.peers.R[o] + (uint64_t)r * P.own_stride[o] + P.slice_slot[g];
+  }
+  return true;
+}
+
+// Scheduler side of a reduce: contributions of every rank (the owner's own straight from
+// its gradient) and every replica to write, master first.
+__device__ void prepare_reduce(const CommArgs& a, uint32_t li, uint32_t g, Job* job) {
+  const PlanDev& P = a.plan;
+  const LocalDev& L = a.loc[li];
+  const uint32_t o = L.rank, l = P.slice_layer[g], N = P.world;
+  const uint32_t q = threadIdx.x & 31;
+  const uint64_t woff = P.layer_woff[l] + P.slice_off[g];
+  if (q == 0) (void)ld_acquire_sys(a.peers.arrivals[o] + g);  // all N pushes are visible
+  __syncwarp();
+  uintptr_t al = 0;
+  if (q < N) {
+    const float* src = q == o ? reinterpret_cast<const float*>(ld_relaxed_gpu64(L.gptr + l)) + P.slice_off[g]
+                              : a.peers.R[o] + (uint64_t)q * P.own_stride[o] + P.slice_slot[g];
+    float* dst = a.peers.W[q] + woff;
+    job->src[q] = src;
+    job->dst[q == o ? 0 : (q < o ? q + 1 : q)] = dst;
+    al = (uintptr_t)src | (uintptr_t)dst;
+  }
+  float* v = L.V ? L.V + P.slice_slot[g] : nullptr;
+#pragma unroll
+  for (int off = 16; off; off >>= 1) al |= __shfl_xor_sync(FULL_MASK, (unsigned long long)al, off);
+  if (q == 0) {
+    job->kind = JOB_REDUCE;
+    job->li = li;
+    job->g = g;
+    job->layer = l;
+    job->rank = o;
+    job->len = P.slice_len[g];
+    job->n = N;
+    job->v = v;
+    job->aligned = ((al | (uintptr_t)v) & 15) == 0;
+  }
+}
+
+// Mover side: move the data, then one mover publishes completion (release, system scope
+// when a peer is on another GPU).
+__device__ void run_job(const CommArgs& a, const Job& j, uint32_t tid, uint32_t nthr) {
+  const PlanDev& P = a.plan;
+  const LocalDev& L = a.loc[j.li];
+  if (j.kind == JOB_PUSH) {
+    cta_copy(j.dst[0], j.src[0], j.len, tid, nthr);
+    bar_sync(BAR_MOVERS, nthr);
+    if (tid == 0) {
+      if (a.remote) __threadfence_system(); else __threadfence();
+      atomicAdd(L.bytes + 1, 4ull * j.len);
+      const uint32_t old = atom_add_release_sys(a.peers.arrivals[j.rank] + j.g, 1u);
+      if (old + 1 == (a.k + 1) * P.world) red_add_release_sys(a.peers.hint[j.rank] + j.layer, 1u);
+    }
+  } else {
+    cta_update_generic(j.dst[0], j.dst, (int)j.n, j.src, (int)j.n, j.v, j.len, j.aligned != 0,
+                       make_coef(j.n, a.lr, a.momentum), tid, nthr);
+    bar_sync(BAR_MOVERS, nthr);
+    if (tid == 0) {
+      if (a.remote) __threadfence_system(); else __threadfence();
+      for (uint32_t q = 0; q < j.n; ++q) red_add_release_sys(a.peers.done[q] + j.layer, 1u);
+      atomicAdd(L.bytes + 0, 4ull * j.len * (j.n - 1));  // pushes received
+      atomicAdd(L.bytes + 1, 4ull * j.len * (j.n - 1));  // broadcasts sent
+      trace_append(L, a.k, j.layer, j.g - P.layer_first[j.layer], j.rank, P3_EV_BCAST);
+    }
+  }
+}
+
+// Comm kernel: warp 0 of every CTA is the scheduler, warps 1.. are movers.
+//   scheduler: pick the next job — server work first (a reduced slice unblocks the next
+//   forward pass), then the most urgent published slice of the local worker queues — and
+//   prepare its pointers while the movers are still busy with the previous job;
+//   movers: wait for a job, copy it to registers, release the slot, move the data,
+//   publish completion.
+// The queue is re-read for every pick, so a layer published while the kernel runs
+// preempts less urgent slices at slice granularity. DRAIN launches (one per published
+// layer) exit as soon as nothing is available: a kernel spinning on unpublished gradients
+// would hold SMs that the compute producing them may need (co-residency-bound library
+// kernels, lazy module loading). The FINISH launch of an iteration ends once every local
+// slice is pushed and every owned slice reduced; it waits only for peers' pushes.
+__global__ void __launch_bounds__(512, 1) k_comm(const __grid_constant__ CommArgs a) {
+  __shared__ Job slots[2];  // double-buffered: the scheduler fills one while movers run the other
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t nthr = blockDim.x;
+  const uint32_t movers = nthr - 32;
+  if (warp == 0) {
+    uint32_t* phase = (lane == 0 && blockIdx.x < P3_DBG_CTAS) ? a.loc[0].cta_phase + blockIdx.x : nullptr;
+    const uint64_t t0 = globaltimer();
+    uint32_t backoff = 0, b = 0;
+    bool pending[2] = {false, false};
+    for (uint32_t iter = 0;; ++iter) {
+      if (phase) *(volatile uint32_t*)phase = (a.k << 24) | (1u << 20) | (iter & 0xfffff);
+      uint32_t kind = JOB_NONE, li = 0, g = P3_NONE;
+      for (uint32_t t = 0; t < a.n_local && kind == JOB_NONE; ++t) {
+        li = (blockIdx.x + t) % a.n_local;
+        g = warp_server_pick(a, a.loc[li], phase);
+        if (g != P3_NONE) kind = JOB_REDUCE;
+      }
+      for (uint32_t t = 0; t < a.n_local && kind == JOB_NONE; ++t) {
         li = (blockIdx.x + t) % a.n_local;
         g = warp_pop(queue_of(a, a.loc[li]), a.k + 1, phase);
         if (g != P3_NONE) {
-          job = 2;
-          if (lane == 0) {
-            // the transmission sequence is the pop order (the moment _priority_sender
-            // hands a slice to the link, worker.py:184-190)
-            const LocalDev& L = a.loc[li];
-            atomicAdd(&L.it->pushed, 1u);
-            const uint32_t l = a.plan.slice_layer[g];
-            trace_append(L, a.k, l, g - a.plan.layer_first[l], L.rank, P3_EV_PUSH);
-          }
+          if (lane == 0) atomicAdd(&a.loc[li].it->pushed, 1u);
+          kind = JOB_PUSH;
         }
       }
-      if (job == 0 && a.mode == P3_COMM_DRAIN) {
-        job = 3;  // nothing published is pending: leave the SMs to compute
-      } else if (job == 0) {
+      if (kind == JOB_NONE) {
         // decided by lane 0 and broadcast: a per-lane decision could split the warp
-        uint32_t verdict = 0;  // 0 keep waiting, 1 done or failed elsewhere, 2 timed out
+        uint32_t verdict = 0;  // 0 keep looking, 1 leave, 2 timed out
         if (lane == 0) {
-          bool fin = true;
-          for (uint32_t t = 0; t < a.n_local; ++t) {
-            const LocalDev& L = a.loc[t];
-            fin = fin && ld_relaxed_gpu(&L.it->pushed) >= a.plan.total_slices &&
-                  ld_relaxed_gpu(&L.it->reduced) >= a.plan.own_total[L.rank];
+          if (a.mode == P3_COMM_DRAIN) {
+            verdict = 1;
+          } else {
+            bool fin = true;
+            for (uint32_t t = 0; t < a.n_local; ++t) {
+              const LocalDev& L = a.loc[t];
+              fin = fin && ld_relaxed_gpu(&L.it->pushed) >= a.plan.total_slices &&
+                    ld_relaxed_gpu(&L.it->reduced) >= a.plan.own_total[L.rank];
+            }
+            verdict = (fin || ld_relaxed_gpu(a.err) != 0) ? 1u : (globaltimer() - t0 > a.timeout_ns ? 2u : 0u);
           }
-          verdict = (fin || ld_relaxed_gpu(a.err) != 0) ? 1u : (globaltimer() - t0 > a.timeout_ns ? 2u : 0u);
-        }
-        verdict = __shfl_sync(FULL_MASK, verdict, 0);
-        if (verdict == 1) {
-          job = 3;
-        } else if (verdict == 2) {
-          job = 3;
-          if (lane == 0 && atomicCAS(a.err, 0u, (uint32_t)P3_ETIMEOUT) == 0u) {
-            // diagnostics for the host (p3_sync_all), then release every forward gate of the
-            // local ranks so the compute streams drain
+          if (verdict == 2 && atomicCAS(a.err, 0u, (uint32_t)P3_ETIMEOUT) == 0u) {
+            // diagnostics for the host (p3_sync_all), then release every forward gate of
+            // the local ranks so the compute streams drain
             a.err[1] = a.k;
             for (uint32_t t = 0; t < a.n_local; ++t) {
               a.err[2 + 2 * t] = ld_relaxed_gpu(&a.loc[t].it->pushed);
               a.err[3 + 2 * t] = ld_relaxed_gpu(&a.loc[t].it->reduced);
             }
             for (uint32_t t = 0; t < a.n_local; ++t)
-              for (uint32_t l = 0; l < a.plan.n_layers; ++l)
-                atomicAdd(a.peers.done[a.loc[t].rank] + l, 0x40000000u);
+              for (uint32_t l = 0; l < a.plan.n_layers; ++l) atomicAdd(a.peers.done[a.loc[t].rank] + l, 0x40000000u);
           }
         }
+        verdict = __shfl_sync(FULL_MASK, verdict, 0);
+        if (verdict == 0) {
+          backoff = min(2u * backoff + 64u, 4096u);
+          __nanosleep(backoff);
+          continue;
+        }
+        kind = JOB_EXIT;
       }
-      if (lane == 0) {
-        s_job = job;
-        s_li = li;
-        s_g = g;
+      backoff = 0;
+      if (kind == JOB_PUSH && !prepare_push(a, li, g, nullptr)) continue;  // own slice: counted in place
+      if (pending[b]) bar_sync(BAR_EMPTY(b), nthr);  // movers are done with this slot
+      if (kind == JOB_PUSH) {
+        prepare_push(a, li, g, &slots[b]);
+      } else if (kind == JOB_REDUCE) {
+        prepare_reduce(a, li, g, &slots[b]);
+      } else {
+        if (pending[b ^ 1]) bar_sync(BAR_EMPTY(b ^ 1), nthr);  // leave every barrier balanced
+        if (lane == 0) slots[b].kind = JOB_EXIT;
       }
-      backoff = job == 0 ? min(2u * backoff + 64u, 4096u) : 0u;
+      __syncwarp();
+      bar_arrive(BAR_FULL(b), nthr);
+      if (kind == JOB_EXIT) break;
+      pending[b] = true;
+      b ^= 1;
+      if (lane == 0) atomicAdd(&a.loc[0].it->jobs, 1u);
     }
-    __syncthreads();
-    const uint32_t job = s_job;
-    if (job == 3) break;
-    if (phase) *(volatile uint32_t*)phase = (a.k << 24) | ((1u + job) << 20) | (iter & 0xfffff);
-    if (job == 1) do_reduce(a, a.loc[s_li], s_g, &s_red);
-    else if (job == 2) do_push(a, a.loc[s_li], s_g, &s_push);
-    if (job && threadIdx.x == 0) atomicAdd(&a.loc[0].it->jobs, 1u);
-    __syncthreads();
+    if (phase) *(volatile uint32_t*)phase = (a.k << 24) | (5u << 20);
+    if (lane == 0 && a.mode == P3_COMM_FINISH) atomicAdd(&a.loc[0].it->exited, 1u);
+  } else {
+    const uint32_t tid = threadIdx.x - 32;
+    for (uint32_t b = 0;; b ^= 1) {
+      bar_sync(BAR_FULL(b), nthr);
+      const Job& j = slots[b];
+      if (j.kind == JOB_EXIT) break;
+      run_job(a, j, tid, movers);
+      bar_arrive(BAR_EMPTY(b), nthr);
+    }
   }
-  if (phase) *(volatile uint32_t*)phase = (a.k << 24) | (5u << 20);
-  if (threadIdx.x == 0 && a.mode == P3_COMM_FINISH) atomicAdd(&a.loc[0].it->exited, 1u);
 }
 
 // With lazy module loading (CUDA_MODULE_LOADING=LAZY, the CUDA 12 default) the first launch
