@@ -41,6 +41,11 @@ __device__ __forceinline__ uint32_t ld_relaxed_gpu(const uint32_t* p) {
   asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+__device__ __forceinline__ uint32_t ld_relaxed_sys(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
 __device__ __forceinline__ uint64_t ld_relaxed_gpu64(const uint64_t* p) {
   uint64_t v;
   asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
@@ -329,7 +334,7 @@ __device__ uint32_t warp_pop(const QueueView& q, uint32_t tag, uint32_t* dbg = n
       for (uint32_t c = 0; c < 32; ++c) {
         const uint32_t l = group + 32 * c + lane;
         if (l >= q.n_layers) break;
-        const bool ok = (int32_t)(ld_acquire_gpu(q.ready + l) - tag) >= 0 &&
+        const bool ok = (int32_t)(ld_relaxed_gpu(q.ready + l) - tag) >= 0 &&
                         ld_relaxed_gpu(q.cursor + l) < q.nslices[l];
         bits |= (uint32_t)ok << c;
       }
@@ -353,7 +358,7 @@ __device__ uint32_t warp_pop(const QueueView& q, uint32_t tag, uint32_t* dbg = n
     if (dbg && lane == 0) *(volatile uint32_t*)dbg = (6u << 20) | (retry & 0xfffff);
     uint32_t best_key = P3_NONE, best_l = P3_NONE;
     for (uint32_t l = lane; l < q.n_layers; l += 32) {
-      const uint32_t r = ld_acquire_gpu(q.ready + l);
+      const uint32_t r = ld_relaxed_gpu(q.ready + l);
       if ((int32_t)(r - tag) < 0) continue;
       if (ld_relaxed_gpu(q.cursor + l) >= q.nslices[l]) continue;
       const uint32_t key = ld_relaxed_gpu(q.fifo_key + l);
@@ -416,7 +421,7 @@ __device__ uint32_t warp_server_pick(const CommArgs& a, const LocalDev& L, uint3
       const uint32_t oc = lcount[l];
       bool ok = false;
       if (oc) {
-        const uint32_t completed = ld_acquire_sys(hint + l) - k * oc;
+        const uint32_t completed = ld_relaxed_sys(hint + l) - k * oc;
         ok = (int32_t)(completed - ld_relaxed_gpu(L.srv_taken + l)) > 0;
       }
       bits |= (uint32_t)ok << c;
@@ -442,7 +447,7 @@ __device__ uint32_t warp_server_pick(const CommArgs& a, const LocalDev& L, uint3
           if (i < cnt) {
             g = P.own_list[lf + i];
             claimed = ld_relaxed_gpu(L.claim + g) != k;
-            ok = !claimed && (int32_t)(ld_acquire_sys(arrivals + g) - need) >= 0;
+            ok = !claimed && (int32_t)(ld_relaxed_sys(arrivals + g) - need) >= 0;
           }
           if (__all_sync(FULL_MASK, claimed) && lane == 0) atomicMax(L.srv_lo + l, i0 + 32);
           uint32_t m = __ballot_sync(FULL_MASK, ok);
@@ -541,26 +546,38 @@ __device__ __forceinline__ void bar_arrive(uint32_t id, uint32_t n) {
   asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 
-// Scheduler side of a push. With job == nullptr: if the owner is this rank, its
-// contribution stays in place — count the arrival here and return false (no data to move).
-// With a slot: fill it for the movers, who store the slice into the owner's receive slot
-// over NVLink.
-__device__ bool prepare_push(const CommArgs& a, uint32_t li, uint32_t g, Job* job) {
+// Scheduler side of a push. With job == nullptr, classify the popped slice: a remote
+// owner needs the movers (PUSH_REMOTE); for a local owner the contribution stays in place
+// and only the arrival is counted here — and when that arrival completes the slice the
+// scheduler claims its reduction at once (PUSH_REDUCE) instead of leaving it to a later
+// server pick. With a slot: fill it for the movers, who store the slice into the owner's
+// receive slot over NVLink.
+#define PUSH_DONE 0
+#define PUSH_REMOTE 1
+#define PUSH_REDUCE 2
+__device__ uint32_t prepare_push(const CommArgs& a, uint32_t li, uint32_t g, Job* job) {
   const PlanDev& P = a.plan;
   const LocalDev& L = a.loc[li];
   const uint32_t r = L.rank, o = P.slice_owner[g], l = P.slice_layer[g];
   const uint32_t lane = threadIdx.x & 31;
   if (!job) {
+    uint32_t verdict = o == r ? PUSH_DONE : PUSH_REMOTE;
     if (lane == 0) {
       (void)ld_acquire_gpu(L.ready + l);  // the gradient is published: visible from here on
       trace_append(L, a.k, l, g - P.layer_first[l], r, P3_EV_PUSH);
       if (o == r) {
         const uint32_t old = atom_add_release_sys(a.peers.arrivals[o] + g, 1u);
-        if (old + 1 == (a.k + 1) * P.world) red_add_release_sys(a.peers.hint[o] + l, 1u);
+        if (old + 1 == (a.k + 1) * P.world) {
+          red_add_release_sys(a.peers.hint[o] + l, 1u);
+          if (atomicCAS(L.claim + g, a.k, a.k + 1) == a.k) {
+            atomicAdd(L.srv_taken + l, 1u);
+            atomicAdd(&L.it->reduced, 1u);
+            verdict = PUSH_REDUCE;
+          }
+        }
       }
     }
-    __syncwarp();
-    return o != r;
+    return __shfl_sync(FULL_MASK, verdict, 0);
   }
   if (lane == 0) {
     job->kind = JOB_PUSH;
@@ -572,7 +589,7 @@ __device__ bool prepare_push(const CommArgs& a, uint32_t li, uint32_t g, Job* jo
     job->src[0] = reinterpret_cast<const float*>(ld_relaxed_gpu64(L.gptr + l)) + P.slice_off[g];
     job->dst[0] = a.peers.R[o] + (uint64_t)r * P.own_stride[o] + P.slice_slot[g];
   }
-  return true;
+  return PUSH_REMOTE;
 }
 
 // Scheduler side of a reduce: contributions of every rank (the owner's own straight from
@@ -712,7 +729,11 @@ __global__ void __launch_bounds__(512, 1) k_comm(const __grid_constant__ CommArg
         kind = JOB_EXIT;
       }
       backoff = 0;
-      if (kind == JOB_PUSH && !prepare_push(a, li, g, nullptr)) continue;  // own slice: counted in place
+      if (kind == JOB_PUSH) {
+        const uint32_t how = prepare_push(a, li, g, nullptr);
+        if (how == PUSH_DONE) continue;  // own slice, still waiting for peers: counted in place
+        if (how == PUSH_REDUCE) kind = JOB_REDUCE;  // own slice completed it: reduce right away
+      }
       if (pending[b]) bar_sync(BAR_EMPTY(b), nthr);  // movers are done with this slot
       if (kind == JOB_PUSH) {
         prepare_push(a, li, g, &slots[b]);

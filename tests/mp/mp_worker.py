@@ -1,0 +1,88 @@
+"""Multi-process P3 check, one process per GPU (launched by tests/test_multigpu.py under
+torchrun). Emulate-mode digests vs the reference goldens, then torch-mode training parity."""
+
+import json
+import os
+import sys
+from pathlib import Path
+
+REPO = Path(__file__).resolve().parents[2]
+sys.path.insert(0, str(REPO))
+
+import torch
+import torch.distributed as dist
+
+
+def main():
+    rank = int(os.environ["RANK"])
+    world = int(os.environ["WORLD_SIZE"])
+    torch.cuda.set_device(int(os.environ["LOCAL_RANK"]))
+    dist.init_process_group("nccl", device_id=torch.device("cuda", int(os.environ["LOCAL_RANK"])))
+    golden = json.loads((REPO / "tests" / "golden" / "golden.json").read_text())
+    out = {"rank": rank, "world": world, "digests": {}, "errors": []}
+
+    from paper_1905_03960_b200.model import builtin_profile
+    from paper_1905_03960_b200.runtime import SyncContext, TrainingWorker, WorkerConfig
+
+    want = {(d[0], d[1], d[4]): d[5] for d in golden["digests"] if d[2] in (10, 4)}
+    for name in ("toy3", "resnet50-like", "vgg19-like", "sockeye-like"):
+        for kind, iters in (("same", 10), ("distinct", 4)):
+            if (name, world, kind) not in want:
+                continue
+            prof = builtin_profile(name)
+            cfg = WorkerConfig(rank=rank, mode="p3", world=world, iterations=iters, deadlock_timeout=60.0,
+                               emulate_compute=kind == "same", comm_ctas=16, rank_distinct_grads=kind == "distinct",
+                               trace_cap=20_000)
+            ctx = SyncContext(prof.param_counts(), world, [rank], lr=cfg.lr, comm_ctas=16, timeout_s=60.0,
+                              emulate_grads=True, trace_cap=20_000)
+            hs = [None] * world
+            dist.all_gather_object(hs, ctx.ipc_handle(0))
+            ctx.open_peers(hs)
+            dist.barrier()
+            w = TrainingWorker(cfg, prof, ranks=[rank], ctx=ctx)
+            try:
+                w.run()
+                got = f"{w.params_digest(0):016x}"
+            except Exception as e:  # noqa: BLE001
+                got = f"error: {e}"
+            out["digests"][f"{name}/{kind}"] = [got, want[(name, world, kind)]]
+            dist.barrier()
+            w.close()
+
+    # torch mode: identical data on every rank -> mean gradient == local gradient, so the
+    # result must equal single-GPU fp32 SGD bit for bit
+    from paper_1905_03960_b200.ddp import LayerwiseDataParallel, P3DataParallel
+
+    def mlp():
+        torch.manual_seed(0)
+        return torch.nn.Sequential(torch.nn.Linear(64, 300), torch.nn.ReLU(), torch.nn.Linear(300, 233),
+                                   torch.nn.ReLU(), torch.nn.Linear(233, 10)).cuda()
+
+    lr = 0.05
+    ref, mod, mod2 = mlp(), mlp(), mlp()
+    ddp = P3DataParallel(mod, lr=lr, max_slice=1000, comm_ctas=4)
+    lw = LayerwiseDataParallel(mod2, lr=lr)
+    g = torch.Generator(device="cuda").manual_seed(1)
+    for it in range(5):
+        x = torch.randn(32, 64, device="cuda", generator=g)
+        y = torch.randint(0, 10, (32,), device="cuda", generator=g)
+        torch.nn.functional.cross_entropy(ddp(x), y).backward()
+        torch.nn.functional.cross_entropy(lw(x), y).backward()
+        torch.nn.functional.cross_entropy(ref(x), y).backward()
+        with torch.no_grad():
+            for p in ref.parameters():
+                p.sub_(p.grad.mul(lr))
+                p.grad = None
+    ddp.synchronize()
+    lw.synchronize()
+    out["torch_p3_exact"] = all(torch.equal(a, b) for a, b in zip(mod.parameters(), ref.parameters()))
+    out["torch_layerwise_close"] = all(torch.allclose(a, b, atol=1e-5) for a, b in zip(mod2.parameters(), ref.parameters()))
+    ddp.close()
+    lw.close()
+    print("MPRESULT " + json.dumps(out), flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

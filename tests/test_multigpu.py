@@ -1,0 +1,37 @@
+"""Multi-GPU P3 over NVLink (CUDA IPC peer arenas), one process per GPU under torchrun.
+Skipped when fewer than two GPUs are visible."""
+
+import json
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+import pytest
+
+REPO = Path(__file__).resolve().parents[1]
+
+pytestmark = [pytest.mark.gpu, pytest.mark.multigpu]
+
+
+def _ngpu() -> int:
+    import torch
+
+    return torch.cuda.device_count()
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_multiprocess_parity(world):
+    if _ngpu() < world:
+        pytest.skip(f"needs {world} GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+           "--master-addr", "127.0.0.1", "--master-port", str(29500 + world), str(REPO / "tests" / "mp" / "mp_worker.py")]
+    p = subprocess.run(cmd, capture_output=True, text=True, timeout=900)
+    results = [json.loads(l.split("MPRESULT ", 1)[1]) for l in p.stdout.splitlines() if "MPRESULT " in l]
+    assert p.returncode == 0, p.stdout[-3000:] + p.stderr[-3000:]
+    assert len(results) == world
+    for r in results:
+        for k, (got, want) in r["digests"].items():
+            assert got == want, (r["rank"], k, got, want)
+        assert r["torch_p3_exact"], r
+        assert r["torch_layerwise_close"], r
