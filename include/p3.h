@@ -145,6 +145,9 @@ typedef struct p3_config {
   double timeout_s;                    /* device spin deadline (deadlock_timeout) */
   uint32_t trace_cap;                  /* trace records per local rank (0 = off) */
   uint32_t emulate_grads;              /* allocate a gradient arena for gradgen mode */
+  uint64_t drain_bytes;                /* launch a DRAIN comm kernel once this many gradient
+                                          bytes were published since the last one (0: on
+                                          every publication) */
 } p3_config_t;
 
 /* Builds the plan, allocates per-local-rank arenas (parameters W zero-initialised like

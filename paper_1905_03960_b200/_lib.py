@@ -68,6 +68,7 @@ class Config(ctypes.Structure):
         ("timeout_s", ctypes.c_double),
         ("trace_cap", ctypes.c_uint32),
         ("emulate_grads", ctypes.c_uint32),
+        ("drain_bytes", ctypes.c_uint64),
     ]
 
 

@@ -78,7 +78,7 @@ struct PeerLayout {
 // Local arena of one rank. The per-iteration part (cursor | srv_lo | srv_taken | it) is
 // contiguous so one memset resets it before each launch.
 struct LocalLayout {
-  uint64_t ready, fifo_key, gptr, claim, iter_begin, cursor, srv_lo, srv_taken, it, iter_end, V, bytes,
+  uint64_t pub, fifo_key, claim, iter_begin, cursor, srv_lo, srv_taken, it, iter_end, V, bytes,
       trace_n, trace, cta_phase, total;
 };
 
@@ -114,6 +114,7 @@ struct p3_ctx {
   uint64_t open_iter = 0;
   bool iter_open = false;
   uint64_t launches = 0;
+  uint64_t published[P3_MAX_LOCAL]{};  // gradient bytes published since the last DRAIN launch
   bool comm_pending = false;
   uint64_t synced_iterations = 0;
   std::string err;
@@ -161,9 +162,8 @@ LocalLayout local_layout_of(const p3_ctx* c, uint64_t v_elems) {
     field = o;
     o = align_up(o + bytes, 256);
   };
-  take(q.ready, c->L * 4ull);
+  take(q.pub, c->L * 8ull);
   take(q.fifo_key, c->L * 4ull);
-  take(q.gptr, c->L * 8ull);
   take(q.claim, c->S * 4ull);
   q.iter_begin = o;
   take(q.cursor, c->L * 4ull);
@@ -383,9 +383,8 @@ int p3_ctx_create(const p3_config_t* cfg, p3_ctx_t** out) {
     LocalDev& D = c->loc[i];
     D.rank = rank;
     D.trace_cap = cfg->trace_cap;
-    D.ready = reinterpret_cast<uint32_t*>(lb + ll.ready);
+    D.pub = reinterpret_cast<uint64_t*>(lb + ll.pub);
     D.fifo_key = reinterpret_cast<uint32_t*>(lb + ll.fifo_key);
-    D.gptr = reinterpret_cast<uint64_t*>(lb + ll.gptr);
     D.claim = reinterpret_cast<uint32_t*>(lb + ll.claim);
     D.cursor = reinterpret_cast<uint32_t*>(lb + ll.cursor);
     D.srv_lo = reinterpret_cast<uint32_t*>(lb + ll.srv_lo);
@@ -534,23 +533,29 @@ int p3_layer_ready(p3_ctx_t* c, uint32_t li, uint32_t layer, uint64_t k, const f
     if (!c->grads[li]) return fail(c, P3_EUSAGE, "no gradient pointer and no gradient arena");
     grad = c->grads[li] + c->layer_woff[layer];
   }
+  const uint64_t gp = (uint64_t)(uintptr_t)grad;
+  if (gp >> 48) return fail(c, P3_EUSAGE, "gradient pointer does not fit the 48-bit publication word");
   Driver& d = driver();
   const LocalDev& D = c->loc[li];
   CUstream s = (CUstream)stream;
-  CUresult r = d.write32(s, (CUdeviceptr)(D.fifo_key + layer), c->fifo_seq[li]++, 0);
-  const uint64_t gp = (uint64_t)(uintptr_t)grad;
+  CUresult r = CUDA_SUCCESS;
+  if (c->cfg.sched == P3_SCHED_FIFO) r = d.write32(s, (CUdeviceptr)(D.fifo_key + layer), c->fifo_seq[li]++, 0);
+  // one stream-ordered write publishes the slices of the layer (FrameQueue.put_batch is
+  // atomic, queues.py:44-50): the iteration tag and the gradient pointer in one word
+  const uint64_t word = (((k + 1) & 0xffffull) << 48) | gp;
   if (r == CUDA_SUCCESS) {
     if (d.has64) {
-      r = d.write64(s, (CUdeviceptr)(D.gptr + layer), gp, 0);
-    } else {
-      r = d.write32(s, (CUdeviceptr)(D.gptr + layer), (cuuint32_t)(gp & 0xffffffffu), 0);
-      if (r == CUDA_SUCCESS) r = d.write32(s, (CUdeviceptr)(D.gptr + layer) + 4, (cuuint32_t)(gp >> 32), 0);
+      r = d.write64(s, (CUdeviceptr)(D.pub + layer), word, 0);
+    } else {  // low half (pointer) first, then the half holding the tag
+      r = d.write32(s, (CUdeviceptr)(D.pub + layer), (cuuint32_t)(word & 0xffffffffu), 0);
+      if (r == CUDA_SUCCESS) r = d.write32(s, (CUdeviceptr)(D.pub + layer) + 4, (cuuint32_t)(word >> 32), 0);
     }
   }
-  if (r == CUDA_SUCCESS) r = d.write32(s, (CUdeviceptr)(D.ready + layer), (cuuint32_t)(k + 1), 0);
   if (r != CUDA_SUCCESS) return fail(c, P3_ECUDA, "cuStreamWriteValue failed (code " + std::to_string(r) + ")");
-  if (c->iter_open && c->open_iter == k) {
+  c->published[li] += 4ull * c->counts[layer];
+  if (c->iter_open && c->open_iter == k && c->published[li] >= c->cfg.drain_bytes) {
     // the comm stream follows this publication point, then drains what is published
+    c->published[li] = 0;
     CK(cudaEventRecord(c->ready_ev[li], (cudaStream_t)stream));
     CK(cudaStreamWaitEvent(c->comm_stream, c->ready_ev[li], 0));
     if (launch_comm(comm_args(c, P3_COMM_DRAIN), c->cfg.comm_ctas, c->cfg.comm_threads, c->comm_stream) != P3_OK)
@@ -603,11 +608,11 @@ int p3_sync_all(p3_ctx_t* c, uint64_t k, double timeout_s) {
     std::string m = "comm kernel of iteration " + std::to_string(ew[1]) +
                     " stalled (timeout waiting for peers or gradients);";
     for (uint32_t i = 0; i < c->cfg.n_local; ++i) {
-      std::vector<uint32_t> ready(c->L);
-      cudaMemcpyAsync(ready.data(), c->loc[i].ready, c->L * 4ull, cudaMemcpyDeviceToHost, c->poll_stream);
+      std::vector<uint64_t> pub(c->L);
+      cudaMemcpyAsync(pub.data(), c->loc[i].pub, c->L * 8ull, cudaMemcpyDeviceToHost, c->poll_stream);
       cudaStreamSynchronize(c->poll_stream);
       uint32_t nready = 0;
-      for (uint32_t l = 0; l < c->L; ++l) nready += ready[l] > ew[1];
+      for (uint32_t l = 0; l < c->L; ++l) nready += (uint32_t)(pub[l] >> 48) == ((ew[1] + 1) & 0xffffu);
       m += " rank " + std::to_string(c->cfg.local_ranks[i]) + ": pushed " + std::to_string(ew[2 + 2 * i]) + "/" +
            std::to_string(c->S) + " reduced " + std::to_string(ew[3 + 2 * i]) + "/" +
            std::to_string(c->own_total[c->cfg.local_ranks[i]]) + " ready layers " + std::to_string(nready) + "/" +
@@ -688,12 +693,15 @@ int p3_debug_snapshot(p3_ctx_t* c, uint32_t li, uint32_t* out, uint64_t cap, uin
   if (cap < n) return fail(c, P3_EUSAGE, "snapshot buffer too small");
   const LocalDev& D = c->loc[li];
   const uint32_t rank = c->cfg.local_ranks[li];
-  const uint32_t* src[5] = {D.ready, D.cursor, D.srv_taken, c->peers.hint[rank], c->peers.done[rank]};
-  for (int a = 0; a < 5; ++a)
+  const uint32_t* src[5] = {nullptr, D.cursor, D.srv_taken, c->peers.hint[rank], c->peers.done[rank]};
+  for (int a = 1; a < 5; ++a)
     CK(cudaMemcpyAsync(out + (uint64_t)a * c->L, src[a], c->L * 4ull, cudaMemcpyDeviceToHost, c->poll_stream));
+  std::vector<uint64_t> pub(c->L);
+  CK(cudaMemcpyAsync(pub.data(), D.pub, c->L * 8ull, cudaMemcpyDeviceToHost, c->poll_stream));
   CK(cudaMemcpyAsync(out + 5ull * c->L, D.it, 16, cudaMemcpyDeviceToHost, c->poll_stream));
   CK(cudaMemcpyAsync(out + 5ull * c->L + 4, D.cta_phase, P3_DBG_CTAS * 4ull, cudaMemcpyDeviceToHost, c->poll_stream));
   CK(cudaStreamSynchronize(c->poll_stream));
+  for (uint32_t l = 0; l < c->L; ++l) out[l] = (uint32_t)(pub[l] >> 48);  // iteration tag
   return P3_OK;
 }
 
@@ -702,8 +710,9 @@ int p3_debug_snapshot(p3_ctx_t* c, uint32_t li, uint32_t* out, uint64_t cap, uin
 struct p3_queue {
   uint32_t L = 0, sched = 0, tag = 0, seq = 0;
   std::vector<uint32_t> nslices;
-  char* d = nullptr;  // nslices | first | ready | fifo_key | cursor | result
-  uint32_t *d_nslices, *d_first, *d_ready, *d_fifo, *d_cursor, *d_result;
+  char* d = nullptr;  // nslices | first | pub | fifo_key | cursor | result
+  uint32_t *d_nslices, *d_first, *d_fifo, *d_cursor, *d_result;
+  uint64_t* d_pub;
   cudaStream_t s = nullptr;
 };
 
@@ -722,12 +731,12 @@ int p3_queue_create(const uint32_t* layer_nslices, uint32_t n_layers, uint32_t s
     first[l] = (uint32_t)f;
     f += layer_nslices[l];
   }
-  const size_t stride = align_up(n_layers * 4ull, 256);
+  const size_t stride = align_up(n_layers * 8ull, 256);
   cudaError_t e = cudaMalloc(&q->d, stride * 6);
   if (e == cudaSuccess) e = cudaMemset(q->d, 0, stride * 6);
   q->d_nslices = reinterpret_cast<uint32_t*>(q->d);
   q->d_first = reinterpret_cast<uint32_t*>(q->d + stride);
-  q->d_ready = reinterpret_cast<uint32_t*>(q->d + 2 * stride);
+  q->d_pub = reinterpret_cast<uint64_t*>(q->d + 2 * stride);
   q->d_fifo = reinterpret_cast<uint32_t*>(q->d + 3 * stride);
   q->d_cursor = reinterpret_cast<uint32_t*>(q->d + 4 * stride);
   q->d_result = reinterpret_cast<uint32_t*>(q->d + 5 * stride);
@@ -746,9 +755,10 @@ int p3_queue_put_layer(p3_queue_t* q, uint32_t layer, uint32_t iteration) {
   p3_ctx* c = nullptr;
   if (!q || layer >= q->L) return fail(nullptr, P3_EUSAGE, "layer out of range");
   const uint32_t tag = iteration + 1, zero = 0, key = q->seq++;
+  const uint64_t word = ((uint64_t)(tag & 0xffffu)) << 48;
   CK(cudaMemcpyAsync(q->d_cursor + layer, &zero, 4, cudaMemcpyHostToDevice, q->s));
   CK(cudaMemcpyAsync(q->d_fifo + layer, &key, 4, cudaMemcpyHostToDevice, q->s));
-  CK(cudaMemcpyAsync(q->d_ready + layer, &tag, 4, cudaMemcpyHostToDevice, q->s));
+  CK(cudaMemcpyAsync(q->d_pub + layer, &word, 8, cudaMemcpyHostToDevice, q->s));
   CK(cudaStreamSynchronize(q->s));
   q->tag = std::max(q->tag, tag);
   return P3_OK;
@@ -758,7 +768,7 @@ int p3_queue_poll(p3_queue_t* q, uint32_t* layer, uint32_t* slice) {
   p3_ctx* c = nullptr;
   if (!q) return fail(nullptr, P3_EUSAGE, "null queue");
   if (q->tag == 0) return P3_ETIMEOUT;
-  if (launch_queue_pop(q->d_nslices, q->d_first, q->d_ready, q->d_fifo, q->d_cursor, q->L, q->sched, q->tag,
+  if (launch_queue_pop(q->d_nslices, q->d_first, q->d_pub, q->d_fifo, q->d_cursor, q->L, q->sched, q->tag,
                        q->d_result, q->s) != P3_OK)
     return cuda_fail(c, cudaGetLastError(), "queue pop launch");
   uint32_t g = 0;

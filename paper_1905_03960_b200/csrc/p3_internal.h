@@ -68,9 +68,8 @@ struct IterState {
 struct LocalDev {
   uint32_t rank;
   uint32_t trace_cap;
-  uint32_t* ready;      // [L] iteration tag k+1 once the layer's gradient is published
+  uint64_t* pub;        // [L] (iteration tag (k+1) & 0xffff) << 48 | gradient pointer
   uint32_t* fifo_key;   // [L] publish sequence (FIFO discipline)
-  uint64_t* gptr;       // [L] gradient pointer of the layer
   uint32_t* claim;      // [S] server claim tag (monotone: k -> k+1)
   uint32_t* cursor;     // [L] worker claim cursor (per iteration)
   uint32_t* srv_lo;     // [L] server scan watermark (per iteration)
@@ -103,7 +102,7 @@ int preload_kernels();
 int launch_comm(const CommArgs& a, uint32_t ctas, uint32_t threads, void* stream);
 int launch_gradgen(uint64_t seed, uint64_t iteration, uint64_t layer, uint64_t start, uint64_t count,
                    float* out, void* stream);
-int launch_queue_pop(const uint32_t* nslices, const uint32_t* first, const uint32_t* ready,
+int launch_queue_pop(const uint32_t* nslices, const uint32_t* first, const uint64_t* pub,
                      const uint32_t* fifo_key, uint32_t* cursor, uint32_t n_layers, uint32_t sched,
                      uint32_t tag, uint32_t* result, void* stream);
 

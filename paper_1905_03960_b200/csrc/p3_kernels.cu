@@ -46,6 +46,11 @@ __device__ __forceinline__ uint32_t ld_relaxed_sys(const uint32_t* p) {
   asm volatile("ld.relaxed.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+__device__ __forceinline__ uint64_t ld_acquire_gpu64(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
 __device__ __forceinline__ uint64_t ld_relaxed_gpu64(const uint64_t* p) {
   uint64_t v;
   asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
@@ -305,7 +310,8 @@ __global__ void k_sleep(uint64_t ns) {
 
 // ------------------------------------------------------------------ device slice queue
 
-// The outbox of one worker: per layer an iteration tag (ready), a publish sequence
+// The outbox of one worker: per layer a publication word (iteration tag in the top 16 bits,
+// gradient pointer below, written by one stream memory write), a publish sequence
 // (fifo_key) and a claim cursor. The minimum under the FrameQueue order is the lowest ready
 // layer with unclaimed slices (priority == layer index, plan.py:112, ties by slice index
 // through the ascending cursor), or the earliest-published such layer in FIFO mode.
@@ -314,10 +320,15 @@ struct QueueView {
   uint32_t sched;
   const uint32_t* nslices;
   const uint32_t* first;
-  const uint32_t* ready;
+  const uint64_t* pub;
   const uint32_t* fifo_key;
   uint32_t* cursor;
 };
+
+__device__ __forceinline__ bool pub_ready(uint64_t w, uint32_t tag) { return (uint32_t)(w >> 48) == (tag & 0xffffu); }
+__device__ __forceinline__ const float* pub_ptr(uint64_t w) {
+  return reinterpret_cast<const float*>(w & 0x0000ffffffffffffull);
+}
 
 // Executed by one full warp; returns the popped global slice id or P3_NONE.
 // Priority discipline: layers are examined in ascending order 32 at a time (lane i owns
@@ -334,8 +345,7 @@ __device__ uint32_t warp_pop(const QueueView& q, uint32_t tag, uint32_t* dbg = n
       for (uint32_t c = 0; c < 32; ++c) {
         const uint32_t l = group + 32 * c + lane;
         if (l >= q.n_layers) break;
-        const bool ok = (int32_t)(ld_relaxed_gpu(q.ready + l) - tag) >= 0 &&
-                        ld_relaxed_gpu(q.cursor + l) < q.nslices[l];
+        const bool ok = pub_ready(ld_relaxed_gpu64(q.pub + l), tag) && ld_relaxed_gpu(q.cursor + l) < q.nslices[l];
         bits |= (uint32_t)ok << c;
       }
       const uint32_t nchunk = min(32u, (q.n_layers - group + 31) / 32);
@@ -358,8 +368,7 @@ __device__ uint32_t warp_pop(const QueueView& q, uint32_t tag, uint32_t* dbg = n
     if (dbg && lane == 0) *(volatile uint32_t*)dbg = (6u << 20) | (retry & 0xfffff);
     uint32_t best_key = P3_NONE, best_l = P3_NONE;
     for (uint32_t l = lane; l < q.n_layers; l += 32) {
-      const uint32_t r = ld_relaxed_gpu(q.ready + l);
-      if ((int32_t)(r - tag) < 0) continue;
+      if (!pub_ready(ld_relaxed_gpu64(q.pub + l), tag)) continue;
       if (ld_relaxed_gpu(q.cursor + l) >= q.nslices[l]) continue;
       const uint32_t key = ld_relaxed_gpu(q.fifo_key + l);
       if (key < best_key || (key == best_key && l < best_l)) {
@@ -390,10 +399,10 @@ __global__ void k_queue_pop(QueueView q, uint32_t tag, uint32_t* result) {
   if (threadIdx.x == 0) *result = g;
 }
 
-int launch_queue_pop(const uint32_t* nslices, const uint32_t* first, const uint32_t* ready,
+int launch_queue_pop(const uint32_t* nslices, const uint32_t* first, const uint64_t* pub,
                      const uint32_t* fifo_key, uint32_t* cursor, uint32_t n_layers, uint32_t sched,
                      uint32_t tag, uint32_t* result, void* stream) {
-  QueueView q{n_layers, sched, nslices, first, ready, fifo_key, cursor};
+  QueueView q{n_layers, sched, nslices, first, pub, fifo_key, cursor};
   k_queue_pop<<<1, 32, 0, (cudaStream_t)stream>>>(q, tag, result);
   return cudaGetLastError() == cudaSuccess ? P3_OK : P3_ECUDA;
 }
@@ -516,7 +525,7 @@ __device__ __forceinline__ QueueView queue_of(const CommArgs& a, const LocalDev&
   q.sched = a.sched;
   q.nslices = a.plan.layer_nslices;
   q.first = a.plan.layer_first;
-  q.ready = L.ready;
+  q.pub = L.pub;
   q.fifo_key = L.fifo_key;
   q.cursor = L.cursor;
   return q;
@@ -563,7 +572,7 @@ __device__ uint32_t prepare_push(const CommArgs& a, uint32_t li, uint32_t g, Job
   if (!job) {
     uint32_t verdict = o == r ? PUSH_DONE : PUSH_REMOTE;
     if (lane == 0) {
-      (void)ld_acquire_gpu(L.ready + l);  // the gradient is published: visible from here on
+      (void)ld_acquire_gpu64(L.pub + l);  // the gradient is published: visible from here on
       trace_append(L, a.k, l, g - P.layer_first[l], r, P3_EV_PUSH);
       if (o == r) {
         const uint32_t old = atom_add_release_sys(a.peers.arrivals[o] + g, 1u);
@@ -586,7 +595,7 @@ __device__ uint32_t prepare_push(const CommArgs& a, uint32_t li, uint32_t g, Job
     job->layer = l;
     job->rank = o;
     job->len = P.slice_len[g];
-    job->src[0] = reinterpret_cast<const float*>(ld_relaxed_gpu64(L.gptr + l)) + P.slice_off[g];
+    job->src[0] = pub_ptr(ld_relaxed_gpu64(L.pub + l)) + P.slice_off[g];
     job->dst[0] = a.peers.R[o] + (uint64_t)r * P.own_stride[o] + P.slice_slot[g];
   }
   return PUSH_REMOTE;
@@ -604,7 +613,7 @@ __device__ void prepare_reduce(const CommArgs& a, uint32_t li, uint32_t g, Job* 
   __syncwarp();
   uintptr_t al = 0;
   if (q < N) {
-    const float* src = q == o ? reinterpret_cast<const float*>(ld_relaxed_gpu64(L.gptr + l)) + P.slice_off[g]
+    const float* src = q == o ? pub_ptr(ld_relaxed_gpu64(L.pub + l)) + P.slice_off[g]
                               : a.peers.R[o] + (uint64_t)q * P.own_stride[o] + P.slice_slot[g];
     float* dst = a.peers.W[q] + woff;
     job->src[q] = src;

@@ -124,6 +124,7 @@ class P3DataParallel(_HookedDataParallel):
         timeout_s: float = 120.0,
         trace_cap: int = 0,
         priority_mode: bool = True,
+        drain_bytes: int = 4 << 20,
     ) -> None:
         super().__init__(module)
         self.lr = lr
@@ -131,7 +132,7 @@ class P3DataParallel(_HookedDataParallel):
         self.ctx = SyncContext(
             counts, self.world, [self.rank], max_slice=max_slice, lr=lr, momentum=momentum,
             priority_mode=priority_mode, comm_ctas=comm_ctas, comm_threads=comm_threads,
-            timeout_s=timeout_s, trace_cap=trace_cap,
+            timeout_s=timeout_s, trace_cap=trace_cap, drain_bytes=drain_bytes,
         )
         if self.world > 1:
             handles = [None] * self.world

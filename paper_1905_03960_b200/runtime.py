@@ -62,6 +62,7 @@ class SyncContext:
         timeout_s: float = 60.0,
         trace_cap: int = 0,
         emulate_grads: bool = False,
+        drain_bytes: int = 0,
     ) -> None:
         import torch
 
@@ -92,6 +93,7 @@ class SyncContext:
         cfg.timeout_s = timeout_s
         cfg.trace_cap = trace_cap
         cfg.emulate_grads = 1 if emulate_grads else 0
+        cfg.drain_bytes = drain_bytes
         h = ctypes.c_void_p()
         _lib.check(self.lib.p3_ctx_create(ctypes.byref(cfg), ctypes.byref(h)), what="p3_ctx_create")
         self._h = h
