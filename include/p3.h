@@ -136,7 +136,8 @@ typedef struct p3_config {
   uint32_t n_layers;
   const uint64_t* layer_counts;        /* LayerSpec.param_count per layer */
   uint64_t max_slice;                  /* make_p3_plan max_slice (plan.py:22) */
-  uint32_t plan_mode;                  /* P3_PLAN_P3 (baseline plan: future) */
+  uint32_t plan_mode;                  /* P3_PLAN_P3 or P3_PLAN_BASELINE (KVStore layer-wise
+                                          placement, plan.py:122-164) */
   uint32_t sched;                      /* P3_SCHED_PRIORITY (p3) or P3_SCHED_FIFO */
   float lr;                            /* RunConfig.lr (cli.py:69) */
   float momentum;                      /* 0 == the reference's plain SGD */
@@ -148,6 +149,11 @@ typedef struct p3_config {
   uint64_t drain_bytes;                /* launch a DRAIN comm kernel once this many gradient
                                           bytes were published since the last one (0: on
                                           every publication) */
+  uint64_t big_threshold;              /* baseline plan: layers >= this are split N ways */
+  uint64_t rng_seed;                   /* baseline plan: placement seed of small layers */
+  double throttle_bps;                 /* K7 link emulation: per-rank egress rate in bit/s
+                                          (TokenBucket, transport.py:22-55); 0 = full NVLink */
+  uint64_t throttle_burst;             /* bucket depth in bytes (transport.py:18: 50 KiB) */
 } p3_config_t;
 
 /* Builds the plan, allocates per-local-rank arenas (parameters W zero-initialised like

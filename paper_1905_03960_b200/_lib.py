@@ -69,6 +69,10 @@ class Config(ctypes.Structure):
         ("trace_cap", ctypes.c_uint32),
         ("emulate_grads", ctypes.c_uint32),
         ("drain_bytes", ctypes.c_uint64),
+        ("big_threshold", ctypes.c_uint64),
+        ("rng_seed", ctypes.c_uint64),
+        ("throttle_bps", ctypes.c_double),
+        ("throttle_burst", ctypes.c_uint64),
     ]
 
 

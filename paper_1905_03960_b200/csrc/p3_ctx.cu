@@ -79,7 +79,7 @@ struct PeerLayout {
 // contiguous so one memset resets it before each launch.
 struct LocalLayout {
   uint64_t pub, fifo_key, claim, iter_begin, cursor, srv_lo, srv_taken, it, iter_end, V, bytes,
-      trace_n, trace, cta_phase, total;
+      trace_n, trace, cta_phase, vclock, total;
 };
 
 struct p3_ctx {
@@ -176,6 +176,7 @@ LocalLayout local_layout_of(const p3_ctx* c, uint64_t v_elems) {
   take(q.trace_n, 8);
   take(q.trace, (uint64_t)c->cfg.trace_cap * sizeof(p3_trace_rec_t));
   take(q.cta_phase, P3_DBG_CTAS * 4ull);
+  take(q.vclock, 8);
   q.total = o;
   return q;
 }
@@ -224,7 +225,8 @@ int p3_ctx_create(const p3_config_t* cfg, p3_ctx_t** out) {
   if (cfg->world < 1 || cfg->world > P3_MAX_RANKS) return fail(nullptr, P3_EUSAGE, "world must be in [1, 16]");
   if (cfg->n_local < 1 || cfg->n_local > cfg->world) return fail(nullptr, P3_EUSAGE, "bad n_local");
   if (cfg->n_layers < 1 || !cfg->layer_counts) return fail(nullptr, P3_EUSAGE, "profile needs at least one layer");
-  if (cfg->plan_mode != P3_PLAN_P3) return fail(nullptr, P3_EUSAGE, "only the p3 plan runs on the comm kernel");
+  if (cfg->plan_mode != P3_PLAN_P3 && cfg->plan_mode != P3_PLAN_BASELINE) return fail(nullptr, P3_EUSAGE, "bad plan_mode");
+  if (cfg->throttle_bps < 0) return fail(nullptr, P3_EUSAGE, "throttle rate must be >= 0 (0 disables shaping)");
   if (cfg->comm_threads < 64 || cfg->comm_threads > 512 || cfg->comm_threads % 32)
     return fail(nullptr, P3_EUSAGE, "comm_threads must be a multiple of 32 in [64, 512] (one scheduler warp + movers)");
   if (cfg->comm_ctas < 1) return fail(nullptr, P3_EUSAGE, "comm_ctas must be >= 1");
@@ -240,7 +242,9 @@ int p3_ctx_create(const p3_config_t* cfg, p3_ctx_t** out) {
   c->L = cfg->n_layers;
   c->N = cfg->world;
   std::string perr;
-  int rc = build_p3_plan(c->counts.data(), c->L, c->N, cfg->max_slice, &c->plan, &perr);
+  int rc = cfg->plan_mode == P3_PLAN_P3
+               ? build_p3_plan(c->counts.data(), c->L, c->N, cfg->max_slice, &c->plan, &perr)
+               : build_baseline_plan(c->counts.data(), c->L, c->N, cfg->big_threshold, cfg->rng_seed, &c->plan, &perr);
   if (rc != P3_OK) {
     delete c;
     return fail(nullptr, rc, perr);
@@ -395,6 +399,7 @@ int p3_ctx_create(const p3_config_t* cfg, p3_ctx_t** out) {
     D.trace_n = reinterpret_cast<unsigned long long*>(lb + ll.trace_n);
     D.trace = reinterpret_cast<p3_trace_rec_t*>(lb + ll.trace);
     D.cta_phase = reinterpret_cast<uint32_t*>(lb + ll.cta_phase);
+    D.vclock = reinterpret_cast<unsigned long long*>(lb + ll.vclock);
   }
   e = cudaEventCreateWithFlags(&c->comm_done, cudaEventDisableTiming);
   for (uint32_t i = 0; i < cfg->n_local && e == cudaSuccess; ++i)
@@ -494,6 +499,10 @@ static CommArgs comm_args(p3_ctx* c, uint32_t mode) {
   a.momentum = c->cfg.momentum;
   a.timeout_ns = (unsigned long long)(c->cfg.timeout_s * 1e9);
   a.err = c->d_err;
+  if (c->cfg.throttle_bps > 0) {
+    a.ns_per_byte = (float)(8e9 / c->cfg.throttle_bps);
+    a.burst_ns = (unsigned long long)((double)c->cfg.throttle_burst * 8e9 / c->cfg.throttle_bps);
+  }
   return a;
 }
 

@@ -80,6 +80,7 @@ struct LocalDev {
   unsigned long long* trace_n;
   p3_trace_rec_t* trace;
   uint32_t* cta_phase;  // [P3_DBG_CTAS] last phase of each comm CTA (diagnostics)
+  unsigned long long* vclock;  // K7 token bucket: time (ns) at which granted bytes drain
 };
 
 struct CommArgs {
@@ -93,6 +94,8 @@ struct CommArgs {
   uint32_t sched;
   float lr;
   float momentum;
+  float ns_per_byte;  // K7 link emulation (0: unthrottled)
+  unsigned long long burst_ns;
   unsigned long long timeout_ns;
   uint32_t* err;  // device error word (P3_* code)
 };

@@ -555,6 +555,25 @@ __device__ __forceinline__ void bar_arrive(uint32_t id, uint32_t n) {
   asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 
+// K7 link emulation (TokenBucket.consume, transport.py:42-55) on %globaltimer, one bucket
+// per rank's egress: grant `bytes` at the bucket rate with `burst` of slack, and wait until
+// the grant is admissible. The bucket is a virtual clock V: a grant moves it to
+// max(V, now - burst) + bytes/rate and may start once now >= V' - burst.
+__device__ void pace(const CommArgs& a, const LocalDev& L, uint64_t bytes) {
+  if (a.ns_per_byte == 0.f || bytes == 0) return;
+  const unsigned long long cost = (unsigned long long)((double)bytes * a.ns_per_byte);
+  const unsigned long long now = globaltimer();
+  unsigned long long v = *(volatile unsigned long long*)L.vclock, d;
+  for (;;) {
+    const unsigned long long start = max(v, now - a.burst_ns);
+    d = start + cost;
+    const unsigned long long old = atomicCAS(L.vclock, v, d);
+    if (old == v) break;
+    v = old;
+  }
+  while (globaltimer() + a.burst_ns < d) __nanosleep(2000);
+}
+
 // Scheduler side of a push. With job == nullptr, classify the popped slice: a remote
 // owner needs the movers (PUSH_REMOTE); for a local owner the contribution stays in place
 // and only the arrival is counted here — and when that arrival completes the slice the
@@ -742,6 +761,11 @@ __global__ void __launch_bounds__(512, 1) k_comm(const __grid_constant__ CommArg
         const uint32_t how = prepare_push(a, li, g, nullptr);
         if (how == PUSH_DONE) continue;  // own slice, still waiting for peers: counted in place
         if (how == PUSH_REDUCE) kind = JOB_REDUCE;  // own slice completed it: reduce right away
+      }
+      if (kind == JOB_PUSH || kind == JOB_REDUCE) {  // egress bytes of this job on the rank's link
+        const uint64_t bytes = 4ull * a.plan.slice_len[g] * (kind == JOB_PUSH ? 1u : a.plan.world - 1u);
+        if (lane == 0) pace(a, a.loc[li], bytes);
+        __syncwarp();
       }
       if (pending[b]) bar_sync(BAR_EMPTY(b), nthr);  // movers are done with this slot
       if (kind == JOB_PUSH) {

@@ -125,6 +125,10 @@ class P3DataParallel(_HookedDataParallel):
         trace_cap: int = 0,
         priority_mode: bool = True,
         drain_bytes: int = 4 << 20,
+        plan_mode: str = "p3",
+        throttle_bps: float = 0.0,
+        throttle_burst: int = 50 * 1024,
+        big_threshold: int = 1_000_000,
     ) -> None:
         super().__init__(module)
         self.lr = lr
@@ -132,7 +136,8 @@ class P3DataParallel(_HookedDataParallel):
         self.ctx = SyncContext(
             counts, self.world, [self.rank], max_slice=max_slice, lr=lr, momentum=momentum,
             priority_mode=priority_mode, comm_ctas=comm_ctas, comm_threads=comm_threads,
-            timeout_s=timeout_s, trace_cap=trace_cap, drain_bytes=drain_bytes,
+            timeout_s=timeout_s, trace_cap=trace_cap, drain_bytes=drain_bytes, plan_mode=plan_mode,
+            throttle_bps=throttle_bps, throttle_burst=throttle_burst, big_threshold=big_threshold,
         )
         if self.world > 1:
             handles = [None] * self.world

@@ -24,7 +24,7 @@ import numpy as np
 from . import _lib
 from .hashing import FNV_OFFSET, fnv1a64
 from .model import ModelProfile
-from .plan import BASELINE_MODE, P3_MODE, DEFAULT_MAX_SLICE, SliceKey, make_p3_plan
+from .plan import BASELINE_MODE, P3_MODE, DEFAULT_MAX_SLICE, SliceKey, make_baseline_plan, make_p3_plan
 
 
 class _DeviceArray:
@@ -63,6 +63,11 @@ class SyncContext:
         trace_cap: int = 0,
         emulate_grads: bool = False,
         drain_bytes: int = 0,
+        plan_mode: str = "p3",
+        big_threshold: int = 1_000_000,
+        rng_seed: int = 0,
+        throttle_bps: float = 0.0,
+        throttle_burst: int = 50 * 1024,
     ) -> None:
         import torch
 
@@ -84,7 +89,13 @@ class SyncContext:
         self._counts = _lib.u64_array(self.layer_counts)
         cfg.layer_counts = ctypes.cast(self._counts, ctypes.POINTER(ctypes.c_uint64))
         cfg.max_slice = max_slice
-        cfg.plan_mode = _lib.P3_PLAN_P3
+        if plan_mode not in (P3_MODE, BASELINE_MODE):
+            raise ValueError(f"plan_mode must be {P3_MODE!r} or {BASELINE_MODE!r}")
+        cfg.plan_mode = _lib.P3_PLAN_P3 if plan_mode == P3_MODE else _lib.P3_PLAN_BASELINE
+        cfg.big_threshold = big_threshold
+        cfg.rng_seed = rng_seed
+        cfg.throttle_bps = throttle_bps or 0.0
+        cfg.throttle_burst = throttle_burst
         cfg.sched = _lib.P3_SCHED_PRIORITY if priority_mode else _lib.P3_SCHED_FIFO
         cfg.lr = lr
         cfg.momentum = momentum
@@ -103,7 +114,7 @@ class SyncContext:
             self._check(self.lib.p3_ctx_layer_offset(self._h, l, ctypes.byref(off)), "p3_ctx_layer_offset")
             self.layer_offsets.append(int(off.value))
         self.arena_elems = self.layer_offsets[-1] + self.layer_counts[-1]
-        self.slices_per_layer = [(c + max_slice - 1) // max_slice for c in self.layer_counts]
+        self.plan_mode = plan_mode
 
     # ------------------------------------------------------------------ plumbing
     def _check(self, rc: int, what: str) -> None:
@@ -242,6 +253,10 @@ class WorkerConfig:
     comm_threads: int = 512
     trace_cap: int = 0
     rank_distinct_grads: bool = False
+    throttle_rate: float | None = None  # bit/s per rank egress (worker.py:33); None = full NVLink
+    throttle_burst: int = 50 * 1024
+    big_threshold: int = 1_000_000     # baseline plan (cli.py:68)
+    seed: int = 0                      # baseline plan placement seed (cli.py:74)
 
 
 def rank_seed(seed: int, rank: int, distinct: bool) -> int:
@@ -267,12 +282,17 @@ class TrainingWorker:
     def __init__(self, config: WorkerConfig, profile: ModelProfile, ranks: list[int] | None = None, ctx: SyncContext | None = None) -> None:
         import torch
 
-        if config.mode not in (P3_MODE, "fifo"):
-            raise ValueError(f"emulate worker runs the p3 (priority) or fifo discipline, not {config.mode!r}")
+        if config.mode not in (P3_MODE, BASELINE_MODE):
+            raise ValueError(f"mode must be {P3_MODE!r} or {BASELINE_MODE!r}, not {config.mode!r}")
         self.cfg = config
         self.profile = profile
         self.ranks = list(ranks) if ranks is not None else [config.rank]
-        self.plan = make_p3_plan(profile, config.world, config.max_slice)
+        # p3: sliced plan + priority queue; baseline: KVStore placement + FIFO (the reference's
+        # two modes, worker.py:84-93, plan.py:94-164)
+        if config.mode == P3_MODE:
+            self.plan = make_p3_plan(profile, config.world, config.max_slice)
+        else:
+            self.plan = make_baseline_plan(profile, config.world, config.big_threshold, config.seed)
         self.ctx = ctx or SyncContext(
             profile.param_counts(),
             config.world,
@@ -285,6 +305,11 @@ class TrainingWorker:
             timeout_s=config.deadlock_timeout,
             trace_cap=config.trace_cap,
             emulate_grads=True,
+            plan_mode=config.mode,
+            big_threshold=config.big_threshold,
+            rng_seed=config.seed,
+            throttle_bps=config.throttle_rate or 0.0,
+            throttle_burst=config.throttle_burst,
         )
         self.comm_stream = torch.cuda.Stream()
         self.streams = [torch.cuda.Stream() for _ in self.ranks]

@@ -13,12 +13,13 @@ pytestmark = pytest.mark.gpu
 
 
 def run_emulated(profile, world, iterations, lr=0.1, distinct=False, max_slice=50_000, comm_ctas=16,
-                 emulate_compute=False, trace_cap=0, mode="p3"):
+                 emulate_compute=False, trace_cap=0, mode="p3", throttle=None, big_threshold=1_000_000):
     from paper_1905_03960_b200.runtime import TrainingWorker, WorkerConfig
 
     cfg = WorkerConfig(rank=0, mode=mode, world=world, iterations=iterations, lr=lr, max_slice=max_slice,
                        deadlock_timeout=30.0, emulate_compute=emulate_compute, comm_ctas=comm_ctas,
-                       trace_cap=trace_cap, rank_distinct_grads=distinct)
+                       trace_cap=trace_cap, rank_distinct_grads=distinct, throttle_rate=throttle,
+                       big_threshold=big_threshold)
     w = TrainingWorker(cfg, profile, ranks=list(range(world)))
     w.run()
     return w
@@ -232,3 +233,42 @@ def test_layerwise_baseline_single_gpu(cuda):
     for a, b in zip(mod.parameters(), ref.parameters()):
         assert torch.allclose(a, b, rtol=0, atol=1e-6)
     ddp.close()
+
+
+@pytest.mark.parametrize("name", ["toy3", "resnet50-like", "vgg19-like", "sockeye-like"])
+@pytest.mark.parametrize("world", [1, 2, 4])
+def test_cross_mode_bit_equality(cuda, golden, name, world):
+    # SPEC acceptance #3 / tests/test_runtime.py:115-139: the layer-wise baseline (KVStore
+    # placement, FIFO) and P3 (sliced, priority) end with bit-identical parameters
+    from paper_1905_03960_b200.model import builtin_profile
+
+    want = {(d[0], d[1]): d[5] for d in golden["digests"] if d[4] == "same" and d[2] == 10}
+    w = run_emulated(builtin_profile(name), world, 10, mode="baseline", big_threshold=100_000)
+    digests = {f"{w.params_digest(li):016x}" for li in range(world)}
+    w.close()
+    assert digests == {want[(name, world)]}
+
+
+@pytest.mark.parametrize("mode", ["p3", "baseline"])
+def test_throttled_link_rate(cuda, golden, mode):
+    # K7: per-rank egress shaped to 2 Gbit/s; the sync of an iteration cannot beat the
+    # bytes each rank must send, and the values are unchanged
+    import time
+
+    from paper_1905_03960_b200.model import builtin_profile
+    from paper_1905_03960_b200.plan import make_baseline_plan, make_p3_plan
+
+    prof = builtin_profile("resnet50-like")
+    world, iters, rate = 2, 3, 2e9
+    plan = make_p3_plan(prof, world) if mode == "p3" else make_baseline_plan(prof, world)
+    t0 = time.perf_counter()
+    w = run_emulated(prof, world, iters, mode=mode, throttle=rate, comm_ctas=4)
+    dt = time.perf_counter() - t0
+    want = {(d[0], d[1]): d[5] for d in golden["digests"] if d[4] == "same" and d[2] == 10}
+    # egress per rank per iteration: pushes of slices owned elsewhere + broadcasts of owned
+    per_rank = [4 * (sum(s.length for s in plan.slices if s.server != r) +
+                     sum(s.length for s in plan.slices if s.server == r) * (world - 1)) for r in range(world)]
+    floor = iters * max(per_rank) * 8 / rate - iters * 50 * 1024 * 8 / rate
+    assert dt >= floor, (dt, floor)
+    assert dt < 3 * iters * max(per_rank) * 8 / rate + 2.0
+    w.close()
