@@ -47,6 +47,9 @@ def parse_args():
     ap.add_argument("--skip-layerwise", action="store_true")
     ap.add_argument("--skip-cpu", action="store_true")
     ap.add_argument("--sync-reps", type=int, default=10)
+    ap.add_argument("--throttle-gbps", type=float, default=10.0,
+                    help="emulated per-GPU egress for the P3 vs layer-wise comparison on the same kernels "
+                         "(N>1 only; 0 skips it)")
     return ap.parse_args()
 
 
@@ -326,6 +329,23 @@ def run_ours(args):
         del lw, model
         torch.cuda.empty_cache()
 
+    # --- the paper's experiment: emulated slow links (K7 token bucket, SPEC/PAPER tc shaping),
+    #     P3 (50K slices, priority) vs aggressive layer-wise sync (KVStore placement, FIFO) on the
+    #     same comm kernel, same gates, same fused SGD
+    throttled = None
+    if world > 1 and args.throttle_gbps > 0:
+        throttled = {"gbps": args.throttle_gbps, "burst_bytes": 50 * 1024}
+        for arm, kw in (("p3", {}), ("layerwise_fifo", {"plan_mode": "baseline", "priority_mode": False})):
+            model = build(args, rank)
+            d = P3DataParallel(model, lr=args.lr, max_slice=args.max_slice, comm_ctas=4,
+                               throttle_bps=args.throttle_gbps * 1e9, **kw)
+            ms_t, _ = time_training(args, world, rank, d, x, y, max(3, args.steps // 2), 2)
+            throttled[arm] = max(3, args.steps // 2) * batch * world / (ms_t / 1000.0)
+            d.close()
+            del d, model
+            torch.cuda.empty_cache()
+        throttled["p3_vs_layerwise"] = throttled["p3"] / throttled["layerwise_fifo"]
+
     # --- slice-sync kernel roofline
     sync_ms, ctas = sync_only_roofline(args, world, rank, counts)
     peaks = json.loads((REPO / "MEASURED_PEAKS.json").read_text()) if (REPO / "MEASURED_PEAKS.json").exists() else {}
@@ -362,6 +382,7 @@ def run_ours(args):
             "e2e": {"value": e2e_value, "unit": "samples/sec", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 4},
             "layerwise": layerwise,
             "p3_vs_layerwise": (value / layerwise["value"]) if layerwise else None,
+            "throttled": throttled,
             "roofline": roof,
             "slice_sync": {"ms": sync_ms, "GBps_per_gpu": roof["achieved"], "bound": roof["bound"]},
             "cpu_baseline": cpu,
