@@ -1,0 +1,55 @@
+"""Sync-only comm-kernel timing over NVLink: every rank's gradients resident and published,
+one FINISH launch per iteration; max over ranks. torchrun --nproc-per-node N tools/sync_sweep.py"""
+import os, sys, json, statistics
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch, torch.distributed as dist
+from paper_1905_03960_b200.runtime import SyncContext
+from paper_1905_03960_b200.torch_models import real_counts
+
+def main():
+    world = int(os.environ.get("WORLD_SIZE", "1")); rank = int(os.environ.get("RANK", "0"))
+    torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", int(os.environ["LOCAL_RANK"])))
+    models = sys.argv[1].split(",") if len(sys.argv) > 1 else ["resnet50", "vgg19", "seq2seq"]
+    ctas_list = [int(c) for c in sys.argv[2].split(",")] if len(sys.argv) > 2 else [148]
+    slices = [int(c) for c in sys.argv[3].split(",")] if len(sys.argv) > 3 else [50_000]
+    threads = int(sys.argv[4]) if len(sys.argv) > 4 else 512
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    rows = []
+    for m in models:
+        counts = real_counts(m); P = sum(counts)
+        for ms in slices:
+            for ctas in ctas_list:
+                ctx = SyncContext(counts, world, [rank], max_slice=ms, comm_ctas=ctas, comm_threads=threads,
+                                  timeout_s=60.0, emulate_grads=True)
+                if world > 1:
+                    hs = [None] * world; dist.all_gather_object(hs, ctx.ipc_handle(0)); ctx.open_peers(hs)
+                st = torch.cuda.Stream()
+                for l in range(len(counts)): ctx.gradgen_layer(0, 7 + rank, 0, l, st)
+                st.synchronize()
+                ts = []
+                for k in range(8):
+                    with torch.cuda.stream(st): flush.fill_(k)
+                    for l in range(len(counts)): ctx.layer_ready(0, l, k, None, st)
+                    st.synchronize()
+                    if world > 1: dist.barrier()
+                    torch.cuda.synchronize()
+                    s, e = torch.cuda.Event(True), torch.cuda.Event(True)
+                    s.record(st); ctx.iteration_begin(k, st); ctx.iteration_end(k); e.record(st)
+                    ctx.sync_all(k + 1, 60.0); st.synchronize()
+                    t = torch.tensor([s.elapsed_time(e)], device="cuda")
+                    if world > 1: dist.all_reduce(t, op=dist.ReduceOp.MAX)
+                    if k >= 2: ts.append(float(t.item()))
+                ms_ = statistics.mean(ts)
+                nvl = 2 * (world - 1) / world * P * 4 / (ms_ * 1e-3) / 1e9 if world > 1 else None
+                hbm = 12 * P / (ms_ * 1e-3) / 1e9 if world == 1 else None
+                rows.append({"model": m, "world": world, "max_slice": ms, "ctas": ctas, "threads": threads, "ms": round(ms_, 4),
+                             "nvlink_GBps": nvl and round(nvl, 1), "hbm_GBps": hbm and round(hbm, 1)})
+                ctx.close()
+                if world > 1: dist.barrier()
+    if rank == 0:
+        for r in rows: print("SWEEP " + json.dumps(r), flush=True)
+    if world > 1: dist.destroy_process_group()
+
+main()
