@@ -696,7 +696,7 @@ int p3_counters(p3_ctx_t* c, uint32_t li, uint64_t* bytes_in, uint64_t* bytes_ou
 int p3_debug_snapshot(p3_ctx_t* c, uint32_t li, uint32_t* out, uint64_t cap, uint64_t* n_out) {
   int rc = check_local(c, li);
   if (rc) return rc;
-  const uint64_t n = 5ull * c->L + 4 + P3_DBG_CTAS;
+  const uint64_t n = 5ull * c->L + 4 + P3_DBG_CTAS + 2ull * c->S;
   if (n_out) *n_out = n;
   if (!out) return P3_OK;
   if (cap < n) return fail(c, P3_EUSAGE, "snapshot buffer too small");
@@ -709,6 +709,9 @@ int p3_debug_snapshot(p3_ctx_t* c, uint32_t li, uint32_t* out, uint64_t cap, uin
   CK(cudaMemcpyAsync(pub.data(), D.pub, c->L * 8ull, cudaMemcpyDeviceToHost, c->poll_stream));
   CK(cudaMemcpyAsync(out + 5ull * c->L, D.it, 16, cudaMemcpyDeviceToHost, c->poll_stream));
   CK(cudaMemcpyAsync(out + 5ull * c->L + 4, D.cta_phase, P3_DBG_CTAS * 4ull, cudaMemcpyDeviceToHost, c->poll_stream));
+  uint32_t* tail = out + 5ull * c->L + 4 + P3_DBG_CTAS;
+  CK(cudaMemcpyAsync(tail, c->peers.arrivals[rank], c->S * 4ull, cudaMemcpyDeviceToHost, c->poll_stream));
+  CK(cudaMemcpyAsync(tail + c->S, D.claim, c->S * 4ull, cudaMemcpyDeviceToHost, c->poll_stream));
   CK(cudaStreamSynchronize(c->poll_stream));
   for (uint32_t l = 0; l < c->L; ++l) out[l] = (uint32_t)(pub[l] >> 48);  // iteration tag
   return P3_OK;

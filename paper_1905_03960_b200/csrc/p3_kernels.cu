@@ -458,7 +458,9 @@ __device__ uint32_t warp_server_pick(const CommArgs& a, const LocalDev& L, uint3
             claimed = ld_relaxed_gpu(L.claim + g) != k;
             ok = !claimed && (int32_t)(ld_relaxed_sys(arrivals + g) - need) >= 0;
           }
-          if (__all_sync(FULL_MASK, claimed) && lane == 0) atomicMax(L.srv_lo + l, i0 + 32);
+          // advance the watermark only contiguously: a window below this one may still
+          // hold an unclaimed slice even if this window is fully claimed
+          if (__all_sync(FULL_MASK, claimed) && lane == 0) atomicCAS(L.srv_lo + l, i0, i0 + 32);
           uint32_t m = __ballot_sync(FULL_MASK, ok);
           while (m) {
             const int j = __ffs(m) - 1;

@@ -202,7 +202,11 @@ class SyncContext:
         names = ("ready", "cursor", "srv_taken", "hint", "done")
         out = {nm: arr[i * L : (i + 1) * L] for i, nm in enumerate(names)}
         out["pushed"], out["reduced"], out["exited"], out["jobs"] = arr[5 * L : 5 * L + 4]
-        out["cta_phase"] = arr[5 * L + 4 :]
+        base = 5 * L + 4 + 512
+        S = (len(arr) - base) // 2
+        out["cta_phase"] = arr[5 * L + 4 : base]
+        out["arrivals"] = arr[base : base + S]
+        out["claim"] = arr[base + S :]
         return out
 
     def clear_trace(self) -> None:

@@ -37,7 +37,25 @@ def main():
                     torch.cuda.synchronize()
                     s, e = torch.cuda.Event(True), torch.cuda.Event(True)
                     s.record(st); ctx.iteration_begin(k, st); ctx.iteration_end(k); e.record(st)
-                    ctx.sync_all(k + 1, 60.0); st.synchronize()
+                    try:
+                        ctx.sync_all(k + 1, 20.0)
+                    except Exception as ex:
+                        d = ctx.debug_snapshot(0)
+                        from paper_1905_03960_b200.plan import make_p3_plan
+                        from paper_1905_03960_b200.model import ModelProfile, LayerSpec
+                        plan = make_p3_plan(ModelProfile("x", 0, tuple(LayerSpec(i, "l", c, 0, 0) for i, c in enumerate(counts))), world, ms)
+                        bad = [l for l in range(len(counts)) if d["done"][l] < (k + 1) * len(plan.slices_of_layer(l))]
+                        print(f"HANG rank {rank} k {k} ctas {ctas}: {ex}", flush=True)
+                        print(f"HANG rank {rank} pushed {d['pushed']} reduced {d['reduced']} exited {d['exited']} jobs {d['jobs']}", flush=True)
+                        for l in bad[:3] + [32]:
+                            sl = plan.slices_of_layer(l); first = plan.slices.index(sl[0])
+                            print(f"HANG rank {rank} layer {l}: done {d['done'][l]} hint {d['hint'][l]} taken {d['srv_taken'][l]} cursor {d['cursor'][l]} tag {d['ready'][l]}", flush=True)
+                            print(f"HANG rank {rank}   slices(owner,arr,claim): " + " ".join(f"{s.server},{d['arrivals'][first+i]},{d['claim'][first+i]}" for i, s in enumerate(sl)), flush=True)
+                        from collections import Counter
+                        ph = d["cta_phase"][:ctas]
+                        print(f"HANG rank {rank} phases {Counter((p >> 20) & 0xf for p in ph)} {[hex(p) for p in ph if (p >> 20) & 0xf != 5][:8]}", flush=True)
+                        raise
+                    st.synchronize()
                     t = torch.tensor([s.elapsed_time(e)], device="cuda")
                     if world > 1: dist.all_reduce(t, op=dist.ReduceOp.MAX)
                     if k >= 2: ts.append(float(t.item()))
