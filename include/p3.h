@@ -228,8 +228,9 @@ int p3_counters(p3_ctx_t* ctx, uint32_t local_idx, uint64_t* bytes_in, uint64_t*
 
 /* Diagnostics snapshot of a local rank (deadlock dumps, worker.py:291-297): 5 arrays of
  * n_layers u32 — ready tag, claim cursor, server claims, completed-hint, done counter —
- * then the 4 per-iteration counters (pushed, reduced, exited CTAs, jobs), the last phase
- * word of the first 512 comm CTAs, and per slice the arrival counter and server claim tag. Copied on a private stream (never blocks on the
+ * then the per-iteration counters (pushed, reduced, exited CTAs, jobs; then 4 u64 ns totals:
+ * scheduler pick, scheduler slot wait, movers, signaler), the last phase word of the
+ * first 512 comm CTAs, and per slice the arrival counter and server claim tag. Copied on a private stream (never blocks on the
  * compute or comm streams). */
 int p3_debug_snapshot(p3_ctx_t* ctx, uint32_t local_idx, uint32_t* out, uint64_t cap,
                       uint64_t* n_out);

@@ -227,8 +227,8 @@ int p3_ctx_create(const p3_config_t* cfg, p3_ctx_t** out) {
   if (cfg->n_layers < 1 || !cfg->layer_counts) return fail(nullptr, P3_EUSAGE, "profile needs at least one layer");
   if (cfg->plan_mode != P3_PLAN_P3 && cfg->plan_mode != P3_PLAN_BASELINE) return fail(nullptr, P3_EUSAGE, "bad plan_mode");
   if (cfg->throttle_bps < 0) return fail(nullptr, P3_EUSAGE, "throttle rate must be >= 0 (0 disables shaping)");
-  if (cfg->comm_threads < 64 || cfg->comm_threads > 512 || cfg->comm_threads % 32)
-    return fail(nullptr, P3_EUSAGE, "comm_threads must be a multiple of 32 in [64, 512] (one scheduler warp + movers)");
+  if (cfg->comm_threads < 96 || cfg->comm_threads > 512 || cfg->comm_threads % 32)
+    return fail(nullptr, P3_EUSAGE, "comm_threads must be a multiple of 32 in [96, 512] (scheduler + signaler + mover warps)");
   if (cfg->comm_ctas < 1) return fail(nullptr, P3_EUSAGE, "comm_ctas must be >= 1");
   for (uint32_t i = 0; i < cfg->n_local; ++i)
     if (cfg->local_ranks[i] >= cfg->world) return fail(nullptr, P3_EUSAGE, "local rank out of range");
@@ -696,7 +696,7 @@ int p3_counters(p3_ctx_t* c, uint32_t li, uint64_t* bytes_in, uint64_t* bytes_ou
 int p3_debug_snapshot(p3_ctx_t* c, uint32_t li, uint32_t* out, uint64_t cap, uint64_t* n_out) {
   int rc = check_local(c, li);
   if (rc) return rc;
-  const uint64_t n = 5ull * c->L + 4 + P3_DBG_CTAS + 2ull * c->S;
+  const uint64_t n = 5ull * c->L + 12 + P3_DBG_CTAS + 2ull * c->S;
   if (n_out) *n_out = n;
   if (!out) return P3_OK;
   if (cap < n) return fail(c, P3_EUSAGE, "snapshot buffer too small");
@@ -707,9 +707,10 @@ int p3_debug_snapshot(p3_ctx_t* c, uint32_t li, uint32_t* out, uint64_t cap, uin
     CK(cudaMemcpyAsync(out + (uint64_t)a * c->L, src[a], c->L * 4ull, cudaMemcpyDeviceToHost, c->poll_stream));
   std::vector<uint64_t> pub(c->L);
   CK(cudaMemcpyAsync(pub.data(), D.pub, c->L * 8ull, cudaMemcpyDeviceToHost, c->poll_stream));
-  CK(cudaMemcpyAsync(out + 5ull * c->L, D.it, 16, cudaMemcpyDeviceToHost, c->poll_stream));
-  CK(cudaMemcpyAsync(out + 5ull * c->L + 4, D.cta_phase, P3_DBG_CTAS * 4ull, cudaMemcpyDeviceToHost, c->poll_stream));
-  uint32_t* tail = out + 5ull * c->L + 4 + P3_DBG_CTAS;
+  static_assert(sizeof(IterState) == 48, "IterState layout");
+  CK(cudaMemcpyAsync(out + 5ull * c->L, D.it, sizeof(IterState), cudaMemcpyDeviceToHost, c->poll_stream));
+  CK(cudaMemcpyAsync(out + 5ull * c->L + 12, D.cta_phase, P3_DBG_CTAS * 4ull, cudaMemcpyDeviceToHost, c->poll_stream));
+  uint32_t* tail = out + 5ull * c->L + 12 + P3_DBG_CTAS;
   CK(cudaMemcpyAsync(tail, c->peers.arrivals[rank], c->S * 4ull, cudaMemcpyDeviceToHost, c->poll_stream));
   CK(cudaMemcpyAsync(tail + c->S, D.claim, c->S * 4ull, cudaMemcpyDeviceToHost, c->poll_stream));
   CK(cudaStreamSynchronize(c->poll_stream));

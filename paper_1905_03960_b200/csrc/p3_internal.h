@@ -62,6 +62,9 @@ struct IterState {
   uint32_t reduced;  // owned slices claimed
   uint32_t exited;   // CTAs of the FINISH launch that left (diagnostics)
   uint32_t jobs;     // jobs executed (diagnostics)
+  // time (ns, summed over CTAs) spent by the scheduler picking, the scheduler waiting for a
+  // free slot, the movers moving data, the signaler publishing completions (diagnostics)
+  unsigned long long t_pick, t_slot_wait, t_move, t_signal;
 };
 
 // Local-only state of one rank hosted in this process.

@@ -545,11 +545,13 @@ struct Job {
   float* v;
 };
 
-// Named barriers (0 is __syncthreads): per job slot b "slot full" (scheduler -> movers) and
-// "slot free" (movers -> scheduler), plus one among the movers.
+// Named barriers (0 is __syncthreads), per job slot b:
+//   FULL(b)  scheduler arrives, signaler + movers sync      (slot b holds a job)
+//   DONE(b)  movers arrive, signaler syncs                  (the job's data has moved)
+//   EMPTY(b) signaler arrives, scheduler syncs              (slot b may be refilled)
 #define BAR_FULL(b) (1 + (b))
-#define BAR_EMPTY(b) (3 + (b))
-#define BAR_MOVERS 5
+#define BAR_DONE(b) (3 + (b))
+#define BAR_EMPTY(b) (5 + (b))
 __device__ __forceinline__ void bar_sync(uint32_t id, uint32_t n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
@@ -657,58 +659,65 @@ __device__ void prepare_reduce(const CommArgs& a, uint32_t li, uint32_t g, Job* 
   }
 }
 
-// Mover side: move the data, then one mover publishes completion (release, system scope
-// when a peer is on another GPU).
-__device__ void run_job(const CommArgs& a, const Job& j, uint32_t tid, uint32_t nthr) {
-  const PlanDev& P = a.plan;
-  const LocalDev& L = a.loc[j.li];
+// Movers: move the job's data.
+__device__ void move_job(const CommArgs& a, const Job& j, uint32_t tid, uint32_t nthr) {
   if (j.kind == JOB_PUSH) {
     cta_copy(j.dst[0], j.src[0], j.len, tid, nthr);
-    bar_sync(BAR_MOVERS, nthr);
-    if (tid == 0) {
-      if (a.remote) __threadfence_system(); else __threadfence();
-      atomicAdd(L.bytes + 1, 4ull * j.len);
-      const uint32_t old = atom_add_release_sys(a.peers.arrivals[j.rank] + j.g, 1u);
-      if (old + 1 == (a.k + 1) * P.world) red_add_release_sys(a.peers.hint[j.rank] + j.layer, 1u);
-    }
   } else {
     cta_update_generic(j.dst[0], j.dst, (int)j.n, j.src, (int)j.n, j.v, j.len, j.aligned != 0,
                        make_coef(j.n, a.lr, a.momentum), tid, nthr);
-    bar_sync(BAR_MOVERS, nthr);
-    if (tid == 0) {
-      if (a.remote) __threadfence_system(); else __threadfence();
-      for (uint32_t q = 0; q < j.n; ++q) red_add_release_sys(a.peers.done[q] + j.layer, 1u);
-      atomicAdd(L.bytes + 0, 4ull * j.len * (j.n - 1));  // pushes received
-      atomicAdd(L.bytes + 1, 4ull * j.len * (j.n - 1));  // broadcasts sent
-      trace_append(L, a.k, j.layer, j.g - P.layer_first[j.layer], j.rank, P3_EV_BCAST);
-    }
   }
 }
 
-// Comm kernel: warp 0 of every CTA is the scheduler, warps 1.. are movers.
+// Signaler (one thread, after the movers' barrier): publish the job's completion with
+// release semantics at system scope when a peer lives on another GPU. Push: count the
+// arrival at the owner (and the owner's layer hint when it completes the slice). Reduce:
+// bump every replica's done[layer] (the forward gate, worker.py:262-269).
+__device__ void signal_job(const CommArgs& a, const Job& j) {
+  const PlanDev& P = a.plan;
+  const LocalDev& L = a.loc[j.li];
+  if (a.remote) __threadfence_system(); else __threadfence();
+  if (j.kind == JOB_PUSH) {
+    atomicAdd(L.bytes + 1, 4ull * j.len);
+    const uint32_t old = atom_add_release_sys(a.peers.arrivals[j.rank] + j.g, 1u);
+    if (old + 1 == (a.k + 1) * P.world) red_add_release_sys(a.peers.hint[j.rank] + j.layer, 1u);
+  } else {
+    for (uint32_t q = 0; q < j.n; ++q) red_add_release_sys(a.peers.done[q] + j.layer, 1u);
+    atomicAdd(L.bytes + 0, 4ull * j.len * (j.n - 1));  // pushes received
+    atomicAdd(L.bytes + 1, 4ull * j.len * (j.n - 1));  // broadcasts sent
+    trace_append(L, a.k, j.layer, j.g - P.layer_first[j.layer], j.rank, P3_EV_BCAST);
+  }
+}
+
+// Comm kernel. Warp 0 of every CTA is the scheduler, warp 1 the signaler, warps 2.. the
+// movers; two job slots in shared memory.
 //   scheduler: pick the next job — server work first (a reduced slice unblocks the next
 //   forward pass), then the most urgent published slice of the local worker queues — and
-//   prepare its pointers while the movers are still busy with the previous job;
-//   movers: wait for a job, copy it to registers, release the slot, move the data,
-//   publish completion.
+//   prepare its pointers while the movers still run the previous job;
+//   movers: move the data of the job in the current slot, then go straight to the next;
+//   signaler: once the movers are done with a slot, fence and publish the completion
+//   (arrival / done counters), then release the slot to the scheduler.
 // The queue is re-read for every pick, so a layer published while the kernel runs
 // preempts less urgent slices at slice granularity. DRAIN launches (one per published
-// layer) exit as soon as nothing is available: a kernel spinning on unpublished gradients
-// would hold SMs that the compute producing them may need (co-residency-bound library
-// kernels, lazy module loading). The FINISH launch of an iteration ends once every local
-// slice is pushed and every owned slice reduced; it waits only for peers' pushes.
+// batch of layers) exit as soon as nothing is available: a kernel spinning on unpublished
+// gradients would hold SMs that the compute producing them may need (co-residency-bound
+// library kernels, lazy module loading). The FINISH launch of an iteration ends once every
+// local slice is pushed and every owned slice reduced; it waits only for peers' pushes.
 __global__ void __launch_bounds__(512, 1) k_comm(const __grid_constant__ CommArgs a) {
   __shared__ Job slots[2];  // double-buffered: the scheduler fills one while movers run the other
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t nthr = blockDim.x;
-  const uint32_t movers = nthr - 32;
+  const uint32_t movers = nthr - 64;
+  IterState* stats = a.loc[0].it;
   if (warp == 0) {
     uint32_t* phase = (lane == 0 && blockIdx.x < P3_DBG_CTAS) ? a.loc[0].cta_phase + blockIdx.x : nullptr;
     const uint64_t t0 = globaltimer();
+    uint64_t t_pick = 0, t_wait = 0;
     uint32_t backoff = 0, b = 0;
     bool pending[2] = {false, false};
     for (uint32_t iter = 0;; ++iter) {
       if (phase) *(volatile uint32_t*)phase = (a.k << 24) | (1u << 20) | (iter & 0xfffff);
+      const uint64_t tp = globaltimer();
       uint32_t kind = JOB_NONE, li = 0, g = P3_NONE;
       for (uint32_t t = 0; t < a.n_local && kind == JOB_NONE; ++t) {
         li = (blockIdx.x + t) % a.n_local;
@@ -769,33 +778,60 @@ __global__ void __launch_bounds__(512, 1) k_comm(const __grid_constant__ CommArg
         if (lane == 0) pace(a, a.loc[li], bytes);
         __syncwarp();
       }
-      if (pending[b]) bar_sync(BAR_EMPTY(b), nthr);  // movers are done with this slot
+      const uint64_t tw = globaltimer();
+      t_pick += tw - tp;
+      if (pending[b]) bar_sync(BAR_EMPTY(b), 64);  // the signaler released this slot
       if (kind == JOB_PUSH) {
         prepare_push(a, li, g, &slots[b]);
       } else if (kind == JOB_REDUCE) {
         prepare_reduce(a, li, g, &slots[b]);
       } else {
-        if (pending[b ^ 1]) bar_sync(BAR_EMPTY(b ^ 1), nthr);  // leave every barrier balanced
+        if (pending[b ^ 1]) bar_sync(BAR_EMPTY(b ^ 1), 64);  // leave every barrier balanced
         if (lane == 0) slots[b].kind = JOB_EXIT;
       }
+      t_wait += globaltimer() - tw;
       __syncwarp();
       bar_arrive(BAR_FULL(b), nthr);
       if (kind == JOB_EXIT) break;
       pending[b] = true;
       b ^= 1;
-      if (lane == 0) atomicAdd(&a.loc[0].it->jobs, 1u);
+      if (lane == 0) atomicAdd(&stats->jobs, 1u);
+    }
+    if (lane == 0) {
+      atomicAdd(&stats->t_pick, (unsigned long long)t_pick);
+      atomicAdd(&stats->t_slot_wait, (unsigned long long)t_wait);
+      if (a.mode == P3_COMM_FINISH) atomicAdd(&stats->exited, 1u);
     }
     if (phase) *(volatile uint32_t*)phase = (a.k << 24) | (5u << 20);
-    if (lane == 0 && a.mode == P3_COMM_FINISH) atomicAdd(&a.loc[0].it->exited, 1u);
-  } else {
-    const uint32_t tid = threadIdx.x - 32;
+  } else if (warp == 1) {
+    uint64_t t_sig = 0;
     for (uint32_t b = 0;; b ^= 1) {
       bar_sync(BAR_FULL(b), nthr);
       const Job& j = slots[b];
       if (j.kind == JOB_EXIT) break;
-      run_job(a, j, tid, movers);
-      bar_arrive(BAR_EMPTY(b), nthr);
+      bar_sync(BAR_DONE(b), nthr - 32);
+      if (lane == 0) {
+        const uint64_t ts = globaltimer();
+        signal_job(a, j);
+        t_sig += globaltimer() - ts;
+      }
+      __syncwarp();
+      bar_arrive(BAR_EMPTY(b), 64);
     }
+    if (lane == 0) atomicAdd(&stats->t_signal, (unsigned long long)t_sig);
+  } else {
+    const uint32_t tid = threadIdx.x - 64;
+    uint64_t t_move = 0;
+    for (uint32_t b = 0;; b ^= 1) {
+      bar_sync(BAR_FULL(b), nthr);
+      const Job& j = slots[b];
+      if (j.kind == JOB_EXIT) break;
+      const uint64_t tm = tid == 0 ? globaltimer() : 0;
+      move_job(a, j, tid, movers);
+      if (tid == 0) t_move += globaltimer() - tm;
+      bar_arrive(BAR_DONE(b), nthr - 32);
+    }
+    if (tid == 0) atomicAdd(&stats->t_move, (unsigned long long)t_move);
   }
 }
 

@@ -202,9 +202,12 @@ class SyncContext:
         names = ("ready", "cursor", "srv_taken", "hint", "done")
         out = {nm: arr[i * L : (i + 1) * L] for i, nm in enumerate(names)}
         out["pushed"], out["reduced"], out["exited"], out["jobs"] = arr[5 * L : 5 * L + 4]
-        base = 5 * L + 4 + 512
+        t = arr[5 * L + 4 : 5 * L + 12]
+        for i, nm in enumerate(("t_pick_ns", "t_slot_wait_ns", "t_move_ns", "t_signal_ns")):
+            out[nm] = t[2 * i] | (t[2 * i + 1] << 32)
+        base = 5 * L + 12 + 512
         S = (len(arr) - base) // 2
-        out["cta_phase"] = arr[5 * L + 4 : base]
+        out["cta_phase"] = arr[5 * L + 12 : base]
         out["arrivals"] = arr[base : base + S]
         out["claim"] = arr[base + S :]
         return out

@@ -60,10 +60,14 @@ def main():
                     if world > 1: dist.all_reduce(t, op=dist.ReduceOp.MAX)
                     if k >= 2: ts.append(float(t.item()))
                 ms_ = statistics.mean(ts)
+                dsn = ctx.debug_snapshot(0)
+                jobs = max(dsn["jobs"], 1)
+                stats = {k2: round(dsn[k2] / jobs / 1000, 2) for k2 in ("t_pick_ns", "t_slot_wait_ns", "t_move_ns", "t_signal_ns")}
+                stats["jobs"] = dsn["jobs"]
                 nvl = 2 * (world - 1) / world * P * 4 / (ms_ * 1e-3) / 1e9 if world > 1 else None
                 hbm = 12 * P / (ms_ * 1e-3) / 1e9 if world == 1 else None
                 rows.append({"model": m, "world": world, "max_slice": ms, "ctas": ctas, "threads": threads, "ms": round(ms_, 4),
-                             "nvlink_GBps": nvl and round(nvl, 1), "hbm_GBps": hbm and round(hbm, 1)})
+                             "nvlink_GBps": nvl and round(nvl, 1), "hbm_GBps": hbm and round(hbm, 1), "us_per_job": stats})
                 ctx.close()
                 if world > 1: dist.barrier()
     if rank == 0:
