@@ -61,6 +61,16 @@ __device__ __forceinline__ uint32_t atom_add_release_sys(uint32_t* p, uint32_t v
   asm volatile("atom.release.sys.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
   return old;
 }
+__device__ __forceinline__ void red_add_relaxed_sys(uint32_t* p, uint32_t v) {
+  asm volatile("red.relaxed.sys.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t atom_add_relaxed_gpu(uint32_t* p, uint32_t v) {
+  uint32_t old;
+  asm volatile("atom.relaxed.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+__device__ __forceinline__ void fence_acq_rel_sys() { asm volatile("fence.acq_rel.sys;" ::: "memory"); }
+__device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 __device__ __forceinline__ void red_add_release_sys(uint32_t* p, uint32_t v) {
   asm volatile("red.release.sys.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
@@ -430,8 +440,10 @@ __device__ uint32_t warp_server_pick(const CommArgs& a, const LocalDev& L, uint3
       const uint32_t oc = lcount[l];
       bool ok = false;
       if (oc) {
-        const uint32_t completed = ld_relaxed_sys(hint + l) - k * oc;
-        ok = (int32_t)(completed - ld_relaxed_gpu(L.srv_taken + l)) > 0;
+        // pushes that arrived this iteration for the layer's owned slices, minus those of
+        // slices already claimed: >= N means some owned slice may be complete
+        const uint32_t pushes = ld_relaxed_sys(hint + l) - k * P.world * oc;
+        ok = (int32_t)(pushes - P.world * ld_relaxed_gpu(L.srv_taken + l)) >= (int32_t)P.world;
       }
       bits |= (uint32_t)ok << c;
     }
@@ -598,9 +610,10 @@ __device__ uint32_t prepare_push(const CommArgs& a, uint32_t li, uint32_t g, Job
       (void)ld_acquire_gpu64(L.pub + l);  // the gradient is published: visible from here on
       trace_append(L, a.k, l, g - P.layer_first[l], r, P3_EV_PUSH);
       if (o == r) {
-        const uint32_t old = atom_add_release_sys(a.peers.arrivals[o] + g, 1u);
+        // the contribution stays in place (published to this rank by the acquire above)
+        const uint32_t old = atom_add_relaxed_gpu(a.peers.arrivals[o] + g, 1u);
+        red_add_relaxed_sys(a.peers.hint[o] + l, 1u);
         if (old + 1 == (a.k + 1) * P.world) {
-          red_add_release_sys(a.peers.hint[o] + l, 1u);
           if (atomicCAS(L.claim + g, a.k, a.k + 1) == a.k) {
             atomicAdd(L.srv_taken + l, 1u);
             atomicAdd(&L.it->reduced, 1u);
@@ -676,13 +689,15 @@ __device__ void move_job(const CommArgs& a, const Job& j, uint32_t tid, uint32_t
 __device__ void signal_job(const CommArgs& a, const Job& j) {
   const PlanDev& P = a.plan;
   const LocalDev& L = a.loc[j.li];
-  if (a.remote) __threadfence_system(); else __threadfence();
+  // one fence releases every store the movers made (ordered before it by the DONE barrier);
+  // the counter updates after it are plain relaxed reductions (fire and forget)
+  if (a.remote) fence_acq_rel_sys(); else fence_acq_rel_gpu();
   if (j.kind == JOB_PUSH) {
+    red_add_relaxed_sys(a.peers.arrivals[j.rank] + j.g, 1u);
+    red_add_relaxed_sys(a.peers.hint[j.rank] + j.layer, 1u);
     atomicAdd(L.bytes + 1, 4ull * j.len);
-    const uint32_t old = atom_add_release_sys(a.peers.arrivals[j.rank] + j.g, 1u);
-    if (old + 1 == (a.k + 1) * P.world) red_add_release_sys(a.peers.hint[j.rank] + j.layer, 1u);
   } else {
-    for (uint32_t q = 0; q < j.n; ++q) red_add_release_sys(a.peers.done[q] + j.layer, 1u);
+    for (uint32_t q = 0; q < j.n; ++q) red_add_relaxed_sys(a.peers.done[q] + j.layer, 1u);
     atomicAdd(L.bytes + 0, 4ull * j.len * (j.n - 1));  // pushes received
     atomicAdd(L.bytes + 1, 4ull * j.len * (j.n - 1));  // broadcasts sent
     trace_append(L, a.k, j.layer, j.g - P.layer_first[j.layer], j.rank, P3_EV_BCAST);
@@ -810,13 +825,22 @@ __global__ void __launch_bounds__(512, 1) k_comm(const __grid_constant__ CommArg
       const Job& j = slots[b];
       if (j.kind == JOB_EXIT) break;
       bar_sync(BAR_DONE(b), nthr - 32);
+      Job mine;  // what the signal needs, so the slot can be refilled right away
+      mine.kind = j.kind;
+      mine.li = j.li;
+      mine.g = j.g;
+      mine.layer = j.layer;
+      mine.rank = j.rank;
+      mine.len = j.len;
+      mine.n = j.n;
+      __syncwarp();
+      bar_arrive(BAR_EMPTY(b), 64);
       if (lane == 0) {
         const uint64_t ts = globaltimer();
-        signal_job(a, j);
+        signal_job(a, mine);
         t_sig += globaltimer() - ts;
       }
       __syncwarp();
-      bar_arrive(BAR_EMPTY(b), 64);
     }
     if (lane == 0) atomicAdd(&stats->t_signal, (unsigned long long)t_sig);
   } else {
