@@ -69,6 +69,11 @@ __device__ __forceinline__ uint32_t atom_add_relaxed_gpu(uint32_t* p, uint32_t v
   asm volatile("atom.relaxed.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
   return old;
 }
+__device__ __forceinline__ uint32_t atom_add_relaxed_sys(uint32_t* p, uint32_t v) {
+  uint32_t old;
+  asm volatile("atom.relaxed.sys.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
 __device__ __forceinline__ void fence_acq_rel_sys() { asm volatile("fence.acq_rel.sys;" ::: "memory"); }
 __device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 __device__ __forceinline__ void red_add_release_sys(uint32_t* p, uint32_t v) {
@@ -439,11 +444,9 @@ __device__ uint32_t warp_server_pick(const CommArgs& a, const LocalDev& L, uint3
       if (l >= nl) break;
       const uint32_t oc = lcount[l];
       bool ok = false;
-      if (oc) {
-        // pushes that arrived this iteration for the layer's owned slices, minus those of
-        // slices already claimed: >= N means some owned slice may be complete
-        const uint32_t pushes = ld_relaxed_sys(hint + l) - k * P.world * oc;
-        ok = (int32_t)(pushes - P.world * ld_relaxed_gpu(L.srv_taken + l)) >= (int32_t)P.world;
+      if (oc) {  // owned slices completed this iteration and not yet claimed
+        const uint32_t completed = ld_relaxed_sys(hint + l) - k * oc;
+        ok = (int32_t)(completed - ld_relaxed_gpu(L.srv_taken + l)) > 0;
       }
       bits |= (uint32_t)ok << c;
     }
@@ -612,8 +615,8 @@ __device__ uint32_t prepare_push(const CommArgs& a, uint32_t li, uint32_t g, Job
       if (o == r) {
         // the contribution stays in place (published to this rank by the acquire above)
         const uint32_t old = atom_add_relaxed_gpu(a.peers.arrivals[o] + g, 1u);
-        red_add_relaxed_sys(a.peers.hint[o] + l, 1u);
-        if (old + 1 == (a.k + 1) * P.world) {
+        if (old + 1 == (a.k + 1) * P.world) {  // the last arrival: the slice is complete
+          red_add_relaxed_sys(a.peers.hint[o] + l, 1u);
           if (atomicCAS(L.claim + g, a.k, a.k + 1) == a.k) {
             atomicAdd(L.srv_taken + l, 1u);
             atomicAdd(&L.it->reduced, 1u);
@@ -693,8 +696,9 @@ __device__ void signal_job(const CommArgs& a, const Job& j) {
   // the counter updates after it are plain relaxed reductions (fire and forget)
   if (a.remote) fence_acq_rel_sys(); else fence_acq_rel_gpu();
   if (j.kind == JOB_PUSH) {
-    red_add_relaxed_sys(a.peers.arrivals[j.rank] + j.g, 1u);
-    red_add_relaxed_sys(a.peers.hint[j.rank] + j.layer, 1u);
+    // the last arriver completes the slice and tells the owner's scheduler (hint)
+    const uint32_t old = atom_add_relaxed_sys(a.peers.arrivals[j.rank] + j.g, 1u);
+    if (old + 1 == (a.k + 1) * P.world) red_add_relaxed_sys(a.peers.hint[j.rank] + j.layer, 1u);
     atomicAdd(L.bytes + 1, 4ull * j.len);
   } else {
     for (uint32_t q = 0; q < j.n; ++q) red_add_relaxed_sys(a.peers.done[q] + j.layer, 1u);
