@@ -154,6 +154,9 @@ typedef struct p3_config {
   double throttle_bps;                 /* K7 link emulation: per-rank egress rate in bit/s
                                           (TokenBucket, transport.py:22-55); 0 = full NVLink */
   uint64_t throttle_burst;             /* bucket depth in bytes (transport.py:18: 50 KiB) */
+  const uint32_t* gate_groups;         /* optional per-layer forward-gate group id (layers of
+                                          one module gated together); NULL = one group per
+                                          layer. Ids must be 0..G-1 */
 } p3_config_t;
 
 /* Builds the plan, allocates per-local-rank arenas (parameters W zero-initialised like
@@ -209,6 +212,11 @@ int p3_gradgen_layer(p3_ctx_t* ctx, uint32_t local_idx, uint64_t seed, uint64_t 
  * the parameters for forward pass `iteration` (flags[layer] >= iteration). A stream
  * memory wait: no SM is occupied. */
 int p3_wait_layer(p3_ctx_t* ctx, uint32_t local_idx, uint32_t layer, uint64_t iteration,
+                  void* stream);
+
+/* _wait_layer for a gate group: wait until every layer of `group` holds the parameters
+ * for forward pass `iteration` — one stream memory wait for a whole module. */
+int p3_wait_group(p3_ctx_t* ctx, uint32_t local_idx, uint32_t group, uint64_t iteration,
                   void* stream);
 
 /* TrainingWorker._wait_all (worker.py:287-289) + error check: block the host until the

@@ -73,6 +73,7 @@ class Config(ctypes.Structure):
         ("rng_seed", ctypes.c_uint64),
         ("throttle_bps", ctypes.c_double),
         ("throttle_burst", ctypes.c_uint64),
+        ("gate_groups", ctypes.POINTER(ctypes.c_uint32)),
     ]
 
 
@@ -108,6 +109,7 @@ SIGNATURES = {
     "p3_layer_ready": (ctypes.c_int, [_P, _U32, _U32, _U64, _P, _P]),
     "p3_gradgen_layer": (ctypes.c_int, [_P, _U32, _U64, _U64, _U32, _P]),
     "p3_wait_layer": (ctypes.c_int, [_P, _U32, _U32, _U64, _P]),
+    "p3_wait_group": (ctypes.c_int, [_P, _U32, _U32, _U64, _P]),
     "p3_sync_all": (ctypes.c_int, [_P, _U64, ctypes.c_double]),
     "p3_trace_read": (ctypes.c_int, [_P, _U32, ctypes.POINTER(TraceRec), _U64, _PU64]),
     "p3_trace_clear": (ctypes.c_int, [_P]),

@@ -72,7 +72,7 @@ using namespace p3;
 
 // Peer-visible arena of one rank: W | R | arrivals | hint | done (256-byte aligned parts).
 struct PeerLayout {
-  uint64_t w, r, arrivals, hint, done, bytes;
+  uint64_t w, r, arrivals, hint, done, gdone, bytes;
 };
 
 // Local arena of one rank. The per-iteration part (cursor | srv_lo | srv_taken | it) is
@@ -86,7 +86,8 @@ struct p3_ctx {
   p3_config_t cfg;
   std::vector<uint64_t> counts;
   std::vector<p3_slice_t> plan;
-  uint32_t L = 0, S = 0, N = 0;
+  uint32_t L = 0, S = 0, N = 0, G = 0;
+  std::vector<uint32_t> layer_group, group_slices;
   std::vector<uint64_t> layer_woff;
   std::vector<uint32_t> layer_nslices, layer_first;
   std::vector<uint32_t> own_total;
@@ -151,6 +152,8 @@ PeerLayout peer_layout_of(const p3_ctx* c, uint32_t rank) {
   o = align_up(o + (uint64_t)c->L * 4, 256);
   p.done = o;
   o = align_up(o + (uint64_t)c->L * 4, 256);
+  p.gdone = o;
+  o = align_up(o + (uint64_t)c->G * 4, 256);
   p.bytes = o;
   return p;
 }
@@ -188,6 +191,7 @@ void set_peer_pointers(p3_ctx* c, uint32_t rank, char* base) {
   c->peers.arrivals[rank] = reinterpret_cast<uint32_t*>(base + p.arrivals);
   c->peers.hint[rank] = reinterpret_cast<uint32_t*>(base + p.hint);
   c->peers.done[rank] = reinterpret_cast<uint32_t*>(base + p.done);
+  c->peers.gdone[rank] = reinterpret_cast<uint32_t*>(base + p.gdone);
 }
 
 int check_local(p3_ctx* c, uint32_t li) {
@@ -239,6 +243,7 @@ int p3_ctx_create(const p3_config_t* cfg, p3_ctx_t** out) {
   c->cfg = *cfg;
   c->counts.assign(cfg->layer_counts, cfg->layer_counts + cfg->n_layers);
   c->cfg.layer_counts = c->counts.data();
+  c->cfg.gate_groups = nullptr;  // consumed below, not retained
   c->L = cfg->n_layers;
   c->N = cfg->world;
   std::string perr;
@@ -312,6 +317,17 @@ int p3_ctx_create(const p3_config_t* cfg, p3_ctx_t** out) {
         if (slice_owner[g] != r) c->bcast_in_bytes[r] += 4ull * slice_len[g];
   }
 
+  // ---- forward-gate groups
+  c->layer_group.resize(L);
+  for (uint32_t l = 0; l < L; ++l) c->layer_group[l] = cfg->gate_groups ? cfg->gate_groups[l] : l;
+  for (uint32_t l = 0; l < L; ++l) c->G = std::max(c->G, c->layer_group[l] + 1);
+  if (c->G > L) {
+    delete c;
+    return fail(nullptr, P3_EUSAGE, "gate group ids must be < n_layers");
+  }
+  c->group_slices.assign(c->G, 0);
+  for (uint32_t l = 0; l < L; ++l) c->group_slices[c->layer_group[l]] += c->layer_nslices[l];
+
   // ---- device plan tables: one allocation
   std::vector<char> blob;
   auto put = [&](const void* src, size_t bytes) -> size_t {
@@ -333,6 +349,7 @@ int p3_ctx_create(const p3_config_t* cfg, p3_ctx_t** out) {
   const size_t o_olc = put(own_lcount.data(), own_lcount.size() * 4ull);
   const size_t o_ot = put(c->own_total.data(), N * 4ull);
   const size_t o_ost = put(c->own_stride.data(), N * 8ull);
+  const size_t o_lg = put(c->layer_group.data(), L * 4ull);
   cudaError_t e = cudaMalloc(&c->d_plan, blob.size());
   if (e == cudaSuccess) e = cudaMemcpy(c->d_plan, blob.data(), blob.size(), cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaMalloc(&c->d_err, 256);
@@ -360,6 +377,7 @@ int p3_ctx_create(const p3_config_t* cfg, p3_ctx_t** out) {
   P.own_lcount = reinterpret_cast<const uint32_t*>(pb + o_olc);
   P.own_total = reinterpret_cast<const uint32_t*>(pb + o_ot);
   P.own_stride = reinterpret_cast<const uint64_t*>(pb + o_ost);
+  P.layer_group = reinterpret_cast<const uint32_t*>(pb + o_lg);
 
   // ---- per-rank arenas
   for (uint32_t r = 0; r < N; ++r) c->peer_layout[r] = peer_layout_of(c, r);
@@ -548,16 +566,22 @@ int p3_layer_ready(p3_ctx_t* c, uint32_t li, uint32_t layer, uint64_t k, const f
   const LocalDev& D = c->loc[li];
   CUstream s = (CUstream)stream;
   CUresult r = CUDA_SUCCESS;
-  if (c->cfg.sched == P3_SCHED_FIFO) r = d.write32(s, (CUdeviceptr)(D.fifo_key + layer), c->fifo_seq[li]++, 0);
+  if (c->cfg.sched == P3_SCHED_FIFO)
+    r = d.write32(s, (CUdeviceptr)(D.fifo_key + layer), c->fifo_seq[li]++, CU_STREAM_WRITE_VALUE_NO_MEMORY_BARRIER);
   // one stream-ordered write publishes the slices of the layer (FrameQueue.put_batch is
   // atomic, queues.py:44-50): the iteration tag and the gradient pointer in one word
   const uint64_t word = (((k + 1) & 0xffffull) << 48) | gp;
+  // The write follows the kernel that produced the gradient in stream order and its only
+  // consumer is this device's comm kernel (peers read pushed copies, fenced by the comm
+  // kernel), so the system-scope flush of the default write is not needed: it costs ~3 us
+  // of stream time per layer (measured, tools/exp_memop_cost.py).
+  const unsigned nb = CU_STREAM_WRITE_VALUE_NO_MEMORY_BARRIER;
   if (r == CUDA_SUCCESS) {
     if (d.has64) {
-      r = d.write64(s, (CUdeviceptr)(D.pub + layer), word, 0);
+      r = d.write64(s, (CUdeviceptr)(D.pub + layer), word, nb);
     } else {  // low half (pointer) first, then the half holding the tag
-      r = d.write32(s, (CUdeviceptr)(D.pub + layer), (cuuint32_t)(word & 0xffffffffu), 0);
-      if (r == CUDA_SUCCESS) r = d.write32(s, (CUdeviceptr)(D.pub + layer) + 4, (cuuint32_t)(word >> 32), 0);
+      r = d.write32(s, (CUdeviceptr)(D.pub + layer), (cuuint32_t)(word & 0xffffffffu), nb);
+      if (r == CUDA_SUCCESS) r = d.write32(s, (CUdeviceptr)(D.pub + layer) + 4, (cuuint32_t)(word >> 32), nb);
     }
   }
   if (r != CUDA_SUCCESS) return fail(c, P3_ECUDA, "cuStreamWriteValue failed (code " + std::to_string(r) + ")");
@@ -591,6 +615,18 @@ int p3_wait_layer(p3_ctx_t* c, uint32_t li, uint32_t layer, uint64_t k, void* st
   if (k == 0) return P3_OK;  // forward pass 0 reads the initial parameters
   const uint32_t target = (uint32_t)(k * c->layer_nslices[layer]);
   uint32_t* flag = c->peers.done[c->cfg.local_ranks[li]] + layer;
+  CUresult r = driver().wait32((CUstream)stream, (CUdeviceptr)flag, target, CU_STREAM_WAIT_VALUE_GEQ);
+  if (r != CUDA_SUCCESS) return fail(c, P3_ECUDA, "cuStreamWaitValue32 failed (code " + std::to_string(r) + ")");
+  return P3_OK;
+}
+
+int p3_wait_group(p3_ctx_t* c, uint32_t li, uint32_t group, uint64_t k, void* stream) {
+  int rc = check_local(c, li);
+  if (rc) return rc;
+  if (group >= c->G) return fail(c, P3_EUSAGE, "gate group out of range");
+  if (k == 0) return P3_OK;
+  const uint32_t target = (uint32_t)(k * c->group_slices[group]);
+  uint32_t* flag = c->peers.gdone[c->cfg.local_ranks[li]] + group;
   CUresult r = driver().wait32((CUstream)stream, (CUdeviceptr)flag, target, CU_STREAM_WAIT_VALUE_GEQ);
   if (r != CUDA_SUCCESS) return fail(c, P3_ECUDA, "cuStreamWaitValue32 failed (code " + std::to_string(r) + ")");
   return P3_OK;

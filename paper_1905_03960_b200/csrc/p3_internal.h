@@ -45,6 +45,7 @@ struct PlanDev {
   const uint32_t* own_lcount;     // [world*L] owned slices of (owner, layer)
   const uint32_t* own_total;      // [world] owned slices per owner
   const uint64_t* own_stride;     // [world] R block stride (padded owned elements)
+  const uint32_t* layer_group;    // [L] forward-gate group of the layer
 };
 
 // Peer-visible state of every rank (pointers valid in this process: local or IPC-mapped).
@@ -54,6 +55,7 @@ struct PeersDev {
   uint32_t* arrivals[P3_MAX_RANKS];  // [S] pushes received per owned slice (monotone)
   uint32_t* hint[P3_MAX_RANKS];      // [L] owned slices completed per layer (monotone)
   uint32_t* done[P3_MAX_RANKS];      // [L] slices of a layer broadcast into W (monotone)
+  uint32_t* gdone[P3_MAX_RANKS];     // [G] slices of a gate group broadcast into W (monotone)
 };
 
 // Per-iteration scratch of one local rank; zeroed before each comm launch.

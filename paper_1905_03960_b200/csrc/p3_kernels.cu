@@ -701,7 +701,11 @@ __device__ void signal_job(const CommArgs& a, const Job& j) {
     if (old + 1 == (a.k + 1) * P.world) red_add_relaxed_sys(a.peers.hint[j.rank] + j.layer, 1u);
     atomicAdd(L.bytes + 1, 4ull * j.len);
   } else {
-    for (uint32_t q = 0; q < j.n; ++q) red_add_relaxed_sys(a.peers.done[q] + j.layer, 1u);
+    const uint32_t grp = P.layer_group[j.layer];
+    for (uint32_t q = 0; q < j.n; ++q) {
+      red_add_relaxed_sys(a.peers.done[q] + j.layer, 1u);
+      red_add_relaxed_sys(a.peers.gdone[q] + grp, 1u);
+    }
     atomicAdd(L.bytes + 0, 4ull * j.len * (j.n - 1));  // pushes received
     atomicAdd(L.bytes + 1, 4ull * j.len * (j.n - 1));  // broadcasts sent
     trace_append(L, a.k, j.layer, j.g - P.layer_first[j.layer], j.rank, P3_EV_BCAST);
@@ -775,7 +779,10 @@ __global__ void __launch_bounds__(512, 1) k_comm(const __grid_constant__ CommArg
               a.err[3 + 2 * t] = ld_relaxed_gpu(&a.loc[t].it->reduced);
             }
             for (uint32_t t = 0; t < a.n_local; ++t)
-              for (uint32_t l = 0; l < a.plan.n_layers; ++l) atomicAdd(a.peers.done[a.loc[t].rank] + l, 0x40000000u);
+              for (uint32_t l = 0; l < a.plan.n_layers; ++l) {
+                atomicAdd(a.peers.done[a.loc[t].rank] + l, 0x40000000u);
+                atomicAdd(a.peers.gdone[a.loc[t].rank] + a.plan.layer_group[l], 0x40000000u);
+              }
           }
         }
         verdict = __shfl_sync(FULL_MASK, verdict, 0);

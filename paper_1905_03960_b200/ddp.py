@@ -133,11 +133,19 @@ class P3DataParallel(_HookedDataParallel):
         super().__init__(module)
         self.lr = lr
         counts = [p.numel() for p in self.params]
+        # one forward gate per module: all parameters a module owns share a gate group
+        self._module_layers = _param_modules(module, self.params)
+        groups = [0] * len(self.params)
+        for gi, (_, layers) in enumerate(self._module_layers):
+            for l in layers:
+                groups[l] = gi
+        self._group_of = groups
         self.ctx = SyncContext(
             counts, self.world, [self.rank], max_slice=max_slice, lr=lr, momentum=momentum,
             priority_mode=priority_mode, comm_ctas=comm_ctas, comm_threads=comm_threads,
             timeout_s=timeout_s, trace_cap=trace_cap, drain_bytes=drain_bytes, plan_mode=plan_mode,
             throttle_bps=throttle_bps, throttle_burst=throttle_burst, big_threshold=big_threshold,
+            gate_groups=groups,
         )
         if self.world > 1:
             handles = [None] * self.world
@@ -178,6 +186,16 @@ class P3DataParallel(_HookedDataParallel):
 
     def _gate(self, l: int) -> None:
         self.ctx.wait_layer(0, l, self.k)
+
+    def _make_gate(self, layers):
+        group = self._group_of[layers[0]]
+
+        def hook(mod, inputs):
+            if layers[0] not in self._gated:
+                self.ctx.wait_group(0, group, self.k)
+                self._gated.update(layers)
+
+        return hook
 
     def _publish(self, l: int, grad) -> None:
         p = self.params[l]

@@ -68,6 +68,7 @@ class SyncContext:
         rng_seed: int = 0,
         throttle_bps: float = 0.0,
         throttle_burst: int = 50 * 1024,
+        gate_groups: list[int] | None = None,
     ) -> None:
         import torch
 
@@ -96,6 +97,11 @@ class SyncContext:
         cfg.rng_seed = rng_seed
         cfg.throttle_bps = throttle_bps or 0.0
         cfg.throttle_burst = throttle_burst
+        if gate_groups is not None:
+            if len(gate_groups) != len(self.layer_counts):
+                raise ValueError("gate_groups needs one group id per layer")
+            self._groups = (ctypes.c_uint32 * len(gate_groups))(*gate_groups)
+            cfg.gate_groups = ctypes.cast(self._groups, ctypes.POINTER(ctypes.c_uint32))
         cfg.sched = _lib.P3_SCHED_PRIORITY if priority_mode else _lib.P3_SCHED_FIFO
         cfg.lr = lr
         cfg.momentum = momentum
@@ -178,6 +184,9 @@ class SyncContext:
 
     def wait_layer(self, li: int, layer: int, k: int, stream=None) -> None:
         self._check(self.lib.p3_wait_layer(self._h, li, layer, k, _lib.stream_handle(stream)), "p3_wait_layer")
+
+    def wait_group(self, li: int, group: int, k: int, stream=None) -> None:
+        self._check(self.lib.p3_wait_group(self._h, li, group, k, _lib.stream_handle(stream)), "p3_wait_group")
 
     def sync_all(self, k: int, timeout_s: float | None = None) -> None:
         self._check(self.lib.p3_sync_all(self._h, k, self.timeout_s if timeout_s is None else timeout_s), "p3_sync_all")
