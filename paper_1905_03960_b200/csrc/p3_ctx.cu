@@ -535,6 +535,7 @@ int p3_iteration_begin(p3_ctx_t* c, uint64_t k, void* stream) {
   for (uint32_t i = 0; i < c->cfg.n_local; ++i)
     CK(cudaMemsetAsync(static_cast<char*>(c->local_arena[i]) + ll.iter_begin, 0, ll.iter_end - ll.iter_begin, s));
   c->comm_stream = s;
+  for (uint32_t i = 0; i < c->cfg.n_local; ++i) c->fifo_seq[i] = 0;
   c->open_iter = k;
   c->iter_open = true;
   return P3_OK;
@@ -561,29 +562,26 @@ int p3_layer_ready(p3_ctx_t* c, uint32_t li, uint32_t layer, uint64_t k, const f
     grad = c->grads[li] + c->layer_woff[layer];
   }
   const uint64_t gp = (uint64_t)(uintptr_t)grad;
-  if (gp >> 48) return fail(c, P3_EUSAGE, "gradient pointer does not fit the 48-bit publication word");
+  if ((gp >> 48) || (gp & 255))
+    return fail(c, P3_EUSAGE, "gradient pointer must be 256-byte aligned and below 2^48");
   Driver& d = driver();
   const LocalDev& D = c->loc[li];
   CUstream s = (CUstream)stream;
-  CUresult r = CUDA_SUCCESS;
-  if (c->cfg.sched == P3_SCHED_FIFO)
-    r = d.write32(s, (CUdeviceptr)(D.fifo_key + layer), c->fifo_seq[li]++, CU_STREAM_WRITE_VALUE_NO_MEMORY_BARRIER);
-  // one stream-ordered write publishes the slices of the layer (FrameQueue.put_batch is
-  // atomic, queues.py:44-50): the iteration tag and the gradient pointer in one word
-  const uint64_t word = (((k + 1) & 0xffffull) << 48) | gp;
-  // The write follows the kernel that produced the gradient in stream order and its only
+  // Both writes follow the kernel that produced the gradient in stream order and their only
   // consumer is this device's comm kernel (peers read pushed copies, fenced by the comm
-  // kernel), so the system-scope flush of the default write is not needed: it costs ~3 us
-  // of stream time per layer (measured, tools/exp_memop_cost.py).
+  // kernel), so the system-scope flush of the default write is not needed: it costs ~3 us of
+  // stream time per layer (measured, tools/exp_memop_cost.py). Without it the two halves may
+  // land in either order; each carries the tag (see pub_ready in p3_kernels.cu).
   const unsigned nb = CU_STREAM_WRITE_VALUE_NO_MEMORY_BARRIER;
-  if (r == CUDA_SUCCESS) {
-    if (d.has64) {
-      r = d.write64(s, (CUdeviceptr)(D.pub + layer), word, nb);
-    } else {  // low half (pointer) first, then the half holding the tag
-      r = d.write32(s, (CUdeviceptr)(D.pub + layer), (cuuint32_t)(word & 0xffffffffu), nb);
-      if (r == CUDA_SUCCESS) r = d.write32(s, (CUdeviceptr)(D.pub + layer) + 4, (cuuint32_t)(word >> 32), nb);
-    }
-  }
+  CUresult r = CUDA_SUCCESS;
+  // FrameQueue.put_batch is atomic (queues.py:44-50): the layer's slices become poppable at once
+  const uint32_t tag = (uint32_t)((k + 1) & 0xfffu) << 20;
+  // FIFO discipline: the publish sequence of this iteration, tagged like the halves below
+  if (c->cfg.sched == P3_SCHED_FIFO)
+    r = d.write32(s, (CUdeviceptr)(D.fifo_key + layer), tag | (c->fifo_seq[li]++ & 0xfffffu), nb);
+  const uint32_t lo = tag | (uint32_t)((gp >> 8) & 0xfffffu), hi = tag | (uint32_t)((gp >> 28) & 0xfffffu);
+  if (r == CUDA_SUCCESS) r = d.write32(s, (CUdeviceptr)(D.pub + layer), lo, nb);
+  if (r == CUDA_SUCCESS) r = d.write32(s, (CUdeviceptr)(D.pub + layer) + 4, hi, nb);
   if (r != CUDA_SUCCESS) return fail(c, P3_ECUDA, "cuStreamWriteValue failed (code " + std::to_string(r) + ")");
   c->published[li] += 4ull * c->counts[layer];
   if (c->iter_open && c->open_iter == k && c->published[li] >= c->cfg.drain_bytes) {
@@ -657,7 +655,7 @@ int p3_sync_all(p3_ctx_t* c, uint64_t k, double timeout_s) {
       cudaMemcpyAsync(pub.data(), c->loc[i].pub, c->L * 8ull, cudaMemcpyDeviceToHost, c->poll_stream);
       cudaStreamSynchronize(c->poll_stream);
       uint32_t nready = 0;
-      for (uint32_t l = 0; l < c->L; ++l) nready += (uint32_t)(pub[l] >> 48) == ((ew[1] + 1) & 0xffffu);
+      for (uint32_t l = 0; l < c->L; ++l) nready += (uint32_t)(pub[l] >> 52) == ((ew[1] + 1) & 0xfffu);
       m += " rank " + std::to_string(c->cfg.local_ranks[i]) + ": pushed " + std::to_string(ew[2 + 2 * i]) + "/" +
            std::to_string(c->S) + " reduced " + std::to_string(ew[3 + 2 * i]) + "/" +
            std::to_string(c->own_total[c->cfg.local_ranks[i]]) + " ready layers " + std::to_string(nready) + "/" +
@@ -750,7 +748,7 @@ int p3_debug_snapshot(p3_ctx_t* c, uint32_t li, uint32_t* out, uint64_t cap, uin
   CK(cudaMemcpyAsync(tail, c->peers.arrivals[rank], c->S * 4ull, cudaMemcpyDeviceToHost, c->poll_stream));
   CK(cudaMemcpyAsync(tail + c->S, D.claim, c->S * 4ull, cudaMemcpyDeviceToHost, c->poll_stream));
   CK(cudaStreamSynchronize(c->poll_stream));
-  for (uint32_t l = 0; l < c->L; ++l) out[l] = (uint32_t)(pub[l] >> 48);  // iteration tag
+  for (uint32_t l = 0; l < c->L; ++l) out[l] = (uint32_t)(pub[l] >> 52);  // iteration tag (12 bits)
   return P3_OK;
 }
 
@@ -803,8 +801,8 @@ int p3_queue_create(const uint32_t* layer_nslices, uint32_t n_layers, uint32_t s
 int p3_queue_put_layer(p3_queue_t* q, uint32_t layer, uint32_t iteration) {
   p3_ctx* c = nullptr;
   if (!q || layer >= q->L) return fail(nullptr, P3_EUSAGE, "layer out of range");
-  const uint32_t tag = iteration + 1, zero = 0, key = q->seq++;
-  const uint64_t word = ((uint64_t)(tag & 0xffffu)) << 48;
+  const uint32_t tag = iteration + 1, zero = 0, key = ((tag & 0xfffu) << 20) | (q->seq++ & 0xfffffu);
+  const uint64_t word = ((uint64_t)(tag & 0xfffu) << 52) | ((uint64_t)(tag & 0xfffu) << 20);
   CK(cudaMemcpyAsync(q->d_cursor + layer, &zero, 4, cudaMemcpyHostToDevice, q->s));
   CK(cudaMemcpyAsync(q->d_fifo + layer, &key, 4, cudaMemcpyHostToDevice, q->s));
   CK(cudaMemcpyAsync(q->d_pub + layer, &word, 8, cudaMemcpyHostToDevice, q->s));

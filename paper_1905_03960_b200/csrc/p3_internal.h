@@ -73,7 +73,7 @@ struct IterState {
 struct LocalDev {
   uint32_t rank;
   uint32_t trace_cap;
-  uint64_t* pub;        // [L] (iteration tag (k+1) & 0xffff) << 48 | gradient pointer
+  uint64_t* pub;        // [L] publication word: iteration tag + 256-B aligned gradient pointer
   uint32_t* fifo_key;   // [L] publish sequence (FIFO discipline)
   uint32_t* claim;      // [S] server claim tag (monotone: k -> k+1)
   uint32_t* cursor;     // [L] worker claim cursor (per iteration)

@@ -340,9 +340,18 @@ struct QueueView {
   uint32_t* cursor;
 };
 
-__device__ __forceinline__ bool pub_ready(uint64_t w, uint32_t tag) { return (uint32_t)(w >> 48) == (tag & 0xffffu); }
+// Publication word: two 32-bit halves, each (tag12 << 20 | 20 pointer bits) — bits 27..8
+// of the 256-byte aligned gradient pointer in the low half, bits 47..28 in the high half.
+// Each half is written by its own stream memory write, and the two may land in either
+// order (no memory barrier), so a layer counts as published only when BOTH halves carry
+// the iteration's tag.
+__device__ __forceinline__ bool pub_ready(uint64_t w, uint32_t tag) {
+  const uint32_t t = tag & 0xfffu;
+  return (uint32_t)(w >> 20 & 0xfffu) == t && (uint32_t)(w >> 52) == t;
+}
 __device__ __forceinline__ const float* pub_ptr(uint64_t w) {
-  return reinterpret_cast<const float*>(w & 0x0000ffffffffffffull);
+  const uint64_t lo = w & 0xfffffull, hi = (w >> 32) & 0xfffffull;
+  return reinterpret_cast<const float*>((hi << 28) | (lo << 8));
 }
 
 // Executed by one full warp; returns the popped global slice id or P3_NONE.
@@ -385,7 +394,9 @@ __device__ uint32_t warp_pop(const QueueView& q, uint32_t tag, uint32_t* dbg = n
     for (uint32_t l = lane; l < q.n_layers; l += 32) {
       if (!pub_ready(ld_relaxed_gpu64(q.pub + l), tag)) continue;
       if (ld_relaxed_gpu(q.cursor + l) >= q.nslices[l]) continue;
-      const uint32_t key = ld_relaxed_gpu(q.fifo_key + l);
+      const uint32_t fk = ld_relaxed_gpu(q.fifo_key + l);
+      if ((fk >> 20) != (tag & 0xfffu)) continue;  // sequence of this iteration not visible yet
+      const uint32_t key = fk & 0xfffffu;
       if (key < best_key || (key == best_key && l < best_l)) {
         best_key = key;
         best_l = l;

@@ -199,7 +199,7 @@ class P3DataParallel(_HookedDataParallel):
 
     def _publish(self, l: int, grad) -> None:
         p = self.params[l]
-        if grad.dtype != torch.float32 or grad.stride() != p.stride():
+        if grad.dtype != torch.float32 or grad.stride() != p.stride() or grad.data_ptr() % 256:
             grad = _relayout(grad, p)
             p.grad = grad
         self.ctx.layer_ready(0, l, self.k, grad)
