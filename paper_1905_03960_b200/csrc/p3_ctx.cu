@@ -3,6 +3,7 @@
 // the per-iteration launch of the comm kernel.
 #include <cuda.h>
 #include <cuda_runtime.h>
+#include <dlfcn.h>
 
 #include <algorithm>
 #include <chrono>
@@ -39,6 +40,21 @@ static Driver& driver() {
   static Driver d;
   static std::once_flag once;
   std::call_once(once, [] {
+    // the v2 stream memory operations (CUDA >= 11.7 semantics, incl. NO_MEMORY_BARRIER on
+    // writes) straight from the driver library the runtime already loaded
+    if (void* h = dlopen("libcuda.so.1", RTLD_NOW | RTLD_NOLOAD)) {
+      d.wait32 = (PFN_wait32)dlsym(h, "cuStreamWaitValue32_v2");
+      d.write32 = (PFN_write32)dlsym(h, "cuStreamWriteValue32_v2");
+      d.write64 = (PFN_write64)dlsym(h, "cuStreamWriteValue64_v2");
+      d.attr = (PFN_attr)dlsym(h, "cuDeviceGetAttribute");
+      if (d.wait32 && d.write32 && d.write64 && d.attr) {
+        d.ok = true;
+        int dev = 0, v = 0;
+        cudaGetDevice(&dev);
+        if (d.attr(&v, CU_DEVICE_ATTRIBUTE_CAN_USE_64_BIT_STREAM_MEM_OPS, dev) == CUDA_SUCCESS) d.has64 = v != 0;
+        return;
+      }
+    }
     cudaDriverEntryPointQueryResult q;
     void* fp = nullptr;
     bool ok = true;
