@@ -42,7 +42,7 @@ def parse_args():
     ap.add_argument("--model", choices=["resnet50", "vgg19", "seq2seq"], default="resnet50")
     ap.add_argument("--batch", type=int, default=0, help="per-GPU batch (default per model)")
     ap.add_argument("--max-slice", type=int, default=50_000)
-    ap.add_argument("--comm-ctas", type=int, default=16)
+    ap.add_argument("--comm-ctas", type=int, default=8)
     ap.add_argument("--lr", type=float, default=0.01)
     ap.add_argument("--skip-layerwise", action="store_true")
     ap.add_argument("--skip-cpu", action="store_true")

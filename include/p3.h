@@ -186,13 +186,15 @@ int p3_ctx_grads(p3_ctx_t* ctx, uint32_t local_idx, float** grads_dev);
 int p3_iteration_begin(p3_ctx_t* ctx, uint64_t iteration, void* comm_stream);
 
 /* TrainingWorker.enqueue_layer (worker.py:173-182): publish all slices of `layer` for
- * `iteration` atomically with stream-ordered writes on `stream` (gradient pointer, then
- * the iteration tag). `grad_dev` is the layer's fp32 gradient (param_count elements);
- * NULL = the context's gradient arena. When an iteration is open, the comm stream then
- * waits for this point of `stream` and launches the comm kernel in DRAIN mode: it pops
- * the most urgent published slices (including layers published while it runs: slice-
- * granular preemption), reduces owned slices whose pushes are complete, and exits once
- * nothing is poppable — it never spins on compute that has not been published. */
+ * `iteration` atomically (one word: iteration tag + gradient pointer). `grad_dev` is the
+ * layer's fp32 gradient (param_count elements); NULL = the context's gradient arena.
+ * When an iteration is open, the comm stream is ordered after this point of `stream` (an
+ * event) and the publication rides on the next comm launch; once `drain_bytes` of
+ * gradients (or 40 layers) are pending, a DRAIN launch is issued: it publishes its batch,
+ * pops the most urgent published slices (including layers published while it runs:
+ * slice-granular preemption), reduces owned slices whose pushes are complete, and exits
+ * once nothing is poppable — it never spins on compute that has not been published.
+ * Outside an open iteration the word is written at once with a stream memory write. */
 int p3_layer_ready(p3_ctx_t* ctx, uint32_t local_idx, uint32_t layer, uint64_t iteration,
                    const float* grad_dev, void* stream);
 

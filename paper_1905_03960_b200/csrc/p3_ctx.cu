@@ -4,6 +4,8 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <dlfcn.h>
+#include <cstdio>
+#include <cstdlib>
 
 #include <algorithm>
 #include <chrono>
@@ -132,6 +134,10 @@ struct p3_ctx {
   bool iter_open = false;
   uint64_t launches = 0;
   uint64_t published[P3_MAX_LOCAL]{};  // gradient bytes published since the last DRAIN launch
+  // publications waiting for the next comm launch of a local rank (batched publication)
+  std::vector<uint32_t> pend_layer[P3_MAX_LOCAL], pend_key[P3_MAX_LOCAL];
+  std::vector<unsigned long long> pend_word[P3_MAX_LOCAL];
+  cudaStream_t pend_stream[P3_MAX_LOCAL]{};
   bool comm_pending = false;
   uint64_t synced_iterations = 0;
   std::string err;
@@ -243,7 +249,8 @@ int p3_ctx_create(const p3_config_t* cfg, p3_ctx_t** out) {
   p3_ctx* c = nullptr;
   if (!cfg || !out) return fail(nullptr, P3_EUSAGE, "null argument");
   if (cfg->world < 1 || cfg->world > P3_MAX_RANKS) return fail(nullptr, P3_EUSAGE, "world must be in [1, 16]");
-  if (cfg->n_local < 1 || cfg->n_local > cfg->world) return fail(nullptr, P3_EUSAGE, "bad n_local");
+  if (cfg->n_local < 1 || cfg->n_local > cfg->world || cfg->n_local > P3_MAX_LOCAL)
+    return fail(nullptr, P3_EUSAGE, "bad n_local (1..min(world, 8))");
   if (cfg->n_layers < 1 || !cfg->layer_counts) return fail(nullptr, P3_EUSAGE, "profile needs at least one layer");
   if (cfg->plan_mode != P3_PLAN_P3 && cfg->plan_mode != P3_PLAN_BASELINE) return fail(nullptr, P3_EUSAGE, "bad plan_mode");
   if (cfg->throttle_bps < 0) return fail(nullptr, P3_EUSAGE, "throttle rate must be >= 0 (0 disables shaping)");
@@ -540,6 +547,31 @@ static CommArgs comm_args(p3_ctx* c, uint32_t mode) {
   return a;
 }
 
+// Launch the comm kernel on the comm stream carrying local rank li's pending publications.
+static int launch_with_batch(p3_ctx* c, uint32_t mode, int li) {
+  CommArgs a = comm_args(c, mode);
+  if (li >= 0) {
+    // order the comm stream after everything submitted so far on the producing stream
+    CK(cudaEventRecord(c->ready_ev[li], c->pend_stream[li]));
+    CK(cudaStreamWaitEvent(c->comm_stream, c->ready_ev[li], 0));
+    a.pub_li = (uint32_t)li;
+    a.pub_n = (uint32_t)c->pend_layer[li].size();
+    for (uint32_t i = 0; i < a.pub_n; ++i) {
+      a.pub_layer[i] = c->pend_layer[li][i];
+      a.pub_key[i] = c->pend_key[li][i];
+      a.pub_word[i] = c->pend_word[li][i];
+    }
+    c->pend_layer[li].clear();
+    c->pend_key[li].clear();
+    c->pend_word[li].clear();
+    c->published[li] = 0;
+  }
+  if (launch_comm(a, c->cfg.comm_ctas, c->cfg.comm_threads, c->comm_stream) != P3_OK)
+    return cuda_fail(c, cudaGetLastError(), "comm kernel launch");
+  c->launches++;
+  return P3_OK;
+}
+
 int p3_iteration_begin(p3_ctx_t* c, uint64_t k, void* stream) {
   if (!c) return fail(nullptr, P3_EUSAGE, "null context");
   if (k >= 0x3fffffffull) return fail(c, P3_EUSAGE, "iteration out of range");
@@ -551,7 +583,6 @@ int p3_iteration_begin(p3_ctx_t* c, uint64_t k, void* stream) {
   for (uint32_t i = 0; i < c->cfg.n_local; ++i)
     CK(cudaMemsetAsync(static_cast<char*>(c->local_arena[i]) + ll.iter_begin, 0, ll.iter_end - ll.iter_begin, s));
   c->comm_stream = s;
-  for (uint32_t i = 0; i < c->cfg.n_local; ++i) c->fifo_seq[i] = 0;
   c->open_iter = k;
   c->iter_open = true;
   return P3_OK;
@@ -560,10 +591,20 @@ int p3_iteration_begin(p3_ctx_t* c, uint64_t k, void* stream) {
 int p3_iteration_end(p3_ctx_t* c, uint64_t k) {
   if (!c) return fail(nullptr, P3_EUSAGE, "null context");
   if (!c->iter_open || c->open_iter != k) return fail(c, P3_EUSAGE, "iteration not open");
-  if (launch_comm(comm_args(c, P3_COMM_FINISH), c->cfg.comm_ctas, c->cfg.comm_threads, c->comm_stream) != P3_OK)
-    return cuda_fail(c, cudaGetLastError(), "comm kernel launch");
+  // publications still pending: every local rank but the last drains its own batch, the
+  // FINISH launch carries the last one
+  int last = -1;
+  for (uint32_t i = 0; i < c->cfg.n_local; ++i) {
+    if (c->pend_layer[i].empty()) continue;
+    if (last >= 0) {
+      int rc = launch_with_batch(c, P3_COMM_DRAIN, last);
+      if (rc) return rc;
+    }
+    last = (int)i;
+  }
+  int rc = launch_with_batch(c, P3_COMM_FINISH, last);
+  if (rc) return rc;
   CK(cudaEventRecord(c->comm_done, c->comm_stream));
-  c->launches++;
   c->comm_pending = true;
   c->iter_open = false;
   return P3_OK;
@@ -578,37 +619,38 @@ int p3_layer_ready(p3_ctx_t* c, uint32_t li, uint32_t layer, uint64_t k, const f
     grad = c->grads[li] + c->layer_woff[layer];
   }
   const uint64_t gp = (uint64_t)(uintptr_t)grad;
-  if ((gp >> 48) || (gp & 255))
-    return fail(c, P3_EUSAGE, "gradient pointer must be 256-byte aligned and below 2^48");
+  if (gp >> 48) return fail(c, P3_EUSAGE, "gradient pointer does not fit the 48-bit publication word");
+  // FrameQueue.put_batch is atomic (queues.py:44-50): one word makes every slice of the layer
+  // poppable — the iteration tag and the gradient pointer together
+  const uint64_t word = (((k + 1) & 0xffffull) << 48) | gp;
+  if (c->iter_open && c->open_iter == k) {
+    // Batched publication: the layer becomes poppable when the comm launch that carries it
+    // starts — stream-ordered after this point of `stream` by an event — so no stream memory
+    // write is needed (each costs ~3 us of stream time, tools/exp_memop_cost.py).
+    c->pend_layer[li].push_back(layer);
+    c->pend_key[li].push_back(c->fifo_seq[li]++);
+    c->pend_word[li].push_back(word);
+    c->published[li] += 4ull * c->counts[layer];
+    c->pend_stream[li] = (cudaStream_t)stream;
+    if (c->published[li] >= c->cfg.drain_bytes || c->pend_layer[li].size() == P3_PUB_BATCH)
+      return launch_with_batch(c, P3_COMM_DRAIN, (int)li);
+    return P3_OK;
+  }
+  // no iteration open: publish right away with stream memory writes on `stream`
   Driver& d = driver();
   const LocalDev& D = c->loc[li];
   CUstream s = (CUstream)stream;
-  // Both writes follow the kernel that produced the gradient in stream order and their only
-  // consumer is this device's comm kernel (peers read pushed copies, fenced by the comm
-  // kernel), so the system-scope flush of the default write is not needed: it costs ~3 us of
-  // stream time per layer (measured, tools/exp_memop_cost.py). Without it the two halves may
-  // land in either order; each carries the tag (see pub_ready in p3_kernels.cu).
-  const unsigned nb = CU_STREAM_WRITE_VALUE_NO_MEMORY_BARRIER;
   CUresult r = CUDA_SUCCESS;
-  // FrameQueue.put_batch is atomic (queues.py:44-50): the layer's slices become poppable at once
-  const uint32_t tag = (uint32_t)((k + 1) & 0xfffu) << 20;
-  // FIFO discipline: the publish sequence of this iteration, tagged like the halves below
-  if (c->cfg.sched == P3_SCHED_FIFO)
-    r = d.write32(s, (CUdeviceptr)(D.fifo_key + layer), tag | (c->fifo_seq[li]++ & 0xfffffu), nb);
-  const uint32_t lo = tag | (uint32_t)((gp >> 8) & 0xfffffu), hi = tag | (uint32_t)((gp >> 28) & 0xfffffu);
-  if (r == CUDA_SUCCESS) r = d.write32(s, (CUdeviceptr)(D.pub + layer), lo, nb);
-  if (r == CUDA_SUCCESS) r = d.write32(s, (CUdeviceptr)(D.pub + layer) + 4, hi, nb);
-  if (r != CUDA_SUCCESS) return fail(c, P3_ECUDA, "cuStreamWriteValue failed (code " + std::to_string(r) + ")");
-  c->published[li] += 4ull * c->counts[layer];
-  if (c->iter_open && c->open_iter == k && c->published[li] >= c->cfg.drain_bytes) {
-    // the comm stream follows this publication point, then drains what is published
-    c->published[li] = 0;
-    CK(cudaEventRecord(c->ready_ev[li], (cudaStream_t)stream));
-    CK(cudaStreamWaitEvent(c->comm_stream, c->ready_ev[li], 0));
-    if (launch_comm(comm_args(c, P3_COMM_DRAIN), c->cfg.comm_ctas, c->cfg.comm_threads, c->comm_stream) != P3_OK)
-      return cuda_fail(c, cudaGetLastError(), "comm kernel launch");
-    c->launches++;
+  if (c->cfg.sched == P3_SCHED_FIFO) r = d.write32(s, (CUdeviceptr)(D.fifo_key + layer), c->fifo_seq[li]++, 0);
+  if (r == CUDA_SUCCESS) {
+    if (d.has64) {
+      r = d.write64(s, (CUdeviceptr)(D.pub + layer), word, 0);
+    } else {  // low half (pointer) first, then the half holding the tag
+      r = d.write32(s, (CUdeviceptr)(D.pub + layer), (cuuint32_t)(word & 0xffffffffu), 0);
+      if (r == CUDA_SUCCESS) r = d.write32(s, (CUdeviceptr)(D.pub + layer) + 4, (cuuint32_t)(word >> 32), 0);
+    }
   }
+  if (r != CUDA_SUCCESS) return fail(c, P3_ECUDA, "cuStreamWriteValue failed (code " + std::to_string(r) + ")");
   return P3_OK;
 }
 
@@ -671,7 +713,7 @@ int p3_sync_all(p3_ctx_t* c, uint64_t k, double timeout_s) {
       cudaMemcpyAsync(pub.data(), c->loc[i].pub, c->L * 8ull, cudaMemcpyDeviceToHost, c->poll_stream);
       cudaStreamSynchronize(c->poll_stream);
       uint32_t nready = 0;
-      for (uint32_t l = 0; l < c->L; ++l) nready += (uint32_t)(pub[l] >> 52) == ((ew[1] + 1) & 0xfffu);
+      for (uint32_t l = 0; l < c->L; ++l) nready += (uint32_t)(pub[l] >> 48) == ((ew[1] + 1) & 0xffffu);
       m += " rank " + std::to_string(c->cfg.local_ranks[i]) + ": pushed " + std::to_string(ew[2 + 2 * i]) + "/" +
            std::to_string(c->S) + " reduced " + std::to_string(ew[3 + 2 * i]) + "/" +
            std::to_string(c->own_total[c->cfg.local_ranks[i]]) + " ready layers " + std::to_string(nready) + "/" +
@@ -764,7 +806,7 @@ int p3_debug_snapshot(p3_ctx_t* c, uint32_t li, uint32_t* out, uint64_t cap, uin
   CK(cudaMemcpyAsync(tail, c->peers.arrivals[rank], c->S * 4ull, cudaMemcpyDeviceToHost, c->poll_stream));
   CK(cudaMemcpyAsync(tail + c->S, D.claim, c->S * 4ull, cudaMemcpyDeviceToHost, c->poll_stream));
   CK(cudaStreamSynchronize(c->poll_stream));
-  for (uint32_t l = 0; l < c->L; ++l) out[l] = (uint32_t)(pub[l] >> 52);  // iteration tag (12 bits)
+  for (uint32_t l = 0; l < c->L; ++l) out[l] = (uint32_t)(pub[l] >> 48);  // iteration tag
   return P3_OK;
 }
 
@@ -817,8 +859,8 @@ int p3_queue_create(const uint32_t* layer_nslices, uint32_t n_layers, uint32_t s
 int p3_queue_put_layer(p3_queue_t* q, uint32_t layer, uint32_t iteration) {
   p3_ctx* c = nullptr;
   if (!q || layer >= q->L) return fail(nullptr, P3_EUSAGE, "layer out of range");
-  const uint32_t tag = iteration + 1, zero = 0, key = ((tag & 0xfffu) << 20) | (q->seq++ & 0xfffffu);
-  const uint64_t word = ((uint64_t)(tag & 0xfffu) << 52) | ((uint64_t)(tag & 0xfffu) << 20);
+  const uint32_t tag = iteration + 1, zero = 0, key = q->seq++;
+  const uint64_t word = ((uint64_t)(tag & 0xffffu)) << 48;
   CK(cudaMemcpyAsync(q->d_cursor + layer, &zero, 4, cudaMemcpyHostToDevice, q->s));
   CK(cudaMemcpyAsync(q->d_fifo + layer, &key, 4, cudaMemcpyHostToDevice, q->s));
   CK(cudaMemcpyAsync(q->d_pub + layer, &word, 8, cudaMemcpyHostToDevice, q->s));

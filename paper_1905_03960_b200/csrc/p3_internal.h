@@ -8,7 +8,8 @@
 
 #include "../../include/p3.h"
 
-#define P3_MAX_LOCAL P3_MAX_RANKS
+#define P3_MAX_LOCAL 8      // ranks one process hosts (1 per GPU; up to 8 when emulating)
+#define P3_PUB_BATCH 40     // layer publications carried by one comm launch
 #define P3_DBG_CTAS 512
 #define P3_COMM_DRAIN 0   // exit as soon as nothing is poppable or reducible
 #define P3_COMM_FINISH 1  // exit when the iteration's local work is complete
@@ -99,6 +100,11 @@ struct CommArgs {
   uint32_t sched;
   float lr;
   float momentum;
+  uint32_t pub_li;    // layers published by this launch (of local rank pub_li): the
+  uint32_t pub_n;     // launch writes their publication words before its first pick
+  uint32_t pub_layer[P3_PUB_BATCH];
+  uint32_t pub_key[P3_PUB_BATCH];
+  unsigned long long pub_word[P3_PUB_BATCH];
   float ns_per_byte;  // K7 link emulation (0: unthrottled)
   unsigned long long burst_ns;
   unsigned long long timeout_ns;

@@ -340,18 +340,11 @@ struct QueueView {
   uint32_t* cursor;
 };
 
-// Publication word: two 32-bit halves, each (tag12 << 20 | 20 pointer bits) — bits 27..8
-// of the 256-byte aligned gradient pointer in the low half, bits 47..28 in the high half.
-// Each half is written by its own stream memory write, and the two may land in either
-// order (no memory barrier), so a layer counts as published only when BOTH halves carry
-// the iteration's tag.
-__device__ __forceinline__ bool pub_ready(uint64_t w, uint32_t tag) {
-  const uint32_t t = tag & 0xfffu;
-  return (uint32_t)(w >> 20 & 0xfffu) == t && (uint32_t)(w >> 52) == t;
-}
+// Publication word: iteration tag (16 bits) above the 48-bit gradient pointer, written by one
+// 64-bit stream memory write, so the tag and the pointer become visible together.
+__device__ __forceinline__ bool pub_ready(uint64_t w, uint32_t tag) { return (uint32_t)(w >> 48) == (tag & 0xffffu); }
 __device__ __forceinline__ const float* pub_ptr(uint64_t w) {
-  const uint64_t lo = w & 0xfffffull, hi = (w >> 32) & 0xfffffull;
-  return reinterpret_cast<const float*>((hi << 28) | (lo << 8));
+  return reinterpret_cast<const float*>(w & 0x0000ffffffffffffull);
 }
 
 // Executed by one full warp; returns the popped global slice id or P3_NONE.
@@ -394,9 +387,7 @@ __device__ uint32_t warp_pop(const QueueView& q, uint32_t tag, uint32_t* dbg = n
     for (uint32_t l = lane; l < q.n_layers; l += 32) {
       if (!pub_ready(ld_relaxed_gpu64(q.pub + l), tag)) continue;
       if (ld_relaxed_gpu(q.cursor + l) >= q.nslices[l]) continue;
-      const uint32_t fk = ld_relaxed_gpu(q.fifo_key + l);
-      if ((fk >> 20) != (tag & 0xfffu)) continue;  // sequence of this iteration not visible yet
-      const uint32_t key = fk & 0xfffffu;
+      const uint32_t key = ld_relaxed_gpu(q.fifo_key + l);
       if (key < best_key || (key == best_key && l < best_l)) {
         best_key = key;
         best_l = l;
@@ -743,6 +734,17 @@ __global__ void __launch_bounds__(512, 1) k_comm(const __grid_constant__ CommArg
   const uint32_t nthr = blockDim.x;
   const uint32_t movers = nthr - 64;
   IterState* stats = a.loc[0].it;
+  if (warp == 0 && a.pub_n) {
+    // publications carried by this launch (enqueue_layer, worker.py:173-182): the kernels that
+    // produced these gradients completed before this launch started (stream event), so the
+    // layers become poppable here. Every CTA writes the same words before its first pick.
+    const LocalDev& P = a.loc[a.pub_li];
+    for (uint32_t i = lane; i < a.pub_n; i += 32) {
+      if (a.sched == P3_SCHED_FIFO) P.fifo_key[a.pub_layer[i]] = a.pub_key[i];
+      *(volatile unsigned long long*)(P.pub + a.pub_layer[i]) = a.pub_word[i];
+    }
+    __syncwarp();
+  }
   if (warp == 0) {
     uint32_t* phase = (lane == 0 && blockIdx.x < P3_DBG_CTAS) ? a.loc[0].cta_phase + blockIdx.x : nullptr;
     const uint64_t t0 = globaltimer();

@@ -119,7 +119,7 @@ class P3DataParallel(_HookedDataParallel):
         lr: float,
         momentum: float = 0.0,
         max_slice: int = DEFAULT_MAX_SLICE,
-        comm_ctas: int = 16,
+        comm_ctas: int = 8,
         comm_threads: int = 512,
         timeout_s: float = 120.0,
         trace_cap: int = 0,
@@ -199,7 +199,7 @@ class P3DataParallel(_HookedDataParallel):
 
     def _publish(self, l: int, grad) -> None:
         p = self.params[l]
-        if grad.dtype != torch.float32 or grad.stride() != p.stride() or grad.data_ptr() % 256:
+        if grad.dtype != torch.float32 or grad.stride() != p.stride():
             grad = _relayout(grad, p)
             p.grad = grad
         self.ctx.layer_ready(0, l, self.k, grad)
