@@ -46,6 +46,8 @@ def parse_args():
     ap.add_argument("--lr", type=float, default=0.01)
     ap.add_argument("--skip-layerwise", action="store_true")
     ap.add_argument("--skip-cpu", action="store_true")
+    ap.add_argument("--skip-e2e", action="store_true")
+    ap.add_argument("--skip-sync", action="store_true")
     ap.add_argument("--sync-reps", type=int, default=10)
     ap.add_argument("--throttle-gbps", type=float, default=10.0,
                     help="emulated per-GPU egress for the P3 vs layer-wise comparison on the same kernels "
@@ -307,11 +309,13 @@ def run_ours(args):
     gpu_launches = (ddp.ctx.launches() - launches0) * args.steps // (args.steps + args.warmup)
 
     # --- e2e through the public API: pinned host batch copied in, loss copied out, every step
-    xh, yh = synthetic_batch(args.model, batch, seed=1234 + rank, pinned_host=True)
-    lh = [torch.empty((), dtype=torch.float32).pin_memory() for _ in range(args.steps)]
-    ms_e2e, _ = time_training(args, world, rank, ddp, None, None, args.steps, 1, e2e=(xh, yh, lh))
-    e2e_value = args.steps * batch * world / (ms_e2e / 1000.0)
-    h2d = xh.numel() * xh.element_size() + yh.numel() * yh.element_size()
+    e2e_value, h2d = None, 0
+    if not args.skip_e2e:
+        xh, yh = synthetic_batch(args.model, batch, seed=1234 + rank, pinned_host=True)
+        lh = [torch.empty((), dtype=torch.float32).pin_memory() for _ in range(args.steps)]
+        ms_e2e, _ = time_training(args, world, rank, ddp, None, None, args.steps, 1, e2e=(xh, yh, lh))
+        e2e_value = args.steps * batch * world / (ms_e2e / 1000.0)
+        h2d = xh.numel() * xh.element_size() + yh.numel() * yh.element_size()
     ddp.close()
     del ddp, model
     torch.cuda.empty_cache()
@@ -347,7 +351,7 @@ def run_ours(args):
         throttled["p3_vs_layerwise"] = throttled["p3"] / throttled["layerwise_fifo"]
 
     # --- slice-sync kernel roofline
-    sync_ms, ctas = sync_only_roofline(args, world, rank, counts)
+    sync_ms, ctas = sync_only_roofline(args, world, rank, counts) if not args.skip_sync else (float("nan"), 0)
     peaks = json.loads((REPO / "MEASURED_PEAKS.json").read_text()) if (REPO / "MEASURED_PEAKS.json").exists() else {}
     if world == 1:
         alg = 12 * P  # read G + read W + write W per element (SURVEY §8(d), K4 with N=1)
@@ -379,7 +383,8 @@ def run_ours(args):
                        "model": args.model, "per_gpu_batch": batch, "global_batch": batch * world,
                        "max_slice": args.max_slice, "comm_ctas": args.comm_ctas, "parallelism": f"dp{world}",
                        "params": P, "tensors": len(counts), "l2": "activations >> 126 MB L2 each step"},
-            "e2e": {"value": e2e_value, "unit": "samples/sec", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 4},
+            "e2e": {"value": e2e_value, "unit": "samples/sec", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 4}
+                   if e2e_value else None,
             "layerwise": layerwise,
             "p3_vs_layerwise": (value / layerwise["value"]) if layerwise else None,
             "throttled": throttled,
