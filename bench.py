@@ -341,7 +341,7 @@ def run_ours(args):
         throttled = {"gbps": args.throttle_gbps, "burst_bytes": 50 * 1024}
         for arm, kw in (("p3", {}), ("layerwise_fifo", {"plan_mode": "baseline", "priority_mode": False})):
             model = build(args, rank)
-            d = P3DataParallel(model, lr=args.lr, max_slice=args.max_slice, comm_ctas=4,
+            d = P3DataParallel(model, lr=args.lr, max_slice=args.max_slice, comm_ctas=4, pub_batch_bytes=0,
                                throttle_bps=args.throttle_gbps * 1e9, **kw)
             ms_t, _ = time_training(args, world, rank, d, x, y, max(3, args.steps // 2), 2)
             throttled[arm] = max(3, args.steps // 2) * batch * world / (ms_t / 1000.0)

@@ -154,6 +154,9 @@ typedef struct p3_config {
   double throttle_bps;                 /* K7 link emulation: per-rank egress rate in bit/s
                                           (TokenBucket, transport.py:22-55); 0 = full NVLink */
   uint64_t throttle_burst;             /* bucket depth in bytes (transport.py:18: 50 KiB) */
+  uint64_t pub_batch_bytes;            /* publish (one stream memory write of the ring tail)
+                                          once this many gradient bytes were enqueued
+                                          (0: every layer at once — finest preemption) */
   const uint32_t* gate_groups;         /* optional per-layer forward-gate group id (layers of
                                           one module gated together); NULL = one group per
                                           layer. Ids must be 0..G-1 */
@@ -188,13 +191,14 @@ int p3_iteration_begin(p3_ctx_t* ctx, uint64_t iteration, void* comm_stream);
 /* TrainingWorker.enqueue_layer (worker.py:173-182): publish all slices of `layer` for
  * `iteration` atomically (one word: iteration tag + gradient pointer). `grad_dev` is the
  * layer's fp32 gradient (param_count elements); NULL = the context's gradient arena.
- * When an iteration is open, the comm stream is ordered after this point of `stream` (an
- * event) and the publication rides on the next comm launch; once `drain_bytes` of
- * gradients (or 40 layers) are pending, a DRAIN launch is issued: it publishes its batch,
- * pops the most urgent published slices (including layers published while it runs:
- * slice-granular preemption), reduces owned slices whose pushes are complete, and exits
- * once nothing is poppable — it never spins on compute that has not been published.
- * Outside an open iteration the word is written at once with a stream memory write. */
+ * When an iteration is open the entry goes to a pinned, device-mapped ring; once
+ * `pub_batch_bytes` are pending one stream memory write on `stream` advances the ring tail
+ * (so the entries become visible only after the kernels that produced them), and any
+ * running comm kernel picks them up at its next pick (slice-granular preemption). Once
+ * `drain_bytes` are pending a DRAIN launch is queued on the comm stream behind this point
+ * of `stream`: it pops the most urgent published slices, reduces owned slices whose pushes
+ * are complete and exits once nothing is poppable — it never spins on compute that has not
+ * been published. Outside an open iteration the word is written at once. */
 int p3_layer_ready(p3_ctx_t* ctx, uint32_t local_idx, uint32_t layer, uint64_t iteration,
                    const float* grad_dev, void* stream);
 

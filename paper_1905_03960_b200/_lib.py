@@ -73,6 +73,7 @@ class Config(ctypes.Structure):
         ("rng_seed", ctypes.c_uint64),
         ("throttle_bps", ctypes.c_double),
         ("throttle_burst", ctypes.c_uint64),
+        ("pub_batch_bytes", ctypes.c_uint64),
         ("gate_groups", ctypes.POINTER(ctypes.c_uint32)),
     ]
 

@@ -97,7 +97,7 @@ struct PeerLayout {
 // contiguous so one memset resets it before each launch.
 struct LocalLayout {
   uint64_t pub, fifo_key, claim, iter_begin, cursor, srv_lo, srv_taken, it, iter_end, V, bytes,
-      trace_n, trace, cta_phase, vclock, total;
+      trace_n, trace, cta_phase, vclock, pubseq, ingested, total;
 };
 
 struct p3_ctx {
@@ -134,9 +134,11 @@ struct p3_ctx {
   bool iter_open = false;
   uint64_t launches = 0;
   uint64_t published[P3_MAX_LOCAL]{};  // gradient bytes published since the last DRAIN launch
-  // publications waiting for the next comm launch of a local rank (batched publication)
-  std::vector<uint32_t> pend_layer[P3_MAX_LOCAL], pend_key[P3_MAX_LOCAL];
-  std::vector<unsigned long long> pend_word[P3_MAX_LOCAL];
+  // publication ring (pinned, device-mapped) of each local rank
+  PubEntry* ring_host[P3_MAX_LOCAL]{};
+  uint32_t* ring_ingested_host[P3_MAX_LOCAL]{};
+  uint32_t ring_tail[P3_MAX_LOCAL]{}, ring_flushed[P3_MAX_LOCAL]{};
+  uint64_t pub_pending[P3_MAX_LOCAL]{};
   cudaStream_t pend_stream[P3_MAX_LOCAL]{};
   bool comm_pending = false;
   uint64_t synced_iterations = 0;
@@ -202,6 +204,8 @@ LocalLayout local_layout_of(const p3_ctx* c, uint64_t v_elems) {
   take(q.trace, (uint64_t)c->cfg.trace_cap * sizeof(p3_trace_rec_t));
   take(q.cta_phase, P3_DBG_CTAS * 4ull);
   take(q.vclock, 8);
+  take(q.pubseq, 4);
+  take(q.ingested, 4);
   q.total = o;
   return q;
 }
@@ -441,6 +445,25 @@ int p3_ctx_create(const p3_config_t* cfg, p3_ctx_t** out) {
     D.trace = reinterpret_cast<p3_trace_rec_t*>(lb + ll.trace);
     D.cta_phase = reinterpret_cast<uint32_t*>(lb + ll.cta_phase);
     D.vclock = reinterpret_cast<unsigned long long*>(lb + ll.vclock);
+    D.pubseq = reinterpret_cast<uint32_t*>(lb + ll.pubseq);
+    D.ingested = reinterpret_cast<uint32_t*>(lb + ll.ingested);
+    D.ring_cap = 4 * L + 64;
+    if (e == cudaSuccess)
+      e = cudaHostAlloc((void**)&c->ring_host[i], D.ring_cap * sizeof(PubEntry) + 256, cudaHostAllocMapped);
+    if (e == cudaSuccess) {
+      std::memset(c->ring_host[i], 0, D.ring_cap * sizeof(PubEntry) + 256);
+      c->ring_ingested_host[i] = reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(c->ring_host[i]) +
+                                                             D.ring_cap * sizeof(PubEntry));
+      void* dp = nullptr;
+      e = cudaHostGetDevicePointer(&dp, c->ring_host[i], 0);
+      D.ring = static_cast<const PubEntry*>(dp);
+      D.ingested_host = reinterpret_cast<uint32_t*>(static_cast<char*>(dp) + D.ring_cap * sizeof(PubEntry));
+    }
+    if (e != cudaSuccess) {
+      int r2 = cuda_fail(c, e, "publication ring");
+      p3_ctx_destroy(c);
+      return r2;
+    }
   }
   e = cudaEventCreateWithFlags(&c->comm_done, cudaEventDisableTiming);
   for (uint32_t i = 0; i < cfg->n_local && e == cudaSuccess; ++i)
@@ -465,6 +488,7 @@ int p3_ctx_destroy(p3_ctx_t* c) {
     if (c->peer_arena[i]) cudaFree(c->peer_arena[i]);
     if (c->local_arena[i]) cudaFree(c->local_arena[i]);
     if (c->grads[i]) cudaFree(c->grads[i]);
+    if (c->ring_host[i]) cudaFreeHost(c->ring_host[i]);
   }
   if (c->d_plan) cudaFree(c->d_plan);
   if (c->d_err) cudaFree(c->d_err);
@@ -547,26 +571,26 @@ static CommArgs comm_args(p3_ctx* c, uint32_t mode) {
   return a;
 }
 
-// Launch the comm kernel on the comm stream carrying local rank li's pending publications.
-static int launch_with_batch(p3_ctx* c, uint32_t mode, int li) {
-  CommArgs a = comm_args(c, mode);
+// Publish local rank li's ring entries up to its tail: one stream memory write of the tail,
+// ordered after the kernels that produced those gradients on their stream.
+static int flush_publications(p3_ctx* c, uint32_t li) {
+  if (c->ring_flushed[li] == c->ring_tail[li]) return P3_OK;
+  CUresult r = driver().write32((CUstream)c->pend_stream[li], (CUdeviceptr)c->loc[li].pubseq, c->ring_tail[li], 0);
+  if (r != CUDA_SUCCESS) return fail(c, P3_ECUDA, "cuStreamWriteValue32 failed (code " + std::to_string(r) + ")");
+  c->ring_flushed[li] = c->ring_tail[li];
+  c->pub_pending[li] = 0;
+  return P3_OK;
+}
+
+// Launch the comm kernel on the comm stream, ordered after everything submitted so far on
+// the stream that published local rank li's gradients (li < 0: no extra dependency).
+static int launch_after(p3_ctx* c, uint32_t mode, int li) {
   if (li >= 0) {
-    // order the comm stream after everything submitted so far on the producing stream
     CK(cudaEventRecord(c->ready_ev[li], c->pend_stream[li]));
     CK(cudaStreamWaitEvent(c->comm_stream, c->ready_ev[li], 0));
-    a.pub_li = (uint32_t)li;
-    a.pub_n = (uint32_t)c->pend_layer[li].size();
-    for (uint32_t i = 0; i < a.pub_n; ++i) {
-      a.pub_layer[i] = c->pend_layer[li][i];
-      a.pub_key[i] = c->pend_key[li][i];
-      a.pub_word[i] = c->pend_word[li][i];
-    }
-    c->pend_layer[li].clear();
-    c->pend_key[li].clear();
-    c->pend_word[li].clear();
     c->published[li] = 0;
   }
-  if (launch_comm(a, c->cfg.comm_ctas, c->cfg.comm_threads, c->comm_stream) != P3_OK)
+  if (launch_comm(comm_args(c, mode), c->cfg.comm_ctas, c->cfg.comm_threads, c->comm_stream) != P3_OK)
     return cuda_fail(c, cudaGetLastError(), "comm kernel launch");
   c->launches++;
   return P3_OK;
@@ -591,18 +615,16 @@ int p3_iteration_begin(p3_ctx_t* c, uint64_t k, void* stream) {
 int p3_iteration_end(p3_ctx_t* c, uint64_t k) {
   if (!c) return fail(nullptr, P3_EUSAGE, "null context");
   if (!c->iter_open || c->open_iter != k) return fail(c, P3_EUSAGE, "iteration not open");
-  // publications still pending: every local rank but the last drains its own batch, the
-  // FINISH launch carries the last one
-  int last = -1;
+  // publish what is still pending and order the FINISH launch after every producing stream
   for (uint32_t i = 0; i < c->cfg.n_local; ++i) {
-    if (c->pend_layer[i].empty()) continue;
-    if (last >= 0) {
-      int rc = launch_with_batch(c, P3_COMM_DRAIN, last);
-      if (rc) return rc;
-    }
-    last = (int)i;
+    if (!c->pend_stream[i]) continue;
+    int rc = flush_publications(c, i);
+    if (rc) return rc;
+    CK(cudaEventRecord(c->ready_ev[i], c->pend_stream[i]));
+    CK(cudaStreamWaitEvent(c->comm_stream, c->ready_ev[i], 0));
+    c->published[i] = 0;
   }
-  int rc = launch_with_batch(c, P3_COMM_FINISH, last);
+  int rc = launch_after(c, P3_COMM_FINISH, -1);
   if (rc) return rc;
   CK(cudaEventRecord(c->comm_done, c->comm_stream));
   c->comm_pending = true;
@@ -627,13 +649,31 @@ int p3_layer_ready(p3_ctx_t* c, uint32_t li, uint32_t layer, uint64_t k, const f
     // Batched publication: the layer becomes poppable when the comm launch that carries it
     // starts — stream-ordered after this point of `stream` by an event — so no stream memory
     // write is needed (each costs ~3 us of stream time, tools/exp_memop_cost.py).
-    c->pend_layer[li].push_back(layer);
-    c->pend_key[li].push_back(c->fifo_seq[li]++);
-    c->pend_word[li].push_back(word);
-    c->published[li] += 4ull * c->counts[layer];
+    const LocalDev& D = c->loc[li];
+    // back-pressure: never overwrite an entry the device has not ingested yet
+    const auto t0 = std::chrono::steady_clock::now();
+    while (c->ring_tail[li] - *(volatile uint32_t*)c->ring_ingested_host[li] >= D.ring_cap) {
+      if (std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() > c->cfg.timeout_s)
+        return fail(c, P3_ETIMEOUT, "publication ring full: the comm kernels stopped ingesting");
+      std::this_thread::sleep_for(std::chrono::microseconds(20));
+    }
+    PubEntry& e = c->ring_host[li][c->ring_tail[li] % D.ring_cap];
+    e.layer = layer;
+    e.key = c->fifo_seq[li]++;
+    e.word = word;
+    c->ring_tail[li]++;
     c->pend_stream[li] = (cudaStream_t)stream;
-    if (c->published[li] >= c->cfg.drain_bytes || c->pend_layer[li].size() == P3_PUB_BATCH)
-      return launch_with_batch(c, P3_COMM_DRAIN, (int)li);
+    c->published[li] += 4ull * c->counts[layer];
+    c->pub_pending[li] += 4ull * c->counts[layer];
+    if (c->pub_pending[li] >= c->cfg.pub_batch_bytes) {
+      rc = flush_publications(c, li);
+      if (rc) return rc;
+    }
+    if (c->published[li] >= c->cfg.drain_bytes) {
+      rc = flush_publications(c, li);  // a DRAIN launch must see what it was queued for
+      if (rc) return rc;
+      return launch_after(c, P3_COMM_DRAIN, (int)li);
+    }
     return P3_OK;
   }
   // no iteration open: publish right away with stream memory writes on `stream`

@@ -9,7 +9,6 @@
 #include "../../include/p3.h"
 
 #define P3_MAX_LOCAL 8      // ranks one process hosts (1 per GPU; up to 8 when emulating)
-#define P3_PUB_BATCH 40     // layer publications carried by one comm launch
 #define P3_DBG_CTAS 512
 #define P3_COMM_DRAIN 0   // exit as soon as nothing is poppable or reducible
 #define P3_COMM_FINISH 1  // exit when the iteration's local work is complete
@@ -71,6 +70,15 @@ struct IterState {
 };
 
 // Local-only state of one rank hosted in this process.
+// One publication (enqueue_layer) in the host-written ring: written by the host when the
+// layer's backward is issued, consumed by the device once a stream-ordered write of the
+// ring tail says the producing kernels have run.
+struct PubEntry {
+  uint32_t layer;
+  uint32_t key;             // FIFO publish sequence
+  unsigned long long word;  // publication word: iteration tag << 48 | gradient pointer
+};
+
 struct LocalDev {
   uint32_t rank;
   uint32_t trace_cap;
@@ -87,6 +95,11 @@ struct LocalDev {
   p3_trace_rec_t* trace;
   uint32_t* cta_phase;  // [P3_DBG_CTAS] last phase of each comm CTA (diagnostics)
   unsigned long long* vclock;  // K7 token bucket: time (ns) at which granted bytes drain
+  const PubEntry* ring;        // host-mapped publication ring
+  uint32_t ring_cap;
+  uint32_t* pubseq;            // ring entries published (stream memory write, monotone)
+  uint32_t* ingested;          // ring entries turned into publication words (monotone)
+  uint32_t* ingested_host;     // host-mapped mirror of `ingested` (host back-pressure)
 };
 
 struct CommArgs {
@@ -100,11 +113,6 @@ struct CommArgs {
   uint32_t sched;
   float lr;
   float momentum;
-  uint32_t pub_li;    // layers published by this launch (of local rank pub_li): the
-  uint32_t pub_n;     // launch writes their publication words before its first pick
-  uint32_t pub_layer[P3_PUB_BATCH];
-  uint32_t pub_key[P3_PUB_BATCH];
-  unsigned long long pub_word[P3_PUB_BATCH];
   float ns_per_byte;  // K7 link emulation (0: unthrottled)
   unsigned long long burst_ns;
   unsigned long long timeout_ns;

@@ -595,6 +595,32 @@ __device__ void pace(const CommArgs& a, const LocalDev& L, uint64_t bytes) {
   while (globaltimer() + a.burst_ns < d) __nanosleep(2000);
 }
 
+// Turn newly published ring entries into publication words (one warp). The ring tail is
+// advanced by a stream memory write ordered after the kernels that produced the gradients,
+// so entries below it are safe to expose; the first warp to move `ingested` forward copies
+// them, the others see the layers on a later pick.
+__device__ void ingest(const LocalDev& L, uint32_t sched) {
+  const uint32_t lane = threadIdx.x & 31;
+  uint32_t lo = 0, hi = 0, won = 0;
+  if (lane == 0) {
+    hi = ld_acquire_gpu(L.pubseq);
+    lo = ld_relaxed_gpu(L.ingested);
+    if ((int32_t)(hi - lo) > 0) won = atomicCAS(L.ingested, lo, hi) == lo;
+  }
+  won = __shfl_sync(FULL_MASK, won, 0);
+  if (!won) return;
+  lo = __shfl_sync(FULL_MASK, lo, 0);
+  hi = __shfl_sync(FULL_MASK, hi, 0);
+  for (uint32_t i = lo + lane; (int32_t)(hi - i) > 0; i += 32) {
+    const volatile PubEntry* e = L.ring + (i % L.ring_cap);
+    const uint32_t layer = e->layer;
+    if (sched == P3_SCHED_FIFO) L.fifo_key[layer] = e->key;
+    *(volatile unsigned long long*)(L.pub + layer) = e->word;
+  }
+  __syncwarp();
+  if (lane == 0) *(volatile uint32_t*)L.ingested_host = hi;  // host may reuse the entries
+}
+
 // Scheduler side of a push. With job == nullptr, classify the popped slice: a remote
 // owner needs the movers (PUSH_REMOTE); for a local owner the contribution stays in place
 // and only the arrival is counted here — and when that arrival completes the slice the
@@ -734,17 +760,6 @@ __global__ void __launch_bounds__(512, 1) k_comm(const __grid_constant__ CommArg
   const uint32_t nthr = blockDim.x;
   const uint32_t movers = nthr - 64;
   IterState* stats = a.loc[0].it;
-  if (warp == 0 && a.pub_n) {
-    // publications carried by this launch (enqueue_layer, worker.py:173-182): the kernels that
-    // produced these gradients completed before this launch started (stream event), so the
-    // layers become poppable here. Every CTA writes the same words before its first pick.
-    const LocalDev& P = a.loc[a.pub_li];
-    for (uint32_t i = lane; i < a.pub_n; i += 32) {
-      if (a.sched == P3_SCHED_FIFO) P.fifo_key[a.pub_layer[i]] = a.pub_key[i];
-      *(volatile unsigned long long*)(P.pub + a.pub_layer[i]) = a.pub_word[i];
-    }
-    __syncwarp();
-  }
   if (warp == 0) {
     uint32_t* phase = (lane == 0 && blockIdx.x < P3_DBG_CTAS) ? a.loc[0].cta_phase + blockIdx.x : nullptr;
     const uint64_t t0 = globaltimer();
@@ -762,6 +777,7 @@ __global__ void __launch_bounds__(512, 1) k_comm(const __grid_constant__ CommArg
       }
       for (uint32_t t = 0; t < a.n_local && kind == JOB_NONE; ++t) {
         li = (blockIdx.x + t) % a.n_local;
+        ingest(a.loc[li], a.sched);
         g = warp_pop(queue_of(a, a.loc[li]), a.k + 1, phase);
         if (g != P3_NONE) {
           if (lane == 0) atomicAdd(&a.loc[li].it->pushed, 1u);

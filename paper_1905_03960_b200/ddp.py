@@ -125,6 +125,7 @@ class P3DataParallel(_HookedDataParallel):
         trace_cap: int = 0,
         priority_mode: bool = True,
         drain_bytes: int = 4 << 20,
+        pub_batch_bytes: int = 1 << 20,
         plan_mode: str = "p3",
         throttle_bps: float = 0.0,
         throttle_burst: int = 50 * 1024,
@@ -145,7 +146,7 @@ class P3DataParallel(_HookedDataParallel):
             priority_mode=priority_mode, comm_ctas=comm_ctas, comm_threads=comm_threads,
             timeout_s=timeout_s, trace_cap=trace_cap, drain_bytes=drain_bytes, plan_mode=plan_mode,
             throttle_bps=throttle_bps, throttle_burst=throttle_burst, big_threshold=big_threshold,
-            gate_groups=groups,
+            gate_groups=groups, pub_batch_bytes=pub_batch_bytes,
         )
         if self.world > 1:
             handles = [None] * self.world

@@ -69,6 +69,7 @@ class SyncContext:
         throttle_bps: float = 0.0,
         throttle_burst: int = 50 * 1024,
         gate_groups: list[int] | None = None,
+        pub_batch_bytes: int = 0,
     ) -> None:
         import torch
 
@@ -97,6 +98,7 @@ class SyncContext:
         cfg.rng_seed = rng_seed
         cfg.throttle_bps = throttle_bps or 0.0
         cfg.throttle_burst = throttle_burst
+        cfg.pub_batch_bytes = pub_batch_bytes
         if gate_groups is not None:
             if len(gate_groups) != len(self.layer_counts):
                 raise ValueError("gate_groups needs one group id per layer")
