@@ -139,7 +139,8 @@ struct p3_ctx {
   uint32_t* ring_ingested_host[P3_MAX_LOCAL]{};
   uint32_t ring_tail[P3_MAX_LOCAL]{}, ring_flushed[P3_MAX_LOCAL]{};
   uint64_t pub_pending[P3_MAX_LOCAL]{};
-  cudaStream_t pend_stream[P3_MAX_LOCAL]{};
+  cudaStream_t pend_stream[P3_MAX_LOCAL]{};  // may be the legacy default stream (NULL)
+  bool pend_valid[P3_MAX_LOCAL]{};           // pend_stream holds a publishing stream
   bool comm_pending = false;
   uint64_t synced_iterations = 0;
   std::string err;
@@ -617,7 +618,7 @@ int p3_iteration_end(p3_ctx_t* c, uint64_t k) {
   if (!c->iter_open || c->open_iter != k) return fail(c, P3_EUSAGE, "iteration not open");
   // publish what is still pending and order the FINISH launch after every producing stream
   for (uint32_t i = 0; i < c->cfg.n_local; ++i) {
-    if (!c->pend_stream[i]) continue;
+    if (!c->pend_valid[i]) continue;
     int rc = flush_publications(c, i);
     if (rc) return rc;
     CK(cudaEventRecord(c->ready_ev[i], c->pend_stream[i]));
@@ -663,6 +664,7 @@ int p3_layer_ready(p3_ctx_t* c, uint32_t li, uint32_t layer, uint64_t k, const f
     e.word = word;
     c->ring_tail[li]++;
     c->pend_stream[li] = (cudaStream_t)stream;
+    c->pend_valid[li] = true;
     c->published[li] += 4ull * c->counts[layer];
     c->pub_pending[li] += 4ull * c->counts[layer];
     if (c->pub_pending[li] >= c->cfg.pub_batch_bytes) {

@@ -60,7 +60,7 @@ def main():
 
     lr = 0.05
     ref, mod, mod2 = mlp(), mlp(), mlp()
-    ddp = P3DataParallel(mod, lr=lr, max_slice=1000, comm_ctas=4)
+    ddp = P3DataParallel(mod, lr=lr, max_slice=1000, comm_ctas=4, timeout_s=30.0)
     lw = LayerwiseDataParallel(mod2, lr=lr)
     g = torch.Generator(device="cuda").manual_seed(1)
     for it in range(5):

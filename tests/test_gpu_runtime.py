@@ -192,7 +192,7 @@ def test_p3_dataparallel_matches_plain_sgd(cuda, max_slice):
 
     lr = 0.05
     ref, mod = _mlp(0), _mlp(0)
-    ddp = P3DataParallel(mod, lr=lr, max_slice=max_slice, comm_ctas=4)
+    ddp = P3DataParallel(mod, lr=lr, max_slice=max_slice, comm_ctas=4, timeout_s=20.0)
     g = torch.Generator(device="cuda").manual_seed(1)
     for it in range(6):
         x = torch.randint(0, 1000, (32, 8), device="cuda", generator=g)
