@@ -79,6 +79,9 @@ def main():
     out["torch_layerwise_close"] = all(torch.allclose(a, b, atol=1e-5) for a, b in zip(mod2.parameters(), ref.parameters()))
     ddp.close()
     lw.close()
+    out_dir = os.environ.get("P3_MP_OUT")
+    if out_dir:
+        Path(out_dir, f"rank{rank}.json").write_text(json.dumps(out))
     print("MPRESULT " + json.dumps(out), flush=True)
     dist.barrier()
     dist.destroy_process_group()

@@ -21,13 +21,14 @@ def _ngpu() -> int:
 
 
 @pytest.mark.parametrize("world", [2, 4, 8])
-def test_multiprocess_parity(world):
+def test_multiprocess_parity(world, tmp_path):
     if _ngpu() < world:
         pytest.skip(f"needs {world} GPUs")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
            "--master-addr", "127.0.0.1", "--master-port", str(29500 + world), str(REPO / "tests" / "mp" / "mp_worker.py")]
-    p = subprocess.run(cmd, capture_output=True, text=True, timeout=900)
-    results = [json.loads(l.split("MPRESULT ", 1)[1]) for l in p.stdout.splitlines() if "MPRESULT " in l]
+    env = dict(os.environ, P3_MP_OUT=str(tmp_path))
+    p = subprocess.run(cmd, capture_output=True, text=True, timeout=900, env=env)
+    results = [json.loads(f.read_text()) for f in sorted(tmp_path.glob("rank*.json"))]
     assert p.returncode == 0, p.stdout[-3000:] + p.stderr[-3000:]
     assert len(results) == world
     for r in results:
