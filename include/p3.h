@@ -157,6 +157,10 @@ typedef struct p3_config {
   uint64_t pub_batch_bytes;            /* publish (one stream memory write of the ring tail)
                                           once this many gradient bytes were enqueued
                                           (0: every layer at once — finest preemption) */
+  uint32_t drain_linger_us;            /* a DRAIN launch with nothing to do keeps waiting this
+                                          long while peers' pushes of partially arrived owned
+                                          slices are outstanding (never for local compute) */
+  uint32_t finish_ctas;                /* CTAs of the FINISH launch (0: comm_ctas) */
   const uint32_t* gate_groups;         /* optional per-layer forward-gate group id (layers of
                                           one module gated together); NULL = one group per
                                           layer. Ids must be 0..G-1 */

@@ -74,6 +74,8 @@ class Config(ctypes.Structure):
         ("throttle_bps", ctypes.c_double),
         ("throttle_burst", ctypes.c_uint64),
         ("pub_batch_bytes", ctypes.c_uint64),
+        ("drain_linger_us", ctypes.c_uint32),
+        ("finish_ctas", ctypes.c_uint32),
         ("gate_groups", ctypes.POINTER(ctypes.c_uint32)),
     ]
 

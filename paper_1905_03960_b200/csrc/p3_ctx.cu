@@ -90,7 +90,7 @@ using namespace p3;
 
 // Peer-visible arena of one rank: W | R | arrivals | hint | done (256-byte aligned parts).
 struct PeerLayout {
-  uint64_t w, r, arrivals, hint, done, gdone, bytes;
+  uint64_t w, r, arrivals, hint, tally, done, gdone, bytes;
 };
 
 // Local arena of one rank. The per-iteration part (cursor | srv_lo | srv_taken | it) is
@@ -175,6 +175,8 @@ PeerLayout peer_layout_of(const p3_ctx* c, uint32_t rank) {
   o = align_up(o + (uint64_t)c->S * 4, 256);
   p.hint = o;
   o = align_up(o + (uint64_t)c->L * 4, 256);
+  p.tally = o;
+  o = align_up(o + 8, 256);
   p.done = o;
   o = align_up(o + (uint64_t)c->L * 4, 256);
   p.gdone = o;
@@ -217,6 +219,7 @@ void set_peer_pointers(p3_ctx* c, uint32_t rank, char* base) {
   c->peers.R[rank] = reinterpret_cast<float*>(base + p.r);
   c->peers.arrivals[rank] = reinterpret_cast<uint32_t*>(base + p.arrivals);
   c->peers.hint[rank] = reinterpret_cast<uint32_t*>(base + p.hint);
+  c->peers.tally[rank] = reinterpret_cast<uint32_t*>(base + p.tally);
   c->peers.done[rank] = reinterpret_cast<uint32_t*>(base + p.done);
   c->peers.gdone[rank] = reinterpret_cast<uint32_t*>(base + p.gdone);
 }
@@ -565,6 +568,7 @@ static CommArgs comm_args(p3_ctx* c, uint32_t mode) {
   a.momentum = c->cfg.momentum;
   a.timeout_ns = (unsigned long long)(c->cfg.timeout_s * 1e9);
   a.err = c->d_err;
+  a.linger_ns = (unsigned long long)c->cfg.drain_linger_us * 1000ull;
   if (c->cfg.throttle_bps > 0) {
     a.ns_per_byte = (float)(8e9 / c->cfg.throttle_bps);
     a.burst_ns = (unsigned long long)((double)c->cfg.throttle_burst * 8e9 / c->cfg.throttle_bps);
@@ -591,7 +595,8 @@ static int launch_after(p3_ctx* c, uint32_t mode, int li) {
     CK(cudaStreamWaitEvent(c->comm_stream, c->ready_ev[li], 0));
     c->published[li] = 0;
   }
-  if (launch_comm(comm_args(c, mode), c->cfg.comm_ctas, c->cfg.comm_threads, c->comm_stream) != P3_OK)
+  const uint32_t ctas = mode == P3_COMM_FINISH && c->cfg.finish_ctas ? c->cfg.finish_ctas : c->cfg.comm_ctas;
+  if (launch_comm(comm_args(c, mode), ctas, c->cfg.comm_threads, c->comm_stream) != P3_OK)
     return cuda_fail(c, cudaGetLastError(), "comm kernel launch");
   c->launches++;
   return P3_OK;

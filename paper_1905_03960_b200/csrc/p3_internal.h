@@ -54,6 +54,7 @@ struct PeersDev {
   float* R[P3_MAX_RANKS];          // receive slots [world][own_stride]
   uint32_t* arrivals[P3_MAX_RANKS];  // [S] pushes received per owned slice (monotone)
   uint32_t* hint[P3_MAX_RANKS];      // [L] owned slices completed per layer (monotone)
+  uint32_t* tally[P3_MAX_RANKS];     // [2] pushes arrived, owned slices completed (monotone)
   uint32_t* done[P3_MAX_RANKS];      // [L] slices of a layer broadcast into W (monotone)
   uint32_t* gdone[P3_MAX_RANKS];     // [G] slices of a gate group broadcast into W (monotone)
 };
@@ -113,6 +114,7 @@ struct CommArgs {
   uint32_t sched;
   float lr;
   float momentum;
+  unsigned long long linger_ns;  // DRAIN: wait this long for peers' pushes of partial slices
   float ns_per_byte;  // K7 link emulation (0: unthrottled)
   unsigned long long burst_ns;
   unsigned long long timeout_ns;

@@ -643,8 +643,10 @@ __device__ uint32_t prepare_push(const CommArgs& a, uint32_t li, uint32_t g, Job
       if (o == r) {
         // the contribution stays in place (published to this rank by the acquire above)
         const uint32_t old = atom_add_relaxed_gpu(a.peers.arrivals[o] + g, 1u);
+        red_add_relaxed_sys(a.peers.tally[o], 1u);
         if (old + 1 == (a.k + 1) * P.world) {  // the last arrival: the slice is complete
           red_add_relaxed_sys(a.peers.hint[o] + l, 1u);
+          red_add_relaxed_sys(a.peers.tally[o] + 1, 1u);
           if (atomicCAS(L.claim + g, a.k, a.k + 1) == a.k) {
             atomicAdd(L.srv_taken + l, 1u);
             atomicAdd(&L.it->reduced, 1u);
@@ -726,7 +728,11 @@ __device__ void signal_job(const CommArgs& a, const Job& j) {
   if (j.kind == JOB_PUSH) {
     // the last arriver completes the slice and tells the owner's scheduler (hint)
     const uint32_t old = atom_add_relaxed_sys(a.peers.arrivals[j.rank] + j.g, 1u);
-    if (old + 1 == (a.k + 1) * P.world) red_add_relaxed_sys(a.peers.hint[j.rank] + j.layer, 1u);
+    red_add_relaxed_sys(a.peers.tally[j.rank], 1u);
+    if (old + 1 == (a.k + 1) * P.world) {
+      red_add_relaxed_sys(a.peers.hint[j.rank] + j.layer, 1u);
+      red_add_relaxed_sys(a.peers.tally[j.rank] + 1, 1u);
+    }
     atomicAdd(L.bytes + 1, 4ull * j.len);
   } else {
     const uint32_t grp = P.layer_group[j.layer];
@@ -765,6 +771,7 @@ __global__ void __launch_bounds__(512, 1) k_comm(const __grid_constant__ CommArg
     const uint64_t t0 = globaltimer();
     uint64_t t_pick = 0, t_wait = 0;
     uint32_t backoff = 0, b = 0;
+    uint64_t idle_since = 0;  // DRAIN linger start (lane 0)
     bool pending[2] = {false, false};
     for (uint32_t iter = 0;; ++iter) {
       if (phase) *(volatile uint32_t*)phase = (a.k << 24) | (1u << 20) | (iter & 0xfffff);
@@ -789,7 +796,18 @@ __global__ void __launch_bounds__(512, 1) k_comm(const __grid_constant__ CommArg
         uint32_t verdict = 0;  // 0 keep looking, 1 leave, 2 timed out
         if (lane == 0) {
           if (a.mode == P3_COMM_DRAIN) {
-            verdict = 1;
+            // Nothing to do. Linger (bounded) while some owned slice has part of its pushes:
+            // the rest come from peers' comm kernels, never from this rank's compute, and
+            // reducing it now keeps it off the post-backward tail.
+            bool partial = false;
+            for (uint32_t t = 0; t < a.n_local && !partial; ++t) {
+              const uint32_t o = a.loc[t].rank, ot = a.plan.own_total[o], N = a.plan.world;
+              const uint32_t arrived = ld_relaxed_sys(a.peers.tally[o]) - a.k * N * ot;
+              const uint32_t completed = ld_relaxed_sys(a.peers.tally[o] + 1) - a.k * ot;
+              partial = (int32_t)(arrived - N * completed) > 0;
+            }
+            if (!partial || idle_since == 0 || globaltimer() - idle_since > a.linger_ns) verdict = 1;
+            if (idle_since == 0) idle_since = globaltimer();
           } else {
             bool fin = true;
             for (uint32_t t = 0; t < a.n_local; ++t) {
@@ -823,6 +841,7 @@ __global__ void __launch_bounds__(512, 1) k_comm(const __grid_constant__ CommArg
         kind = JOB_EXIT;
       }
       backoff = 0;
+      idle_since = 0;
       if (kind == JOB_PUSH) {
         const uint32_t how = prepare_push(a, li, g, nullptr);
         if (how == PUSH_DONE) continue;  // own slice, still waiting for peers: counted in place

@@ -126,6 +126,8 @@ class P3DataParallel(_HookedDataParallel):
         priority_mode: bool = True,
         drain_bytes: int = 4 << 20,
         pub_batch_bytes: int = 1 << 20,
+        drain_linger_us: int = 200,
+        finish_ctas: int = 0,
         plan_mode: str = "p3",
         throttle_bps: float = 0.0,
         throttle_burst: int = 50 * 1024,
@@ -146,7 +148,8 @@ class P3DataParallel(_HookedDataParallel):
             priority_mode=priority_mode, comm_ctas=comm_ctas, comm_threads=comm_threads,
             timeout_s=timeout_s, trace_cap=trace_cap, drain_bytes=drain_bytes, plan_mode=plan_mode,
             throttle_bps=throttle_bps, throttle_burst=throttle_burst, big_threshold=big_threshold,
-            gate_groups=groups, pub_batch_bytes=pub_batch_bytes,
+            gate_groups=groups, pub_batch_bytes=pub_batch_bytes, drain_linger_us=drain_linger_us,
+            finish_ctas=finish_ctas,
         )
         if self.world > 1:
             handles = [None] * self.world

@@ -70,6 +70,8 @@ class SyncContext:
         throttle_burst: int = 50 * 1024,
         gate_groups: list[int] | None = None,
         pub_batch_bytes: int = 0,
+        drain_linger_us: int = 0,
+        finish_ctas: int = 0,
     ) -> None:
         import torch
 
@@ -99,6 +101,8 @@ class SyncContext:
         cfg.throttle_bps = throttle_bps or 0.0
         cfg.throttle_burst = throttle_burst
         cfg.pub_batch_bytes = pub_batch_bytes
+        cfg.drain_linger_us = drain_linger_us
+        cfg.finish_ctas = finish_ctas
         if gate_groups is not None:
             if len(gate_groups) != len(self.layer_counts):
                 raise ValueError("gate_groups needs one group id per layer")
