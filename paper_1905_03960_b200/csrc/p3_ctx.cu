@@ -130,6 +130,10 @@ struct p3_ctx {
   cudaEvent_t ready_ev[P3_MAX_LOCAL]{};
   cudaStream_t poll_stream = nullptr;
   cudaStream_t comm_stream = nullptr;
+  cudaStream_t side[P3_SIDE_STREAMS]{};
+  cudaEvent_t side_ev[P3_SIDE_STREAMS]{};
+  cudaEvent_t iter_ev = nullptr;
+  uint32_t side_next = 0;
   uint64_t open_iter = 0;
   bool iter_open = false;
   uint64_t launches = 0;
@@ -472,6 +476,15 @@ int p3_ctx_create(const p3_config_t* cfg, p3_ctx_t** out) {
   e = cudaEventCreateWithFlags(&c->comm_done, cudaEventDisableTiming);
   for (uint32_t i = 0; i < cfg->n_local && e == cudaSuccess; ++i)
     e = cudaEventCreateWithFlags(&c->ready_ev[i], cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->iter_ev, cudaEventDisableTiming);
+  {
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    for (int j = 0; j < P3_SIDE_STREAMS && e == cudaSuccess; ++j) {
+      e = cudaStreamCreateWithPriority(&c->side[j], cudaStreamNonBlocking, hi);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->side_ev[j], cudaEventDisableTiming);
+    }
+  }
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->poll_stream, cudaStreamNonBlocking);
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
   if (e != cudaSuccess) {
@@ -497,6 +510,11 @@ int p3_ctx_destroy(p3_ctx_t* c) {
   if (c->d_plan) cudaFree(c->d_plan);
   if (c->d_err) cudaFree(c->d_err);
   if (c->comm_done) cudaEventDestroy(c->comm_done);
+  if (c->iter_ev) cudaEventDestroy(c->iter_ev);
+  for (int j = 0; j < P3_SIDE_STREAMS; ++j) {
+    if (c->side[j]) cudaStreamDestroy(c->side[j]);
+    if (c->side_ev[j]) cudaEventDestroy(c->side_ev[j]);
+  }
   for (uint32_t i = 0; i < P3_MAX_LOCAL; ++i)
     if (c->ready_ev[i]) cudaEventDestroy(c->ready_ev[i]);
   if (c->poll_stream) cudaStreamDestroy(c->poll_stream);
@@ -587,16 +605,17 @@ static int flush_publications(p3_ctx* c, uint32_t li) {
   return P3_OK;
 }
 
-// Launch the comm kernel on the comm stream, ordered after everything submitted so far on
-// the stream that published local rank li's gradients (li < 0: no extra dependency).
-static int launch_after(p3_ctx* c, uint32_t mode, int li) {
-  if (li >= 0) {
-    CK(cudaEventRecord(c->ready_ev[li], c->pend_stream[li]));
-    CK(cudaStreamWaitEvent(c->comm_stream, c->ready_ev[li], 0));
-    c->published[li] = 0;
-  }
-  const uint32_t ctas = mode == P3_COMM_FINISH && c->cfg.finish_ctas ? c->cfg.finish_ctas : c->cfg.comm_ctas;
-  if (launch_comm(comm_args(c, mode), ctas, c->cfg.comm_threads, c->comm_stream) != P3_OK)
+// DRAIN launches rotate over side streams so a long-running launch (link-bound, or down to
+// its last CTAs while it keeps ingesting newly published layers) never holds back the next
+// one: concurrent launches share the device queue. Each side stream starts the iteration
+// after the per-iteration reset on the main comm stream; the FINISH launch on the main comm
+// stream comes after all of them.
+static int launch_drain(p3_ctx* c, int li) {
+  cudaStream_t s = c->side[c->side_next++ % P3_SIDE_STREAMS];
+  CK(cudaEventRecord(c->ready_ev[li], c->pend_stream[li]));
+  CK(cudaStreamWaitEvent(s, c->ready_ev[li], 0));
+  c->published[li] = 0;
+  if (launch_comm(comm_args(c, P3_COMM_DRAIN), c->cfg.comm_ctas, c->cfg.comm_threads, s) != P3_OK)
     return cuda_fail(c, cudaGetLastError(), "comm kernel launch");
   c->launches++;
   return P3_OK;
@@ -612,6 +631,8 @@ int p3_iteration_begin(p3_ctx_t* c, uint64_t k, void* stream) {
   const LocalLayout& ll = c->local_layout;
   for (uint32_t i = 0; i < c->cfg.n_local; ++i)
     CK(cudaMemsetAsync(static_cast<char*>(c->local_arena[i]) + ll.iter_begin, 0, ll.iter_end - ll.iter_begin, s));
+  CK(cudaEventRecord(c->iter_ev, s));
+  for (int j = 0; j < P3_SIDE_STREAMS; ++j) CK(cudaStreamWaitEvent(c->side[j], c->iter_ev, 0));
   c->comm_stream = s;
   c->open_iter = k;
   c->iter_open = true;
@@ -630,8 +651,14 @@ int p3_iteration_end(p3_ctx_t* c, uint64_t k) {
     CK(cudaStreamWaitEvent(c->comm_stream, c->ready_ev[i], 0));
     c->published[i] = 0;
   }
-  int rc = launch_after(c, P3_COMM_FINISH, -1);
-  if (rc) return rc;
+  for (int j = 0; j < P3_SIDE_STREAMS; ++j) {
+    CK(cudaEventRecord(c->side_ev[j], c->side[j]));
+    CK(cudaStreamWaitEvent(c->comm_stream, c->side_ev[j], 0));
+  }
+  const uint32_t ctas = c->cfg.finish_ctas ? c->cfg.finish_ctas : c->cfg.comm_ctas;
+  if (launch_comm(comm_args(c, P3_COMM_FINISH), ctas, c->cfg.comm_threads, c->comm_stream) != P3_OK)
+    return cuda_fail(c, cudaGetLastError(), "comm kernel launch");
+  c->launches++;
   CK(cudaEventRecord(c->comm_done, c->comm_stream));
   c->comm_pending = true;
   c->iter_open = false;
@@ -679,7 +706,7 @@ int p3_layer_ready(p3_ctx_t* c, uint32_t li, uint32_t layer, uint64_t k, const f
     if (c->published[li] >= c->cfg.drain_bytes) {
       rc = flush_publications(c, li);  // a DRAIN launch must see what it was queued for
       if (rc) return rc;
-      return launch_after(c, P3_COMM_DRAIN, (int)li);
+      return launch_drain(c, (int)li);
     }
     return P3_OK;
   }

@@ -9,6 +9,7 @@
 #include "../../include/p3.h"
 
 #define P3_MAX_LOCAL 8      // ranks one process hosts (1 per GPU; up to 8 when emulating)
+#define P3_SIDE_STREAMS 4   // comm streams DRAIN launches rotate over
 #define P3_DBG_CTAS 512
 #define P3_COMM_DRAIN 0   // exit as soon as nothing is poppable or reducible
 #define P3_COMM_FINISH 1  // exit when the iteration's local work is complete

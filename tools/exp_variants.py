@@ -21,6 +21,10 @@ variants = {
     "drain64M": {"drain_bytes": 64 << 20},
     "ctas32": {"comm_ctas": 32},
     "linger0": {"drain_linger_us": 0},
+    "t256c16": {"comm_threads": 256, "comm_ctas": 16},
+    "t128c32": {"comm_threads": 128, "comm_ctas": 32},
+    "t128c16": {"comm_threads": 128, "comm_ctas": 16},
+    "t256c32": {"comm_threads": 256, "comm_ctas": 32},
     "linger1000": {"drain_linger_us": 1000},
     "fin148": {"finish_ctas": 148},
     "fin148_linger0": {"finish_ctas": 148, "drain_linger_us": 0},
