@@ -218,7 +218,18 @@ class P3DataParallel(_HookedDataParallel):
         torch.cuda.current_stream().wait_stream(self.comm_stream)
 
     def close(self) -> None:
+        """Detach: parameters get their own storage again (a copy of the synced values)
+        before the context (and its parameter arena) is destroyed."""
         self.remove_hooks()
+        try:
+            self.synchronize()
+        except Exception:  # noqa: BLE001 - detach anyway
+            pass
+        with torch.no_grad():
+            for p in self.params:
+                p.data = p.data.clone(memory_format=torch.preserve_format)
+                p.grad = None
+        torch.cuda.synchronize()
         self.ctx.close()
 
 
