@@ -118,3 +118,16 @@ def test_compute_calls_fail_loudly_without_gpu():
         pytest.skip("GPU present")
     sm = _lib.ctypes.c_int()
     assert _lib.load().p3_device_info(_lib.ctypes.byref(sm), None, None, None) == _lib.P3_ECUDA
+
+
+def test_graft_entry_importable():
+    # the driver imports __graft_entry__ for build() and smoke()
+    import importlib.util
+
+    spec = importlib.util.spec_from_file_location("graft_entry", HEADER.parents[1] / "__graft_entry__.py")
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    assert callable(mod.build) and callable(mod.smoke)
+    import py_compile
+
+    py_compile.compile(str(HEADER.parents[1] / "bench.py"), doraise=True)
