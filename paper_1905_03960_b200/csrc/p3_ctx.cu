@@ -571,7 +571,7 @@ int p3_ctx_layer_offset(p3_ctx_t* c, uint32_t layer, uint64_t* off) {
   return P3_OK;
 }
 
-static CommArgs comm_args(p3_ctx* c, uint32_t mode) {
+static CommArgs comm_args(p3_ctx* c, uint32_t mode, uint32_t ctas) {
   CommArgs a;
   std::memset(&a, 0, sizeof(a));
   a.plan = c->plan_dev;
@@ -587,6 +587,8 @@ static CommArgs comm_args(p3_ctx* c, uint32_t mode) {
   a.timeout_ns = (unsigned long long)(c->cfg.timeout_s * 1e9);
   a.err = c->d_err;
   a.linger_ns = (unsigned long long)c->cfg.drain_linger_us * 1000ull;
+  // single rank: about two jobs per CTA, at most 8 slices per job
+  a.pop_run = std::max<uint32_t>(1, std::min<uint32_t>(8, c->S / std::max<uint32_t>(1, 2 * ctas)));
   if (c->cfg.throttle_bps > 0) {
     a.ns_per_byte = (float)(8e9 / c->cfg.throttle_bps);
     a.burst_ns = (unsigned long long)((double)c->cfg.throttle_burst * 8e9 / c->cfg.throttle_bps);
@@ -615,7 +617,7 @@ static int launch_drain(p3_ctx* c, int li) {
   CK(cudaEventRecord(c->ready_ev[li], c->pend_stream[li]));
   CK(cudaStreamWaitEvent(s, c->ready_ev[li], 0));
   c->published[li] = 0;
-  if (launch_comm(comm_args(c, P3_COMM_DRAIN), c->cfg.comm_ctas, c->cfg.comm_threads, s) != P3_OK)
+  if (launch_comm(comm_args(c, P3_COMM_DRAIN, c->cfg.comm_ctas), c->cfg.comm_ctas, c->cfg.comm_threads, s) != P3_OK)
     return cuda_fail(c, cudaGetLastError(), "comm kernel launch");
   c->launches++;
   return P3_OK;
@@ -656,7 +658,7 @@ int p3_iteration_end(p3_ctx_t* c, uint64_t k) {
     CK(cudaStreamWaitEvent(c->comm_stream, c->side_ev[j], 0));
   }
   const uint32_t ctas = c->cfg.finish_ctas ? c->cfg.finish_ctas : c->cfg.comm_ctas;
-  if (launch_comm(comm_args(c, P3_COMM_FINISH), ctas, c->cfg.comm_threads, c->comm_stream) != P3_OK)
+  if (launch_comm(comm_args(c, P3_COMM_FINISH, ctas), ctas, c->cfg.comm_threads, c->comm_stream) != P3_OK)
     return cuda_fail(c, cudaGetLastError(), "comm kernel launch");
   c->launches++;
   CK(cudaEventRecord(c->comm_done, c->comm_stream));

@@ -116,6 +116,7 @@ struct CommArgs {
   float lr;
   float momentum;
   unsigned long long linger_ns;  // DRAIN: wait this long for peers' pushes of partial slices
+  uint32_t pop_run;   // single rank: consecutive slices claimed per pop
   float ns_per_byte;  // K7 link emulation (0: unthrottled)
   unsigned long long burst_ns;
   unsigned long long timeout_ns;

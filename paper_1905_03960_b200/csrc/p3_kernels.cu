@@ -353,7 +353,10 @@ __device__ __forceinline__ const float* pub_ptr(uint64_t w) {
 // loads, one memory round trip), then the warp walks the availability ballots in layer
 // order and claims the first slice it wins. A lost race moves on to the next candidate
 // without rescanning. FIFO discipline: arg-min of the publish sequence, then claim.
-__device__ uint32_t warp_pop(const QueueView& q, uint32_t tag, uint32_t* dbg = nullptr) {
+// `want` > 1 claims up to that many consecutive slices of the chosen layer at once (they
+// would be the next pops anyway); `*run` receives how many were claimed.
+__device__ uint32_t warp_pop(const QueueView& q, uint32_t tag, uint32_t* dbg = nullptr, uint32_t want = 1,
+                             uint32_t* run = nullptr) {
   const uint32_t lane = threadIdx.x & 31;
   if (q.sched == P3_SCHED_PRIORITY) {
     for (uint32_t group = 0; group < q.n_layers; group += 32 * 32) {
@@ -372,9 +375,12 @@ __device__ uint32_t warp_pop(const QueueView& q, uint32_t tag, uint32_t* dbg = n
           const uint32_t j = __ffs(m) - 1;
           const uint32_t l = group + 32 * c + j;
           uint32_t s = 0;
-          if (lane == j) s = atomicAdd(q.cursor + l, 1u);
+          if (lane == j) s = atomicAdd(q.cursor + l, want);
           s = __shfl_sync(FULL_MASK, s, j);
-          if (s < q.nslices[l]) return q.first[l] + s;
+          if (s < q.nslices[l]) {
+            if (run) *run = min(want, q.nslices[l] - s);
+            return q.first[l] + s;
+          }
           m &= m - 1;  // lost the race for the layer's last slice: next candidate
         }
       }
@@ -404,9 +410,12 @@ __device__ uint32_t warp_pop(const QueueView& q, uint32_t tag, uint32_t* dbg = n
     }
     if (best_l == P3_NONE) return P3_NONE;
     uint32_t s = 0;
-    if (lane == 0) s = atomicAdd(q.cursor + best_l, 1u);
+    if (lane == 0) s = atomicAdd(q.cursor + best_l, want);
     s = __shfl_sync(FULL_MASK, s, 0);
-    if (s < q.nslices[best_l]) return q.first[best_l] + s;
+    if (s < q.nslices[best_l]) {
+      if (run) *run = min(want, q.nslices[best_l] - s);
+      return q.first[best_l] + s;
+    }
     // lost the race for the last slice of that layer: rescan
   }
 }
@@ -556,7 +565,7 @@ __device__ __forceinline__ QueueView queue_of(const CommArgs& a, const LocalDev&
 #define JOB_PUSH 2
 #define JOB_EXIT 3
 struct Job {
-  uint32_t kind, li, g, layer, slice, rank, len, n, aligned;
+  uint32_t kind, li, g, layer, slice, rank, len, n, aligned, run;
   const float* src[P3_MAX_RANKS];  // PUSH: src[0]; REDUCE: contributions in rank order
   float* dst[P3_MAX_RANKS];        // PUSH: dst[0]; REDUCE: replicas, dst[0] = owner's master
   float* v;
@@ -659,6 +668,7 @@ __device__ uint32_t prepare_push(const CommArgs& a, uint32_t li, uint32_t g, Job
   }
   if (lane == 0) {
     job->kind = JOB_PUSH;
+    job->run = 1;
     job->li = li;
     job->g = g;
     job->layer = l;
@@ -672,7 +682,7 @@ __device__ uint32_t prepare_push(const CommArgs& a, uint32_t li, uint32_t g, Job
 
 // Scheduler side of a reduce: contributions of every rank (the owner's own straight from
 // its gradient) and every replica to write, master first.
-__device__ void prepare_reduce(const CommArgs& a, uint32_t li, uint32_t g, Job* job) {
+__device__ void prepare_reduce(const CommArgs& a, uint32_t li, uint32_t g, Job* job, uint32_t run = 1) {
   const PlanDev& P = a.plan;
   const LocalDev& L = a.loc[li];
   const uint32_t o = L.rank, l = P.slice_layer[g], N = P.world;
@@ -692,13 +702,16 @@ __device__ void prepare_reduce(const CommArgs& a, uint32_t li, uint32_t g, Job* 
   float* v = L.V ? L.V + P.slice_slot[g] : nullptr;
 #pragma unroll
   for (int off = 16; off; off >>= 1) al |= __shfl_xor_sync(FULL_MASK, (unsigned long long)al, off);
+  uint32_t len = P.slice_len[g];
+  for (uint32_t i = 1; i < run; ++i) len += P.slice_len[g + i];  // consecutive slices: contiguous
   if (q == 0) {
     job->kind = JOB_REDUCE;
     job->li = li;
     job->g = g;
     job->layer = l;
     job->rank = o;
-    job->len = P.slice_len[g];
+    job->run = run;
+    job->len = len;
     job->n = N;
     job->v = v;
     job->aligned = ((al | (uintptr_t)v) & 15) == 0;
@@ -737,12 +750,13 @@ __device__ void signal_job(const CommArgs& a, const Job& j) {
   } else {
     const uint32_t grp = P.layer_group[j.layer];
     for (uint32_t q = 0; q < j.n; ++q) {
-      red_add_relaxed_sys(a.peers.done[q] + j.layer, 1u);
-      red_add_relaxed_sys(a.peers.gdone[q] + grp, 1u);
+      red_add_relaxed_sys(a.peers.done[q] + j.layer, j.run);
+      red_add_relaxed_sys(a.peers.gdone[q] + grp, j.run);
     }
     atomicAdd(L.bytes + 0, 4ull * j.len * (j.n - 1));  // pushes received
     atomicAdd(L.bytes + 1, 4ull * j.len * (j.n - 1));  // broadcasts sent
-    trace_append(L, a.k, j.layer, j.g - P.layer_first[j.layer], j.rank, P3_EV_BCAST);
+    for (uint32_t i = 0; i < j.run; ++i)
+      trace_append(L, a.k, j.layer, j.g + i - P.layer_first[j.layer], j.rank, P3_EV_BCAST);
   }
 }
 
@@ -776,13 +790,34 @@ __global__ void __launch_bounds__(512, 1) k_comm(const __grid_constant__ CommArg
     for (uint32_t iter = 0;; ++iter) {
       if (phase) *(volatile uint32_t*)phase = (a.k << 24) | (1u << 20) | (iter & 0xfffff);
       const uint64_t tp = globaltimer();
-      uint32_t kind = JOB_NONE, li = 0, g = P3_NONE;
-      for (uint32_t t = 0; t < a.n_local && kind == JOB_NONE; ++t) {
+      uint32_t kind = JOB_NONE, li = 0, g = P3_NONE, run = 1;
+      if (a.plan.world == 1) {
+        // single rank: a popped slice is complete the moment it is popped (the owner's own
+        // contribution is read in place), so the pop claims the reduction directly — no
+        // arrival counting, no server role — and takes up to pop_run consecutive slices of
+        // the layer (contiguous in memory) as one job
+        const LocalDev& L = a.loc[0];
+        ingest(L, a.sched);
+        g = warp_pop(queue_of(a, L), a.k + 1, phase, L.V ? 1u : a.pop_run, &run);
+        if (g != P3_NONE) {
+          if (lane == 0) {
+            (void)ld_acquire_gpu64(L.pub + a.plan.slice_layer[g]);
+            atomicAdd(&L.it->pushed, run);
+            atomicAdd(&L.it->reduced, run);
+            for (uint32_t i = 0; i < run; ++i) {
+              const uint32_t l = a.plan.slice_layer[g];
+              trace_append(L, a.k, l, g + i - a.plan.layer_first[l], L.rank, P3_EV_PUSH);
+            }
+          }
+          kind = JOB_REDUCE;
+        }
+      }
+      for (uint32_t t = 0; t < a.n_local && kind == JOB_NONE && a.plan.world > 1; ++t) {
         li = (blockIdx.x + t) % a.n_local;
         g = warp_server_pick(a, a.loc[li], phase);
         if (g != P3_NONE) kind = JOB_REDUCE;
       }
-      for (uint32_t t = 0; t < a.n_local && kind == JOB_NONE; ++t) {
+      for (uint32_t t = 0; t < a.n_local && kind == JOB_NONE && a.plan.world > 1; ++t) {
         li = (blockIdx.x + t) % a.n_local;
         ingest(a.loc[li], a.sched);
         g = warp_pop(queue_of(a, a.loc[li]), a.k + 1, phase);
@@ -858,7 +893,7 @@ __global__ void __launch_bounds__(512, 1) k_comm(const __grid_constant__ CommArg
       if (kind == JOB_PUSH) {
         prepare_push(a, li, g, &slots[b]);
       } else if (kind == JOB_REDUCE) {
-        prepare_reduce(a, li, g, &slots[b]);
+        prepare_reduce(a, li, g, &slots[b], run);
       } else {
         if (pending[b ^ 1]) bar_sync(BAR_EMPTY(b ^ 1), 64);  // leave every barrier balanced
         if (lane == 0) slots[b].kind = JOB_EXIT;
@@ -892,6 +927,7 @@ __global__ void __launch_bounds__(512, 1) k_comm(const __grid_constant__ CommArg
       mine.rank = j.rank;
       mine.len = j.len;
       mine.n = j.n;
+      mine.run = j.run;
       __syncwarp();
       bar_arrive(BAR_EMPTY(b), 64);
       if (lane == 0) {
