@@ -161,6 +161,9 @@ typedef struct p3_config {
                                           long while peers' pushes of partially arrived owned
                                           slices are outstanding (never for local compute) */
   uint32_t finish_ctas;                /* CTAs of the FINISH launch (0: comm_ctas) */
+  uint32_t pop_relax;                  /* concurrent comm CTAs may each pop any of this many most
+                                          urgent published layers (0: 8; 1: strict order);
+                                          capped at the CTA count */
   const uint32_t* gate_groups;         /* optional per-layer forward-gate group id (layers of
                                           one module gated together); NULL = one group per
                                           layer. Ids must be 0..G-1 */

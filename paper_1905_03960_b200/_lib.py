@@ -76,6 +76,7 @@ class Config(ctypes.Structure):
         ("pub_batch_bytes", ctypes.c_uint64),
         ("drain_linger_us", ctypes.c_uint32),
         ("finish_ctas", ctypes.c_uint32),
+        ("pop_relax", ctypes.c_uint32),
         ("gate_groups", ctypes.POINTER(ctypes.c_uint32)),
     ]
 

@@ -333,6 +333,7 @@ __global__ void k_sleep(uint64_t ns) {
 struct QueueView {
   uint32_t n_layers;
   uint32_t sched;
+  uint32_t relax;  // pops may take any of the `relax` most urgent layers (1: strict)
   const uint32_t* nslices;
   const uint32_t* first;
   const uint64_t* pub;
@@ -369,10 +370,22 @@ __device__ uint32_t warp_pop(const QueueView& q, uint32_t tag, uint32_t* dbg = n
         bits |= (uint32_t)ok << c;
       }
       const uint32_t nchunk = min(32u, (q.n_layers - group + 31) / 32);
+      bool first = true;
       for (uint32_t c = 0; c < nchunk; ++c) {
         uint32_t m = __ballot_sync(FULL_MASK, (bits >> c) & 1u);
         while (m) {
-          const uint32_t j = __ffs(m) - 1;
+          uint32_t j = __ffs(m) - 1;
+          if (first && q.relax > 1) {
+            // many concurrent consumers would all race for the same most urgent layer: each
+            // CTA first tries one of the `relax` most urgent available layers (a pop is then
+            // among the `relax` smallest, as with `relax` consumers popping at once), then
+            // falls back to strict order
+            const uint32_t pick = blockIdx.x % min((uint32_t)__popc(m), q.relax);
+            uint32_t mm = m;
+            for (uint32_t t = 0; t < pick; ++t) mm &= mm - 1;
+            j = __ffs(mm) - 1;
+          }
+          first = false;
           const uint32_t l = group + 32 * c + j;
           uint32_t s = 0;
           if (lane == j) s = atomicAdd(q.cursor + l, want);
@@ -381,7 +394,7 @@ __device__ uint32_t warp_pop(const QueueView& q, uint32_t tag, uint32_t* dbg = n
             if (run) *run = min(want, q.nslices[l] - s);
             return q.first[l] + s;
           }
-          m &= m - 1;  // lost the race for the layer's last slice: next candidate
+          m &= ~(1u << j);  // lost the race for the layer's last slice: next candidate
         }
       }
     }
@@ -428,7 +441,7 @@ __global__ void k_queue_pop(QueueView q, uint32_t tag, uint32_t* result) {
 int launch_queue_pop(const uint32_t* nslices, const uint32_t* first, const uint64_t* pub,
                      const uint32_t* fifo_key, uint32_t* cursor, uint32_t n_layers, uint32_t sched,
                      uint32_t tag, uint32_t* result, void* stream) {
-  QueueView q{n_layers, sched, nslices, first, pub, fifo_key, cursor};
+  QueueView q{n_layers, sched, 1u, nslices, first, pub, fifo_key, cursor};
   k_queue_pop<<<1, 32, 0, (cudaStream_t)stream>>>(q, tag, result);
   return cudaGetLastError() == cudaSuccess ? P3_OK : P3_ECUDA;
 }
@@ -551,6 +564,7 @@ __device__ __forceinline__ QueueView queue_of(const CommArgs& a, const LocalDev&
   QueueView q;
   q.n_layers = a.plan.n_layers;
   q.sched = a.sched;
+  q.relax = a.pop_relax;
   q.nslices = a.plan.layer_nslices;
   q.first = a.plan.layer_first;
   q.pub = L.pub;

@@ -72,6 +72,7 @@ class SyncContext:
         pub_batch_bytes: int = 0,
         drain_linger_us: int = 0,
         finish_ctas: int = 0,
+        pop_relax: int = 0,
     ) -> None:
         import torch
 
@@ -103,6 +104,7 @@ class SyncContext:
         cfg.pub_batch_bytes = pub_batch_bytes
         cfg.drain_linger_us = drain_linger_us
         cfg.finish_ctas = finish_ctas
+        cfg.pop_relax = pop_relax
         if gate_groups is not None:
             if len(gate_groups) != len(self.layer_counts):
                 raise ValueError("gate_groups needs one group id per layer")
