@@ -360,16 +360,23 @@ __device__ uint32_t warp_pop(const QueueView& q, uint32_t tag, uint32_t* dbg = n
                              uint32_t* run = nullptr) {
   const uint32_t lane = threadIdx.x & 31;
   if (q.sched == P3_SCHED_PRIORITY) {
-    for (uint32_t group = 0; group < q.n_layers; group += 32 * 32) {
-      uint32_t bits = 0;  // bit c: layer group + 32*c + lane is poppable
-#pragma unroll 4
-      for (uint32_t c = 0; c < 32; ++c) {
+    constexpr uint32_t CH = 8;  // chunks of 32 layers examined per memory round trip
+    for (uint32_t group = 0; group < q.n_layers; group += 32 * CH) {
+      // all loads of the group issued before any is used: one round trip, not 2*CH
+      uint64_t w[CH];
+      uint32_t cur[CH], ns[CH];
+#pragma unroll
+      for (uint32_t c = 0; c < CH; ++c) {
         const uint32_t l = group + 32 * c + lane;
-        if (l >= q.n_layers) break;
-        const bool ok = pub_ready(ld_relaxed_gpu64(q.pub + l), tag) && ld_relaxed_gpu(q.cursor + l) < q.nslices[l];
-        bits |= (uint32_t)ok << c;
+        const bool in = l < q.n_layers;
+        w[c] = in ? ld_relaxed_gpu64(q.pub + l) : 0ull;
+        cur[c] = in ? ld_relaxed_gpu(q.cursor + l) : 0u;
+        ns[c] = in ? q.nslices[l] : 0u;
       }
-      const uint32_t nchunk = min(32u, (q.n_layers - group + 31) / 32);
+      uint32_t bits = 0;  // bit c: layer group + 32*c + lane is poppable
+#pragma unroll
+      for (uint32_t c = 0; c < CH; ++c) bits |= (uint32_t)(pub_ready(w[c], tag) && cur[c] < ns[c]) << c;
+      const uint32_t nchunk = min(CH, (q.n_layers - group + 31) / 32);
       bool first = true;
       for (uint32_t c = 0; c < nchunk; ++c) {
         uint32_t m = __ballot_sync(FULL_MASK, (bits >> c) & 1u);
