@@ -356,8 +356,19 @@ __device__ __forceinline__ const float* pub_ptr(uint64_t w) {
 // without rescanning. FIFO discipline: arg-min of the publish sequence, then claim.
 // `want` > 1 claims up to that many consecutive slices of the chosen layer at once (they
 // would be the next pops anyway); `*run` receives how many were claimed.
+// Priority discipline with a stash: up to P3_MULTI candidate layers are claimed with one
+// round of atomics (one per lane); the most urgent win is returned, the other wins are
+// appended to the caller's stash (processed next by the same CTA). Against many concurrent
+// consumers this turns a walk of lost races into one memory round trip.
+#define P3_MULTI 4
+struct Stash {
+  uint32_t n;
+  uint32_t g[P3_MULTI];
+  uint32_t run[P3_MULTI];
+};
+
 __device__ uint32_t warp_pop(const QueueView& q, uint32_t tag, uint32_t* dbg = nullptr, uint32_t want = 1,
-                             uint32_t* run = nullptr) {
+                             uint32_t* run = nullptr, Stash* stash = nullptr) {
   const uint32_t lane = threadIdx.x & 31;
   if (q.sched == P3_SCHED_PRIORITY) {
     constexpr uint32_t CH = 8;  // chunks of 32 layers examined per memory round trip
@@ -380,28 +391,48 @@ __device__ uint32_t warp_pop(const QueueView& q, uint32_t tag, uint32_t* dbg = n
       bool first = true;
       for (uint32_t c = 0; c < nchunk; ++c) {
         uint32_t m = __ballot_sync(FULL_MASK, (bits >> c) & 1u);
+        uint32_t my_ns = 0;
+#pragma unroll
+        for (uint32_t cc = 0; cc < CH; ++cc) my_ns = cc == c ? ns[cc] : my_ns;
         while (m) {
-          uint32_t j = __ffs(m) - 1;
+          // candidates: the most urgent available layers of the chunk — starting, on the
+          // first round, at a CTA-dependent one of the `relax` most urgent (a pop is then
+          // among the `relax` smallest, as with `relax` consumers popping at once)
+          uint32_t mm = m;
           if (first && q.relax > 1) {
-            // many concurrent consumers would all race for the same most urgent layer: each
-            // CTA first tries one of the `relax` most urgent available layers (a pop is then
-            // among the `relax` smallest, as with `relax` consumers popping at once), then
-            // falls back to strict order
-            const uint32_t pick = blockIdx.x % min((uint32_t)__popc(m), q.relax);
-            uint32_t mm = m;
-            for (uint32_t t = 0; t < pick; ++t) mm &= mm - 1;
-            j = __ffs(mm) - 1;
+            const uint32_t skip = blockIdx.x % min((uint32_t)__popc(m), q.relax);
+            for (uint32_t t = 0; t < skip; ++t) mm &= mm - 1;
           }
           first = false;
-          const uint32_t l = group + 32 * c + j;
-          uint32_t s = 0;
-          if (lane == j) s = atomicAdd(q.cursor + l, want);
-          s = __shfl_sync(FULL_MASK, s, j);
-          if (s < q.nslices[l]) {
-            if (run) *run = min(want, q.nslices[l] - s);
-            return q.first[l] + s;
+          uint32_t cand = 0;
+          const uint32_t k = stash ? P3_MULTI : 1u;
+          for (uint32_t t = 0; t < k && mm; ++t) {
+            cand |= mm & (~mm + 1);  // lowest remaining set bit
+            mm &= mm - 1;
           }
-          m &= ~(1u << j);  // lost the race for the layer's last slice: next candidate
+          uint32_t s = 0;
+          bool won = false;
+          if ((cand >> lane) & 1u) {
+            s = atomicAdd(q.cursor + group + 32 * c + lane, want);
+            won = s < my_ns;
+          }
+          const uint32_t wm = __ballot_sync(FULL_MASK, won);
+          if (wm) {
+            const uint32_t l = group + 32 * c + lane;
+            const uint32_t my_g = won ? q.first[l] + s : 0u, my_run = won ? min(want, my_ns - s) : 0u;
+            const uint32_t j0 = __ffs(wm) - 1;
+            if (won && lane != j0) {  // the other wins: next jobs of this CTA, in layer order
+              const uint32_t idx = stash->n + __popc(wm & ((1u << lane) - 1u)) - 1u;
+              stash->g[idx] = my_g;
+              stash->run[idx] = my_run;
+            }
+            __syncwarp();
+            if (lane == 0 && stash) stash->n += __popc(wm) - 1u;
+            __syncwarp();
+            if (run) *run = __shfl_sync(FULL_MASK, my_run, j0);
+            return __shfl_sync(FULL_MASK, my_g, j0);
+          }
+          m &= ~cand;  // every candidate lost the race for its layer's last slices
         }
       }
     }
@@ -781,6 +812,23 @@ __device__ void signal_job(const CommArgs& a, const Job& j) {
   }
 }
 
+// Next stashed claim (one warp; the stash is in layer order).
+__device__ uint32_t take_stash(Stash* st, uint32_t* run) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t g = st->g[0];
+  *run = st->run[0];
+  __syncwarp();
+  if (lane == 0) {
+    for (uint32_t i = 1; i < st->n; ++i) {
+      st->g[i - 1] = st->g[i];
+      st->run[i - 1] = st->run[i];
+    }
+    st->n -= 1;
+  }
+  __syncwarp();
+  return g;
+}
+
 // Comm kernel. Warp 0 of every CTA is the scheduler, warp 1 the signaler, warps 2.. the
 // movers; two job slots in shared memory.
 //   scheduler: pick the next job — server work first (a reduced slice unblocks the next
@@ -807,6 +855,10 @@ __global__ void __launch_bounds__(512, 1) k_comm(const __grid_constant__ CommArg
     uint64_t t_pick = 0, t_wait = 0;
     uint32_t backoff = 0, b = 0;
     uint64_t idle_since = 0;  // DRAIN linger start (lane 0)
+    __shared__ Stash stash;   // slices claimed by this CTA's scheduler, not yet dispatched
+    __shared__ uint32_t stash_li;
+    if (lane == 0) stash.n = 0;
+    __syncwarp();
     bool pending[2] = {false, false};
     for (uint32_t iter = 0;; ++iter) {
       if (phase) *(volatile uint32_t*)phase = (a.k << 24) | (1u << 20) | (iter & 0xfffff);
@@ -818,8 +870,12 @@ __global__ void __launch_bounds__(512, 1) k_comm(const __grid_constant__ CommArg
         // arrival counting, no server role — and takes up to pop_run consecutive slices of
         // the layer (contiguous in memory) as one job
         const LocalDev& L = a.loc[0];
-        ingest(L, a.sched);
-        g = warp_pop(queue_of(a, L), a.k + 1, phase, L.V ? 1u : a.pop_run, &run);
+        if (stash.n) {
+          g = take_stash(&stash, &run);
+        } else {
+          ingest(L, a.sched);
+          g = warp_pop(queue_of(a, L), a.k + 1, phase, L.V ? 1u : a.pop_run, &run, &stash);
+        }
         if (g != P3_NONE) {
           if (lane == 0) {
             (void)ld_acquire_gpu64(L.pub + a.plan.slice_layer[g]);
@@ -838,10 +894,18 @@ __global__ void __launch_bounds__(512, 1) k_comm(const __grid_constant__ CommArg
         g = warp_server_pick(a, a.loc[li], phase);
         if (g != P3_NONE) kind = JOB_REDUCE;
       }
+      if (kind == JOB_NONE && a.plan.world > 1 && stash.n) {
+        li = stash_li;
+        g = take_stash(&stash, &run);
+        if (lane == 0) atomicAdd(&a.loc[li].it->pushed, 1u);
+        kind = JOB_PUSH;
+      }
       for (uint32_t t = 0; t < a.n_local && kind == JOB_NONE && a.plan.world > 1; ++t) {
         li = (blockIdx.x + t) % a.n_local;
         ingest(a.loc[li], a.sched);
-        g = warp_pop(queue_of(a, a.loc[li]), a.k + 1, phase);
+        g = warp_pop(queue_of(a, a.loc[li]), a.k + 1, phase, 1u, &run, &stash);
+        if (lane == 0) stash_li = li;
+        __syncwarp();
         if (g != P3_NONE) {
           if (lane == 0) atomicAdd(&a.loc[li].it->pushed, 1u);
           kind = JOB_PUSH;
