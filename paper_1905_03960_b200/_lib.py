@@ -77,6 +77,8 @@ class Config(ctypes.Structure):
         ("drain_linger_us", ctypes.c_uint32),
         ("finish_ctas", ctypes.c_uint32),
         ("pop_relax", ctypes.c_uint32),
+        ("pop_run", ctypes.c_uint32),
+        ("pop_multi", ctypes.c_uint32),
         ("gate_groups", ctypes.POINTER(ctypes.c_uint32)),
     ]
 

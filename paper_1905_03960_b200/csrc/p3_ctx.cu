@@ -588,7 +588,9 @@ static CommArgs comm_args(p3_ctx* c, uint32_t mode, uint32_t ctas) {
   a.err = c->d_err;
   a.linger_ns = (unsigned long long)c->cfg.drain_linger_us * 1000ull;
   // single rank: about two jobs per CTA, at most 8 slices per job
-  a.pop_run = std::max<uint32_t>(1, std::min<uint32_t>(8, c->S / std::max<uint32_t>(1, 2 * ctas)));
+  a.pop_run = c->cfg.pop_run ? c->cfg.pop_run
+                             : std::max<uint32_t>(1, std::min<uint32_t>(8, c->S / std::max<uint32_t>(1, 2 * ctas)));
+  a.pop_multi = std::max<uint32_t>(1, std::min<uint32_t>(4, c->cfg.pop_multi ? c->cfg.pop_multi : 4));
   // bounded relaxation of the pop order: never more than the number of concurrent consumers
   a.pop_relax = std::min<uint32_t>(ctas, c->cfg.pop_relax ? c->cfg.pop_relax : 8);
   if (c->cfg.throttle_bps > 0) {

@@ -334,6 +334,7 @@ struct QueueView {
   uint32_t n_layers;
   uint32_t sched;
   uint32_t relax;  // pops may take any of the `relax` most urgent layers (1: strict)
+  uint32_t multi;  // candidate layers claimed per round of atomics (<= P3_MULTI)
   const uint32_t* nslices;
   const uint32_t* first;
   const uint64_t* pub;
@@ -405,7 +406,7 @@ __device__ uint32_t warp_pop(const QueueView& q, uint32_t tag, uint32_t* dbg = n
           }
           first = false;
           uint32_t cand = 0;
-          const uint32_t k = stash ? P3_MULTI : 1u;
+          const uint32_t k = stash ? q.multi : 1u;
           for (uint32_t t = 0; t < k && mm; ++t) {
             cand |= mm & (~mm + 1);  // lowest remaining set bit
             mm &= mm - 1;
@@ -479,7 +480,7 @@ __global__ void k_queue_pop(QueueView q, uint32_t tag, uint32_t* result) {
 int launch_queue_pop(const uint32_t* nslices, const uint32_t* first, const uint64_t* pub,
                      const uint32_t* fifo_key, uint32_t* cursor, uint32_t n_layers, uint32_t sched,
                      uint32_t tag, uint32_t* result, void* stream) {
-  QueueView q{n_layers, sched, 1u, nslices, first, pub, fifo_key, cursor};
+  QueueView q{n_layers, sched, 1u, 1u, nslices, first, pub, fifo_key, cursor};
   k_queue_pop<<<1, 32, 0, (cudaStream_t)stream>>>(q, tag, result);
   return cudaGetLastError() == cudaSuccess ? P3_OK : P3_ECUDA;
 }
@@ -603,6 +604,7 @@ __device__ __forceinline__ QueueView queue_of(const CommArgs& a, const LocalDev&
   q.n_layers = a.plan.n_layers;
   q.sched = a.sched;
   q.relax = a.pop_relax;
+  q.multi = a.pop_multi;
   q.nslices = a.plan.layer_nslices;
   q.first = a.plan.layer_first;
   q.pub = L.pub;

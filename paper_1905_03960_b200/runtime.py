@@ -73,6 +73,8 @@ class SyncContext:
         drain_linger_us: int = 0,
         finish_ctas: int = 0,
         pop_relax: int = 0,
+        pop_run: int = 0,
+        pop_multi: int = 0,
     ) -> None:
         import torch
 
@@ -105,6 +107,8 @@ class SyncContext:
         cfg.drain_linger_us = drain_linger_us
         cfg.finish_ctas = finish_ctas
         cfg.pop_relax = pop_relax
+        cfg.pop_run = pop_run
+        cfg.pop_multi = pop_multi
         if gate_groups is not None:
             if len(gate_groups) != len(self.layer_counts):
                 raise ValueError("gate_groups needs one group id per layer")

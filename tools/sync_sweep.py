@@ -15,6 +15,7 @@ def main():
     ctas_list = [int(c) for c in sys.argv[2].split(",")] if len(sys.argv) > 2 else [148]
     slices = [int(c) for c in sys.argv[3].split(",")] if len(sys.argv) > 3 else [50_000]
     threads = int(sys.argv[4]) if len(sys.argv) > 4 else 512
+    extra = json.loads(sys.argv[5]) if len(sys.argv) > 5 else {}
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     rows = []
     for m in models:
@@ -22,7 +23,7 @@ def main():
         for ms in slices:
             for ctas in ctas_list:
                 ctx = SyncContext(counts, world, [rank], max_slice=ms, comm_ctas=ctas, comm_threads=threads,
-                                  timeout_s=60.0, emulate_grads=True)
+                                  timeout_s=60.0, emulate_grads=True, **extra)
                 if world > 1:
                     hs = [None] * world; dist.all_gather_object(hs, ctx.ipc_handle(0)); ctx.open_peers(hs)
                 st = torch.cuda.Stream()
@@ -66,7 +67,7 @@ def main():
                 stats["jobs"] = dsn["jobs"]
                 nvl = 2 * (world - 1) / world * P * 4 / (ms_ * 1e-3) / 1e9 if world > 1 else None
                 hbm = 12 * P / (ms_ * 1e-3) / 1e9 if world == 1 else None
-                rows.append({"model": m, "world": world, "max_slice": ms, "ctas": ctas, "threads": threads, "ms": round(ms_, 4),
+                rows.append({"extra": extra, "model": m, "world": world, "max_slice": ms, "ctas": ctas, "threads": threads, "ms": round(ms_, 4),
                              "nvlink_GBps": nvl and round(nvl, 1), "hbm_GBps": hbm and round(hbm, 1), "us_per_job": stats})
                 ctx.close()
                 if world > 1: dist.barrier()
