@@ -165,7 +165,7 @@ typedef struct p3_config {
                                           urgent published layers (0: 8; 1: strict order);
                                           capped at the CTA count */
   uint32_t pop_run;                    /* single rank: consecutive slices per job (0: auto) */
-  uint32_t pop_multi;                  /* layers claimed per round of pop atomics, 1..4 (0: 4) */
+  uint32_t pop_multi;                  /* layers claimed per round of pop atomics, 1..4 (0: 1) */
   const uint32_t* gate_groups;         /* optional per-layer forward-gate group id (layers of
                                           one module gated together); NULL = one group per
                                           layer. Ids must be 0..G-1 */

@@ -588,9 +588,11 @@ static CommArgs comm_args(p3_ctx* c, uint32_t mode, uint32_t ctas) {
   a.err = c->d_err;
   a.linger_ns = (unsigned long long)c->cfg.drain_linger_us * 1000ull;
   // single rank: about two jobs per CTA, at most 8 slices per job
+  // (measured, tools/sync_sweep.py: about four jobs per CTA balances per-job overhead and the
+  // tail; a stash of extra claims loses more to imbalance than it saves in pick time)
   a.pop_run = c->cfg.pop_run ? c->cfg.pop_run
-                             : std::max<uint32_t>(1, std::min<uint32_t>(8, c->S / std::max<uint32_t>(1, 2 * ctas)));
-  a.pop_multi = std::max<uint32_t>(1, std::min<uint32_t>(4, c->cfg.pop_multi ? c->cfg.pop_multi : 4));
+                             : std::max<uint32_t>(1, std::min<uint32_t>(8, c->S / std::max<uint32_t>(1, 4 * ctas)));
+  a.pop_multi = std::max<uint32_t>(1, std::min<uint32_t>(4, c->cfg.pop_multi ? c->cfg.pop_multi : 1));
   // bounded relaxation of the pop order: never more than the number of concurrent consumers
   a.pop_relax = std::min<uint32_t>(ctas, c->cfg.pop_relax ? c->cfg.pop_relax : 8);
   if (c->cfg.throttle_bps > 0) {
