@@ -140,3 +140,27 @@ def test_shard_protocol_errors(cuda):
         s.on_push(0, 0, np.zeros(4, np.float32))
     with pytest.raises(ProtocolError, match="aggregate"):
         s.aggregate_and_update()
+
+
+@pytest.mark.parametrize("nw", [1, 3, 4])
+def test_shard_update_momentum(cuda, nw):
+    # extension (not in the reference): v = mu*v + mean(g); p -= lr*v, every op rounded
+    import torch
+
+    from paper_1905_03960_b200.server import shard_update_device
+
+    rng = np.random.RandomState(nw)
+    n = 10_007
+    p = rng.uniform(-1, 1, n).astype(np.float32)
+    v = rng.uniform(-1, 1, n).astype(np.float32)
+    grads = {r: rng.uniform(-1, 1, n).astype(np.float32) for r in range(nw)}
+    pd, vd = torch.from_numpy(p).cuda(), torch.from_numpy(v).cuda()
+    shard_update_device(pd, [torch.from_numpy(grads[r]).cuda() for r in range(nw)], 0.3, momentum=0.9, momentum_buf=vd)
+    acc = np.zeros(n, np.float32)
+    for r in range(nw):
+        acc = acc + grads[r]
+    g = acc / np.float32(nw)
+    v2 = np.float32(0.9) * v + g
+    p2 = p - np.float32(0.3) * v2
+    assert vd.cpu().numpy().tobytes() == v2.astype(np.float32).tobytes()
+    assert pd.cpu().numpy().tobytes() == p2.astype(np.float32).tobytes()

@@ -272,3 +272,49 @@ def test_throttled_link_rate(cuda, golden, mode):
     assert dt >= floor, (dt, floor)
     assert dt < 3 * iters * max(per_rank) * 8 / rate + 2.0
     w.close()
+
+
+def test_p3_dataparallel_momentum(cuda):
+    # fused momentum SGD in the comm kernel == separately rounded torch ops
+    import torch
+
+    from paper_1905_03960_b200.ddp import P3DataParallel
+
+    lr, mu = 0.05, 0.9
+    ref, mod = _mlp(3), _mlp(3)
+    ddp = P3DataParallel(mod, lr=lr, momentum=mu, comm_ctas=4, timeout_s=20.0)
+    bufs = [torch.zeros_like(p) for p in ref.parameters()]
+    g = torch.Generator(device="cuda").manual_seed(2)
+    for it in range(4):
+        x = torch.randint(0, 1000, (16, 8), device="cuda", generator=g)
+        y = torch.randint(0, 10, (16,), device="cuda", generator=g)
+        torch.nn.functional.cross_entropy(ddp(x), y).backward()
+        torch.nn.functional.cross_entropy(ref(x), y).backward()
+        with torch.no_grad():
+            for p, b in zip(ref.parameters(), bufs):
+                b.mul_(mu).add_(p.grad)
+                p.sub_(b.mul(lr))
+                p.grad = None
+    ddp.synchronize()
+    for a, b in zip(mod.parameters(), ref.parameters()):
+        assert torch.equal(a, b)
+    ddp.close()
+
+
+def test_metrics_sampler_on_device_counters(cuda):
+    from paper_1905_03960_b200.metrics import DeviceNetCounters, NetSampler, idle_fraction
+    from paper_1905_03960_b200.model import builtin_profile
+
+    prof = builtin_profile("vgg19-like")
+    from paper_1905_03960_b200.runtime import TrainingWorker, WorkerConfig
+
+    cfg = WorkerConfig(rank=0, mode="p3", world=2, iterations=3, emulate_compute=True, comm_ctas=4)
+    w = TrainingWorker(cfg, prof, ranks=[0, 1])
+    smp = NetSampler(DeviceNetCounters(w.ctx, 0), period_ms=10)
+    smp.start()
+    w.run()
+    smp.stop()
+    b_in, b_out = smp.samples[-1].bytes_in, smp.samples[-1].bytes_out
+    assert b_out > 0 and b_in > 0
+    assert 0.0 <= idle_fraction(smp.samples, 4096) <= 1.0
+    w.close()
