@@ -124,6 +124,47 @@ int p3_queue_put_layer(p3_queue_t* q, uint32_t layer, uint32_t iteration);
 int p3_queue_poll(p3_queue_t* q, uint32_t* layer, uint32_t* slice);
 int p3_queue_destroy(p3_queue_t* q);
 
+/* ------------------------------------------------------------- schedule model (host) */
+
+/* sim.py:26-34: policies and resources of the discrete-event model. */
+#define P3_SIM_AGGRESSIVE_COARSE 0
+#define P3_SIM_AGGRESSIVE_SLICED 1
+#define P3_SIM_PRIORITY_SLICED 2
+#define P3_SIM_COMPUTE 0
+#define P3_SIM_UPLINK 1
+#define P3_SIM_UPDATE 2
+#define P3_SIM_DOWNLINK 3
+#define P3_SIM_FWD 0
+#define P3_SIM_BWD 1
+#define P3_SIM_UP 2
+#define P3_SIM_UPD 3
+#define P3_SIM_DOWN 4
+
+typedef struct p3_sim_stage { int64_t up, update, down; } p3_sim_stage_t;  /* StageCost, sim.py:41-45 */
+
+typedef struct p3_sim_scenario {      /* Scenario, sim.py:48-57 */
+  uint32_t n_layers;
+  const int64_t* fwd;                 /* LayerSpec.fwd_time per layer (ticks) */
+  const int64_t* bwd;                 /* LayerSpec.bwd_time per layer (ticks) */
+  const p3_sim_stage_t* stages;
+  uint32_t policy;                    /* P3_SIM_* */
+  int64_t slice_ticks;
+  int64_t iterations;
+  int64_t per_slice_overhead;
+  uint32_t serial_update;
+  uint32_t device_queue;              /* 1: the uplink pops from the device slice queue */
+} p3_sim_scenario_t;
+
+typedef struct p3_sim_entry {         /* TimelineEntry, sim.py:135-140 (item = op:k:Ll[:ss]) */
+  uint32_t resource, op;
+  int64_t iteration, layer, slice, start, end;
+} p3_sim_entry_t;
+
+/* simulate (sim.py:241-365): the timeline entries in creation order. With device_queue the
+ * uplink transmission order comes from the device priority/FIFO queue (the same warp_pop
+ * the comm kernel runs), which must reproduce the reference's sequences exactly. */
+int p3_simulate(const p3_sim_scenario_t* scenario, p3_sim_entry_t* out, uint64_t cap, uint64_t* n_out);
+
 /* --------------------------------------------------------------- sync context (K3) */
 
 typedef struct p3_ctx p3_ctx_t;

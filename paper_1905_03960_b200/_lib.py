@@ -98,6 +98,7 @@ SIGNATURES = {
     "p3_gradient_block": (ctypes.c_int, [_U64, _U64, _U64, _U64, _U64, _P, _P]),
     "p3_shard_update": (ctypes.c_int, [_P, ctypes.POINTER(_P), _U32, _U64, ctypes.c_float, ctypes.c_float, _P, _P]),
     "p3_emulate_compute": (ctypes.c_int, [_U64, _P]),
+    "p3_simulate": (ctypes.c_int, [_P, _P, _U64, _PU64]),
     "p3_queue_create": (ctypes.c_int, [_PU32, _U32, _U32, ctypes.POINTER(_P)]),
     "p3_queue_put_layer": (ctypes.c_int, [_P, _U32, _U32]),
     "p3_queue_poll": (ctypes.c_int, [_P, _PU32, _PU32]),

@@ -17,6 +17,7 @@ import sys
 from pathlib import Path
 
 import numpy as np
+from dataclasses import replace as dataclasses_replace
 
 import p3sync
 from p3sync import hashing, plan as rplan, sim as rsim
@@ -156,6 +157,52 @@ def main() -> None:
                      "items": [e.item for e in sorted(tl.entries_for(rsim.UPLINK), key=lambda e: e.start)],
                      "delay": tl.inter_iteration_delay()})
     out["fig4"] = fig4
+
+    # 8. Full simulator timelines (sim.py) for the figure scenarios, the shipped scenario files
+    #    and seeded random scenarios (every policy, serial update, per-slice overhead)
+    import random
+
+    cases = []
+
+    def add(sc):
+        tl = rsim.simulate(sc)
+        cases.append({"scenario": rsim.scenario_to_dict(sc), "csv": tl.to_csv(), "summary": tl.summary()})
+
+    for policy in (rsim.AGGRESSIVE_COARSE, rsim.AGGRESSIVE_SLICED, rsim.PRIORITY_SLICED):
+        add(rsim.Scenario(profile=ModelProfile("fig4", 0, tuple(LayerSpec(i, f"L{i}", 1, 1, 1) for i in range(3))),
+                          stages=(rsim.StageCost(2, 0, 0),) * 3, policy=policy, slice_ticks=1, num_iterations=1))
+        add(rsim.Scenario(profile=ModelProfile("fig6", 0, tuple(LayerSpec(i, f"L{i}", 1, 0, 0) for i in range(3))),
+                          stages=(rsim.StageCost(1, 1, 1), rsim.StageCost(3, 3, 3), rsim.StageCost(1, 1, 1)),
+                          policy=policy, slice_ticks=1, num_iterations=1))
+    for f in ("fig4.json", "fig6.json"):
+        path = Path("/root/reference/pkg/scenarios") / f
+        if path.exists():
+            sc = rsim.load_scenario(path)
+            for policy in rsim.POLICIES:
+                add(dataclasses_replace(sc, policy=policy))
+    rng = random.Random(1905)
+    while len(cases) < 60:
+        n = rng.randint(2, 7)
+        T = rng.choice([1, 2, 3])
+        layers, stages = [], []
+        for i in range(n):
+            layers.append(LayerSpec(i, f"L{i}", 1, rng.randint(0, 4), rng.randint(0, 4)))
+            k = rng.randint(1, 4)
+            stages.append(rsim.StageCost(k * T * rng.choice([0, 1, 1, 2]), k * rng.randint(0, 2), k * rng.randint(0, 2)))
+        sc = rsim.Scenario(profile=ModelProfile("rnd", 0, tuple(layers)), stages=tuple(stages),
+                           policy=rng.choice(rsim.POLICIES), slice_ticks=T, num_iterations=rng.randint(1, 3),
+                           per_slice_overhead=rng.choice([0, 0, 1]), serial_update=rng.random() < 0.4)
+        try:
+            sc.validate()
+        except rsim.ScenarioError:
+            continue
+        add(sc)
+    out["sim_cases"] = cases
+    sw = rsim.Scenario(profile=ModelProfile("sw", 0, tuple(LayerSpec(i, f"L{i}", 1, 2, 3) for i in range(4))),
+                       stages=tuple(rsim.StageCost(24, 0, 24) for _ in range(4)), policy=rsim.PRIORITY_SLICED,
+                       slice_ticks=1, num_iterations=2, per_slice_overhead=1)
+    out["sweep"] = {"scenario": rsim.scenario_to_dict(sw), "sizes": [1, 2, 3, 4, 6, 8, 12, 24],
+                    "result": rsim.sweep_slice_size(sw, [1, 2, 3, 4, 6, 8, 12, 24])}
 
     (HERE / "golden.json").write_text(json.dumps(out, indent=1) + "\n")
     print("wrote", HERE / "golden.json")

@@ -318,3 +318,13 @@ def test_metrics_sampler_on_device_counters(cuda):
     assert b_out > 0 and b_in > 0
     assert 0.0 <= idle_fraction(smp.samples, 4096) <= 1.0
     w.close()
+
+
+def test_simulator_device_queue_replay(cuda, golden):
+    # the C++ schedule model with the uplink popping from the GPU slice queue reproduces the
+    # reference simulator's full timelines (priority and FIFO policies)
+    from paper_1905_03960_b200.sim import scenario_from_dict, simulate
+
+    for case in golden["sim_cases"]:
+        sc = scenario_from_dict(case["scenario"])
+        assert simulate(sc, device_queue=True).to_csv() == case["csv"], case["scenario"]["name"]
