@@ -144,19 +144,24 @@ def time_training(args, world, rank, ddp, x, y, steps, warmup, e2e=None):
 
     from paper_1905_03960_b200.torch_models import loss_fn
 
+    from paper_1905_03960_b200.loader import DevicePrefetcher
+
+    feed = None
+
     def step(i):
         if e2e is None:
             loss = loss_fn(args.model, ddp, x, y)
             loss.backward()
             return loss
-        xh, yh, lh = e2e
-        xd = xh.to("cuda", non_blocking=True)
-        yd = yh.to("cuda", non_blocking=True)
+        xd, yd = next(feed)  # pinned host batch, copied in on the copy stream
         loss = loss_fn(args.model, ddp, xd, yd)
         loss.backward()
         lh[i % len(lh)].copy_(loss.detach(), non_blocking=True)
         return loss
 
+    if e2e is not None:
+        xh, yh, lh = e2e
+        feed = DevicePrefetcher([(xh, yh)] * warmup)
     for i in range(warmup):
         step(i)
     ddp.synchronize()
@@ -164,6 +169,8 @@ def time_training(args, world, rank, ddp, x, y, steps, warmup, e2e=None):
     clocks = ClockSampler(torch.cuda.current_device()) if rank == 0 else None
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     s.record()
+    if e2e is not None:  # every timed step's input copy is issued inside the timed region
+        feed = DevicePrefetcher([(xh, yh)] * steps)
     for i in range(steps):
         step(i)
     ddp.synchronize()
