@@ -207,6 +207,9 @@ typedef struct p3_config {
                                           capped at the CTA count */
   uint32_t pop_run;                    /* single rank: consecutive slices per job (0: auto) */
   uint32_t pop_multi;                  /* layers claimed per round of pop atomics, 1..4 (0: 1) */
+  uint32_t push_bf16;                  /* declared lossy transport: pushes carry bf16 (RNE)
+                                          contributions, summed in fp32 in rank order;
+                                          parameters, update and broadcasts stay fp32 */
   const uint32_t* gate_groups;         /* optional per-layer forward-gate group id (layers of
                                           one module gated together); NULL = one group per
                                           layer. Ids must be 0..G-1 */

@@ -165,6 +165,25 @@ def replay_params(counts: list[int], seed: int, world: int, iterations: int, lr:
     return params
 
 
+def to_bf16(x: np.ndarray) -> np.ndarray:
+    """fp32 -> bf16 -> fp32, round to nearest even (finite inputs): the declared lossy
+    transport of the B200 path (not in the reference)."""
+    b = np.ascontiguousarray(x, dtype=np.float32).view(np.uint32).astype(np.uint64)
+    b = (b + 0x7FFF + ((b >> 16) & 1)) & 0xFFFF0000
+    return b.astype(np.uint32).view(np.float32)
+
+
+def replay_params_bf16(counts: list[int], seed: int, world: int, iterations: int, lr: float,
+                       distinct: bool = True) -> list[np.ndarray]:
+    """replay_params with every rank's contribution rounded to bf16 before the fp32 sum."""
+    params = [np.zeros(c, dtype=np.float32) for c in counts]
+    for k in range(iterations):
+        for layer, c in enumerate(counts):
+            grads = {r: to_bf16(grad_block(rank_seed(seed, r, distinct), k, layer, 0, c)) for r in range(world)}
+            params[layer] = shard_update(params[layer], grads, lr)
+    return params
+
+
 def digest(params: list[np.ndarray]) -> int:
     """TrainingWorker.params_digest, worker.py:372-376."""
     h = FNV_BASIS

@@ -79,6 +79,7 @@ class Config(ctypes.Structure):
         ("pop_relax", ctypes.c_uint32),
         ("pop_run", ctypes.c_uint32),
         ("pop_multi", ctypes.c_uint32),
+        ("push_bf16", ctypes.c_uint32),
         ("gate_groups", ctypes.POINTER(ctypes.c_uint32)),
     ]
 

@@ -593,6 +593,7 @@ static CommArgs comm_args(p3_ctx* c, uint32_t mode, uint32_t ctas) {
   a.pop_run = c->cfg.pop_run ? c->cfg.pop_run
                              : std::max<uint32_t>(1, std::min<uint32_t>(8, c->S / std::max<uint32_t>(1, 4 * ctas)));
   a.pop_multi = std::max<uint32_t>(1, std::min<uint32_t>(4, c->cfg.pop_multi ? c->cfg.pop_multi : 1));
+  a.push_bf16 = c->cfg.push_bf16 ? 1u : 0u;
   // bounded relaxation of the pop order: never more than the number of concurrent consumers
   a.pop_relax = std::min<uint32_t>(ctas, c->cfg.pop_relax ? c->cfg.pop_relax : 8);
   if (c->cfg.throttle_bps > 0) {

@@ -119,6 +119,7 @@ struct CommArgs {
   uint32_t pop_run;   // single rank: consecutive slices claimed per pop
   uint32_t pop_relax; // a pop may take any of this many most urgent layers (1: strict)
   uint32_t pop_multi; // candidate layers claimed per round of pop atomics
+  uint32_t push_bf16; // pushes travel as bf16
   float ns_per_byte;  // K7 link emulation (0: unthrottled)
   unsigned long long burst_ns;
   unsigned long long timeout_ns;

@@ -14,6 +14,7 @@
 // Floating point follows the reference's numpy fp32 semantics exactly: the sum is taken in
 // ascending rank order starting from +0.0, then divided by N, then p - lr*g with the multiply
 // and the subtract rounded separately (explicit _rn intrinsics: no FMA contraction).
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -620,6 +621,7 @@ __device__ __forceinline__ QueueView queue_of(const CommArgs& a, const LocalDev&
 #define JOB_EXIT 3
 struct Job {
   uint32_t kind, li, g, layer, slice, rank, len, n, aligned, run;
+  uint32_t bf16;  // pushes travel as bf16 (declared lossy mode); own = index of the fp32 source
   const float* src[P3_MAX_RANKS];  // PUSH: src[0]; REDUCE: contributions in rank order
   float* dst[P3_MAX_RANKS];        // PUSH: dst[0]; REDUCE: replicas, dst[0] = owner's master
   float* v;
@@ -729,7 +731,10 @@ __device__ uint32_t prepare_push(const CommArgs& a, uint32_t li, uint32_t g, Job
     job->rank = o;
     job->len = P.slice_len[g];
     job->src[0] = pub_ptr(ld_relaxed_gpu64(L.pub + l)) + P.slice_off[g];
-    job->dst[0] = a.peers.R[o] + (uint64_t)r * P.own_stride[o] + P.slice_slot[g];
+    job->bf16 = a.push_bf16;
+    const uint64_t ri = (uint64_t)r * P.own_stride[o] + P.slice_slot[g];
+    job->dst[0] = a.push_bf16 ? reinterpret_cast<float*>(reinterpret_cast<__nv_bfloat16*>(a.peers.R[o]) + ri)
+                              : a.peers.R[o] + ri;
   }
   return PUSH_REMOTE;
 }
@@ -746,8 +751,10 @@ __device__ void prepare_reduce(const CommArgs& a, uint32_t li, uint32_t g, Job* 
   __syncwarp();
   uintptr_t al = 0;
   if (q < N) {
-    const float* src = q == o ? pub_ptr(ld_relaxed_gpu64(L.pub + l)) + P.slice_off[g]
-                              : a.peers.R[o] + (uint64_t)q * P.own_stride[o] + P.slice_slot[g];
+    const uint64_t ri = (uint64_t)q * P.own_stride[o] + P.slice_slot[g];
+    const float* rsrc = a.push_bf16 ? reinterpret_cast<const float*>(reinterpret_cast<__nv_bfloat16*>(a.peers.R[o]) + ri)
+                                    : a.peers.R[o] + ri;
+    const float* src = q == o ? pub_ptr(ld_relaxed_gpu64(L.pub + l)) + P.slice_off[g] : rsrc;
     float* dst = a.peers.W[q] + woff;
     job->src[q] = src;
     job->dst[q == o ? 0 : (q < o ? q + 1 : q)] = dst;
@@ -768,14 +775,56 @@ __device__ void prepare_reduce(const CommArgs& a, uint32_t li, uint32_t g, Job* 
     job->len = len;
     job->n = N;
     job->v = v;
+    job->bf16 = a.push_bf16 ? 1u + o : 0u;  // 1 + index of the owner's own (fp32) contribution
     job->aligned = ((al | (uintptr_t)v) & 15) == 0;
+  }
+}
+
+// bf16 transport (declared lossy mode): each rank's contribution is rounded to bf16 (round
+// to nearest even) — the owner's own one too, so every rank counts alike — then summed in
+// fp32 in ascending rank order; the update and the broadcast parameters stay fp32.
+__device__ __forceinline__ float bf16_round(float x) { return __bfloat162float(__float2bfloat16_rn(x)); }
+
+__device__ void cta_copy_to_bf16(__nv_bfloat16* dst, const float* src, uint32_t n, uint32_t tid, uint32_t nthr) {
+  uint32_t done = 0;
+  if ((((uintptr_t)src & 15) | ((uintptr_t)dst & 7)) == 0) {
+    const uint32_t n4 = n / 4;
+    for (uint32_t j = tid; j < n4; j += nthr) {
+      const float4 v = __ldcg(reinterpret_cast<const float4*>(src) + j);
+      __nv_bfloat162 lo = __floats2bfloat162_rn(v.x, v.y), hi = __floats2bfloat162_rn(v.z, v.w);
+      uint2 w;
+      w.x = *reinterpret_cast<uint32_t*>(&lo);
+      w.y = *reinterpret_cast<uint32_t*>(&hi);
+      *reinterpret_cast<uint2*>(dst + 4 * j) = w;
+    }
+    done = 4 * n4;
+  }
+  for (uint32_t i = done + tid; i < n; i += nthr) dst[i] = __float2bfloat16_rn(__ldcg(src + i));
+}
+
+__device__ void cta_update_bf16(float* const* dst, int ndst, const float* const* src, int nw, int own, float* v,
+                                uint64_t n, const UpdCoef& c, uint32_t tid, uint32_t nthr) {
+  for (uint64_t i = tid; i < n; i += nthr) {
+    float acc = 0.f;
+    for (int q = 0; q < nw; ++q) {
+      const float x = q == own ? bf16_round(__ldcg(src[q] + i))
+                               : __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(src[q])[i]);
+      acc = __fadd_rn(acc, x);
+    }
+    const float p = sgd_step(__ldcg(dst[0] + i), acc, c, v ? v + i : nullptr);
+    for (int d = 0; d < ndst; ++d) dst[d][i] = p;
   }
 }
 
 // Movers: move the job's data.
 __device__ void move_job(const CommArgs& a, const Job& j, uint32_t tid, uint32_t nthr) {
-  if (j.kind == JOB_PUSH) {
+  if (j.kind == JOB_PUSH && j.bf16) {
+    cta_copy_to_bf16(reinterpret_cast<__nv_bfloat16*>(j.dst[0]), j.src[0], j.len, tid, nthr);
+  } else if (j.kind == JOB_PUSH) {
     cta_copy(j.dst[0], j.src[0], j.len, tid, nthr);
+  } else if (j.bf16) {
+    cta_update_bf16(j.dst, (int)j.n, j.src, (int)j.n, (int)j.bf16 - 1, j.v, j.len, make_coef(j.n, a.lr, a.momentum),
+                    tid, nthr);
   } else {
     cta_update_generic(j.dst[0], j.dst, (int)j.n, j.src, (int)j.n, j.v, j.len, j.aligned != 0,
                        make_coef(j.n, a.lr, a.momentum), tid, nthr);
@@ -800,14 +849,14 @@ __device__ void signal_job(const CommArgs& a, const Job& j) {
       red_add_relaxed_sys(a.peers.hint[j.rank] + j.layer, 1u);
       red_add_relaxed_sys(a.peers.tally[j.rank] + 1, 1u);
     }
-    atomicAdd(L.bytes + 1, 4ull * j.len);
+    atomicAdd(L.bytes + 1, (j.bf16 ? 2ull : 4ull) * j.len);
   } else {
     const uint32_t grp = P.layer_group[j.layer];
     for (uint32_t q = 0; q < j.n; ++q) {
       red_add_relaxed_sys(a.peers.done[q] + j.layer, j.run);
       red_add_relaxed_sys(a.peers.gdone[q] + grp, j.run);
     }
-    atomicAdd(L.bytes + 0, 4ull * j.len * (j.n - 1));  // pushes received
+    atomicAdd(L.bytes + 0, (j.bf16 ? 2ull : 4ull) * j.len * (j.n - 1));  // pushes received
     atomicAdd(L.bytes + 1, 4ull * j.len * (j.n - 1));  // broadcasts sent
     for (uint32_t i = 0; i < j.run; ++i)
       trace_append(L, a.k, j.layer, j.g + i - P.layer_first[j.layer], j.rank, P3_EV_BCAST);
@@ -970,7 +1019,8 @@ __global__ void __launch_bounds__(512, 1) k_comm(const __grid_constant__ CommArg
         if (how == PUSH_REDUCE) kind = JOB_REDUCE;  // own slice completed it: reduce right away
       }
       if (kind == JOB_PUSH || kind == JOB_REDUCE) {  // egress bytes of this job on the rank's link
-        const uint64_t bytes = 4ull * a.plan.slice_len[g] * (kind == JOB_PUSH ? 1u : a.plan.world - 1u);
+        const uint64_t bytes = (kind == JOB_PUSH && a.push_bf16 ? 2ull : 4ull) * a.plan.slice_len[g] *
+                               (kind == JOB_PUSH ? 1u : a.plan.world - 1u);
         if (lane == 0) pace(a, a.loc[li], bytes);
         __syncwarp();
       }
@@ -1015,6 +1065,7 @@ __global__ void __launch_bounds__(512, 1) k_comm(const __grid_constant__ CommArg
       mine.len = j.len;
       mine.n = j.n;
       mine.run = j.run;
+      mine.bf16 = j.bf16;
       __syncwarp();
       bar_arrive(BAR_EMPTY(b), 64);
       if (lane == 0) {

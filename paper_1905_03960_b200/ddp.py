@@ -149,7 +149,7 @@ class P3DataParallel(_HookedDataParallel):
             timeout_s=timeout_s, trace_cap=trace_cap, drain_bytes=drain_bytes, plan_mode=plan_mode,
             throttle_bps=throttle_bps, throttle_burst=throttle_burst, big_threshold=big_threshold,
             gate_groups=groups, pub_batch_bytes=pub_batch_bytes, drain_linger_us=drain_linger_us,
-            finish_ctas=finish_ctas,
+            finish_ctas=finish_ctas, push_dtype=push_dtype,
         )
         if self.world > 1:
             handles = [None] * self.world

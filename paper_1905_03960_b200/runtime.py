@@ -75,6 +75,7 @@ class SyncContext:
         pop_relax: int = 0,
         pop_run: int = 0,
         pop_multi: int = 0,
+        push_dtype: str = "fp32",
     ) -> None:
         import torch
 
@@ -109,6 +110,10 @@ class SyncContext:
         cfg.pop_relax = pop_relax
         cfg.pop_run = pop_run
         cfg.pop_multi = pop_multi
+        if push_dtype not in ("fp32", "bf16"):
+            raise ValueError("push_dtype must be 'fp32' or 'bf16'")
+        cfg.push_bf16 = 1 if push_dtype == "bf16" else 0
+        self.push_dtype = push_dtype
         if gate_groups is not None:
             if len(gate_groups) != len(self.layer_counts):
                 raise ValueError("gate_groups needs one group id per layer")
@@ -285,6 +290,7 @@ class WorkerConfig:
     throttle_burst: int = 50 * 1024
     big_threshold: int = 1_000_000     # baseline plan (cli.py:68)
     seed: int = 0                      # baseline plan placement seed (cli.py:74)
+    push_dtype: str = "fp32"           # "bf16": declared lossy transport of pushes
 
 
 def rank_seed(seed: int, rank: int, distinct: bool) -> int:
@@ -338,6 +344,7 @@ class TrainingWorker:
             rng_seed=config.seed,
             throttle_bps=config.throttle_rate or 0.0,
             throttle_burst=config.throttle_burst,
+            push_dtype=config.push_dtype,
         )
         self.comm_stream = torch.cuda.Stream()
         self.streams = [torch.cuda.Stream() for _ in self.ranks]

@@ -328,3 +328,25 @@ def test_simulator_device_queue_replay(cuda, golden):
     for case in golden["sim_cases"]:
         sc = scenario_from_dict(case["scenario"])
         assert simulate(sc, device_queue=True).to_csv() == case["csv"], case["scenario"]["name"]
+
+
+@pytest.mark.parametrize("world", [1, 2, 4])
+def test_bf16_push_matches_oracle(cuda, world):
+    # declared lossy transport: bf16 contributions (RNE), fp32 sum in rank order and update
+    from paper_1905_03960_b200.model import builtin_profile
+    from paper_1905_03960_b200.runtime import TrainingWorker, WorkerConfig
+
+    prof = builtin_profile("resnet50-like")
+    cfg = WorkerConfig(rank=0, mode="p3", world=world, iterations=3, lr=0.1, emulate_compute=False, comm_ctas=8,
+                       rank_distinct_grads=True, push_dtype="bf16")
+    w = TrainingWorker(cfg, prof, ranks=list(range(world)))
+    w.run()
+    want = O.replay_params_bf16(prof.param_counts(), prof.seed, world, 3, 0.1, distinct=True)
+    for li in range(world):
+        for a, b in zip(w.params(li), want):
+            assert a.tobytes() == b.tobytes()
+    # the bf16 result stays within bf16 rounding of the fp32 path
+    ref = O.replay_params(prof.param_counts(), prof.seed, world, 3, 0.1, distinct=True)
+    for a, b in zip(w.params(0), ref):
+        assert np.max(np.abs(a - b)) <= 3 * 0.1 * 2.0 ** -8
+    w.close()

@@ -146,3 +146,14 @@ def test_heap_queue_order():
     f.put_layer(2, 1)
     f.put_layer(0, 1)
     assert [f.poll(), f.poll(), f.poll()] == [(2, 0), (0, 0), None]
+
+
+def test_bf16_rounding_matches_torch():
+    # pin the oracle's RNE bf16 rounding against torch's conversion
+    import torch
+
+    rng = np.random.RandomState(0)
+    x = np.concatenate([rng.uniform(-3, 3, 100_000), rng.standard_normal(10_000) * 1e-30,
+                        np.array([0.0, -0.0, 1.0, 1.00390625, 1.01171875, 65504.0, 3.4e38])]).astype(np.float32)
+    want = torch.from_numpy(x).to(torch.bfloat16).to(torch.float32).numpy()
+    assert O.to_bf16(x).tobytes() == want.tobytes()
