@@ -128,6 +128,7 @@ class P3DataParallel(_HookedDataParallel):
         pub_batch_bytes: int = 1 << 20,
         drain_linger_us: int = 200,
         finish_ctas: int = 0,
+        push_dtype: str = "fp32",
         plan_mode: str = "p3",
         throttle_bps: float = 0.0,
         throttle_burst: int = 50 * 1024,
