@@ -346,7 +346,8 @@ def run_ours(args):
     throttled = None
     if world > 1 and args.throttle_gbps > 0:
         throttled = {"gbps": args.throttle_gbps, "burst_bytes": 50 * 1024}
-        for arm, kw in (("p3", {}), ("layerwise_fifo", {"plan_mode": "baseline", "priority_mode": False})):
+        for arm, kw in (("p3", {}), ("layerwise_fifo", {"plan_mode": "baseline", "priority_mode": False}),
+                        ("p3_bf16_push", {"push_dtype": "bf16"})):
             model = build(args, rank)
             d = P3DataParallel(model, lr=args.lr, max_slice=args.max_slice, comm_ctas=4, pub_batch_bytes=0,
                                throttle_bps=args.throttle_gbps * 1e9, **kw)

@@ -49,6 +49,30 @@ def main():
             dist.barrier()
             w.close()
 
+    # the layer-wise baseline (KVStore placement + FIFO) on the same kernels across processes:
+    # bit-identical to P3 (SPEC acceptance #3)
+    for name in ("toy3", "vgg19-like"):
+        if (name, world, "same") not in want:
+            continue
+        prof = builtin_profile(name)
+        cfg = WorkerConfig(rank=rank, mode="baseline", world=world, iterations=10, deadlock_timeout=60.0,
+                           emulate_compute=False, comm_ctas=8, big_threshold=100_000)
+        ctx = SyncContext(prof.param_counts(), world, [rank], lr=cfg.lr, comm_ctas=8, timeout_s=60.0,
+                          emulate_grads=True, plan_mode="baseline", priority_mode=False, big_threshold=100_000)
+        hs = [None] * world
+        dist.all_gather_object(hs, ctx.ipc_handle(0))
+        ctx.open_peers(hs)
+        dist.barrier()
+        w = TrainingWorker(cfg, prof, ranks=[rank], ctx=ctx)
+        try:
+            w.run()
+            got = f"{w.params_digest(0):016x}"
+        except Exception as e:  # noqa: BLE001
+            got = f"error: {e}"
+        out["digests"][f"{name}/baseline"] = [got, want[(name, world, "same")]]
+        dist.barrier()
+        w.close()
+
     # torch mode: identical data on every rank -> mean gradient == local gradient, so the
     # result must equal single-GPU fp32 SGD bit for bit
     from paper_1905_03960_b200.ddp import LayerwiseDataParallel, P3DataParallel
