@@ -217,8 +217,10 @@ def sync_only_roofline(args, world, rank, counts):
         stream.synchronize()
         barrier(world)
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(stream):
+            torch.cuda._sleep(200_000)  # ~0.1 ms: the host enqueues the launch before the GPU gets there
+        ctx.iteration_begin(k, stream)  # per-iteration counter reset (memset) — not the kernel
         s.record(stream)
-        ctx.iteration_begin(k, stream)
         ctx.iteration_end(k)  # one FINISH launch does the whole iteration
         e.record(stream)
         ctx.sync_all(k + 1, 60.0)

@@ -202,9 +202,9 @@ typedef struct p3_config {
                                           long while peers' pushes of partially arrived owned
                                           slices are outstanding (never for local compute) */
   uint32_t finish_ctas;                /* CTAs of the FINISH launch (0: comm_ctas) */
-  uint32_t pop_relax;                  /* concurrent comm CTAs may each pop any of this many most
-                                          urgent published layers (0: 8; 1: strict order);
-                                          capped at the CTA count */
+  uint32_t pop_relax;                  /* bounded relaxation: a pop takes one of this many most
+                                          urgent published slices (0: the launch's CTA count;
+                                          1: strict order); capped at the CTA count */
   uint32_t pop_run;                    /* single rank: consecutive slices per job (0: auto) */
   uint32_t pop_multi;                  /* layers claimed per round of pop atomics, 1..4 (0: 1) */
   uint32_t push_bf16;                  /* declared lossy transport: pushes carry bf16 (RNE)

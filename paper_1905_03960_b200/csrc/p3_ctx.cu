@@ -134,6 +134,7 @@ struct p3_ctx {
   cudaEvent_t side_ev[P3_SIDE_STREAMS]{};
   cudaEvent_t iter_ev = nullptr;
   uint32_t side_next = 0;
+  uint32_t side_used = 0;  // side streams that carry a DRAIN launch of the open iteration
   uint64_t open_iter = 0;
   bool iter_open = false;
   uint64_t launches = 0;
@@ -594,8 +595,11 @@ static CommArgs comm_args(p3_ctx* c, uint32_t mode, uint32_t ctas) {
                              : std::max<uint32_t>(1, std::min<uint32_t>(8, c->S / std::max<uint32_t>(1, 4 * ctas)));
   a.pop_multi = std::max<uint32_t>(1, std::min<uint32_t>(4, c->cfg.pop_multi ? c->cfg.pop_multi : 1));
   a.push_bf16 = c->cfg.push_bf16 ? 1u : 0u;
-  // bounded relaxation of the pop order: never more than the number of concurrent consumers
-  a.pop_relax = std::min<uint32_t>(ctas, c->cfg.pop_relax ? c->cfg.pop_relax : 8);
+  // bounded relaxation of the pop order: a pop takes one of the C most urgent slices, C =
+  // the launch's concurrent consumers (its CTAs) unless configured lower
+  // (measured, tools/sync_sweep.py, ResNet-50 N=1 sync-only: C=8 2.2 TB/s, C=148 3.4 TB/s —
+  // 148 schedulers racing for the same few one-slice layers lose an atomic round trip per try)
+  a.pop_relax = std::min<uint32_t>(ctas, c->cfg.pop_relax ? c->cfg.pop_relax : ctas);
   if (c->cfg.throttle_bps > 0) {
     a.ns_per_byte = (float)(8e9 / c->cfg.throttle_bps);
     a.burst_ns = (unsigned long long)((double)c->cfg.throttle_burst * 8e9 / c->cfg.throttle_bps);
@@ -620,7 +624,12 @@ static int flush_publications(p3_ctx* c, uint32_t li) {
 // after the per-iteration reset on the main comm stream; the FINISH launch on the main comm
 // stream comes after all of them.
 static int launch_drain(p3_ctx* c, int li) {
-  cudaStream_t s = c->side[c->side_next++ % P3_SIDE_STREAMS];
+  const uint32_t j = c->side_next++ % P3_SIDE_STREAMS;
+  cudaStream_t s = c->side[j];
+  if (!(c->side_used & (1u << j))) {  // first launch of the iteration here: after the reset
+    CK(cudaStreamWaitEvent(s, c->iter_ev, 0));
+    c->side_used |= 1u << j;
+  }
   CK(cudaEventRecord(c->ready_ev[li], c->pend_stream[li]));
   CK(cudaStreamWaitEvent(s, c->ready_ev[li], 0));
   c->published[li] = 0;
@@ -640,8 +649,8 @@ int p3_iteration_begin(p3_ctx_t* c, uint64_t k, void* stream) {
   const LocalLayout& ll = c->local_layout;
   for (uint32_t i = 0; i < c->cfg.n_local; ++i)
     CK(cudaMemsetAsync(static_cast<char*>(c->local_arena[i]) + ll.iter_begin, 0, ll.iter_end - ll.iter_begin, s));
-  CK(cudaEventRecord(c->iter_ev, s));
-  for (int j = 0; j < P3_SIDE_STREAMS; ++j) CK(cudaStreamWaitEvent(c->side[j], c->iter_ev, 0));
+  CK(cudaEventRecord(c->iter_ev, s));  // side streams wait for it when they get a DRAIN launch
+  c->side_used = 0;
   c->comm_stream = s;
   c->open_iter = k;
   c->iter_open = true;
@@ -660,7 +669,8 @@ int p3_iteration_end(p3_ctx_t* c, uint64_t k) {
     CK(cudaStreamWaitEvent(c->comm_stream, c->ready_ev[i], 0));
     c->published[i] = 0;
   }
-  for (int j = 0; j < P3_SIDE_STREAMS; ++j) {
+  for (int j = 0; j < P3_SIDE_STREAMS; ++j) {  // only the side streams used this iteration
+    if (!(c->side_used & (1u << j))) continue;
     CK(cudaEventRecord(c->side_ev[j], c->side[j]));
     CK(cudaStreamWaitEvent(c->comm_stream, c->side_ev[j], 0));
   }

@@ -367,10 +367,21 @@ struct Stash {
   uint32_t n;
   uint32_t g[P3_MULTI];
   uint32_t run[P3_MULTI];
+  uint32_t layer[P3_MULTI];
+  uint64_t word[P3_MULTI];
+};
+
+// What a pop hands to the caller besides the slice id: the slice's layer and the layer's
+// publication word (already loaded by the pop), so preparing the job needs no dependent
+// round trip through slice_layer[] / pub[].
+struct Popped {
+  uint32_t run;
+  uint32_t layer;
+  uint64_t word;
 };
 
 __device__ uint32_t warp_pop(const QueueView& q, uint32_t tag, uint32_t* dbg = nullptr, uint32_t want = 1,
-                             uint32_t* run = nullptr, Stash* stash = nullptr) {
+                             Popped* out = nullptr, Stash* stash = nullptr) {
   const uint32_t lane = threadIdx.x & 31;
   if (q.sched == P3_SCHED_PRIORITY) {
     constexpr uint32_t CH = 8;  // chunks of 32 layers examined per memory round trip
@@ -391,11 +402,73 @@ __device__ uint32_t warp_pop(const QueueView& q, uint32_t tag, uint32_t* dbg = n
       for (uint32_t c = 0; c < CH; ++c) bits |= (uint32_t)(pub_ready(w[c], tag) && cur[c] < ns[c]) << c;
       const uint32_t nchunk = min(CH, (q.n_layers - group + 31) / 32);
       bool first = true;
+      if (q.relax > 1 && !(stash && q.multi > 1)) {
+        // Bounded relaxation, ranked by slice: with `relax` consumers popping at once, this
+        // CTA aims at the (blockIdx % relax)-th most urgent available slice of the group —
+        // one claim that rarely collides, where racing for the same few most urgent layers
+        // (one-slice layers: most of ResNet-50) costs a lost atomic round trip per try.
+        uint32_t tot[CH], total = 0;
+#pragma unroll
+        for (uint32_t c = 0; c < CH; ++c) {
+          tot[c] = __reduce_add_sync(FULL_MASK, ((bits >> c) & 1u) ? ns[c] - cur[c] : 0u);
+          total += tot[c];
+        }
+        if (total) {
+          uint32_t t = (blockIdx.x % q.relax) % total, tc = 0;
+#pragma unroll
+          for (uint32_t c = 0; c < CH; ++c) {  // chunk holding rank t (uniform)
+            if (c == tc && t >= tot[c] && c + 1 < CH) {
+              t -= tot[c];
+              tc = c + 1;
+            }
+          }
+          uint32_t r = 0, my_ns = 0;
+          uint64_t my_w = 0;
+#pragma unroll
+          for (uint32_t c = 0; c < CH; ++c) {
+            if (c == tc) {
+              r = ((bits >> c) & 1u) ? ns[c] - cur[c] : 0u;
+              my_ns = ns[c];
+              my_w = w[c];
+            }
+          }
+          uint32_t incl = r;  // inclusive scan over the lanes (layer order)
+#pragma unroll
+          for (int off = 1; off < 32; off <<= 1) {
+            const uint32_t y = __shfl_up_sync(FULL_MASK, incl, off);
+            if (lane >= (uint32_t)off) incl += y;
+          }
+          const bool hit = r && incl - r <= t && t < incl;
+          uint32_t s = 0;
+          bool won = false;
+          if (hit) {
+            s = atomicAdd(q.cursor + group + 32 * tc + lane, want);
+            won = s < my_ns;
+          }
+          const uint32_t wm = __ballot_sync(FULL_MASK, won);
+          if (wm) {
+            const uint32_t j0 = __ffs(wm) - 1;
+            const uint32_t l = group + 32 * tc + j0;
+            const uint32_t g0 = __shfl_sync(FULL_MASK, won ? q.first[l] + s : 0u, j0);
+            if (out) {
+              out->run = __shfl_sync(FULL_MASK, won ? min(want, my_ns - s) : 0u, j0);
+              out->layer = l;
+              out->word = __shfl_sync(FULL_MASK, (unsigned long long)my_w, j0);
+            }
+            return g0;
+          }
+        }
+        first = false;  // lost (or nothing here): strict order from the most urgent
+      }
       for (uint32_t c = 0; c < nchunk; ++c) {
         uint32_t m = __ballot_sync(FULL_MASK, (bits >> c) & 1u);
         uint32_t my_ns = 0;
+        uint64_t my_w = 0;
 #pragma unroll
-        for (uint32_t cc = 0; cc < CH; ++cc) my_ns = cc == c ? ns[cc] : my_ns;
+        for (uint32_t cc = 0; cc < CH; ++cc) {
+          my_ns = cc == c ? ns[cc] : my_ns;
+          my_w = cc == c ? w[cc] : my_w;
+        }
         while (m) {
           // candidates: the most urgent available layers of the chunk — starting, on the
           // first round, at a CTA-dependent one of the `relax` most urgent (a pop is then
@@ -427,11 +500,17 @@ __device__ uint32_t warp_pop(const QueueView& q, uint32_t tag, uint32_t* dbg = n
               const uint32_t idx = stash->n + __popc(wm & ((1u << lane) - 1u)) - 1u;
               stash->g[idx] = my_g;
               stash->run[idx] = my_run;
+              stash->layer[idx] = l;
+              stash->word[idx] = my_w;
             }
             __syncwarp();
             if (lane == 0 && stash) stash->n += __popc(wm) - 1u;
             __syncwarp();
-            if (run) *run = __shfl_sync(FULL_MASK, my_run, j0);
+            if (out) {
+              out->run = __shfl_sync(FULL_MASK, my_run, j0);
+              out->layer = group + 32 * c + j0;
+              out->word = __shfl_sync(FULL_MASK, (unsigned long long)my_w, j0);
+            }
             return __shfl_sync(FULL_MASK, my_g, j0);
           }
           m &= ~cand;  // every candidate lost the race for its layer's last slices
@@ -443,22 +522,27 @@ __device__ uint32_t warp_pop(const QueueView& q, uint32_t tag, uint32_t* dbg = n
   for (uint32_t retry = 0;; ++retry) {
     if (dbg && lane == 0) *(volatile uint32_t*)dbg = (6u << 20) | (retry & 0xfffff);
     uint32_t best_key = P3_NONE, best_l = P3_NONE;
+    uint64_t best_w = 0;
     for (uint32_t l = lane; l < q.n_layers; l += 32) {
-      if (!pub_ready(ld_relaxed_gpu64(q.pub + l), tag)) continue;
+      const uint64_t w = ld_relaxed_gpu64(q.pub + l);
+      if (!pub_ready(w, tag)) continue;
       if (ld_relaxed_gpu(q.cursor + l) >= q.nslices[l]) continue;
       const uint32_t key = ld_relaxed_gpu(q.fifo_key + l);
       if (key < best_key || (key == best_key && l < best_l)) {
         best_key = key;
         best_l = l;
+        best_w = w;
       }
     }
 #pragma unroll
     for (int off = 16; off; off >>= 1) {
       const uint32_t ok = __shfl_xor_sync(FULL_MASK, best_key, off);
       const uint32_t ol = __shfl_xor_sync(FULL_MASK, best_l, off);
+      const uint64_t ow = __shfl_xor_sync(FULL_MASK, (unsigned long long)best_w, off);
       if (ok < best_key || (ok == best_key && ol < best_l)) {
         best_key = ok;
         best_l = ol;
+        best_w = ow;
       }
     }
     if (best_l == P3_NONE) return P3_NONE;
@@ -466,7 +550,11 @@ __device__ uint32_t warp_pop(const QueueView& q, uint32_t tag, uint32_t* dbg = n
     if (lane == 0) s = atomicAdd(q.cursor + best_l, want);
     s = __shfl_sync(FULL_MASK, s, 0);
     if (s < q.nslices[best_l]) {
-      if (run) *run = min(want, q.nslices[best_l] - s);
+      if (out) {
+        out->run = min(want, q.nslices[best_l] - s);
+        out->layer = best_l;
+        out->word = best_w;
+      }
       return q.first[best_l] + s;
     }
     // lost the race for the last slice of that layer: rescan
@@ -491,7 +579,8 @@ int launch_queue_pop(const uint32_t* nslices, const uint32_t* first, const uint6
 // Server role pick (one warp): the lowest layer with a completed, unclaimed owned slice,
 // then the first such slice of that layer (ascending slice index). The inbox of
 // ServerEngine is priority ordered (server.py:118), so the same order is used here.
-__device__ uint32_t warp_server_pick(const CommArgs& a, const LocalDev& L, uint32_t* dbg = nullptr) {
+__device__ uint32_t warp_server_pick(const CommArgs& a, const LocalDev& L, uint32_t* layer_out,
+                                     uint32_t* dbg = nullptr) {
   const uint32_t lane = threadIdx.x & 31;
   const PlanDev& P = a.plan;
   const uint32_t o = L.rank, nl = P.n_layers, k = a.k;
@@ -553,7 +642,10 @@ __device__ uint32_t warp_server_pick(const CommArgs& a, const LocalDev& L, uint3
               }
             }
             won = __shfl_sync(FULL_MASK, won, 0);
-            if (won) return gj;
+            if (won) {
+              *layer_out = l;
+              return gj;
+            }
             m &= m - 1;
           }
         }
@@ -668,14 +760,18 @@ __device__ void ingest(const LocalDev& L, uint32_t sched) {
   const uint32_t lane = threadIdx.x & 31;
   uint32_t lo = 0, hi = 0, won = 0;
   if (lane == 0) {
+    lo = ld_relaxed_gpu(L.ingested);  // issued first: both loads share one round trip
     hi = ld_acquire_gpu(L.pubseq);
-    lo = ld_relaxed_gpu(L.ingested);
     if ((int32_t)(hi - lo) > 0) won = atomicCAS(L.ingested, lo, hi) == lo;
   }
   won = __shfl_sync(FULL_MASK, won, 0);
   if (!won) return;
   lo = __shfl_sync(FULL_MASK, lo, 0);
   hi = __shfl_sync(FULL_MASK, hi, 0);
+  // release: a consumer that reads a publication word relaxed and then fences (acquire
+  // pattern) sees the gradients the memory write of pubseq was ordered after
+  __syncwarp();
+  fence_acq_rel_gpu();
   for (uint32_t i = lo + lane; (int32_t)(hi - i) > 0; i += 32) {
     const volatile PubEntry* e = L.ring + (i % L.ring_cap);
     const uint32_t layer = e->layer;
@@ -695,15 +791,17 @@ __device__ void ingest(const LocalDev& L, uint32_t sched) {
 #define PUSH_DONE 0
 #define PUSH_REMOTE 1
 #define PUSH_REDUCE 2
-__device__ uint32_t prepare_push(const CommArgs& a, uint32_t li, uint32_t g, Job* job) {
+__device__ uint32_t prepare_push(const CommArgs& a, uint32_t li, uint32_t g, uint32_t l, uint64_t w, Job* job) {
   const PlanDev& P = a.plan;
   const LocalDev& L = a.loc[li];
-  const uint32_t r = L.rank, o = P.slice_owner[g], l = P.slice_layer[g];
+  const uint32_t r = L.rank, o = P.slice_owner[g];
   const uint32_t lane = threadIdx.x & 31;
   if (!job) {
     uint32_t verdict = o == r ? PUSH_DONE : PUSH_REMOTE;
     if (lane == 0) {
-      (void)ld_acquire_gpu64(L.pub + l);  // the gradient is published: visible from here on
+      // the pop read the publication word relaxed: this fence makes it an acquire, so the
+      // gradient is visible from here on (ingest released it)
+      fence_acq_rel_gpu();
       trace_append(L, a.k, l, g - P.layer_first[l], r, P3_EV_PUSH);
       if (o == r) {
         // the contribution stays in place (published to this rank by the acquire above)
@@ -730,7 +828,7 @@ __device__ uint32_t prepare_push(const CommArgs& a, uint32_t li, uint32_t g, Job
     job->layer = l;
     job->rank = o;
     job->len = P.slice_len[g];
-    job->src[0] = pub_ptr(ld_relaxed_gpu64(L.pub + l)) + P.slice_off[g];
+    job->src[0] = pub_ptr(w) + P.slice_off[g];
     job->bf16 = a.push_bf16;
     const uint64_t ri = (uint64_t)r * P.own_stride[o] + P.slice_slot[g];
     job->dst[0] = a.push_bf16 ? reinterpret_cast<float*>(reinterpret_cast<__nv_bfloat16*>(a.peers.R[o]) + ri)
@@ -741,30 +839,42 @@ __device__ uint32_t prepare_push(const CommArgs& a, uint32_t li, uint32_t g, Job
 
 // Scheduler side of a reduce: contributions of every rank (the owner's own straight from
 // its gradient) and every replica to write, master first.
-__device__ void prepare_reduce(const CommArgs& a, uint32_t li, uint32_t g, Job* job, uint32_t run = 1) {
+// `w` is the layer's publication word when the caller already holds it (0: load it).
+__device__ void prepare_reduce(const CommArgs& a, uint32_t li, uint32_t g, uint32_t l, uint64_t w, Job* job,
+                               uint32_t run = 1) {
   const PlanDev& P = a.plan;
   const LocalDev& L = a.loc[li];
-  const uint32_t o = L.rank, l = P.slice_layer[g], N = P.world;
+  const uint32_t o = L.rank, N = P.world;
   const uint32_t q = threadIdx.x & 31;
-  const uint64_t woff = P.layer_woff[l] + P.slice_off[g];
-  if (q == 0) (void)ld_acquire_sys(a.peers.arrivals[o] + g);  // all N pushes are visible
+  // independent loads first (one round trip), then the acquire that orders the data reads
+  const uint64_t soff = P.slice_off[g];
+  const uint64_t woff = P.layer_woff[l] + soff;
+  const uint64_t slot = P.slice_slot[g];
+  const uint64_t stride = P.own_stride[o];
+  uint32_t len = q < run ? P.slice_len[g + q] : 0u;  // consecutive slices: contiguous
+  if (!w) w = ld_relaxed_gpu64(L.pub + l);
+  if (N > 1) {
+    if (q == 0) (void)ld_acquire_sys(a.peers.arrivals[o] + g);  // all N pushes are visible
+  } else if (q == 0) {
+    fence_acq_rel_gpu();  // acquire of the publication word (single rank: nothing arrives)
+  }
   __syncwarp();
   uintptr_t al = 0;
   if (q < N) {
-    const uint64_t ri = (uint64_t)q * P.own_stride[o] + P.slice_slot[g];
+    const uint64_t ri = (uint64_t)q * stride + slot;
     const float* rsrc = a.push_bf16 ? reinterpret_cast<const float*>(reinterpret_cast<__nv_bfloat16*>(a.peers.R[o]) + ri)
                                     : a.peers.R[o] + ri;
-    const float* src = q == o ? pub_ptr(ld_relaxed_gpu64(L.pub + l)) + P.slice_off[g] : rsrc;
+    const float* src = q == o ? pub_ptr(w) + soff : rsrc;
     float* dst = a.peers.W[q] + woff;
     job->src[q] = src;
     job->dst[q == o ? 0 : (q < o ? q + 1 : q)] = dst;
     al = (uintptr_t)src | (uintptr_t)dst;
   }
-  float* v = L.V ? L.V + P.slice_slot[g] : nullptr;
+  float* v = L.V ? L.V + slot : nullptr;
 #pragma unroll
   for (int off = 16; off; off >>= 1) al |= __shfl_xor_sync(FULL_MASK, (unsigned long long)al, off);
-  uint32_t len = P.slice_len[g];
-  for (uint32_t i = 1; i < run; ++i) len += P.slice_len[g + i];  // consecutive slices: contiguous
+#pragma unroll
+  for (int off = 16; off; off >>= 1) len += __shfl_xor_sync(FULL_MASK, len, off);
   if (q == 0) {
     job->kind = JOB_REDUCE;
     job->li = li;
@@ -864,15 +974,19 @@ __device__ void signal_job(const CommArgs& a, const Job& j) {
 }
 
 // Next stashed claim (one warp; the stash is in layer order).
-__device__ uint32_t take_stash(Stash* st, uint32_t* run) {
+__device__ uint32_t take_stash(Stash* st, Popped* out) {
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t g = st->g[0];
-  *run = st->run[0];
+  out->run = st->run[0];
+  out->layer = st->layer[0];
+  out->word = st->word[0];
   __syncwarp();
   if (lane == 0) {
     for (uint32_t i = 1; i < st->n; ++i) {
       st->g[i - 1] = st->g[i];
       st->run[i - 1] = st->run[i];
+      st->layer[i - 1] = st->layer[i];
+      st->word[i - 1] = st->word[i];
     }
     st->n -= 1;
   }
@@ -914,7 +1028,11 @@ __global__ void __launch_bounds__(512, 1) k_comm(const __grid_constant__ CommArg
     for (uint32_t iter = 0;; ++iter) {
       if (phase) *(volatile uint32_t*)phase = (a.k << 24) | (1u << 20) | (iter & 0xfffff);
       const uint64_t tp = globaltimer();
-      uint32_t kind = JOB_NONE, li = 0, g = P3_NONE, run = 1;
+      uint32_t kind = JOB_NONE, li = 0, g = P3_NONE;
+      Popped pp;
+      pp.run = 1;
+      pp.layer = 0;
+      pp.word = 0;
       if (a.plan.world == 1) {
         // single rank: a popped slice is complete the moment it is popped (the owner's own
         // contribution is read in place), so the pop claims the reduction directly — no
@@ -922,39 +1040,38 @@ __global__ void __launch_bounds__(512, 1) k_comm(const __grid_constant__ CommArg
         // the layer (contiguous in memory) as one job
         const LocalDev& L = a.loc[0];
         if (stash.n) {
-          g = take_stash(&stash, &run);
+          g = take_stash(&stash, &pp);
         } else {
           ingest(L, a.sched);
-          g = warp_pop(queue_of(a, L), a.k + 1, phase, L.V ? 1u : a.pop_run, &run, &stash);
+          g = warp_pop(queue_of(a, L), a.k + 1, phase, L.V ? 1u : a.pop_run, &pp, &stash);
         }
         if (g != P3_NONE) {
           if (lane == 0) {
-            (void)ld_acquire_gpu64(L.pub + a.plan.slice_layer[g]);
-            atomicAdd(&L.it->pushed, run);
-            atomicAdd(&L.it->reduced, run);
-            for (uint32_t i = 0; i < run; ++i) {
-              const uint32_t l = a.plan.slice_layer[g];
-              trace_append(L, a.k, l, g + i - a.plan.layer_first[l], L.rank, P3_EV_PUSH);
-            }
+            // (the acquire of the publication word is the fence in prepare_reduce)
+            atomicAdd(&L.it->pushed, pp.run);
+            atomicAdd(&L.it->reduced, pp.run);
+            if (L.trace_cap)
+              for (uint32_t i = 0; i < pp.run; ++i)
+                trace_append(L, a.k, pp.layer, g + i - a.plan.layer_first[pp.layer], L.rank, P3_EV_PUSH);
           }
           kind = JOB_REDUCE;
         }
       }
       for (uint32_t t = 0; t < a.n_local && kind == JOB_NONE && a.plan.world > 1; ++t) {
         li = (blockIdx.x + t) % a.n_local;
-        g = warp_server_pick(a, a.loc[li], phase);
+        g = warp_server_pick(a, a.loc[li], &pp.layer, phase);
         if (g != P3_NONE) kind = JOB_REDUCE;
       }
       if (kind == JOB_NONE && a.plan.world > 1 && stash.n) {
         li = stash_li;
-        g = take_stash(&stash, &run);
+        g = take_stash(&stash, &pp);
         if (lane == 0) atomicAdd(&a.loc[li].it->pushed, 1u);
         kind = JOB_PUSH;
       }
       for (uint32_t t = 0; t < a.n_local && kind == JOB_NONE && a.plan.world > 1; ++t) {
         li = (blockIdx.x + t) % a.n_local;
         ingest(a.loc[li], a.sched);
-        g = warp_pop(queue_of(a, a.loc[li]), a.k + 1, phase, 1u, &run, &stash);
+        g = warp_pop(queue_of(a, a.loc[li]), a.k + 1, phase, 1u, &pp, &stash);
         if (lane == 0) stash_li = li;
         __syncwarp();
         if (g != P3_NONE) {
@@ -1014,7 +1131,7 @@ __global__ void __launch_bounds__(512, 1) k_comm(const __grid_constant__ CommArg
       backoff = 0;
       idle_since = 0;
       if (kind == JOB_PUSH) {
-        const uint32_t how = prepare_push(a, li, g, nullptr);
+        const uint32_t how = prepare_push(a, li, g, pp.layer, pp.word, nullptr);
         if (how == PUSH_DONE) continue;  // own slice, still waiting for peers: counted in place
         if (how == PUSH_REDUCE) kind = JOB_REDUCE;  // own slice completed it: reduce right away
       }
@@ -1028,9 +1145,9 @@ __global__ void __launch_bounds__(512, 1) k_comm(const __grid_constant__ CommArg
       t_pick += tw - tp;
       if (pending[b]) bar_sync(BAR_EMPTY(b), 64);  // the signaler released this slot
       if (kind == JOB_PUSH) {
-        prepare_push(a, li, g, &slots[b]);
+        prepare_push(a, li, g, pp.layer, pp.word, &slots[b]);
       } else if (kind == JOB_REDUCE) {
-        prepare_reduce(a, li, g, &slots[b], run);
+        prepare_reduce(a, li, g, pp.layer, pp.word, &slots[b], pp.run);
       } else {
         if (pending[b ^ 1]) bar_sync(BAR_EMPTY(b ^ 1), 64);  // leave every barrier balanced
         if (lane == 0) slots[b].kind = JOB_EXIT;

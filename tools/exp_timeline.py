@@ -1,0 +1,76 @@
+"""Timeline of one sync-only FINISH launch at N=1 from the device trace (pick = PUSH event,
+signal = BCAST event, %globaltimer ns): when the first / median / last jobs complete, the
+bytes completed per 5 us bin, and the kernel's event-timed duration.
+python tools/exp_timeline.py resnet50 '{"pop_relax":148}'"""
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+
+from paper_1905_03960_b200.runtime import SyncContext
+from paper_1905_03960_b200.torch_models import real_counts
+from paper_1905_03960_b200.plan import make_p3_plan
+from paper_1905_03960_b200.model import ModelProfile, LayerSpec
+
+
+def main():
+    m = sys.argv[1] if len(sys.argv) > 1 else "resnet50"
+    extra = json.loads(sys.argv[2]) if len(sys.argv) > 2 else {}
+    counts = [1024] if m == "tiny" else real_counts(m)
+    plan = make_p3_plan(ModelProfile("x", 0, tuple(LayerSpec(i, "l", c, 0, 0) for i, c in enumerate(counts))), 1, 50_000)
+    first = {}
+    for i, s in enumerate(plan.slices):
+        first.setdefault(s.key.layer_index, i)
+    lens = [s.length for s in plan.slices]
+    ctx = SyncContext(counts, 1, [0], comm_ctas=148, comm_threads=512, timeout_s=30.0, emulate_grads=True,
+                      trace_cap=1 << 16, **extra)
+    st = torch.cuda.Stream()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    for l in range(len(counts)):
+        ctx.gradgen_layer(0, 7, 0, l, st)
+    st.synchronize()
+    for k in range(4):
+        with torch.cuda.stream(st):
+            flush.fill_(k)
+        for l in range(len(counts)):
+            ctx.layer_ready(0, l, k, None, st)
+        st.synchronize()
+        ctx.clear_trace()
+        s, e, s1 = torch.cuda.Event(True), torch.cuda.Event(True), torch.cuda.Event(True)
+        with torch.cuda.stream(st):
+            torch.cuda._sleep(200_000)  # the host enqueues everything below before the GPU gets there
+        s.record(st)
+        ctx.iteration_begin(k, st)
+        s1.record(st)
+        ctx.iteration_end(k)
+        e.record(st)
+        ctx.sync_all(k + 1, 30.0)
+        st.synchronize()
+        tr = [r for r in ctx.trace(0) if r.iteration == k]
+        picks = sorted(r.t_ns for r in tr if r.event == 0)
+        sig = sorted((r.t_ns, lens[first[r.layer] + r.slice]) for r in tr if r.event == 1)
+        t0 = picks[0]
+        tot = sum(b for _, b in sig)
+        bins = {}
+        for t, n in sig:
+            bins[(t - t0) // 5000] = bins.get((t - t0) // 5000, 0) + n
+        print(json.dumps({"model": m, "k": k, "event_ms": round(s.elapsed_time(e), 4), "launch_ms": round(s1.elapsed_time(e), 4), "jobs": len(sig),
+                          "first_pick_to_last_signal_us": round((sig[-1][0] - t0) / 1e3, 1),
+                          "first_signal_us": round((sig[0][0] - t0) / 1e3, 1),
+                          "half_bytes_us": round((next(t for t, c in _cum(sig) if c >= tot / 2) - t0) / 1e3, 1),
+                          "p90_bytes_us": round((next(t for t, c in _cum(sig) if c >= 0.9 * tot) - t0) / 1e3, 1),
+                          "elems_per_5us_bin_M": [round(bins.get(i, 0) / 1e6, 2) for i in range(max(bins) + 1)]}),
+              flush=True)
+    ctx.close()
+
+
+def _cum(sig):
+    c = 0
+    for t, n in sig:
+        c += n
+        yield t, c
+
+
+main()
