@@ -373,7 +373,15 @@ def run_ours(args):
         peak = 770.0
         roof = {"bound": "nvlink", "achieved": alg / (sync_ms * 1e-3) / 1e9, "peak": peak, "unit": "GB/s",
                 "peak_source": "B200_PROFILING.md measured peer copy 770 GB/s per direction"}
-    roof.update({"frac": roof["achieved"] / peak, "traffic": None, "kernel": "k_comm (K3 push + K4 reduce/SGD/bcast)",
+    # DRAM bytes per launch of the same kernel configuration from the committed ncu --set full
+    # capture (profiles/ncu_traffic.json), when one exists for this model and world size
+    traffic = None
+    tf = REPO / "profiles" / "ncu_traffic.json"
+    if tf.exists():
+        t = json.loads(tf.read_text()).get(args.model)
+        if t and t["world"] == world and t["max_slice"] == args.max_slice:
+            traffic = t["dram_bytes_read"] + t["dram_bytes_write"]
+    roof.update({"frac": roof["achieved"] / peak, "traffic": traffic, "kernel": "k_comm (K3 push + K4 reduce/SGD/bcast)",
                  "algorithmic_bytes_per_launch": alg, "launch_ms": sync_ms, "ctas": ctas,
                  "measured_in": "sync-only phase: all layers' gradients in HBM and published, one launch per "
                                 "iteration over the whole GPU, L2 flushed (256 MB write) between launches"})

@@ -194,26 +194,26 @@ __device__ __forceinline__ float4 sgd4(float4 p, const float4& acc, const UpdCoe
 // is also the master copy read as p), src[0..NW) are the gradient sources in rank order,
 // v the optional momentum. U float4 columns per thread are loaded before any arithmetic
 // so each thread keeps (NW + 1) * U independent 16-byte loads in flight.
-template <int NW, int U>
+template <int NW, int U, bool MOM>
 __device__ void cta_update_vec(const float* p_src, float* const* dst, int ndst, const float* const* src,
                                float* v, uint64_t n4, const UpdCoef& c, uint32_t tid, uint32_t nthr) {
   const uint64_t stride = nthr;
   uint64_t j = tid;
   for (; j + (U - 1) * stride < n4; j += U * stride) {
-    float4 g[U][NW], p[U], vv[U];
+    float4 g[U][NW], p[U], vv[MOM ? U : 1];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const uint64_t i = 4 * (j + u * stride);
 #pragma unroll
       for (int q = 0; q < NW; ++q) g[u][q] = __ldcg(reinterpret_cast<const float4*>(src[q] + i));
       p[u] = __ldcg(reinterpret_cast<const float4*>(p_src + i));
-      if (v) vv[u] = __ldcg(reinterpret_cast<const float4*>(v + i));
+      if (MOM) vv[MOM ? u : 0] = __ldcg(reinterpret_cast<const float4*>(v + i));
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const uint64_t i = 4 * (j + u * stride);
-      const float4 r = sgd4(p[u], sum_in_rank_order<NW>(g[u]), c, v ? &vv[u] : nullptr);
-      if (v) *reinterpret_cast<float4*>(v + i) = vv[u];
+      const float4 r = sgd4(p[u], sum_in_rank_order<NW>(g[u]), c, MOM ? &vv[MOM ? u : 0] : nullptr);
+      if (MOM) *reinterpret_cast<float4*>(v + i) = vv[MOM ? u : 0];
       for (int d = 0; d < ndst; ++d) *reinterpret_cast<float4*>(dst[d] + i) = r;
     }
   }
@@ -237,8 +237,13 @@ __device__ void cta_update_generic(const float* p_src, float* const* dst, int nd
   if (aligned) {
     const uint64_t n4 = n / 4;
     switch (nw) {
-#define P3_CASE(K) \
-  case K: cta_update_vec<K, (K <= 1 ? 4 : K <= 2 ? 2 : 1)>(p_src, dst, ndst, src, v, n4, c, tid, nthr); break;
+#define P3_CASE(K)                                                                                      \
+  case K:                                                                                               \
+    if (v)                                                                                              \
+      cta_update_vec<K, (K <= 1 ? 4 : K <= 2 ? 2 : 1), true>(p_src, dst, ndst, src, v, n4, c, tid, nthr);  \
+    else                                                                                                \
+      cta_update_vec<K, (K <= 1 ? 8 : K <= 2 ? 4 : K <= 4 ? 2 : 1), false>(p_src, dst, ndst, src, v, n4, c, tid, nthr); \
+    break;
       P3_CASE(1) P3_CASE(2) P3_CASE(3) P3_CASE(4) P3_CASE(5) P3_CASE(6) P3_CASE(7) P3_CASE(8)
 #undef P3_CASE
       default: aligned = false; break;
@@ -385,7 +390,7 @@ __device__ uint32_t warp_pop(const QueueView& q, uint32_t tag, uint32_t* dbg = n
   const uint32_t lane = threadIdx.x & 31;
   if (q.sched == P3_SCHED_PRIORITY) {
     constexpr uint32_t CH = 8;  // chunks of 32 layers examined per memory round trip
-    for (uint32_t group = 0; group < q.n_layers; group += 32 * CH) {
+    for (uint32_t group = 0, attempt = 0; group < q.n_layers; ++attempt) {
       // all loads of the group issued before any is used: one round trip, not 2*CH
       uint64_t w[CH];
       uint32_t cur[CH], ns[CH];
@@ -402,19 +407,25 @@ __device__ uint32_t warp_pop(const QueueView& q, uint32_t tag, uint32_t* dbg = n
       for (uint32_t c = 0; c < CH; ++c) bits |= (uint32_t)(pub_ready(w[c], tag) && cur[c] < ns[c]) << c;
       const uint32_t nchunk = min(CH, (q.n_layers - group + 31) / 32);
       bool first = true;
-      if (q.relax > 1 && !(stash && q.multi > 1)) {
+      if (q.relax > 1 && !(stash && q.multi > 1) && attempt < 4) {
         // Bounded relaxation, ranked by slice: with `relax` consumers popping at once, this
-        // CTA aims at the (blockIdx % relax)-th most urgent available slice of the group —
-        // one claim that rarely collides, where racing for the same few most urgent layers
-        // (one-slice layers: most of ResNet-50) costs a lost atomic round trip per try.
+        // CTA aims at the job of rank (blockIdx % relax) among the most urgent available
+        // slices of the group — one claim that rarely collides, where racing for the same few
+        // most urgent layers (one-slice layers: most of ResNet-50) costs a lost atomic round
+        // trip per try. A lost claim reloads the group and aims again (the snapshot is stale).
         uint32_t tot[CH], total = 0;
 #pragma unroll
         for (uint32_t c = 0; c < CH; ++c) {
           tot[c] = __reduce_add_sync(FULL_MASK, ((bits >> c) & 1u) ? ns[c] - cur[c] : 0u);
           total += tot[c];
         }
-        if (total) {
-          uint32_t t = (blockIdx.x % q.relax) % total, tc = 0;
+        if (!total) {  // nothing available in this group
+          group += 32 * CH;
+          attempt = 0;
+          continue;
+        }
+        {
+          uint32_t t = ((blockIdx.x % q.relax) * want) % total, tc = 0;
 #pragma unroll
           for (uint32_t c = 0; c < CH; ++c) {  // chunk holding rank t (uniform)
             if (c == tc && t >= tot[c] && c + 1 < CH) {
@@ -458,7 +469,7 @@ __device__ uint32_t warp_pop(const QueueView& q, uint32_t tag, uint32_t* dbg = n
             return g0;
           }
         }
-        first = false;  // lost (or nothing here): strict order from the most urgent
+        continue;  // lost the claim: reload the group and aim again
       }
       for (uint32_t c = 0; c < nchunk; ++c) {
         uint32_t m = __ballot_sync(FULL_MASK, (bits >> c) & 1u);
@@ -516,6 +527,8 @@ __device__ uint32_t warp_pop(const QueueView& q, uint32_t tag, uint32_t* dbg = n
           m &= ~cand;  // every candidate lost the race for its layer's last slices
         }
       }
+      group += 32 * CH;
+      attempt = 0;
     }
     return P3_NONE;
   }
@@ -969,7 +982,7 @@ __device__ void signal_job(const CommArgs& a, const Job& j) {
     atomicAdd(L.bytes + 0, (j.bf16 ? 2ull : 4ull) * j.len * (j.n - 1));  // pushes received
     atomicAdd(L.bytes + 1, 4ull * j.len * (j.n - 1));  // broadcasts sent
     for (uint32_t i = 0; i < j.run; ++i)
-      trace_append(L, a.k, j.layer, j.g + i - P.layer_first[j.layer], j.rank, P3_EV_BCAST);
+      trace_append(L, a.k, j.layer, j.g + i - P.layer_first[j.layer], a.trace_cta ? blockIdx.x : j.rank, P3_EV_BCAST);
   }
 }
 
@@ -1052,7 +1065,8 @@ __global__ void __launch_bounds__(512, 1) k_comm(const __grid_constant__ CommArg
             atomicAdd(&L.it->reduced, pp.run);
             if (L.trace_cap)
               for (uint32_t i = 0; i < pp.run; ++i)
-                trace_append(L, a.k, pp.layer, g + i - a.plan.layer_first[pp.layer], L.rank, P3_EV_PUSH);
+                trace_append(L, a.k, pp.layer, g + i - a.plan.layer_first[pp.layer], a.trace_cta ? blockIdx.x : L.rank,
+                             P3_EV_PUSH);
           }
           kind = JOB_REDUCE;
         }
