@@ -267,8 +267,9 @@ int p3_ctx_create(const p3_config_t* cfg, p3_ctx_t** out) {
   if (cfg->n_layers < 1 || !cfg->layer_counts) return fail(nullptr, P3_EUSAGE, "profile needs at least one layer");
   if (cfg->plan_mode != P3_PLAN_P3 && cfg->plan_mode != P3_PLAN_BASELINE) return fail(nullptr, P3_EUSAGE, "bad plan_mode");
   if (cfg->throttle_bps < 0) return fail(nullptr, P3_EUSAGE, "throttle rate must be >= 0 (0 disables shaping)");
-  if (cfg->comm_threads < 96 || cfg->comm_threads > 512 || cfg->comm_threads % 32)
-    return fail(nullptr, P3_EUSAGE, "comm_threads must be a multiple of 32 in [96, 512] (scheduler + signaler + mover warps)");
+  if (cfg->comm_threads < 128 || cfg->comm_threads > 512 || cfg->comm_threads % 32)
+    return fail(nullptr, P3_EUSAGE,
+                "comm_threads must be a multiple of 32 in [128, 512] (scheduler + signaler + producer + consumer warps)");
   if (cfg->comm_ctas < 1) return fail(nullptr, P3_EUSAGE, "comm_ctas must be >= 1");
   for (uint32_t i = 0; i < cfg->n_local; ++i)
     if (cfg->local_ranks[i] >= cfg->world) return fail(nullptr, P3_EUSAGE, "local rank out of range");
@@ -596,6 +597,10 @@ static CommArgs comm_args(p3_ctx* c, uint32_t mode, uint32_t ctas) {
   a.pop_multi = std::max<uint32_t>(1, std::min<uint32_t>(4, c->cfg.pop_multi ? c->cfg.pop_multi : 1));
   a.push_bf16 = c->cfg.push_bf16 ? 1u : 0u;
   a.trace_cta = getenv("P3_TRACE_CTA") != nullptr;
+  {
+    const char* e = getenv("P3_TMA");
+    a.use_tma = e ? (uint32_t)atoi(e) : 1u;
+  }
   // bounded relaxation of the pop order: a pop takes one of the C most urgent slices, C =
   // the launch's concurrent consumers (its CTAs) unless configured lower
   // (measured, tools/sync_sweep.py, ResNet-50 N=1 sync-only: C=8 2.2 TB/s, C=148 3.4 TB/s —

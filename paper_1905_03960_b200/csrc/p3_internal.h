@@ -120,6 +120,7 @@ struct CommArgs {
   uint32_t pop_relax; // a pop may take any of this many most urgent layers (1: strict)
   uint32_t pop_multi; // candidate layers claimed per round of pop atomics
   uint32_t push_bf16; // pushes travel as bf16
+  uint32_t use_tma;   // movers stage sources through shared memory with TMA (else direct loads)
   uint32_t trace_cta; // diagnostics (P3_TRACE_CTA=1): trace records carry the CTA index as `rank`
   float ns_per_byte;  // K7 link emulation (0: unthrottled)
   unsigned long long burst_ns;

@@ -80,10 +80,45 @@ __device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_re
 __device__ __forceinline__ void red_add_release_sys(uint32_t* p, uint32_t v) {
   asm volatile("red.release.sys.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+// mbarrier / TMA bulk copy (cp.async.bulk, 1-D) helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* b, uint32_t tx) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(tx) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(uint64_t* b, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+      : "=r"(ok)
+      : "r"(smem_u32(b)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void tma_load_1d(void* sdst, const void* gsrc, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(sdst)),
+               "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
 __device__ __forceinline__ uint64_t globaltimer() {
   uint64_t t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
+}
+// Bounded mbarrier wait: every wait of the stage pipeline ends within the iteration timeout
+// (the scheduler posts EXIT by then), so one that outlives it is a protocol bug — trap (the
+// host sees a launch failure) rather than hang the GPU.
+__device__ __forceinline__ void mbar_wait_bounded(uint64_t* b, uint32_t parity, const CommArgs& a) {
+  if (mbar_try_wait(b, parity)) return;
+  const uint64_t t0 = globaltimer();
+  while (!mbar_try_wait(b, parity))
+    if (globaltimer() - t0 > a.timeout_ns + 2000000000ull) __trap();
 }
 
 // ------------------------------------------------------------------ K1: gradient source
@@ -197,13 +232,17 @@ __device__ __forceinline__ float4 sgd4(float4 p, const float4& acc, const UpdCoe
 template <int NW, int U, bool MOM>
 __device__ void cta_update_vec(const float* p_src, float* const* dst, int ndst, const float* const* src,
                                float* v, uint64_t n4, const UpdCoef& c, uint32_t tid, uint32_t nthr) {
-  const uint64_t stride = nthr;
-  uint64_t j = tid;
-  for (; j + (U - 1) * stride < n4; j += U * stride) {
+  // Every round issues all of its (predicated) loads before any use, including the last,
+  // partial round: a remainder walked one float4 at a time would cost one memory round trip
+  // per element per thread (measured: ~4 us of a 50K-element job).
+  const uint32_t stride = nthr, m4 = (uint32_t)n4;  // a job is < 2^32 elements
+  for (uint32_t j = tid; j < m4; j += U * stride) {
     float4 g[U][NW], p[U], vv[MOM ? U : 1];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      const uint64_t i = 4 * (j + u * stride);
+      // out-of-range columns reload column j (in range) instead of branching: the loads stay
+      // unconditional, only the stores are predicated
+      const uint32_t i = 4 * (j + u * stride < m4 ? j + u * stride : j);
 #pragma unroll
       for (int q = 0; q < NW; ++q) g[u][q] = __ldcg(reinterpret_cast<const float4*>(src[q] + i));
       p[u] = __ldcg(reinterpret_cast<const float4*>(p_src + i));
@@ -211,28 +250,20 @@ __device__ void cta_update_vec(const float* p_src, float* const* dst, int ndst, 
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      const uint64_t i = 4 * (j + u * stride);
-      const float4 r = sgd4(p[u], sum_in_rank_order<NW>(g[u]), c, MOM ? &vv[MOM ? u : 0] : nullptr);
-      if (MOM) *reinterpret_cast<float4*>(v + i) = vv[MOM ? u : 0];
-      for (int d = 0; d < ndst; ++d) *reinterpret_cast<float4*>(dst[d] + i) = r;
+      const uint32_t i = 4 * (j + u * stride);
+      if (j + u * stride < m4) {
+        const float4 r = sgd4(p[u], sum_in_rank_order<NW>(g[u]), c, MOM ? &vv[MOM ? u : 0] : nullptr);
+        if (MOM) *reinterpret_cast<float4*>(v + i) = vv[MOM ? u : 0];
+        for (int d = 0; d < ndst; ++d) *reinterpret_cast<float4*>(dst[d] + i) = r;
+      }
     }
-  }
-  for (; j < n4; j += stride) {
-    const uint64_t i = 4 * j;
-    float4 g1[NW];
-#pragma unroll
-    for (int q = 0; q < NW; ++q) g1[q] = __ldcg(reinterpret_cast<const float4*>(src[q] + i));
-    float4 vv1 = v ? __ldcg(reinterpret_cast<const float4*>(v + i)) : make_float4(0.f, 0.f, 0.f, 0.f);
-    const float4 r = sgd4(__ldcg(reinterpret_cast<const float4*>(p_src + i)), sum_in_rank_order<NW>(g1), c,
-                          v ? &vv1 : nullptr);
-    if (v) *reinterpret_cast<float4*>(v + i) = vv1;
-    for (int d = 0; d < ndst; ++d) *reinterpret_cast<float4*>(dst[d] + i) = r;
   }
 }
 
 __device__ void cta_update_generic(const float* p_src, float* const* dst, int ndst, const float* const* src,
                                    int nw, float* v, uint64_t n, bool aligned, const UpdCoef& c, uint32_t tid,
                                    uint32_t nthr) {
+  // (callers pass pointers already offset to the range; see move_range for sub-ranges)
   uint64_t done = 0;
   if (aligned) {
     const uint64_t n4 = n / 4;
@@ -691,15 +722,14 @@ __device__ void cta_copy(float* dst, const float* src, uint32_t n, uint32_t tid,
     const uint32_t n4 = n / 4;
     const float4* s4 = reinterpret_cast<const float4*>(src);
     float4* d4 = reinterpret_cast<float4*>(dst);
-    uint32_t j = tid;
-    for (; j + (U - 1) * nthr < n4; j += U * nthr) {
+    for (uint32_t j = tid; j < n4; j += U * nthr) {  // the partial last round predicated, not serial
       float4 r[U];
 #pragma unroll
-      for (int u = 0; u < U; ++u) r[u] = __ldcg(s4 + j + u * nthr);
+      for (int u = 0; u < U; ++u) r[u] = __ldcg(s4 + (j + u * nthr < n4 ? j + u * nthr : j));
 #pragma unroll
-      for (int u = 0; u < U; ++u) d4[j + u * nthr] = r[u];
+      for (int u = 0; u < U; ++u)
+        if (j + u * nthr < n4) d4[j + u * nthr] = r[u];
     }
-    for (; j < n4; j += nthr) d4[j] = __ldcg(s4 + j);
     done = 4 * n4;
   }
   for (uint32_t i = done + tid; i < n; i += nthr) dst[i] = __ldcg(src + i);
@@ -739,6 +769,7 @@ struct Job {
 #define BAR_FULL(b) (1 + (b))
 #define BAR_DONE(b) (3 + (b))
 #define BAR_EMPTY(b) (5 + (b))
+#define BAR_RANGE 7  // consumers among themselves (direct-path scratch)
 __device__ __forceinline__ void bar_sync(uint32_t id, uint32_t n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
@@ -908,17 +939,32 @@ __device__ void prepare_reduce(const CommArgs& a, uint32_t li, uint32_t g, uint3
 // fp32 in ascending rank order; the update and the broadcast parameters stay fp32.
 __device__ __forceinline__ float bf16_round(float x) { return __bfloat162float(__float2bfloat16_rn(x)); }
 
+__device__ __forceinline__ uint2 to_bf16x4(const float4& v) {
+  __nv_bfloat162 lo = __floats2bfloat162_rn(v.x, v.y), hi = __floats2bfloat162_rn(v.z, v.w);
+  uint2 w;
+  w.x = *reinterpret_cast<uint32_t*>(&lo);
+  w.y = *reinterpret_cast<uint32_t*>(&hi);
+  return w;
+}
+__device__ __forceinline__ float4 from_bf16x4(const uint2& w) {
+  const __nv_bfloat162 lo = *reinterpret_cast<const __nv_bfloat162*>(&w.x);
+  const __nv_bfloat162 hi = *reinterpret_cast<const __nv_bfloat162*>(&w.y);
+  const float2 a = __bfloat1622float2(lo), b = __bfloat1622float2(hi);
+  return make_float4(a.x, a.y, b.x, b.y);
+}
+
 __device__ void cta_copy_to_bf16(__nv_bfloat16* dst, const float* src, uint32_t n, uint32_t tid, uint32_t nthr) {
   uint32_t done = 0;
   if ((((uintptr_t)src & 15) | ((uintptr_t)dst & 7)) == 0) {
+    constexpr int U = 8;
     const uint32_t n4 = n / 4;
-    for (uint32_t j = tid; j < n4; j += nthr) {
-      const float4 v = __ldcg(reinterpret_cast<const float4*>(src) + j);
-      __nv_bfloat162 lo = __floats2bfloat162_rn(v.x, v.y), hi = __floats2bfloat162_rn(v.z, v.w);
-      uint2 w;
-      w.x = *reinterpret_cast<uint32_t*>(&lo);
-      w.y = *reinterpret_cast<uint32_t*>(&hi);
-      *reinterpret_cast<uint2*>(dst + 4 * j) = w;
+    for (uint32_t j = tid; j < n4; j += U * nthr) {
+      float4 v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) v[u] = __ldcg(reinterpret_cast<const float4*>(src) + (j + u * nthr < n4 ? j + u * nthr : j));
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (j + u * nthr < n4) *reinterpret_cast<uint2*>(dst + 4 * (j + u * nthr)) = to_bf16x4(v[u]);
     }
     done = 4 * n4;
   }
@@ -927,7 +973,58 @@ __device__ void cta_copy_to_bf16(__nv_bfloat16* dst, const float* src, uint32_t 
 
 __device__ void cta_update_bf16(float* const* dst, int ndst, const float* const* src, int nw, int own, float* v,
                                 uint64_t n, const UpdCoef& c, uint32_t tid, uint32_t nthr) {
-  for (uint64_t i = tid; i < n; i += nthr) {
+  uintptr_t al8 = 0, al16 = (uintptr_t)v;
+  for (int q = 0; q < nw; ++q) {
+    if (q == own) al16 |= (uintptr_t)src[q];
+    else al8 |= (uintptr_t)src[q];
+  }
+  for (int d = 0; d < ndst; ++d) al16 |= (uintptr_t)dst[d];
+  uint64_t done = 0;
+  if ((al8 & 7) == 0 && (al16 & 15) == 0) {
+    // 4 elements per vector: the other ranks' bf16 contributions as 8-byte loads, the own
+    // fp32 one rounded here; per rank U loads in flight, summed in ascending rank order
+    constexpr int U = 4;
+    const uint32_t m4 = (uint32_t)(n / 4);
+    for (uint32_t j = tid; j < m4; j += U * nthr) {
+      float4 acc[U], p[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        acc[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+        p[u] = __ldcg(reinterpret_cast<const float4*>(dst[0]) + (j + u * nthr < m4 ? j + u * nthr : j));
+      }
+      for (int q = 0; q < nw; ++q) {
+        float4 x[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const uint32_t e = j + u * nthr < m4 ? j + u * nthr : j;
+          if (q == own) {
+            const float4 f = __ldcg(reinterpret_cast<const float4*>(src[q]) + e);
+            x[u] = make_float4(bf16_round(f.x), bf16_round(f.y), bf16_round(f.z), bf16_round(f.w));
+          } else {
+            x[u] = from_bf16x4(__ldcg(reinterpret_cast<const uint2*>(src[q]) + e));
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          acc[u].x = __fadd_rn(acc[u].x, x[u].x);
+          acc[u].y = __fadd_rn(acc[u].y, x[u].y);
+          acc[u].z = __fadd_rn(acc[u].z, x[u].z);
+          acc[u].w = __fadd_rn(acc[u].w, x[u].w);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const uint32_t e = j + u * nthr;
+        if (e >= m4) continue;
+        float4 vv = v ? __ldcg(reinterpret_cast<const float4*>(v) + e) : make_float4(0.f, 0.f, 0.f, 0.f);
+        const float4 r = sgd4(p[u], acc[u], c, v ? &vv : nullptr);
+        if (v) reinterpret_cast<float4*>(v)[e] = vv;
+        for (int d = 0; d < ndst; ++d) reinterpret_cast<float4*>(dst[d])[e] = r;
+      }
+    }
+    done = 4 * (uint64_t)m4;
+  }
+  for (uint64_t i = done + tid; i < n; i += nthr) {
     float acc = 0.f;
     for (int q = 0; q < nw; ++q) {
       const float x = q == own ? bf16_round(__ldcg(src[q] + i))
@@ -939,18 +1036,172 @@ __device__ void cta_update_bf16(float* const* dst, int ndst, const float* const*
   }
 }
 
-// Movers: move the job's data.
-__device__ void move_job(const CommArgs& a, const Job& j, uint32_t tid, uint32_t nthr) {
-  if (j.kind == JOB_PUSH && j.bf16) {
-    cta_copy_to_bf16(reinterpret_cast<__nv_bfloat16*>(j.dst[0]), j.src[0], j.len, tid, nthr);
-  } else if (j.kind == JOB_PUSH) {
-    cta_copy(j.dst[0], j.src[0], j.len, tid, nthr);
-  } else if (j.bf16) {
-    cta_update_bf16(j.dst, (int)j.n, j.src, (int)j.n, (int)j.bf16 - 1, j.v, j.len, make_coef(j.n, a.lr, a.momentum),
-                    tid, nthr);
-  } else {
-    cta_update_generic(j.dst[0], j.dst, (int)j.n, j.src, (int)j.n, j.v, j.len, j.aligned != 0,
+// Consumers, direct path: elements [e0, e0 + n) of the job straight from global memory
+// (jobs the TMA path cannot take — unaligned sources — and the < 8-element residue of the
+// others). `ptrs` is consumer-shared scratch for the offset pointer arrays.
+struct RangePtrs {
+  const float* src[P3_MAX_RANKS];
+  float* dst[P3_MAX_RANKS];
+};
+__device__ void move_range(const CommArgs& a, const Job& j, uint32_t e0, uint32_t n, RangePtrs* ptrs, uint32_t tid,
+                           uint32_t nthr) {
+  const bool bf = j.bf16 != 0;
+  if (j.kind == JOB_PUSH) {
+    if (bf)
+      cta_copy_to_bf16(reinterpret_cast<__nv_bfloat16*>(j.dst[0]) + e0, j.src[0] + e0, n, tid, nthr);
+    else
+      cta_copy(j.dst[0] + e0, j.src[0] + e0, n, tid, nthr);
+    return;
+  }
+  const int own = bf ? (int)j.bf16 - 1 : -1;
+  if (tid < j.n) {  // bf16 receive slots are offset in bf16 elements
+    ptrs->src[tid] = (bf && (int)tid != own)
+                         ? reinterpret_cast<const float*>(reinterpret_cast<const __nv_bfloat16*>(j.src[tid]) + e0)
+                         : j.src[tid] + e0;
+    ptrs->dst[tid] = j.dst[tid] + e0;
+  }
+  bar_sync(BAR_RANGE, nthr);
+  float* v = j.v ? j.v + e0 : nullptr;
+  if (bf)
+    cta_update_bf16(ptrs->dst, (int)j.n, ptrs->src, (int)j.n, own, v, n, make_coef(j.n, a.lr, a.momentum), tid, nthr);
+  else
+    cta_update_generic(ptrs->dst[0], ptrs->dst, (int)j.n, ptrs->src, (int)j.n, v, n, j.aligned != 0,
                        make_coef(j.n, a.lr, a.momentum), tid, nthr);
+  bar_sync(BAR_RANGE, nthr);  // the scratch may be rewritten by the next range
+}
+
+// TMA staging. A stage holds one tile of every source of a job (reduce: the N contributions,
+// the master copy p and the momentum v; push: the gradient) — `tile` elements each, at
+// 4-byte pitch. The producer warp streams tiles of consecutive jobs into the stage ring
+// with cp.async.bulk (no registers, up to P3_STAGES tiles in flight per SM, running ahead
+// across job boundaries); the consumer warps compute from shared memory and store.
+#ifndef P3_STAGES
+#define P3_STAGES 3
+#endif
+#ifndef P3_STAGE_BYTES
+#define P3_STAGE_BYTES (64 * 1024)
+#endif
+#define ST_LAST 1u    // last stage of its job
+#define ST_EXIT 2u    // no more jobs
+#define ST_DIRECT 4u  // consumers take the range straight from global memory
+struct StageDesc {
+  uint32_t b;      // job slot
+  uint32_t e0, n;  // element range of the job
+  uint32_t flags;
+  uint32_t tile;   // elements per source tile (pitch)
+};
+__device__ __forceinline__ uint32_t job_sources(const Job& j) {
+  return j.kind == JOB_PUSH ? 1u : j.n + 1u + (j.v ? 1u : 0u);
+}
+__device__ __forceinline__ uint32_t job_tile(const Job& j) {
+  return (P3_STAGE_BYTES / (4u * job_sources(j))) & ~7u;
+}
+// 16-byte aligned sources (TMA requirement; bf16 receive slots at 2-byte pitch)
+__device__ __forceinline__ bool job_tma_ok(const Job& j) {
+  if (j.kind == JOB_PUSH)  // and the vector stores of the consumers (float4, or 4 x bf16)
+    return ((uintptr_t)j.src[0] & 15) == 0 && ((uintptr_t)j.dst[0] & (j.bf16 ? 7 : 15)) == 0;
+  uintptr_t al = (uintptr_t)j.dst[0] | (uintptr_t)j.v;
+  for (uint32_t q = 0; q < j.n; ++q) al |= (uintptr_t)j.src[q];
+  return (al & 15) == 0 && j.aligned;
+}
+
+// Consumers, staged path: one tile range [e0, e0 + n) (n a multiple of 8) from shared memory.
+// Specialised on the rank count and the mode so the inner loop keeps its pointers in
+// registers (no reloads of the shared job slot per element) and unrolls the rank-ordered sum.
+template <int NW, bool BF, bool MOM>
+__device__ __forceinline__ void consume_reduce(const uint8_t* st, uint32_t pitch, uint32_t n4, uint32_t e4,
+                                               float* const* dstp, float* vp, int own, const UpdCoef& c,
+                                               uint32_t tid, uint32_t nthr) {
+  float4* dst[NW];
+#pragma unroll
+  for (int q = 0; q < NW; ++q) dst[q] = reinterpret_cast<float4*>(dstp[q]) + e4;
+  float4* v = MOM ? reinterpret_cast<float4*>(vp) + e4 : nullptr;
+  const float4* tp = reinterpret_cast<const float4*>(st + NW * pitch);
+  const float4* tv = reinterpret_cast<const float4*>(st + (NW + 1) * pitch);
+  for (uint32_t k = tid; k < n4; k += nthr) {
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int q = 0; q < NW; ++q) {  // ascending rank order from +0.0
+      float4 x;
+      if (!BF) {
+        x = reinterpret_cast<const float4*>(st + q * pitch)[k];
+      } else if (q == own) {
+        const float4 f = reinterpret_cast<const float4*>(st + q * pitch)[k];
+        x = make_float4(bf16_round(f.x), bf16_round(f.y), bf16_round(f.z), bf16_round(f.w));
+      } else {
+        x = from_bf16x4(reinterpret_cast<const uint2*>(st + q * pitch)[k]);
+      }
+      acc.x = __fadd_rn(acc.x, x.x);
+      acc.y = __fadd_rn(acc.y, x.y);
+      acc.z = __fadd_rn(acc.z, x.z);
+      acc.w = __fadd_rn(acc.w, x.w);
+    }
+    float4 vv = MOM ? tv[k] : make_float4(0.f, 0.f, 0.f, 0.f);
+    const float4 r = sgd4(tp[k], acc, c, MOM ? &vv : nullptr);
+    if (MOM) v[k] = vv;
+#pragma unroll
+    for (int q = 0; q < NW; ++q) dst[q][k] = r;
+  }
+}
+
+__device__ void consume_tile(const CommArgs& a, const Job& j, const StageDesc& d, const uint8_t* st, uint32_t tid,
+                             uint32_t nthr) {
+  const uint32_t n4 = d.n / 4, e4 = d.e0 / 4, pitch = d.tile * 4;
+  if (j.kind == JOB_PUSH) {
+    const float4* t0 = reinterpret_cast<const float4*>(st);
+    if (j.bf16) {
+      uint2* out = reinterpret_cast<uint2*>(j.dst[0]) + e4;  // 4 bf16 per 8 bytes
+      for (uint32_t k = tid; k < n4; k += nthr) out[k] = to_bf16x4(t0[k]);
+    } else {
+      float4* out = reinterpret_cast<float4*>(j.dst[0]) + e4;
+      for (uint32_t k = tid; k < n4; k += nthr) out[k] = t0[k];
+    }
+    return;
+  }
+  const uint32_t N = j.n;
+  const bool bf = j.bf16 != 0, mom = j.v != nullptr;
+  const int own = bf ? (int)j.bf16 - 1 : -1;
+  const UpdCoef c = make_coef(N, a.lr, a.momentum);
+  float* const* dst = j.dst;
+  float* v = j.v;
+#define P3_CONSUME(K)                                                                                   \
+  case K:                                                                                               \
+    if (bf) {                                                                                           \
+      if (mom) consume_reduce<K, true, true>(st, pitch, n4, e4, dst, v, own, c, tid, nthr);             \
+      else consume_reduce<K, true, false>(st, pitch, n4, e4, dst, v, own, c, tid, nthr);                \
+    } else {                                                                                            \
+      if (mom) consume_reduce<K, false, true>(st, pitch, n4, e4, dst, v, own, c, tid, nthr);            \
+      else consume_reduce<K, false, false>(st, pitch, n4, e4, dst, v, own, c, tid, nthr);               \
+    }                                                                                                   \
+    return;
+  switch (N) {
+    P3_CONSUME(1) P3_CONSUME(2) P3_CONSUME(3) P3_CONSUME(4) P3_CONSUME(5) P3_CONSUME(6) P3_CONSUME(7)
+    P3_CONSUME(8)
+    default: break;
+  }
+#undef P3_CONSUME
+  // more than 8 ranks: runtime rank loop
+  for (uint32_t k = tid; k < n4; k += nthr) {
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (uint32_t q = 0; q < N; ++q) {
+      float4 x;
+      if (!bf) {
+        x = reinterpret_cast<const float4*>(st + q * pitch)[k];
+      } else if ((int)q == own) {
+        const float4 f = reinterpret_cast<const float4*>(st + q * pitch)[k];
+        x = make_float4(bf16_round(f.x), bf16_round(f.y), bf16_round(f.z), bf16_round(f.w));
+      } else {
+        x = from_bf16x4(reinterpret_cast<const uint2*>(st + q * pitch)[k]);
+      }
+      acc.x = __fadd_rn(acc.x, x.x);
+      acc.y = __fadd_rn(acc.y, x.y);
+      acc.z = __fadd_rn(acc.z, x.z);
+      acc.w = __fadd_rn(acc.w, x.w);
+    }
+    float4 vv = mom ? reinterpret_cast<const float4*>(st + (N + 1) * pitch)[k] : make_float4(0.f, 0.f, 0.f, 0.f);
+    const float4 r = sgd4(reinterpret_cast<const float4*>(st + N * pitch)[k], acc, c, mom ? &vv : nullptr);
+    if (mom) reinterpret_cast<float4*>(v)[e4 + k] = vv;
+    for (uint32_t q = 0; q < N; ++q) reinterpret_cast<float4*>(dst[q])[e4 + k] = r;
   }
 }
 
@@ -1022,11 +1273,23 @@ __device__ uint32_t take_stash(Stash* st, Popped* out) {
 // library kernels, lazy module loading). The FINISH launch of an iteration ends once every
 // local slice is pushed and every owned slice reduced; it waits only for peers' pushes.
 __global__ void __launch_bounds__(512, 1) k_comm(const __grid_constant__ CommArgs a) {
-  __shared__ Job slots[2];  // double-buffered: the scheduler fills one while movers run the other
+  __shared__ Job slots[2];  // double-buffered: the scheduler fills one while the other is moved
+  __shared__ StageDesc sdesc[P3_STAGES];
+  __shared__ __align__(8) uint64_t full_bar[P3_STAGES], empty_bar[P3_STAGES];
+  __shared__ RangePtrs rptrs;
+  extern __shared__ __align__(128) uint8_t stage_mem[];  // P3_STAGES x P3_STAGE_BYTES
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t nthr = blockDim.x;
-  const uint32_t movers = nthr - 64;
+  const uint32_t ncons = nthr - 96;  // consumer threads (warps 3..)
   IterState* stats = a.loc[0].it;
+  if (threadIdx.x == 0) {
+    for (uint32_t i = 0; i < P3_STAGES; ++i) {
+      mbar_init(&full_bar[i], 1);              // the producer's arrive (+ the tile bytes)
+      mbar_init(&empty_bar[i], ncons / 32);    // one arrive per consumer warp
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
   if (warp == 0) {
     uint32_t* phase = (lane == 0 && blockIdx.x < P3_DBG_CTAS) ? a.loc[0].cta_phase + blockIdx.x : nullptr;
     const uint64_t t0 = globaltimer();
@@ -1168,7 +1431,7 @@ __global__ void __launch_bounds__(512, 1) k_comm(const __grid_constant__ CommArg
       }
       t_wait += globaltimer() - tw;
       __syncwarp();
-      bar_arrive(BAR_FULL(b), nthr);
+      bar_arrive(BAR_FULL(b), 96);  // producer + signaler wait on it
       if (kind == JOB_EXIT) break;
       pending[b] = true;
       b ^= 1;
@@ -1181,12 +1444,13 @@ __global__ void __launch_bounds__(512, 1) k_comm(const __grid_constant__ CommArg
     }
     if (phase) *(volatile uint32_t*)phase = (a.k << 24) | (5u << 20);
   } else if (warp == 1) {
+    // signaler: in job order, once the consumers are done with a job, fence and publish
     uint64_t t_sig = 0;
     for (uint32_t b = 0;; b ^= 1) {
-      bar_sync(BAR_FULL(b), nthr);
+      bar_sync(BAR_FULL(b), 96);
       const Job& j = slots[b];
       if (j.kind == JOB_EXIT) break;
-      bar_sync(BAR_DONE(b), nthr - 32);
+      bar_sync(BAR_DONE(b), ncons + 32);
       Job mine;  // what the signal needs, so the slot can be refilled right away
       mine.kind = j.kind;
       mine.li = j.li;
@@ -1207,17 +1471,100 @@ __global__ void __launch_bounds__(512, 1) k_comm(const __grid_constant__ CommArg
       __syncwarp();
     }
     if (lane == 0) atomicAdd(&stats->t_signal, (unsigned long long)t_sig);
-  } else {
-    const uint32_t tid = threadIdx.x - 64;
-    uint64_t t_move = 0;
+  } else if (warp == 2) {
+    // producer: cut each job into stage tiles and stream them in with TMA bulk copies
+    uint32_t it = 0;  // stages issued (ring position and phase)
+    auto next_stage = [&](uint32_t& sidx) {
+      sidx = it % P3_STAGES;
+      if (it >= P3_STAGES) mbar_wait_bounded(&empty_bar[sidx], ((it / P3_STAGES) - 1) & 1u, a);
+      ++it;
+    };
     for (uint32_t b = 0;; b ^= 1) {
-      bar_sync(BAR_FULL(b), nthr);
+      bar_sync(BAR_FULL(b), 96);
       const Job& j = slots[b];
+      if (lane == 0) {
+        uint32_t sidx;
+        if (j.kind == JOB_EXIT) {
+          next_stage(sidx);
+          sdesc[sidx].flags = ST_EXIT;
+          mbar_arrive(&full_bar[sidx]);
+        } else {
+          // the job's sources were published to this CTA through generic-proxy acquires
+          // (scheduler); order them before the async-proxy (TMA) reads
+          asm volatile("fence.proxy.async.global;" ::: "memory");
+          const uint32_t len = j.len;
+          const bool tma = a.use_tma && job_tma_ok(j);
+          const uint32_t tile = job_tile(j), main = tma ? (len & ~7u) : 0u;
+          const uint32_t nsrc = job_sources(j);
+          for (uint32_t e0 = 0; e0 < main; e0 += tile) {
+            const uint32_t n = min(tile, main - e0);
+            next_stage(sidx);
+            StageDesc& d = sdesc[sidx];
+            d.b = b;
+            d.e0 = e0;
+            d.n = n;
+            d.tile = tile;
+            d.flags = (e0 + n == len) ? ST_LAST : 0u;
+            uint8_t* st = stage_mem + (size_t)sidx * P3_STAGE_BYTES;
+            uint32_t bytes = 0;
+            for (uint32_t q = 0; q < nsrc; ++q) {
+              const bool half = j.bf16 && j.kind == JOB_REDUCE && q < j.n && (int)q != (int)j.bf16 - 1;
+              bytes += n * (half ? 2u : 4u);
+            }
+            mbar_arrive_expect_tx(&full_bar[sidx], bytes);
+            for (uint32_t q = 0; q < nsrc; ++q) {
+              const void* g;
+              uint32_t esz = 4;
+              if (j.kind == JOB_PUSH) {
+                g = j.src[0] + e0;
+              } else if (q < j.n) {
+                const bool half = j.bf16 && (int)q != (int)j.bf16 - 1;
+                esz = half ? 2u : 4u;
+                g = half ? (const void*)(reinterpret_cast<const __nv_bfloat16*>(j.src[q]) + e0)
+                         : (const void*)(j.src[q] + e0);
+              } else if (q == j.n) {
+                g = j.dst[0] + e0;  // master copy p
+              } else {
+                g = j.v + e0;
+              }
+              tma_load_1d(st + q * tile * 4, g, n * esz, &full_bar[sidx]);
+            }
+          }
+          if (main < len) {  // unaligned job or the residue: consumers read global memory
+            next_stage(sidx);
+            StageDesc& d = sdesc[sidx];
+            d.b = b;
+            d.e0 = main;
+            d.n = len - main;
+            d.tile = 0;
+            d.flags = ST_LAST | ST_DIRECT;
+            mbar_arrive(&full_bar[sidx]);
+          }
+        }
+      }
+      __syncwarp();
       if (j.kind == JOB_EXIT) break;
+    }
+  } else {
+    // consumers: compute each stage from shared memory, release it, report finished jobs
+    const uint32_t tid = threadIdx.x - 96;
+    uint64_t t_move = 0;
+    for (uint32_t it = 0;; ++it) {
+      const uint32_t sidx = it % P3_STAGES;
+      mbar_wait_bounded(&full_bar[sidx], (it / P3_STAGES) & 1u, a);
+      const StageDesc d = sdesc[sidx];
+      if (d.flags & ST_EXIT) break;
       const uint64_t tm = tid == 0 ? globaltimer() : 0;
-      move_job(a, j, tid, movers);
+      const Job& j = slots[d.b];
+      if (d.flags & ST_DIRECT) {
+        move_range(a, j, d.e0, d.n, &rptrs, tid, ncons);
+      } else {
+        consume_tile(a, j, d, stage_mem + (size_t)sidx * P3_STAGE_BYTES, tid, ncons);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty_bar[sidx]);
       if (tid == 0) t_move += globaltimer() - tm;
-      bar_arrive(BAR_DONE(b), nthr - 32);
+      if (d.flags & ST_LAST) bar_arrive(BAR_DONE(d.b), ncons + 32);
     }
     if (tid == 0) atomicAdd(&stats->t_move, (unsigned long long)t_move);
   }
@@ -1228,6 +1575,9 @@ __global__ void __launch_bounds__(512, 1) k_comm(const __grid_constant__ CommArg
 // A persistent comm kernel waits for work of the compute streams, so every kernel those
 // streams may launch must be loaded before the comm kernel starts: query them all here.
 int preload_kernels() {
+  if (cudaFuncSetAttribute(k_comm, cudaFuncAttributeMaxDynamicSharedMemorySize, P3_STAGES * P3_STAGE_BYTES) !=
+      cudaSuccess)
+    return P3_ECUDA;
   cudaFuncAttributes fa;
   const void* fns[] = {(const void*)k_comm, (const void*)k_gradgen, (const void*)k_sleep,
                        (const void*)k_shard_update, (const void*)k_queue_pop};
@@ -1237,7 +1587,7 @@ int preload_kernels() {
 }
 
 int launch_comm(const CommArgs& a, uint32_t ctas, uint32_t threads, void* stream) {
-  k_comm<<<ctas, threads, 0, (cudaStream_t)stream>>>(a);
+  k_comm<<<ctas, threads, P3_STAGES * P3_STAGE_BYTES, (cudaStream_t)stream>>>(a);
   return cudaGetLastError() == cudaSuccess ? P3_OK : P3_ECUDA;
 }
 
