@@ -108,6 +108,7 @@ struct p3_ctx {
   std::vector<uint32_t> layer_group, group_slices;
   std::vector<uint64_t> layer_woff;
   std::vector<uint32_t> layer_nslices, layer_first;
+  std::vector<uint32_t> slice_opos;  // position of each slice in the owner-grouped list
   std::vector<uint32_t> own_total;
   std::vector<uint64_t> own_stride;
   std::vector<uint64_t> bcast_in_bytes;  // per rank: broadcast payload received per iteration
@@ -330,6 +331,7 @@ int p3_ctx_create(const p3_config_t* cfg, p3_ctx_t** out) {
     }
   }
   own_list.reserve(S);
+  c->slice_opos.assign(S, 0);
   for (uint32_t o = 0; o < N; ++o) {
     uint64_t slot = 0;
     for (uint32_t l = 0; l < L; ++l) {
@@ -337,6 +339,7 @@ int p3_ctx_create(const p3_config_t* cfg, p3_ctx_t** out) {
       for (uint32_t s = 0; s < c->layer_nslices[l]; ++s) {
         const uint32_t g = c->layer_first[l] + s;
         if (slice_owner[g] != o) continue;
+        c->slice_opos[g] = (uint32_t)own_list.size();
         own_list.push_back(g);
         own_lcount[(size_t)o * L + l]++;
         slice_slot[g] = slot;
@@ -382,6 +385,7 @@ int p3_ctx_create(const p3_config_t* cfg, p3_ctx_t** out) {
   const size_t o_sow = put(slice_owner.data(), S * 4ull);
   const size_t o_ss = put(slice_slot.data(), S * 8ull);
   const size_t o_ol = put(own_list.data(), own_list.size() * 4ull);
+  const size_t o_sop = put(c->slice_opos.data(), S * 4ull);
   const size_t o_olf = put(own_lfirst.data(), own_lfirst.size() * 4ull);
   const size_t o_olc = put(own_lcount.data(), own_lcount.size() * 4ull);
   const size_t o_ot = put(c->own_total.data(), N * 4ull);
@@ -410,6 +414,7 @@ int p3_ctx_create(const p3_config_t* cfg, p3_ctx_t** out) {
   P.slice_owner = reinterpret_cast<const uint32_t*>(pb + o_sow);
   P.slice_slot = reinterpret_cast<const uint64_t*>(pb + o_ss);
   P.own_list = reinterpret_cast<const uint32_t*>(pb + o_ol);
+  P.slice_opos = reinterpret_cast<const uint32_t*>(pb + o_sop);
   P.own_lfirst = reinterpret_cast<const uint32_t*>(pb + o_olf);
   P.own_lcount = reinterpret_cast<const uint32_t*>(pb + o_olc);
   P.own_total = reinterpret_cast<const uint32_t*>(pb + o_ot);
@@ -597,6 +602,10 @@ static CommArgs comm_args(p3_ctx* c, uint32_t mode, uint32_t ctas) {
   a.pop_multi = std::max<uint32_t>(1, std::min<uint32_t>(4, c->cfg.pop_multi ? c->cfg.pop_multi : 1));
   a.push_bf16 = c->cfg.push_bf16 ? 1u : 0u;
   a.trace_cta = getenv("P3_TRACE_CTA") != nullptr;
+  {
+    const char* e = getenv("P3_PUSH_SPLIT");
+    a.push_split = e ? (uint32_t)atoi(e) : 0u;
+  }
   {
     const char* e = getenv("P3_TMA");
     a.use_tma = e ? (uint32_t)atoi(e) : 1u;
@@ -906,6 +915,13 @@ int p3_debug_snapshot(p3_ctx_t* c, uint32_t li, uint32_t* out, uint64_t cap, uin
   CK(cudaMemcpyAsync(tail + c->S, D.claim, c->S * 4ull, cudaMemcpyDeviceToHost, c->poll_stream));
   CK(cudaStreamSynchronize(c->poll_stream));
   for (uint32_t l = 0; l < c->L; ++l) out[l] = (uint32_t)(pub[l] >> 48);  // iteration tag
+  {  // arrivals and claims are stored by owner-list position: report them per slice id
+    std::vector<uint32_t> byp(tail, tail + 2ull * c->S);
+    for (uint32_t g = 0; g < c->S; ++g) {
+      tail[g] = byp[c->slice_opos[g]];
+      tail[c->S + g] = byp[c->S + c->slice_opos[g]];
+    }
+  }
   return P3_OK;
 }
 

@@ -42,6 +42,7 @@ struct PlanDev {
   const uint32_t* slice_owner;    // [S]
   const uint64_t* slice_slot;     // [S] element offset in the owner's per-pusher R block
   const uint32_t* own_list;       // [S] slice ids grouped by owner, plan order inside
+  const uint32_t* slice_opos;     // [S] position of the slice in own_list (indexes arrivals, claim)
   const uint32_t* own_lfirst;     // [world*L] index into own_list of (owner, layer)
   const uint32_t* own_lcount;     // [world*L] owned slices of (owner, layer)
   const uint32_t* own_total;      // [world] owned slices per owner
@@ -53,7 +54,7 @@ struct PlanDev {
 struct PeersDev {
   float* W[P3_MAX_RANKS];          // parameter replica
   float* R[P3_MAX_RANKS];          // receive slots [world][own_stride]
-  uint32_t* arrivals[P3_MAX_RANKS];  // [S] pushes received per owned slice (monotone)
+  uint32_t* arrivals[P3_MAX_RANKS];  // [S] pushes received per owned slice, by own_list position (monotone)
   uint32_t* hint[P3_MAX_RANKS];      // [L] owned slices completed per layer (monotone)
   uint32_t* tally[P3_MAX_RANKS];     // [2] pushes arrived, owned slices completed (monotone)
   uint32_t* done[P3_MAX_RANKS];      // [L] slices of a layer broadcast into W (monotone)
@@ -86,7 +87,7 @@ struct LocalDev {
   uint32_t trace_cap;
   uint64_t* pub;        // [L] publication word: iteration tag + 256-B aligned gradient pointer
   uint32_t* fifo_key;   // [L] publish sequence (FIFO discipline)
-  uint32_t* claim;      // [S] server claim tag (monotone: k -> k+1)
+  uint32_t* claim;      // [S] server claim tag by own_list position (monotone: k -> k+1)
   uint32_t* cursor;     // [L] worker claim cursor (per iteration)
   uint32_t* srv_lo;     // [L] server scan watermark (per iteration)
   uint32_t* srv_taken;  // [L] owned slices claimed (per iteration)
@@ -120,6 +121,7 @@ struct CommArgs {
   uint32_t pop_relax; // a pop may take any of this many most urgent layers (1: strict)
   uint32_t pop_multi; // candidate layers claimed per round of pop atomics
   uint32_t push_bf16; // pushes travel as bf16
+  uint32_t push_split; // every push_split-th CTA prefers pushes over server work (0: none)
   uint32_t use_tma;   // movers stage sources through shared memory with TMA (else direct loads)
   uint32_t trace_cta; // diagnostics (P3_TRACE_CTA=1): trace records carry the CTA index as `rank`
   float ns_per_byte;  // K7 link emulation (0: unthrottled)

@@ -623,6 +623,10 @@ int launch_queue_pop(const uint32_t* nslices, const uint32_t* first, const uint6
 // Server role pick (one warp): the lowest layer with a completed, unclaimed owned slice,
 // then the first such slice of that layer (ascending slice index). The inbox of
 // ServerEngine is priority ordered (server.py:118), so the same order is used here.
+// Round trips: one to see whether any owned slice completed unclaimed (the common "no"
+// ends here), one to scan 256 layers, one for a window of 32 owned slices (arrivals and
+// claims are indexed by the slice's position in the owner's list, so no indirection), one
+// claim.
 __device__ uint32_t warp_server_pick(const CommArgs& a, const LocalDev& L, uint32_t* layer_out,
                                      uint32_t* dbg = nullptr) {
   const uint32_t lane = threadIdx.x & 31;
@@ -631,55 +635,72 @@ __device__ uint32_t warp_server_pick(const CommArgs& a, const LocalDev& L, uint3
   const uint32_t* hint = a.peers.hint[o];
   const uint32_t* arrivals = a.peers.arrivals[o];
   const uint32_t* lcount = P.own_lcount + (uint64_t)o * nl;
+  const uint32_t* lfirst = P.own_lfirst + (uint64_t)o * nl;
   const uint32_t need = (k + 1) * P.world;
-  for (uint32_t group = 0; group < nl; group += 32 * 32) {
-    // candidate layers: an owned slice completed this iteration and not yet claimed
-    uint32_t bits = 0;
-#pragma unroll 4
-    for (uint32_t c = 0; c < 32; ++c) {
-      const uint32_t l = group + 32 * c + lane;
-      if (l >= nl) break;
-      const uint32_t oc = lcount[l];
-      bool ok = false;
-      if (oc) {  // owned slices completed this iteration and not yet claimed
-        const uint32_t completed = ld_relaxed_sys(hint + l) - k * oc;
-        ok = (int32_t)(completed - ld_relaxed_gpu(L.srv_taken + l)) > 0;
-      }
-      bits |= (uint32_t)ok << c;
+  {
+    uint32_t any = 0;
+    if (lane == 0) {
+      const uint32_t claimed = ld_relaxed_gpu(&L.it->reduced);
+      const uint32_t completed = ld_relaxed_sys(a.peers.tally[o] + 1) - k * P.own_total[o];
+      any = (int32_t)(completed - claimed) > 0;
     }
-    const uint32_t nchunk = min(32u, (nl - group + 31) / 32);
+    if (!__shfl_sync(FULL_MASK, any, 0)) return P3_NONE;
+  }
+  constexpr uint32_t CH = 8;
+  for (uint32_t group = 0; group < nl; group += 32 * CH) {
+    // candidate layers: an owned slice completed this iteration and not yet claimed
+    uint32_t oc[CH], hv[CH], tk[CH], lo[CH];
+#pragma unroll
+    for (uint32_t c = 0; c < CH; ++c) {
+      const uint32_t l = group + 32 * c + lane;
+      const bool in = l < nl;
+      oc[c] = in ? lcount[l] : 0u;
+      hv[c] = in ? ld_relaxed_sys(hint + l) : 0u;
+      tk[c] = in ? ld_relaxed_gpu(L.srv_taken + l) : 0u;
+      lo[c] = in ? ld_relaxed_gpu(L.srv_lo + l) : 0u;
+    }
+    uint32_t bits = 0;
+#pragma unroll
+    for (uint32_t c = 0; c < CH; ++c)
+      bits |= (uint32_t)(oc[c] && (int32_t)((hv[c] - k * oc[c]) - tk[c]) > 0) << c;
+    const uint32_t nchunk = min(CH, (nl - group + 31) / 32);
     for (uint32_t c = 0; c < nchunk; ++c) {
       uint32_t lm = __ballot_sync(FULL_MASK, (bits >> c) & 1u);
+      uint32_t my_lo = 0, my_oc = 0;
+#pragma unroll
+      for (uint32_t cc = 0; cc < CH; ++cc) {
+        my_lo = cc == c ? lo[cc] : my_lo;
+        my_oc = cc == c ? oc[cc] : my_oc;
+      }
       while (lm) {
-        const uint32_t l = group + 32 * c + (__ffs(lm) - 1);
+        const uint32_t j = __ffs(lm) - 1;
+        const uint32_t l = group + 32 * c + j;
         lm &= lm - 1;
-        const uint32_t lf = P.own_lfirst[(uint64_t)o * nl + l], cnt = lcount[l];
-        // lanes are not guaranteed to execute this load together (independent thread
-        // scheduling) and other CTAs move the watermark: take lane 0's value so the trip
-        // count — and every warp-synchronous call inside — is uniform across the warp
-        uint32_t lo = 0;
-        if (lane == 0) lo = ld_relaxed_gpu(L.srv_lo + l);
-        lo = __shfl_sync(FULL_MASK, lo, 0);
-        for (uint32_t i0 = lo; i0 < cnt; i0 += 32) {
+        // uniform across the warp (lanes need not run these loads together)
+        const uint32_t cnt = __shfl_sync(FULL_MASK, my_oc, j);
+        const uint32_t start = __shfl_sync(FULL_MASK, my_lo, j);
+        const uint32_t lf = lfirst[l];
+        for (uint32_t i0 = start; i0 < cnt; i0 += 32) {
           if (dbg && lane == 0) *(volatile uint32_t*)dbg = (8u << 20) | ((l & 0x3ff) << 10) | (i0 & 0x3ff);
-          const uint32_t i = i0 + lane;
+          const uint32_t i = i0 + lane, pos = lf + i;
           uint32_t g = P3_NONE;
           bool ok = false, claimed = true;
           if (i < cnt) {
-            g = P.own_list[lf + i];
-            claimed = ld_relaxed_gpu(L.claim + g) != k;
-            ok = !claimed && (int32_t)(ld_relaxed_sys(arrivals + g) - need) >= 0;
+            g = P.own_list[pos];
+            claimed = ld_relaxed_gpu(L.claim + pos) != k;
+            ok = !claimed && (int32_t)(ld_relaxed_sys(arrivals + pos) - need) >= 0;
           }
           // advance the watermark only contiguously: a window below this one may still
           // hold an unclaimed slice even if this window is fully claimed
           if (__all_sync(FULL_MASK, claimed) && lane == 0) atomicCAS(L.srv_lo + l, i0, i0 + 32);
           uint32_t m = __ballot_sync(FULL_MASK, ok);
           while (m) {
-            const int j = __ffs(m) - 1;
-            const uint32_t gj = __shfl_sync(FULL_MASK, g, j);
+            const int jj = __ffs(m) - 1;
+            const uint32_t gj = __shfl_sync(FULL_MASK, g, jj);
+            const uint32_t pj = lf + i0 + jj;
             uint32_t won = 0;
             if (lane == 0) {
-              won = atomicCAS(L.claim + gj, k, k + 1) == k;
+              won = atomicCAS(L.claim + pj, k, k + 1) == k;
               if (won) {
                 atomicAdd(L.srv_taken + l, 1u);
                 atomicAdd(&L.it->reduced, 1u);
@@ -755,7 +776,7 @@ __device__ __forceinline__ QueueView queue_of(const CommArgs& a, const LocalDev&
 #define JOB_PUSH 2
 #define JOB_EXIT 3
 struct Job {
-  uint32_t kind, li, g, layer, slice, rank, len, n, aligned, run;
+  uint32_t kind, li, g, layer, opos, rank, len, n, aligned, run;  // opos: position in the owner's list
   uint32_t bf16;  // pushes travel as bf16 (declared lossy mode); own = index of the fp32 source
   const float* src[P3_MAX_RANKS];  // PUSH: src[0]; REDUCE: contributions in rank order
   float* dst[P3_MAX_RANKS];        // PUSH: dst[0]; REDUCE: replicas, dst[0] = owner's master
@@ -838,7 +859,7 @@ __device__ void ingest(const LocalDev& L, uint32_t sched) {
 __device__ uint32_t prepare_push(const CommArgs& a, uint32_t li, uint32_t g, uint32_t l, uint64_t w, Job* job) {
   const PlanDev& P = a.plan;
   const LocalDev& L = a.loc[li];
-  const uint32_t r = L.rank, o = P.slice_owner[g];
+  const uint32_t r = L.rank, o = P.slice_owner[g], opos = P.slice_opos[g];
   const uint32_t lane = threadIdx.x & 31;
   if (!job) {
     uint32_t verdict = o == r ? PUSH_DONE : PUSH_REMOTE;
@@ -849,12 +870,12 @@ __device__ uint32_t prepare_push(const CommArgs& a, uint32_t li, uint32_t g, uin
       trace_append(L, a.k, l, g - P.layer_first[l], r, P3_EV_PUSH);
       if (o == r) {
         // the contribution stays in place (published to this rank by the acquire above)
-        const uint32_t old = atom_add_relaxed_gpu(a.peers.arrivals[o] + g, 1u);
+        const uint32_t old = atom_add_relaxed_gpu(a.peers.arrivals[o] + opos, 1u);
         red_add_relaxed_sys(a.peers.tally[o], 1u);
         if (old + 1 == (a.k + 1) * P.world) {  // the last arrival: the slice is complete
           red_add_relaxed_sys(a.peers.hint[o] + l, 1u);
           red_add_relaxed_sys(a.peers.tally[o] + 1, 1u);
-          if (atomicCAS(L.claim + g, a.k, a.k + 1) == a.k) {
+          if (atomicCAS(L.claim + opos, a.k, a.k + 1) == a.k) {
             atomicAdd(L.srv_taken + l, 1u);
             atomicAdd(&L.it->reduced, 1u);
             verdict = PUSH_REDUCE;
@@ -870,6 +891,7 @@ __device__ uint32_t prepare_push(const CommArgs& a, uint32_t li, uint32_t g, uin
     job->li = li;
     job->g = g;
     job->layer = l;
+    job->opos = opos;
     job->rank = o;
     job->len = P.slice_len[g];
     job->src[0] = pub_ptr(w) + P.slice_off[g];
@@ -894,11 +916,12 @@ __device__ void prepare_reduce(const CommArgs& a, uint32_t li, uint32_t g, uint3
   const uint64_t soff = P.slice_off[g];
   const uint64_t woff = P.layer_woff[l] + soff;
   const uint64_t slot = P.slice_slot[g];
+  const uint32_t opos = N > 1 ? P.slice_opos[g] : 0u;
   const uint64_t stride = P.own_stride[o];
   uint32_t len = q < run ? P.slice_len[g + q] : 0u;  // consecutive slices: contiguous
   if (!w) w = ld_relaxed_gpu64(L.pub + l);
   if (N > 1) {
-    if (q == 0) (void)ld_acquire_sys(a.peers.arrivals[o] + g);  // all N pushes are visible
+    if (q == 0) (void)ld_acquire_sys(a.peers.arrivals[o] + opos);  // all N pushes are visible
   } else if (q == 0) {
     fence_acq_rel_gpu();  // acquire of the publication word (single rank: nothing arrives)
   }
@@ -1217,7 +1240,7 @@ __device__ void signal_job(const CommArgs& a, const Job& j) {
   if (a.remote) fence_acq_rel_sys(); else fence_acq_rel_gpu();
   if (j.kind == JOB_PUSH) {
     // the last arriver completes the slice and tells the owner's scheduler (hint)
-    const uint32_t old = atom_add_relaxed_sys(a.peers.arrivals[j.rank] + j.g, 1u);
+    const uint32_t old = atom_add_relaxed_sys(a.peers.arrivals[j.rank] + j.opos, 1u);
     red_add_relaxed_sys(a.peers.tally[j.rank], 1u);
     if (old + 1 == (a.k + 1) * P.world) {
       red_add_relaxed_sys(a.peers.hint[j.rank] + j.layer, 1u);
@@ -1334,26 +1357,35 @@ __global__ void __launch_bounds__(512, 1) k_comm(const __grid_constant__ CommArg
           kind = JOB_REDUCE;
         }
       }
-      for (uint32_t t = 0; t < a.n_local && kind == JOB_NONE && a.plan.world > 1; ++t) {
-        li = (blockIdx.x + t) % a.n_local;
-        g = warp_server_pick(a, a.loc[li], &pp.layer, phase);
-        if (g != P3_NONE) kind = JOB_REDUCE;
-      }
-      if (kind == JOB_NONE && a.plan.world > 1 && stash.n) {
-        li = stash_li;
-        g = take_stash(&stash, &pp);
-        if (lane == 0) atomicAdd(&a.loc[li].it->pushed, 1u);
-        kind = JOB_PUSH;
-      }
-      for (uint32_t t = 0; t < a.n_local && kind == JOB_NONE && a.plan.world > 1; ++t) {
-        li = (blockIdx.x + t) % a.n_local;
-        ingest(a.loc[li], a.sched);
-        g = warp_pop(queue_of(a, a.loc[li]), a.k + 1, phase, 1u, &pp, &stash);
-        if (lane == 0) stash_li = li;
-        __syncwarp();
-        if (g != P3_NONE) {
-          if (lane == 0) atomicAdd(&a.loc[li].it->pushed, 1u);
-          kind = JOB_PUSH;
+      // Server work (reduce + broadcast of a completed owned slice) and worker pushes both
+      // progress, like the reference's server and sender threads: `push_split` > 0 makes
+      // every push_split-th CTA look for pushes first, the others for server work first.
+      const bool push_first = a.push_split && (blockIdx.x % a.push_split) == a.push_split - 1;
+      for (uint32_t round = 0; round < 2 && kind == JOB_NONE && a.plan.world > 1; ++round) {
+        if ((round == 0) != push_first) {
+          for (uint32_t t = 0; t < a.n_local && kind == JOB_NONE; ++t) {
+            li = (blockIdx.x + t) % a.n_local;
+            g = warp_server_pick(a, a.loc[li], &pp.layer, phase);
+            if (g != P3_NONE) kind = JOB_REDUCE;
+          }
+        } else {
+          if (stash.n) {
+            li = stash_li;
+            g = take_stash(&stash, &pp);
+            if (lane == 0) atomicAdd(&a.loc[li].it->pushed, 1u);
+            kind = JOB_PUSH;
+          }
+          for (uint32_t t = 0; t < a.n_local && kind == JOB_NONE; ++t) {
+            li = (blockIdx.x + t) % a.n_local;
+            ingest(a.loc[li], a.sched);
+            g = warp_pop(queue_of(a, a.loc[li]), a.k + 1, phase, 1u, &pp, &stash);
+            if (lane == 0) stash_li = li;
+            __syncwarp();
+            if (g != P3_NONE) {
+              if (lane == 0) atomicAdd(&a.loc[li].it->pushed, 1u);
+              kind = JOB_PUSH;
+            }
+          }
         }
       }
       if (kind == JOB_NONE) {
@@ -1456,6 +1488,7 @@ __global__ void __launch_bounds__(512, 1) k_comm(const __grid_constant__ CommArg
       mine.li = j.li;
       mine.g = j.g;
       mine.layer = j.layer;
+      mine.opos = j.opos;
       mine.rank = j.rank;
       mine.len = j.len;
       mine.n = j.n;
