@@ -60,8 +60,8 @@ def main():
             per = {}
             for r in tr:
                 per.setdefault(r.rank, []).append((r.t_ns - t0, r.event, lens[first[r.layer] + r.slice]))
-            ends = sorted(max(t for t, ev, _ in v if ev == 1) for v in per.values())
-            starts = sorted(min(t for t, ev, _ in v if ev == 0) for v in per.values())
+            ends = sorted(max(t for t, ev, _ in v) for v in per.values())
+            starts = sorted(min(t for t, ev, _ in v) for v in per.values())
             busy_elems = sorted(sum(n for _, ev, n in v if ev == 1) for v in per.values())
             njobs = sorted(sum(1 for _, ev, _ in v if ev == 1) for v in per.values())
             q = lambda a, f: round(a[min(len(a) - 1, int(f * len(a)))] / 1e3, 1)
@@ -70,7 +70,7 @@ def main():
                                      "elems_per_cta_M": [round(busy_elems[0] / 1e6, 3), round(busy_elems[len(busy_elems) // 2] / 1e6, 3), round(busy_elems[-1] / 1e6, 3)],
                                      "jobs_per_cta": [njobs[0], njobs[len(njobs) // 2], njobs[-1]]}), flush=True)
             # the CTA that finished last: its job sequence
-            last = max(per, key=lambda c: max(t for t, ev, _ in per[c] if ev == 1))
+            last = max(per, key=lambda c: max(t for t, ev, _ in per[c]))
             print("LAST", [(round(t / 1e3, 1), ev, n) for t, ev, n in sorted(per[last])], flush=True)
         print(json.dumps({"model": m, "k": k, "event_ms": round(s.elapsed_time(e), 4), "launch_ms": round(s1.elapsed_time(e), 4), "jobs": len(sig),
                           "first_pick_to_last_signal_us": round((sig[-1][0] - t0) / 1e3, 1),
