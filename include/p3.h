@@ -308,6 +308,55 @@ const char* p3_last_error(p3_ctx_t* ctx);
 /* Device attributes the runtime depends on (stream memory ops, SM count). */
 int p3_device_info(int* sm_count, int* stream_memops, int* cc_major, int* cc_minor);
 
+/* ------------------------------------------------------------------ wire frames (multi-node)
+ * The framed wire protocol of proto.py:18-141 for traffic that leaves the NVSwitch domain
+ * (SURVEY §8(f) item 4): a 39-byte little-endian header "<4sBIQHIIQI" — magic "P3W1",
+ * msg_type u8, priority u32, iteration u64, worker_rank u16, layer u32, slice u32,
+ * offset u64, payload_len u32 — followed by the float32 payload of PUSH / BCAST frames.
+ * Inside one box the comm kernel never serialises (stores go straight over NVLink). */
+#define P3_FRAME_HEADER_BYTES 39
+#define P3_FRAME_DEFAULT_MAX_PAYLOAD (16u * 1024u * 1024u)
+#define P3_MSG_PUSH 0
+#define P3_MSG_BCAST 1
+#define P3_MSG_PULL 2
+#define P3_MSG_NOTIFY 3
+#define P3_MSG_HELLO 4
+#define P3_MSG_FIN 5
+#define P3_EMORE 5 /* p3_frame_decode: incomplete frame, *n_out = bytes still needed */
+
+typedef struct {
+  uint32_t msg_type;    /* P3_MSG_* */
+  uint32_t priority;
+  uint64_t iteration;
+  uint32_t worker_rank; /* u16 on the wire */
+  uint32_t layer;
+  uint32_t slice;
+  uint64_t offset;
+  uint32_t payload_len; /* bytes */
+  uint32_t reserved;
+} p3_frame_t;
+
+/* encode_frame (proto.py:61-79): header + payload into out (cap bytes); *n_out = frame
+ * bytes. P3_EPROTOCOL for a PUSH/BCAST payload that is not a float32 array or a payload on
+ * a control frame; P3_EUSAGE for out-of-range fields or a short buffer. */
+int p3_frame_encode(const p3_frame_t* f, const void* payload, uint8_t* out, uint64_t cap, uint64_t* n_out);
+/* try_decode (proto.py:82-120) of the frame at the head of buf: P3_OK with *n_out = frame
+ * bytes (the payload is buf + P3_FRAME_HEADER_BYTES), P3_EMORE with *n_out = bytes still
+ * needed, or P3_EPROTOCOL (bad magic, unknown msg_type, payload over max_payload, payload on
+ * a control frame; p3_last_error says which). */
+int p3_frame_decode(const uint8_t* buf, uint64_t n, uint64_t max_payload, p3_frame_t* f, uint64_t* n_out);
+/* Device: build n frames in out_dev — frame i at byte out_off_dev[i], its payload copied
+ * from src_dev[i] (payload_len bytes; may be NULL for control frames). All arrays are
+ * device memory; the headers are validated on the host side by the caller (see above). */
+int p3_frames_pack(const p3_frame_t* frames_dev, const float* const* src_dev, const uint64_t* out_off_dev,
+                   uint32_t n, uint8_t* out_dev, void* stream);
+/* Device: decode n frames of in_dev (frame i at byte in_off_dev[i]) into frames_out_dev and
+ * copy each payload to dst_dev[i] (NULL: header only). err_dev[0..2] receive the first
+ * failure: P3_EPROTOCOL, the frame index, the reason (1 magic, 2 msg_type, 3 payload over
+ * max_payload, 4 payload on a control frame); err_dev must be zeroed by the caller. */
+int p3_frames_unpack(const uint8_t* in_dev, const uint64_t* in_off_dev, uint32_t n, uint64_t max_payload,
+                     float* const* dst_dev, p3_frame_t* frames_out_dev, uint32_t* err_dev, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

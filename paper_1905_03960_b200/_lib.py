@@ -16,6 +16,8 @@ P3_EUSAGE = 1
 P3_EPROTOCOL = 2
 P3_ETIMEOUT = 3
 P3_ECUDA = 4
+P3_EMORE = 5
+P3_FRAME_HEADER_BYTES = 39
 
 P3_PLAN_P3 = 0
 P3_PLAN_BASELINE = 1
@@ -48,6 +50,20 @@ class TraceRec(ctypes.Structure):
         ("slice", ctypes.c_uint32),
         ("rank", ctypes.c_uint16),
         ("event", ctypes.c_uint16),
+    ]
+
+
+class FrameT(ctypes.Structure):
+    _fields_ = [
+        ("msg_type", ctypes.c_uint32),
+        ("priority", ctypes.c_uint32),
+        ("iteration", ctypes.c_uint64),
+        ("worker_rank", ctypes.c_uint32),
+        ("layer", ctypes.c_uint32),
+        ("slice", ctypes.c_uint32),
+        ("offset", ctypes.c_uint64),
+        ("payload_len", ctypes.c_uint32),
+        ("reserved", ctypes.c_uint32),
     ]
 
 
@@ -125,6 +141,10 @@ SIGNATURES = {
     "p3_debug_snapshot": (ctypes.c_int, [_P, _U32, _PU32, _U64, _PU64]),
     "p3_last_error": (ctypes.c_char_p, [_P]),
     "p3_device_info": (ctypes.c_int, [ctypes.POINTER(ctypes.c_int)] * 4),
+    "p3_frame_encode": (ctypes.c_int, [ctypes.POINTER(FrameT), _P, _P, _U64, _PU64]),
+    "p3_frame_decode": (ctypes.c_int, [_P, _U64, _U64, ctypes.POINTER(FrameT), _PU64]),
+    "p3_frames_pack": (ctypes.c_int, [_P, _P, _P, _U32, _P, _P]),
+    "p3_frames_unpack": (ctypes.c_int, [_P, _P, _U32, _U64, _P, _P, _P, _P]),
 }
 
 _lib = None

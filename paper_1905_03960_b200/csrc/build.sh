@@ -7,7 +7,7 @@ NVCC="${NVCC:-/usr/local/cuda/bin/nvcc}"
 FLAGS=(-gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC,-O3
        -cudart static -shared -ldl -I"${HERE}/../../include" -Xptxas -v)
 "${NVCC}" "${FLAGS[@]}" -o "${OUT}.tmp" \
-  "${HERE}/p3_host.cpp" "${HERE}/p3_sim.cpp" "${HERE}/p3_kernels.cu" "${HERE}/p3_ctx.cu" 2> "${HERE}/../ptxas.log" || {
+  "${HERE}/p3_host.cpp" "${HERE}/p3_sim.cpp" "${HERE}/p3_kernels.cu" "${HERE}/p3_ctx.cu" "${HERE}/p3_wire.cu" 2> "${HERE}/../ptxas.log" || {
   cat "${HERE}/../ptxas.log" >&2; exit 1; }
 mv "${OUT}.tmp" "${OUT}"
 echo "built ${OUT}"

@@ -204,6 +204,44 @@ def main() -> None:
     out["sweep"] = {"scenario": rsim.scenario_to_dict(sw), "sizes": [1, 2, 3, 4, 6, 8, 12, 24],
                     "result": rsim.sweep_slice_size(sw, [1, 2, 3, 4, 6, 8, 12, 24])}
 
+    # wire frames (proto.py): reference encodings of random frames, and the reference's
+    # verdict on malformed / truncated buffers
+    from p3sync import proto as rproto
+    import random as _random
+
+    rr = _random.Random(1905)
+    frames = []
+    for i in range(40):
+        mt = rproto.MsgType(rr.randrange(6))
+        pay = b""
+        if mt in (rproto.MsgType.PUSH, rproto.MsgType.BCAST):
+            vals = np.array([rr.uniform(-4, 4) for _ in range(rr.randrange(0, 9))], dtype=np.float32)
+            pay = rproto.pack_f32(vals)
+        fr = rproto.Frame(msg_type=mt, priority=rr.randrange(2**32), iteration=rr.randrange(2**64),
+                          worker_rank=rr.randrange(2**16), layer_index=rr.randrange(2**32),
+                          slice_index=rr.randrange(2**32), offset=rr.randrange(2**64), payload=pay)
+        frames.append({"msg_type": int(mt), "priority": fr.priority, "iteration": fr.iteration,
+                       "worker_rank": fr.worker_rank, "layer_index": fr.layer_index, "slice_index": fr.slice_index,
+                       "offset": fr.offset, "payload": pay.hex(), "wire": rproto.encode_frame(fr).hex()})
+    bad = []
+    hello = rproto.encode_frame(rproto.Frame(msg_type=rproto.MsgType.HELLO, worker_rank=3))
+    push = rproto.encode_frame(rproto.Frame(msg_type=rproto.MsgType.PUSH, payload=rproto.pack_f32(np.ones(4, np.float32))))
+    import struct as _struct
+    cases = {
+        "short_header": hello[:10], "short_payload": push[:-3], "bad_magic": b"XXXX" + hello[4:],
+        "bad_type": hello[:4] + bytes([99]) + hello[5:],
+        "oversize": _struct.pack("<4sBIQHIIQI", rproto.MAGIC, 0, 0, 0, 0, 0, 0, 0, rproto.DEFAULT_MAX_PAYLOAD + 4),
+        "control_payload": _struct.pack("<4sBIQHIIQI", rproto.MAGIC, 2, 0, 0, 0, 0, 0, 0, 4) + b"\0" * 4,
+        "two_frames": push + hello,
+    }
+    for name, buf in cases.items():
+        try:
+            fr, n = rproto.try_decode(buf)
+            bad.append({"name": name, "buf": buf.hex(), "ok": fr is not None, "n": n})
+        except rproto.ProtocolError as e:
+            bad.append({"name": name, "buf": buf.hex(), "error": str(e)})
+    out["frames"] = {"frames": frames, "decode_cases": bad}
+
     (HERE / "golden.json").write_text(json.dumps(out, indent=1) + "\n")
     print("wrote", HERE / "golden.json")
 
