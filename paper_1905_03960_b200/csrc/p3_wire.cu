@@ -8,7 +8,7 @@
 // Layout (proto.py:18-21): 39-byte little-endian header "<4sBIQHIIQI" — magic "P3W1",
 // msg_type u8, priority u32, iteration u64, worker_rank u16, layer u32, slice u32, offset
 // u64, payload_len u32 — then payload_len bytes of float32 (PUSH and BCAST only).
-// The payload therefore starts 39 bytes into the frame: device copies move 4-byte words
+// The payload therefore starts 39 bytes into the frame: device copies move 16-byte words
 // between a float-aligned side and a byte-shifted side with funnel shifts.
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -74,31 +74,43 @@ __host__ __device__ inline uint32_t parse_header(const uint8_t* h, uint64_t max_
 constexpr uint32_t kThreads = 256;
 constexpr uint32_t kBlocksPerFrame = 16;
 
-// dst (byte-shifted) <- src (4-byte aligned), `bytes` bytes.
-__device__ void copy_to_shifted(uint8_t* dst, const uint8_t* src, uint32_t bytes, uint32_t t, uint32_t nt) {
-  const uint32_t head = min(bytes, (uint32_t)((4 - ((uintptr_t)dst & 3)) & 3));
-  if (t < head) dst[t] = src[t];
-  const uint32_t words = (bytes - head) / 4;
-  uint32_t* d32 = reinterpret_cast<uint32_t*>(dst + head);
-  const uint32_t* s32 = reinterpret_cast<const uint32_t*>(src);  // byte head + 4k lives in words k, k+1
-  for (uint32_t k = t; k < words; k += nt) {
-    const uint32_t lo = __ldg(s32 + k);
-    d32[k] = head ? __funnelshift_r(lo, __ldg(s32 + k + 1), 8 * head) : lo;
-  }
-  for (uint32_t i = head + 4 * words + t; i < bytes; i += nt) dst[i] = src[i];
+// Bytes [0, n) of src to dst, any alignment of either: byte-wise until dst is 16-byte
+// aligned, then 16-byte stores, each assembled from the two aligned 16-byte source chunks
+// that cover it (funnel shifts by the — per-call uniform — source misalignment), then the
+// tail byte-wise. A chunk load may touch up to 15 bytes past the last byte it needs; the
+// chunk is 16-byte aligned, so it never leaves the allocation granule.
+template <int WO>
+__device__ __forceinline__ uint4 shifted16(const uint4& A, const uint4& B, uint32_t r) {
+  const uint32_t w[8] = {A.x, A.y, A.z, A.w, B.x, B.y, B.z, B.w};
+  uint4 o;
+  o.x = r ? __funnelshift_r(w[WO + 0], w[WO + 1], 8 * r) : w[WO + 0];
+  o.y = r ? __funnelshift_r(w[WO + 1], w[WO + 2], 8 * r) : w[WO + 1];
+  o.z = r ? __funnelshift_r(w[WO + 2], w[WO + 3], 8 * r) : w[WO + 2];
+  o.w = r ? __funnelshift_r(w[WO + 3], w[WO + 4], 8 * r) : w[WO + 3];
+  return o;
 }
 
-// dst (4-byte aligned) <- src (byte-shifted), `bytes` bytes.
-__device__ void copy_from_shifted(uint8_t* dst, const uint8_t* src, uint32_t bytes, uint32_t t, uint32_t nt) {
-  const uint32_t r = (uint32_t)((uintptr_t)src & 3);
-  const uint32_t* s32 = reinterpret_cast<const uint32_t*>(src - r);
-  uint32_t* d32 = reinterpret_cast<uint32_t*>(dst);
-  const uint32_t words = bytes / 4;
-  for (uint32_t k = t; k < words; k += nt) {
-    const uint32_t lo = __ldg(s32 + k);
-    d32[k] = r ? __funnelshift_r(lo, __ldg(s32 + k + 1), 8 * r) : lo;
+__device__ void copy_bytes(uint8_t* dst, const uint8_t* src, uint32_t bytes, uint32_t t, uint32_t nt) {
+  const uint32_t head = min(bytes, (uint32_t)((16 - ((uintptr_t)dst & 15)) & 15));
+  if (t < head) dst[t] = src[t];
+  const uint32_t chunks = (bytes - head) / 16;
+  const uint8_t* s = src + head;
+  const uint32_t q = (uint32_t)((uintptr_t)s & 15), wo = q / 4, r = q % 4;
+  const uint4* s4 = reinterpret_cast<const uint4*>(s - q);
+  uint4* d4 = reinterpret_cast<uint4*>(dst + head);
+  for (uint32_t k = t; k < chunks; k += nt) {
+    const uint4 A = __ldg(s4 + k);
+    const uint4 B = q ? __ldg(s4 + k + 1) : A;
+    uint4 o;
+    switch (wo) {  // uniform across the grid: no divergence
+      case 0: o = shifted16<0>(A, B, r); break;
+      case 1: o = shifted16<1>(A, B, r); break;
+      case 2: o = shifted16<2>(A, B, r); break;
+      default: o = shifted16<3>(A, B, r); break;
+    }
+    d4[k] = o;
   }
-  for (uint32_t i = 4 * words + t; i < bytes; i += nt) dst[i] = src[i];
+  for (uint32_t i = head + 16 * chunks + t; i < bytes; i += nt) dst[i] = src[i];
 }
 
 __global__ void __launch_bounds__(kThreads) k_frames_pack(const p3_frame_t* frames, const float* const* src,
@@ -109,7 +121,7 @@ __global__ void __launch_bounds__(kThreads) k_frames_pack(const p3_frame_t* fram
   if (blockIdx.x == 0 && threadIdx.x < kHeader) base[threadIdx.x] = header_byte(f, threadIdx.x);
   const uint8_t* s = reinterpret_cast<const uint8_t*>(src[i]);
   if (!has_payload(f.msg_type) || !s || f.payload_len == 0) return;
-  copy_to_shifted(base + kHeader, s, f.payload_len, blockIdx.x * kThreads + threadIdx.x, gridDim.x * kThreads);
+  copy_bytes(base + kHeader, s, f.payload_len, blockIdx.x * kThreads + threadIdx.x, gridDim.x * kThreads);
 }
 
 __global__ void __launch_bounds__(kThreads) k_frames_unpack(const uint8_t* in, const uint64_t* in_off, uint32_t first,
@@ -130,8 +142,8 @@ __global__ void __launch_bounds__(kThreads) k_frames_unpack(const uint8_t* in, c
     }
   }
   if (why || !dst || !dst[i] || f.payload_len == 0) return;
-  copy_from_shifted(reinterpret_cast<uint8_t*>(dst[i]), base + kHeader, f.payload_len,
-                    blockIdx.x * kThreads + threadIdx.x, gridDim.x * kThreads);
+  copy_bytes(reinterpret_cast<uint8_t*>(dst[i]), base + kHeader, f.payload_len, blockIdx.x * kThreads + threadIdx.x,
+             gridDim.x * kThreads);
 }
 
 }  // namespace
