@@ -607,6 +607,10 @@ static CommArgs comm_args(p3_ctx* c, uint32_t mode, uint32_t ctas) {
     a.push_split = e ? (uint32_t)atoi(e) : 0u;
   }
   {
+    const char* e = getenv("P3_SRV_FILTER");
+    a.srv_filter = e ? (uint32_t)atoi(e) : 0u;
+  }
+  {
     const char* e = getenv("P3_TMA");
     a.use_tma = e ? (uint32_t)atoi(e) : 1u;
   }

@@ -122,6 +122,7 @@ struct CommArgs {
   uint32_t pop_multi; // candidate layers claimed per round of pop atomics
   uint32_t push_bf16; // pushes travel as bf16
   uint32_t push_split; // every push_split-th CTA prefers pushes over server work (0: none)
+  uint32_t srv_filter; // server picks: only srv_filter x (ready slices) consumers look (0: all)
   uint32_t use_tma;   // movers stage sources through shared memory with TMA (else direct loads)
   uint32_t trace_cta; // diagnostics (P3_TRACE_CTA=1): trace records carry the CTA index as `rank`
   float ns_per_byte;  // K7 link emulation (0: unthrottled)

@@ -638,13 +638,16 @@ __device__ uint32_t warp_server_pick(const CommArgs& a, const LocalDev& L, uint3
   const uint32_t* lfirst = P.own_lfirst + (uint64_t)o * nl;
   const uint32_t need = (k + 1) * P.world;
   {
-    uint32_t any = 0;
+    // completed but unclaimed owned slices (with `srv_filter` > 0, only srv_filter x as many
+    // of the launch's consumers as there are such slices look; the rest go to their pushes)
+    int32_t avail = 0;
     if (lane == 0) {
       const uint32_t claimed = ld_relaxed_gpu(&L.it->reduced);
       const uint32_t completed = ld_relaxed_sys(a.peers.tally[o] + 1) - k * P.own_total[o];
-      any = (int32_t)(completed - claimed) > 0;
+      avail = (int32_t)(completed - claimed);
     }
-    if (!__shfl_sync(FULL_MASK, any, 0)) return P3_NONE;
+    avail = __shfl_sync(FULL_MASK, avail, 0);
+    if (avail <= 0 || (a.srv_filter && (blockIdx.x % a.pop_relax) >= a.srv_filter * (uint32_t)avail)) return P3_NONE;
   }
   constexpr uint32_t CH = 8;
   for (uint32_t group = 0; group < nl; group += 32 * CH) {
@@ -694,8 +697,17 @@ __device__ uint32_t warp_server_pick(const CommArgs& a, const LocalDev& L, uint3
           // hold an unclaimed slice even if this window is fully claimed
           if (__all_sync(FULL_MASK, claimed) && lane == 0) atomicCAS(L.srv_lo + l, i0, i0 + 32);
           uint32_t m = __ballot_sync(FULL_MASK, ok);
-          while (m) {
-            const int jj = __ffs(m) - 1;
+          // first try a CTA-dependent one of the window's ready slices (consumers spread
+          // over them instead of racing for the lowest), then the rest in ascending order
+          int pref = -1;
+          if (m && a.pop_relax > 1) {
+            uint32_t mm = m;
+            for (uint32_t skip = blockIdx.x % __popc(m); skip; --skip) mm &= mm - 1;
+            pref = __ffs(mm) - 1;
+          }
+          for (uint32_t attempt = 0; m; ++attempt) {
+            const int jj = (attempt == 0 && pref >= 0) ? pref : __ffs(m) - 1;
+            m &= ~(1u << jj);
             const uint32_t gj = __shfl_sync(FULL_MASK, g, jj);
             const uint32_t pj = lf + i0 + jj;
             uint32_t won = 0;
@@ -711,7 +723,6 @@ __device__ uint32_t warp_server_pick(const CommArgs& a, const LocalDev& L, uint3
               *layer_out = l;
               return gj;
             }
-            m &= m - 1;
           }
         }
       }
