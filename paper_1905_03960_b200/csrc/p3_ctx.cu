@@ -391,6 +391,11 @@ int p3_ctx_create(const p3_config_t* cfg, p3_ctx_t** out) {
   const size_t o_ot = put(c->own_total.data(), N * 4ull);
   const size_t o_ost = put(c->own_stride.data(), N * 8ull);
   const size_t o_lg = put(c->layer_group.data(), L * 4ull);
+  std::vector<uint32_t> own_base(N, 0);
+  for (uint32_t o = 1; o < N; ++o) own_base[o] = own_base[o - 1] + c->own_total[o - 1];
+  const size_t o_ob = put(own_base.data(), N * 4ull);
+  bool rr = true;
+  for (uint32_t g = 0; g < S && rr; ++g) rr = slice_owner[g] == g % N;
   cudaError_t e = cudaMalloc(&c->d_plan, blob.size());
   if (e == cudaSuccess) e = cudaMemcpy(c->d_plan, blob.data(), blob.size(), cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaMalloc(&c->d_err, 256);
@@ -420,6 +425,8 @@ int p3_ctx_create(const p3_config_t* cfg, p3_ctx_t** out) {
   P.own_total = reinterpret_cast<const uint32_t*>(pb + o_ot);
   P.own_stride = reinterpret_cast<const uint64_t*>(pb + o_ost);
   P.layer_group = reinterpret_cast<const uint32_t*>(pb + o_lg);
+  P.own_base = reinterpret_cast<const uint32_t*>(pb + o_ob);
+  P.rr_owner = rr ? 1u : 0u;
 
   // ---- per-rank arenas
   for (uint32_t r = 0; r < N; ++r) c->peer_layout[r] = peer_layout_of(c, r);

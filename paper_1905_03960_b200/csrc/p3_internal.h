@@ -32,7 +32,7 @@ struct PlanDev {
   uint32_t n_layers;
   uint32_t total_slices;
   uint32_t world;
-  uint32_t pad_;
+  uint32_t rr_owner;  // owner(g) == g % world for every slice (make_p3_plan)
   const uint32_t* layer_nslices;  // [L]
   const uint32_t* layer_first;    // [L] first global slice id of the layer
   const uint64_t* layer_woff;     // [L] element offset of the layer in W / G arenas
@@ -48,6 +48,7 @@ struct PlanDev {
   const uint32_t* own_total;      // [world] owned slices per owner
   const uint64_t* own_stride;     // [world] R block stride (padded owned elements)
   const uint32_t* layer_group;    // [L] forward-gate group of the layer
+  const uint32_t* own_base;       // [world] first own_list position of each owner
 };
 
 // Peer-visible state of every rank (pointers valid in this process: local or IPC-mapped).

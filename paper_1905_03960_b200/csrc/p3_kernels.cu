@@ -870,7 +870,11 @@ __device__ void ingest(const LocalDev& L, uint32_t sched) {
 __device__ uint32_t prepare_push(const CommArgs& a, uint32_t li, uint32_t g, uint32_t l, uint64_t w, Job* job) {
   const PlanDev& P = a.plan;
   const LocalDev& L = a.loc[li];
-  const uint32_t r = L.rank, o = P.slice_owner[g], opos = P.slice_opos[g];
+  const uint32_t r = L.rank;
+  // round-robin plans (make_p3_plan: owner = slice counter % N) need no table load here:
+  // the owner is g % N and its own-list position own_base[o] + g / N
+  const uint32_t o = P.rr_owner ? g % P.world : P.slice_owner[g];
+  const uint32_t opos = P.rr_owner ? P.own_base[o] + g / P.world : P.slice_opos[g];
   const uint32_t lane = threadIdx.x & 31;
   if (!job) {
     uint32_t verdict = o == r ? PUSH_DONE : PUSH_REMOTE;
@@ -878,7 +882,7 @@ __device__ uint32_t prepare_push(const CommArgs& a, uint32_t li, uint32_t g, uin
       // the pop read the publication word relaxed: this fence makes it an acquire, so the
       // gradient is visible from here on (ingest released it)
       fence_acq_rel_gpu();
-      trace_append(L, a.k, l, g - P.layer_first[l], r, P3_EV_PUSH);
+      if (L.trace_cap) trace_append(L, a.k, l, g - P.layer_first[l], r, P3_EV_PUSH);
       if (o == r) {
         // the contribution stays in place (published to this rank by the acquire above)
         const uint32_t old = atom_add_relaxed_gpu(a.peers.arrivals[o] + opos, 1u);
@@ -1266,8 +1270,9 @@ __device__ void signal_job(const CommArgs& a, const Job& j) {
     }
     atomicAdd(L.bytes + 0, (j.bf16 ? 2ull : 4ull) * j.len * (j.n - 1));  // pushes received
     atomicAdd(L.bytes + 1, 4ull * j.len * (j.n - 1));  // broadcasts sent
-    for (uint32_t i = 0; i < j.run; ++i)
-      trace_append(L, a.k, j.layer, j.g + i - P.layer_first[j.layer], a.trace_cta ? blockIdx.x : j.rank, P3_EV_BCAST);
+    if (L.trace_cap)
+      for (uint32_t i = 0; i < j.run; ++i)
+        trace_append(L, a.k, j.layer, j.g + i - P.layer_first[j.layer], a.trace_cta ? blockIdx.x : j.rank, P3_EV_BCAST);
   }
 }
 
