@@ -111,7 +111,8 @@ def max_over_ranks(x: float, world: int) -> float:
     import torch
     import torch.distributed as dist
 
-    t = torch.tensor([x], device="cuda", dtype=torch.float64)
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"  # (gloo: the CPU tests of these helpers)
+    t = torch.tensor([x], device=dev, dtype=torch.float64)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -123,7 +124,8 @@ def barrier(world: int) -> None:
         import torch.distributed as dist
 
         dist.barrier()
-    torch.cuda.synchronize()
+    if torch.cuda.is_available():
+        torch.cuda.synchronize()
 
 
 def build(args, rank):
@@ -190,18 +192,13 @@ def sync_only_roofline(args, world, rank, counts):
     import torch
 
     from paper_1905_03960_b200 import _lib
-    from paper_1905_03960_b200.runtime import SyncContext
+    from paper_1905_03960_b200.runtime import SyncContext, connect
 
     props = torch.cuda.get_device_properties(0)
     ctas = props.multi_processor_count  # one 512-thread comm CTA per SM (126 registers)
     ctx = SyncContext(counts, world, [rank], max_slice=args.max_slice, lr=args.lr, comm_ctas=ctas,
                       comm_threads=512, timeout_s=60.0, emulate_grads=True)
-    if world > 1:
-        import torch.distributed as dist
-
-        hs = [None] * world
-        dist.all_gather_object(hs, ctx.ipc_handle(0))
-        ctx.open_peers(hs)
+    connect(ctx)
     stream = torch.cuda.Stream()
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")  # > 126 MB L2
     for l in range(len(counts)):

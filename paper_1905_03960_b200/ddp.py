@@ -31,7 +31,7 @@ import torch
 import torch.distributed as dist
 
 from .plan import DEFAULT_MAX_SLICE
-from .runtime import SyncContext
+from .runtime import SyncContext, connect
 
 
 def _dist_info() -> tuple[int, int]:
@@ -152,10 +152,7 @@ class P3DataParallel(_HookedDataParallel):
             gate_groups=groups, pub_batch_bytes=pub_batch_bytes, drain_linger_us=drain_linger_us,
             finish_ctas=finish_ctas, push_dtype=push_dtype,
         )
-        if self.world > 1:
-            handles = [None] * self.world
-            dist.all_gather_object(handles, self.ctx.ipc_handle(0))
-            self.ctx.open_peers(handles)
+        connect(self.ctx)  # every rank's arena, after checking all ranks built the same plan
         arena = self.ctx.params_arena(0)
         with torch.no_grad():
             for l, p in enumerate(self.params):

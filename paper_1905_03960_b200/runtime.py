@@ -45,6 +45,44 @@ class TraceEvent:
     event: int  # _lib.P3_EV_PUSH / P3_EV_BCAST
 
 
+def plan_fingerprint(layer_counts, world, max_slice, plan_mode, big_threshold, rng_seed, priority_mode, lr, momentum,
+                     push_dtype) -> str:
+    """What every rank of one sync group must agree on: the plan (layer sizes, world, slice
+    size, placement), the discipline and the update rule. Ranks that disagree would wait on
+    each other forever (a slice one rank never pushes), so ``connect`` refuses them."""
+    key = repr((list(map(int, layer_counts)), int(world), int(max_slice), plan_mode, int(big_threshold), int(rng_seed),
+                bool(priority_mode), float(lr), float(momentum), push_dtype))
+    return f"{fnv1a64(key.encode()):016x}"
+
+
+def exchange_peer_handles(handle: bytes, fingerprint: str, group=None) -> list[bytes]:
+    """All-gather (torch.distributed, any backend) of every rank's IPC handle, in rank order,
+    after checking that all ranks built the same plan (``plan_fingerprint``): the host side of
+    TrainingWorker._connect_all (worker.py:136), which dials every server."""
+    import torch.distributed as dist
+
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    if len(handle) != _lib.P3_IPC_BYTES:
+        raise ValueError(f"IPC handle must be {_lib.P3_IPC_BYTES} bytes")
+    rows = [None] * world
+    dist.all_gather_object(rows, (rank, fingerprint, bytes(handle)), group=group)
+    prints = sorted({r[1] for r in rows})
+    if len(prints) != 1:
+        from .plan import PlanError
+
+        raise PlanError(f"ranks built different sync plans (fingerprints {prints}): same model, world, "
+                        "max_slice, plan mode and update rule are required on every rank")
+    if [r[0] for r in rows] != list(range(world)):
+        raise RuntimeError("handle exchange out of rank order")
+    return [r[2] for r in rows]
+
+
+def connect(ctx: "SyncContext", group=None) -> None:
+    """Open every peer's arena (NVLink / CUDA IPC) for a one-rank-per-process context."""
+    if ctx.world > 1:
+        ctx.open_peers(exchange_peer_handles(ctx.ipc_handle(0), ctx.fingerprint, group))
+
+
 class SyncContext:
     """One p3 sync context (see include/p3.h, p3_ctx_create)."""
 
@@ -138,6 +176,8 @@ class SyncContext:
             self.layer_offsets.append(int(off.value))
         self.arena_elems = self.layer_offsets[-1] + self.layer_counts[-1]
         self.plan_mode = plan_mode
+        self.fingerprint = plan_fingerprint(self.layer_counts, world, max_slice, plan_mode, big_threshold, rng_seed,
+                                            priority_mode, lr, momentum, push_dtype)
 
     # ------------------------------------------------------------------ plumbing
     def _check(self, rc: int, what: str) -> None:
