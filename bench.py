@@ -201,6 +201,7 @@ def sync_only_roofline(args, world, rank, counts):
     connect(ctx)
     stream = torch.cuda.Stream()
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")  # > 126 MB L2
+    align = torch.zeros(1, device="cuda")
     for l in range(len(counts)):
         ctx.gradgen_layer(0, 7, 0, l, stream)
     stream.synchronize()
@@ -216,6 +217,10 @@ def sync_only_roofline(args, world, rank, counts):
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         with torch.cuda.stream(stream):
             torch.cuda._sleep(200_000)  # ~0.1 ms: the host enqueues the launch before the GPU gets there
+            if world > 1:  # align the ranks on the device: a late peer is not this kernel's time
+                import torch.distributed as dist
+
+                dist.all_reduce(align)
         ctx.iteration_begin(k, stream)  # per-iteration counter reset (memset) — not the kernel
         s.record(stream)
         ctx.iteration_end(k)  # one FINISH launch does the whole iteration

@@ -37,7 +37,10 @@ def main():
                     if world > 1: dist.barrier()
                     torch.cuda.synchronize()
                     s, e = torch.cuda.Event(True), torch.cuda.Event(True)
-                    s.record(st); ctx.iteration_begin(k, st); ctx.iteration_end(k); e.record(st)
+                    with torch.cuda.stream(st):
+                        torch.cuda._sleep(200_000)  # the host enqueues the launch ahead of the GPU
+                        if world > 1: dist.all_reduce(torch.zeros(1, device="cuda"))  # ranks aligned on the device
+                    ctx.iteration_begin(k, st); s.record(st); ctx.iteration_end(k); e.record(st)
                     try:
                         ctx.sync_all(k + 1, 20.0)
                     except Exception as ex:
