@@ -1329,6 +1329,8 @@ __global__ void __launch_bounds__(512, 1) k_comm(const __grid_constant__ CommArg
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
+  if (a.trace_cta && threadIdx.x == 0)  // diagnostics: CTA start (event 2)
+    trace_append(a.loc[0], a.k, 0, 0, blockIdx.x, 2);
   if (warp == 0) {
     uint32_t* phase = (lane == 0 && blockIdx.x < P3_DBG_CTAS) ? a.loc[0].cta_phase + blockIdx.x : nullptr;
     const uint64_t t0 = globaltimer();
@@ -1491,6 +1493,7 @@ __global__ void __launch_bounds__(512, 1) k_comm(const __grid_constant__ CommArg
       if (a.mode == P3_COMM_FINISH) atomicAdd(&stats->exited, 1u);
     }
     if (phase) *(volatile uint32_t*)phase = (a.k << 24) | (5u << 20);
+    if (a.trace_cta && lane == 0) trace_append(a.loc[0], a.k, 0, 0, blockIdx.x, 3);  // diagnostics: scheduler exit
   } else if (warp == 1) {
     // signaler: in job order, once the consumers are done with a job, fence and publish
     uint64_t t_sig = 0;

@@ -48,7 +48,10 @@ def main():
         e.record(st)
         ctx.sync_all(k + 1, 30.0)
         st.synchronize()
-        tr = [r for r in ctx.trace(0) if r.iteration == k]
+        tr_all = [r for r in ctx.trace(0) if r.iteration == k]
+        starts_ev = [r.t_ns for r in tr_all if r.event == 2]
+        exits_ev = [r.t_ns for r in tr_all if r.event == 3]
+        tr = [r for r in tr_all if r.event in (0, 1)]
         picks = sorted(r.t_ns for r in tr if r.event == 0)
         sig = sorted((r.t_ns, lens[first[r.layer] + r.slice]) for r in tr if r.event == 1)
         t0 = picks[0]
@@ -72,6 +75,11 @@ def main():
             # the CTA that finished last: its job sequence
             last = max(per, key=lambda c: max(t for t, ev, _ in per[c]))
             print("LAST", [(round(t / 1e3, 1), ev, n) for t, ev, n in sorted(per[last])], flush=True)
+        if starts_ev:
+            print("EDGES", json.dumps({"first_cta_start_to_first_pick_us": round((t0 - min(starts_ev)) / 1e3, 2),
+                                       "cta_start_spread_us": round((max(starts_ev) - min(starts_ev)) / 1e3, 2),
+                                       "last_signal_to_last_exit_us": round((max(exits_ev) - max(t for t, _ in sig)) / 1e3, 2),
+                                       "first_start_to_last_exit_us": round((max(exits_ev) - min(starts_ev)) / 1e3, 2)}))
         print(json.dumps({"model": m, "k": k, "event_ms": round(s.elapsed_time(e), 4), "launch_ms": round(s1.elapsed_time(e), 4), "jobs": len(sig),
                           "first_pick_to_last_signal_us": round((sig[-1][0] - t0) / 1e3, 1),
                           "first_signal_us": round((sig[0][0] - t0) / 1e3, 1),
