@@ -377,7 +377,10 @@ struct QueueView {
   const uint64_t* pub;
   const uint32_t* fifo_key;
   uint32_t* cursor;
+  const LocalDev* ring;  // publication ring to ingest from (nullptr: scripted queue)
 };
+
+__device__ void ingest(const LocalDev& L, uint32_t sched);
 
 // Publication word: iteration tag (16 bits) above the 48-bit gradient pointer, written by one
 // 64-bit stream memory write, so the tag and the pointer become visible together.
@@ -425,6 +428,10 @@ __device__ uint32_t warp_pop(const QueueView& q, uint32_t tag, uint32_t* dbg = n
       // all loads of the group issued before any is used: one round trip, not 2*CH
       uint64_t w[CH];
       uint32_t cur[CH], ns[CH];
+      // the ring check rides on the same round trip as the first group's loads
+      const bool ring_check = q.ring && group == 0 && lane == 0;
+      const uint32_t r_lo = ring_check ? ld_relaxed_gpu(q.ring->ingested) : 0u;
+      const uint32_t r_hi = ring_check ? ld_relaxed_gpu(q.ring->pubseq) : 0u;
 #pragma unroll
       for (uint32_t c = 0; c < CH; ++c) {
         const uint32_t l = group + 32 * c + lane;
@@ -432,6 +439,10 @@ __device__ uint32_t warp_pop(const QueueView& q, uint32_t tag, uint32_t* dbg = n
         w[c] = in ? ld_relaxed_gpu64(q.pub + l) : 0ull;
         cur[c] = in ? ld_relaxed_gpu(q.cursor + l) : 0u;
         ns[c] = in ? q.nslices[l] : 0u;
+      }
+      if (q.ring && group == 0 && __shfl_sync(FULL_MASK, (uint32_t)(r_lo != r_hi), 0)) {
+        ingest(*q.ring, q.sched);  // new publications: turn them into words, then look again
+        continue;
       }
       uint32_t bits = 0;  // bit c: layer group + 32*c + lane is poppable
 #pragma unroll
@@ -563,6 +574,7 @@ __device__ uint32_t warp_pop(const QueueView& q, uint32_t tag, uint32_t* dbg = n
     }
     return P3_NONE;
   }
+  if (q.ring) ingest(*q.ring, q.sched);
   for (uint32_t retry = 0;; ++retry) {
     if (dbg && lane == 0) *(volatile uint32_t*)dbg = (6u << 20) | (retry & 0xfffff);
     uint32_t best_key = P3_NONE, best_l = P3_NONE;
@@ -613,7 +625,7 @@ __global__ void k_queue_pop(QueueView q, uint32_t tag, uint32_t* result) {
 int launch_queue_pop(const uint32_t* nslices, const uint32_t* first, const uint64_t* pub,
                      const uint32_t* fifo_key, uint32_t* cursor, uint32_t n_layers, uint32_t sched,
                      uint32_t tag, uint32_t* result, void* stream) {
-  QueueView q{n_layers, sched, 1u, 1u, nslices, first, pub, fifo_key, cursor};
+  QueueView q{n_layers, sched, 1u, 1u, nslices, first, pub, fifo_key, cursor, nullptr};
   k_queue_pop<<<1, 32, 0, (cudaStream_t)stream>>>(q, tag, result);
   return cudaGetLastError() == cudaSuccess ? P3_OK : P3_ECUDA;
 }
@@ -778,6 +790,7 @@ __device__ __forceinline__ QueueView queue_of(const CommArgs& a, const LocalDev&
   q.pub = L.pub;
   q.fifo_key = L.fifo_key;
   q.cursor = L.cursor;
+  q.ring = &L;
   return q;
 }
 
@@ -1359,7 +1372,6 @@ __global__ void __launch_bounds__(512, 1) k_comm(const __grid_constant__ CommArg
         if (stash.n) {
           g = take_stash(&stash, &pp);
         } else {
-          ingest(L, a.sched);
           g = warp_pop(queue_of(a, L), a.k + 1, phase, L.V ? 1u : a.pop_run, &pp, &stash);
         }
         if (g != P3_NONE) {
@@ -1395,7 +1407,6 @@ __global__ void __launch_bounds__(512, 1) k_comm(const __grid_constant__ CommArg
           }
           for (uint32_t t = 0; t < a.n_local && kind == JOB_NONE; ++t) {
             li = (blockIdx.x + t) % a.n_local;
-            ingest(a.loc[li], a.sched);
             g = warp_pop(queue_of(a, a.loc[li]), a.k + 1, phase, 1u, &pp, &stash);
             if (lane == 0) stash_li = li;
             __syncwarp();
