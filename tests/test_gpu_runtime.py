@@ -350,3 +350,21 @@ def test_bf16_push_matches_oracle(cuda, world):
     for a, b in zip(w.params(0), ref):
         assert np.max(np.abs(a - b)) <= 3 * 0.1 * 2.0 ** -8
     w.close()
+
+
+@pytest.mark.gpu
+def test_device_prefetcher_ring(cuda):
+    """DevicePrefetcher: every batch arrives intact and in order although the two device
+    buffers are refilled while the compute stream still works on the other one."""
+    import torch
+
+    from paper_1905_03960_b200.loader import DevicePrefetcher
+
+    host = [(torch.full((1 << 20,), float(i)).pin_memory(), torch.tensor([i]).pin_memory()) for i in range(7)]
+    feed = DevicePrefetcher(host)
+    got = []
+    for x, y in feed:
+        torch.cuda._sleep(2_000_000)  # a long "step" on the compute stream reading x
+        got.append((float(x.sum().item()) / x.numel(), int(y.item())))
+    assert got == [(float(i), i) for i in range(7)]
+    assert feed.h2d_bytes == sum(a.numel() * 4 + 8 for a, _ in host)
