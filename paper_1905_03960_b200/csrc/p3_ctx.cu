@@ -109,6 +109,12 @@ struct p3_ctx {
   std::vector<uint64_t> layer_woff;
   std::vector<uint32_t> layer_nslices, layer_first;
   std::vector<uint32_t> slice_opos;  // position of each slice in the owner-grouped list
+  // experiment / diagnostics switches, read once from the environment at creation:
+  // P3_TMA=0 (direct loads instead of the TMA stage ring), P3_PUSH_SPLIT=n, P3_SRV_FILTER=n,
+  // P3_TRACE_CTA=1 (trace records carry CTA indices; CTA start / exit records)
+  struct {
+    uint32_t use_tma = 1, push_split = 0, srv_filter = 0, trace_cta = 0;
+  } knobs;
   std::vector<uint32_t> own_total;
   std::vector<uint64_t> own_stride;
   std::vector<uint64_t> bcast_in_bytes;  // per rank: broadcast payload received per iteration
@@ -284,6 +290,16 @@ int p3_ctx_create(const p3_config_t* cfg, p3_ctx_t** out) {
   c->cfg.gate_groups = nullptr;  // consumed below, not retained
   c->L = cfg->n_layers;
   c->N = cfg->world;
+  {
+    auto env_u32 = [](const char* name, uint32_t dflt) {
+      const char* e = getenv(name);
+      return e ? (uint32_t)atoi(e) : dflt;
+    };
+    c->knobs.use_tma = env_u32("P3_TMA", 1);
+    c->knobs.push_split = env_u32("P3_PUSH_SPLIT", 0);
+    c->knobs.srv_filter = env_u32("P3_SRV_FILTER", 0);
+    c->knobs.trace_cta = getenv("P3_TRACE_CTA") != nullptr;
+  }
   std::string perr;
   int rc = cfg->plan_mode == P3_PLAN_P3
                ? build_p3_plan(c->counts.data(), c->L, c->N, cfg->max_slice, &c->plan, &perr)
@@ -608,19 +624,10 @@ static CommArgs comm_args(p3_ctx* c, uint32_t mode, uint32_t ctas) {
                              : std::max<uint32_t>(1, std::min<uint32_t>(8, c->S / std::max<uint32_t>(1, 4 * ctas)));
   a.pop_multi = std::max<uint32_t>(1, std::min<uint32_t>(4, c->cfg.pop_multi ? c->cfg.pop_multi : 1));
   a.push_bf16 = c->cfg.push_bf16 ? 1u : 0u;
-  a.trace_cta = getenv("P3_TRACE_CTA") != nullptr;
-  {
-    const char* e = getenv("P3_PUSH_SPLIT");
-    a.push_split = e ? (uint32_t)atoi(e) : 0u;
-  }
-  {
-    const char* e = getenv("P3_SRV_FILTER");
-    a.srv_filter = e ? (uint32_t)atoi(e) : 0u;
-  }
-  {
-    const char* e = getenv("P3_TMA");
-    a.use_tma = e ? (uint32_t)atoi(e) : 1u;
-  }
+  a.trace_cta = c->knobs.trace_cta;
+  a.push_split = c->knobs.push_split;
+  a.srv_filter = c->knobs.srv_filter;
+  a.use_tma = c->knobs.use_tma;
   // bounded relaxation of the pop order: a pop takes one of the C most urgent slices, C =
   // the launch's concurrent consumers (its CTAs) unless configured lower
   // (measured, tools/sync_sweep.py, ResNet-50 N=1 sync-only: C=8 2.2 TB/s, C=148 3.4 TB/s —
