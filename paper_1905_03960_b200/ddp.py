@@ -124,10 +124,10 @@ class P3DataParallel(_HookedDataParallel):
         timeout_s: float = 120.0,
         trace_cap: int = 0,
         priority_mode: bool = True,
-        drain_bytes: int = 4 << 20,
+        drain_bytes: int | None = None,
         pub_batch_bytes: int = 1 << 20,
         drain_linger_us: int = 200,
-        finish_ctas: int = 0,
+        finish_ctas: int | None = None,
         push_dtype: str = "fp32",
         plan_mode: str = "p3",
         throttle_bps: float = 0.0,
@@ -144,6 +144,13 @@ class P3DataParallel(_HookedDataParallel):
             for l in layers:
                 groups[l] = gi
         self._group_of = groups
+        if drain_bytes is None:
+            # N>1: sync overlaps the backward pass (a DRAIN launch per 4 MB of gradients).
+            # N=1 there is nothing to overlap: no DRAIN launches (the backward keeps every SM)
+            # and one FINISH launch over the whole GPU updates the parameters in priority order
+            drain_bytes = 4 << 20 if self.world > 1 else 1 << 62
+        if finish_ctas is None:
+            finish_ctas = 0 if self.world > 1 else torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
         self.ctx = SyncContext(
             counts, self.world, [self.rank], max_slice=max_slice, lr=lr, momentum=momentum,
             priority_mode=priority_mode, comm_ctas=comm_ctas, comm_threads=comm_threads,
