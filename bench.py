@@ -397,11 +397,12 @@ def run_ours(args):
         out = {
             "metric": METRIC, "value": value, "unit": "samples/sec", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "bf16",
+            "vs_baseline": None, "dtype": "f32",  # the sync path's arithmetic (fp32 sum / SGD / broadcast)
             "data": "synthetic (random-init weights, N(0,1) bf16 images / uniform labels)",
             "config": {"workload": f"{args.model} bf16-autocast training, P3 sliced priority sync",
                        "model": args.model, "per_gpu_batch": batch, "global_batch": batch * world,
                        "max_slice": args.max_slice, "comm_ctas": args.comm_ctas, "parallelism": f"dp{world}",
+                       "model_compute": "bf16 autocast (fp32 master parameters)",
                        "params": P, "tensors": len(counts), "l2": "activations >> 126 MB L2 each step"},
             "e2e": {"value": e2e_value, "unit": "samples/sec", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 4}
                    if e2e_value else None,
