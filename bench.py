@@ -29,7 +29,7 @@ from pathlib import Path
 REPO = Path(__file__).resolve().parent
 sys.path.insert(0, str(REPO))
 
-METRIC = "samples/sec (P3 sliced priority sync, data-parallel training step)"
+METRIC = "samples/sec P3 vs layer-wise sync at 1/2/4/8 B200; slice-sync NVLink GB/s"  # BASELINE.json metric
 DEFAULT_BATCH = {"resnet50": 256, "vgg19": 128, "seq2seq": 128}
 
 
