@@ -662,80 +662,93 @@ __device__ uint32_t warp_server_pick(const CommArgs& a, const LocalDev& L, uint3
     if (avail <= 0 || (a.srv_filter && (blockIdx.x % a.pop_relax) >= a.srv_filter * (uint32_t)avail)) return P3_NONE;
   }
   constexpr uint32_t CH = 8;
-  for (uint32_t group = 0; group < nl; group += 32 * CH) {
-    // candidate layers: an owned slice completed this iteration and not yet claimed
-    uint32_t oc[CH], hv[CH], tk[CH], lo[CH];
+  // A scan is a snapshot: with many consumers the candidates it shows are claimed within
+  // microseconds, and walking a stale list costs a window round trip per dead candidate
+  // (measured: 50 dead candidates, ~50 us per pick, at N=2 for ResNet-50). So each attempt
+  // takes one candidate — the (blockIdx + attempt)-th of the most urgent ones, spreading the
+  // consumers like the pops do — and a miss rescans.
+  for (uint32_t attempt = 0; attempt < 4; ++attempt) {
+    uint32_t ncand = 0, tl = P3_NONE, t_start = 0, t_cnt = 0;
+    for (uint32_t group = 0; group < nl && tl == P3_NONE; group += 32 * CH) {
+      uint32_t oc[CH], hv[CH], tk[CH], lo[CH];
 #pragma unroll
-    for (uint32_t c = 0; c < CH; ++c) {
-      const uint32_t l = group + 32 * c + lane;
-      const bool in = l < nl;
-      oc[c] = in ? lcount[l] : 0u;
-      hv[c] = in ? ld_relaxed_sys(hint + l) : 0u;
-      tk[c] = in ? ld_relaxed_gpu(L.srv_taken + l) : 0u;
-      lo[c] = in ? ld_relaxed_gpu(L.srv_lo + l) : 0u;
-    }
-    uint32_t bits = 0;
-#pragma unroll
-    for (uint32_t c = 0; c < CH; ++c)
-      bits |= (uint32_t)(oc[c] && (int32_t)((hv[c] - k * oc[c]) - tk[c]) > 0) << c;
-    const uint32_t nchunk = min(CH, (nl - group + 31) / 32);
-    for (uint32_t c = 0; c < nchunk; ++c) {
-      uint32_t lm = __ballot_sync(FULL_MASK, (bits >> c) & 1u);
-      uint32_t my_lo = 0, my_oc = 0;
-#pragma unroll
-      for (uint32_t cc = 0; cc < CH; ++cc) {
-        my_lo = cc == c ? lo[cc] : my_lo;
-        my_oc = cc == c ? oc[cc] : my_oc;
+      for (uint32_t c = 0; c < CH; ++c) {
+        const uint32_t l = group + 32 * c + lane;
+        const bool in = l < nl;
+        oc[c] = in ? lcount[l] : 0u;
+        hv[c] = in ? ld_relaxed_sys(hint + l) : 0u;
+        tk[c] = in ? ld_relaxed_gpu(L.srv_taken + l) : 0u;
+        lo[c] = in ? ld_relaxed_gpu(L.srv_lo + l) : 0u;
       }
-      while (lm) {
-        const uint32_t j = __ffs(lm) - 1;
-        const uint32_t l = group + 32 * c + j;
-        lm &= lm - 1;
-        // uniform across the warp (lanes need not run these loads together)
-        const uint32_t cnt = __shfl_sync(FULL_MASK, my_oc, j);
-        const uint32_t start = __shfl_sync(FULL_MASK, my_lo, j);
-        const uint32_t lf = lfirst[l];
-        for (uint32_t i0 = start; i0 < cnt; i0 += 32) {
-          if (dbg && lane == 0) *(volatile uint32_t*)dbg = (8u << 20) | ((l & 0x3ff) << 10) | (i0 & 0x3ff);
-          const uint32_t i = i0 + lane, pos = lf + i;
-          uint32_t g = P3_NONE;
-          bool ok = false, claimed = true;
-          if (i < cnt) {
-            g = P.own_list[pos];
-            claimed = ld_relaxed_gpu(L.claim + pos) != k;
-            ok = !claimed && (int32_t)(ld_relaxed_sys(arrivals + pos) - need) >= 0;
+      uint32_t cnt_c[CH], total = 0;
+#pragma unroll
+      for (uint32_t c = 0; c < CH; ++c) {
+        const bool cand = oc[c] && (int32_t)((hv[c] - k * oc[c]) - tk[c]) > 0 && lo[c] < oc[c];
+        cnt_c[c] = __popc(__ballot_sync(FULL_MASK, cand));
+        total += cnt_c[c];
+        oc[c] = cand ? oc[c] : 0u;  // (reused below as the candidate flag)
+      }
+      if (!total) continue;
+      const uint32_t spread = a.pop_relax > 1 ? min(total, a.pop_relax) : 1u;
+      uint32_t t = (blockIdx.x + attempt) % spread;
+#pragma unroll
+      for (uint32_t c = 0; c < CH; ++c) {
+        const uint32_t m = __ballot_sync(FULL_MASK, oc[c] != 0);
+        if (tl == P3_NONE && t < cnt_c[c]) {
+          uint32_t mm = m;
+          for (uint32_t x = 0; x < t; ++x) mm &= mm - 1;
+          const uint32_t j = __ffs(mm) - 1;
+          tl = group + 32 * c + j;
+          t_cnt = __shfl_sync(FULL_MASK, oc[c], j);
+          t_start = __shfl_sync(FULL_MASK, lo[c], j);
+        } else if (tl == P3_NONE) {
+          t -= cnt_c[c];
+        }
+      }
+      ncand += total;
+    }
+    if (tl == P3_NONE) return P3_NONE;  // nothing completed and unclaimed in the snapshot
+    const uint32_t l = tl, cnt = t_cnt;
+    const uint32_t lf = lfirst[l];
+    for (uint32_t i0 = t_start; i0 < cnt; i0 += 32) {
+      if (dbg && lane == 0) *(volatile uint32_t*)dbg = (8u << 20) | ((l & 0x3ff) << 10) | (i0 & 0x3ff);
+      const uint32_t i = i0 + lane, pos = lf + i;
+      uint32_t g = P3_NONE;
+      bool ok = false, claimed = true;
+      if (i < cnt) {
+        g = P.own_list[pos];
+        claimed = ld_relaxed_gpu(L.claim + pos) != k;
+        ok = !claimed && (int32_t)(ld_relaxed_sys(arrivals + pos) - need) >= 0;
+      }
+      // advance the watermark only contiguously: a window below this one may still
+      // hold an unclaimed slice even if this window is fully claimed
+      if (__all_sync(FULL_MASK, claimed) && lane == 0) atomicCAS(L.srv_lo + l, i0, i0 + 32);
+      uint32_t m = __ballot_sync(FULL_MASK, ok);
+      // first try a CTA-dependent one of the window's ready slices (consumers spread over
+      // them instead of racing for the lowest), then the rest in ascending order
+      int pref = -1;
+      if (m && a.pop_relax > 1) {
+        uint32_t mm = m;
+        for (uint32_t skip = blockIdx.x % __popc(m); skip; --skip) mm &= mm - 1;
+        pref = __ffs(mm) - 1;
+      }
+      for (uint32_t tries = 0; m; ++tries) {
+        const int jj = (tries == 0 && pref >= 0) ? pref : __ffs(m) - 1;
+        m &= ~(1u << jj);
+        const uint32_t gj = __shfl_sync(FULL_MASK, g, jj);
+        const uint32_t pj = lf + i0 + jj;
+        uint32_t won = 0;
+        if (lane == 0) {
+          won = atomicCAS(L.claim + pj, k, k + 1) == k;
+          if (won) {
+            atomicAdd(L.srv_taken + l, 1u);
+            atomicAdd(&L.it->reduced, 1u);
           }
-          // advance the watermark only contiguously: a window below this one may still
-          // hold an unclaimed slice even if this window is fully claimed
-          if (__all_sync(FULL_MASK, claimed) && lane == 0) atomicCAS(L.srv_lo + l, i0, i0 + 32);
-          uint32_t m = __ballot_sync(FULL_MASK, ok);
-          // first try a CTA-dependent one of the window's ready slices (consumers spread
-          // over them instead of racing for the lowest), then the rest in ascending order
-          int pref = -1;
-          if (m && a.pop_relax > 1) {
-            uint32_t mm = m;
-            for (uint32_t skip = blockIdx.x % __popc(m); skip; --skip) mm &= mm - 1;
-            pref = __ffs(mm) - 1;
-          }
-          for (uint32_t attempt = 0; m; ++attempt) {
-            const int jj = (attempt == 0 && pref >= 0) ? pref : __ffs(m) - 1;
-            m &= ~(1u << jj);
-            const uint32_t gj = __shfl_sync(FULL_MASK, g, jj);
-            const uint32_t pj = lf + i0 + jj;
-            uint32_t won = 0;
-            if (lane == 0) {
-              won = atomicCAS(L.claim + pj, k, k + 1) == k;
-              if (won) {
-                atomicAdd(L.srv_taken + l, 1u);
-                atomicAdd(&L.it->reduced, 1u);
-              }
-            }
-            won = __shfl_sync(FULL_MASK, won, 0);
-            if (won) {
-              *layer_out = l;
-              return gj;
-            }
-          }
+        }
+        won = __shfl_sync(FULL_MASK, won, 0);
+        if (won) {
+          *layer_out = l;
+          return gj;
         }
       }
     }
@@ -895,7 +908,7 @@ __device__ uint32_t prepare_push(const CommArgs& a, uint32_t li, uint32_t g, uin
       // the pop read the publication word relaxed: this fence makes it an acquire, so the
       // gradient is visible from here on (ingest released it)
       fence_acq_rel_gpu();
-      if (L.trace_cap) trace_append(L, a.k, l, g - P.layer_first[l], r, P3_EV_PUSH);
+      if (L.trace_cap) trace_append(L, a.k, l, g - P.layer_first[l], a.trace_cta ? blockIdx.x : r, P3_EV_PUSH);
       if (o == r) {
         // the contribution stays in place (published to this rank by the acquire above)
         const uint32_t old = atom_add_relaxed_gpu(a.peers.arrivals[o] + opos, 1u);
@@ -1355,6 +1368,7 @@ __global__ void __launch_bounds__(512, 1) k_comm(const __grid_constant__ CommArg
     if (lane == 0) stash.n = 0;
     __syncwarp();
     bool pending[2] = {false, false};
+    bool pops_done = false;  // FINISH, N > 1: every local slice claimed (see the pop phase)
     for (uint32_t iter = 0;; ++iter) {
       if (phase) *(volatile uint32_t*)phase = (a.k << 24) | (1u << 20) | (iter & 0xfffff);
       const uint64_t tp = globaltimer();
@@ -1405,7 +1419,7 @@ __global__ void __launch_bounds__(512, 1) k_comm(const __grid_constant__ CommArg
             if (lane == 0) atomicAdd(&a.loc[li].it->pushed, 1u);
             kind = JOB_PUSH;
           }
-          for (uint32_t t = 0; t < a.n_local && kind == JOB_NONE; ++t) {
+          for (uint32_t t = 0; t < a.n_local && kind == JOB_NONE && !pops_done; ++t) {
             li = (blockIdx.x + t) % a.n_local;
             g = warp_pop(queue_of(a, a.loc[li]), a.k + 1, phase, 1u, &pp, &stash);
             if (lane == 0) stash_li = li;
@@ -1414,6 +1428,16 @@ __global__ void __launch_bounds__(512, 1) k_comm(const __grid_constant__ CommArg
               if (lane == 0) atomicAdd(&a.loc[li].it->pushed, 1u);
               kind = JOB_PUSH;
             }
+          }
+          if (kind == JOB_NONE && !pops_done && a.mode == P3_COMM_FINISH) {
+            // FINISH runs after every publication of the iteration: once every local slice
+            // is claimed there is nothing left to pop — idle picks then only poll the server
+            // gate (one round trip), so they can poll often
+            uint32_t all = 1;
+            if (lane == 0)
+              for (uint32_t t = 0; t < a.n_local; ++t)
+                all &= ld_relaxed_gpu(&a.loc[t].it->pushed) >= a.plan.total_slices;
+            pops_done = __shfl_sync(FULL_MASK, all, 0) != 0;
           }
         }
       }
@@ -1460,7 +1484,7 @@ __global__ void __launch_bounds__(512, 1) k_comm(const __grid_constant__ CommArg
         }
         verdict = __shfl_sync(FULL_MASK, verdict, 0);
         if (verdict == 0) {
-          backoff = min(2u * backoff + 64u, 4096u);
+          backoff = min(2u * backoff + 64u, pops_done ? 512u : 4096u);
           __nanosleep(backoff);
           continue;
         }

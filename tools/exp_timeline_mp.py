@@ -47,8 +47,9 @@ def main():
         ctx.sync_all(k + 1, 30.0)
         st.synchronize()
         if rank == 0 and k == 3:
-            tr = [r for r in ctx.trace(0) if r.iteration == k]
-            t0 = min(r.t_ns for r in tr)
+            tr_all = [r for r in ctx.trace(0) if r.iteration == k]
+            tr = [r for r in tr_all if r.event in (0, 1)]
+            t0 = min(r.t_ns for r in tr_all)
             push = sorted((r.t_ns - t0) / 1e3 for r in tr if r.event == 0)
             bc = sorted((r.t_ns - t0) / 1e3 for r in tr if r.event == 1)
             per = {}
@@ -57,6 +58,26 @@ def main():
             ends = sorted(max(v) for v in per.values())
             q = lambda a, f: round(a[min(len(a) - 1, int(f * len(a)))], 1) if a else None
             bins = lambda a: [sum(1 for x in a if i * 10 <= x < (i + 1) * 10) for i in range(int(max(a) // 10) + 1)]
+            if os.environ.get("P3_TL_DETAIL"):
+                late = [r for r in tr if r.event == 0 and (r.t_ns - t0) / 1e3 > 60]
+                print("LATE_POPS", len(late), "layers", sorted({r.layer for r in late})[:40], flush=True)
+                for c in sorted(per)[:3]:
+                    seq = sorted((round((r.t_ns - t0) / 1e3, 1), r.event, r.layer, r.slice) for r in tr_all if r.rank == c)
+                    print("CTA", c, seq[:400], flush=True)
+                sig = {}
+                for r in sorted(tr_all, key=lambda r: r.t_ns):
+                    if r.event == 4: sig[r.rank] = r.t_ns
+                    elif r.event == 5 and r.rank in sig: sig.setdefault("d", []).append((r.t_ns - sig.pop(r.rank)) / 1e3)
+                idle = [r for r in tr_all if r.event == 8]
+                if idle:
+                    print("IDLE", len(idle), "first/last us", round((min(r.t_ns for r in idle) - t0) / 1e3, 1),
+                          round((max(r.t_ns for r in idle) - t0) / 1e3, 1), "pushed seen (min,max)",
+                          min(r.layer for r in idle), max(r.layer for r in idle),
+                          "idle with pops left", sum(1 for r in idle if r.layer < 643), flush=True)
+                    c2 = [(round((r.t_ns - t0) / 1e3, 1), r.layer) for r in sorted(idle, key=lambda r: r.t_ns) if r.rank == 2]
+                    print("IDLE_CTA2", c2[:30], flush=True)
+                d = sorted(sig.get("d", []))
+                if d: print("SIGNAL_US", len(d), [round(d[int(f * (len(d) - 1))], 1) for f in (0, .5, .9, .99, 1)], flush=True)
             print(json.dumps({"model": m, "world": world, "kernel_ms": round(s.elapsed_time(e), 4),
                               "pushes": len(push), "bcasts": len(bc),
                               "push_pop_us_q": [q(push, f) for f in (0, .25, .5, .75, 1)],

@@ -68,6 +68,7 @@ def main():
                 jobs = max(dsn["jobs"], 1)
                 stats = {k2: round(dsn[k2] / jobs / 1000, 2) for k2 in ("t_pick_ns", "t_slot_wait_ns", "t_move_ns", "t_signal_ns")}
                 stats["jobs"] = dsn["jobs"]
+                stats["exited"] = dsn["exited"]
                 nvl = 2 * (world - 1) / world * P * 4 / (ms_ * 1e-3) / 1e9 if world > 1 else None
                 hbm = 12 * P / (ms_ * 1e-3) / 1e9 if world == 1 else None
                 rows.append({"extra": extra, "model": m, "world": world, "max_slice": ms, "ctas": ctas, "threads": threads, "ms": round(ms_, 4),
