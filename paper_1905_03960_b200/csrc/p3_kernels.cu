@@ -1419,7 +1419,10 @@ __global__ void __launch_bounds__(512, 1) k_comm(const __grid_constant__ CommArg
             if (lane == 0) atomicAdd(&a.loc[li].it->pushed, 1u);
             kind = JOB_PUSH;
           }
-          for (uint32_t t = 0; t < a.n_local && kind == JOB_NONE && !pops_done; ++t) {
+          // server-reserved CTAs (srv_reserve > 0: every srv_reserve-th CTA) never take pushes,
+          // so a completed slice is reduced while the other CTAs' pipelines hold pushes
+          const bool reserved = a.srv_reserve && (blockIdx.x % a.srv_reserve) == 0;
+          for (uint32_t t = 0; t < a.n_local && kind == JOB_NONE && !pops_done && !reserved; ++t) {
             li = (blockIdx.x + t) % a.n_local;
             g = warp_pop(queue_of(a, a.loc[li]), a.k + 1, phase, 1u, &pp, &stash);
             if (lane == 0) stash_li = li;
