@@ -355,8 +355,8 @@ def run_ours(args):
             model = build(args, rank)
             d = P3DataParallel(model, lr=args.lr, max_slice=args.max_slice, comm_ctas=4, pub_batch_bytes=0,
                                throttle_bps=args.throttle_gbps * 1e9, **kw)
-            ms_t, _ = time_training(args, world, rank, d, x, y, max(3, args.steps // 2), 2)
-            throttled[arm] = max(3, args.steps // 2) * batch * world / (ms_t / 1000.0)
+            ms_t, _ = time_training(args, world, rank, d, x, y, max(5, args.steps), 3)
+            throttled[arm] = max(5, args.steps) * batch * world / (ms_t / 1000.0)
             d.close()
             del d, model
             torch.cuda.empty_cache()
