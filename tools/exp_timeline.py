@@ -28,12 +28,15 @@ def main():
                       trace_cap=1 << 16, **extra)
     st = torch.cuda.Stream()
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    flush2 = torch.zeros(256 << 20, dtype=torch.uint8, device="cuda")
     for l in range(len(counts)):
         ctx.gradgen_layer(0, 7, 0, l, st)
     st.synchronize()
     for k in range(4):
         with torch.cuda.stream(st):
             flush.fill_(k)
+            if os.environ.get("P3_CLEAN_FLUSH"):
+                torch.sum(flush2, dtype=torch.int64)  # read pass: the L2 ends clean
         for l in range(len(counts)):
             ctx.layer_ready(0, l, k, None, st)
         st.synchronize()
