@@ -27,8 +27,8 @@ def main():
         model.load_state_dict(base)
         d = P3DataParallel(model, lr=0.01, comm_ctas=8, pub_batch_bytes=0, timeout_s=300.0, **kw)
         rate = kw.get("throttle_bps", 0)
-        steps = 3 if rate and rate < 50e9 else 6
-        for _ in range(2):
+        steps = 6 if rate and rate < 50e9 else 10
+        for _ in range(3):
             loss_fn(name, d, x, y).backward()
         d.synchronize(); torch.cuda.synchronize()
         if world > 1: dist.barrier()
