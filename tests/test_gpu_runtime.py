@@ -368,3 +368,20 @@ def test_device_prefetcher_ring(cuda):
         got.append((float(x.sum().item()) / x.numel(), int(y.item())))
     assert got == [(float(i), i) for i in range(7)]
     assert feed.h2d_bytes == sum(a.numel() * 4 + 8 for a, _ in host)
+
+
+@pytest.mark.parametrize("model,world,iters", [("resnet50", 4, 2), ("seq2seq", 4, 2), ("vgg19", 2, 1)])
+def test_real_shapes_match_oracle(cuda, model, world, iters):
+    """Full BASELINE shapes (ResNet-50 161 tensors / 25.6M, seq2seq 41 / 34.5M, VGG-19 38 /
+    143.7M parameters): rank-distinct gradients, every rank emulated in one launch, each
+    replica's FNV digest equal to the oracle's replay (bit-exact fp32)."""
+    from paper_1905_03960_b200.model import LayerSpec, ModelProfile
+    from paper_1905_03960_b200.torch_models import real_counts
+
+    counts = real_counts(model)
+    prof = ModelProfile(model, 1905, tuple(LayerSpec(i, f"t{i}", c, 0, 0) for i, c in enumerate(counts)))
+    w = run_emulated(prof, world, iters, distinct=True, comm_ctas=148)
+    got = {f"{w.params_digest(li):016x}" for li in range(world)}
+    w.close()
+    want = f"{O.digest(O.replay_params(counts, 1905, world, iters, 0.1, distinct=True)):016x}"
+    assert got == {want}
