@@ -49,6 +49,34 @@ def main():
             dist.barrier()
             w.close()
 
+    # full ResNet-50 shapes over NVLink, rank-distinct gradients, 148-CTA FINISH launches:
+    # every replica equals the oracle's replay (computed once, on rank 0)
+    sys.path.insert(0, str(REPO / "oracle"))
+    import p3_oracle as O
+    from paper_1905_03960_b200.model import LayerSpec, ModelProfile
+    from paper_1905_03960_b200.torch_models import real_counts
+
+    counts = real_counts("resnet50")
+    prof = ModelProfile("resnet50", 1905, tuple(LayerSpec(i, f"t{i}", c, 0, 0) for i, c in enumerate(counts)))
+    cfg = WorkerConfig(rank=rank, mode="p3", world=world, iterations=2, deadlock_timeout=60.0, emulate_compute=False,
+                       comm_ctas=148, rank_distinct_grads=True)
+    ctx = SyncContext(counts, world, [rank], lr=cfg.lr, comm_ctas=148, timeout_s=60.0, emulate_grads=True)
+    hs = [None] * world
+    dist.all_gather_object(hs, ctx.ipc_handle(0))
+    ctx.open_peers(hs)
+    dist.barrier()
+    w = TrainingWorker(cfg, prof, ranks=[rank], ctx=ctx)
+    try:
+        w.run()
+        got = f"{w.params_digest(0):016x}"
+    except Exception as e:  # noqa: BLE001
+        got = f"error: {e}"
+    ref = [f"{O.digest(O.replay_params(counts, 1905, world, 2, cfg.lr, distinct=True)):016x}" if rank == 0 else None]
+    dist.broadcast_object_list(ref, src=0)
+    out["digests"]["resnet50-real/distinct"] = [got, ref[0]]
+    dist.barrier()
+    w.close()
+
     # the layer-wise baseline (KVStore placement + FIFO) on the same kernels across processes:
     # bit-identical to P3 (SPEC acceptance #3)
     for name in ("toy3", "vgg19-like"):
