@@ -836,9 +836,10 @@ __device__ __forceinline__ void bar_arrive(uint32_t id, uint32_t n) {
 }
 
 // K7 link emulation (TokenBucket.consume, transport.py:42-55) on %globaltimer, one bucket
-// per rank's egress: grant `bytes` at the bucket rate with `burst` of slack, and wait until
-// the grant is admissible. The bucket is a virtual clock V: a grant moves it to
-// max(V, now - burst) + bytes/rate and may start once now >= V' - burst.
+// per rank's egress: take `bytes` tokens at the bucket rate with `burst` of capacity, and
+// wait until they are all taken — the reference's consume() returns at that point. As a
+// virtual clock V (the time the bucket has paid for): a grant moves it to
+// max(V, now - burst) + bytes/rate and may proceed once now >= V'.
 __device__ void pace(const CommArgs& a, const LocalDev& L, uint64_t bytes) {
   if (a.ns_per_byte == 0.f || bytes == 0) return;
   const unsigned long long cost = (unsigned long long)((double)bytes * a.ns_per_byte);
@@ -851,7 +852,7 @@ __device__ void pace(const CommArgs& a, const LocalDev& L, uint64_t bytes) {
     if (old == v) break;
     v = old;
   }
-  while (globaltimer() + a.burst_ns < d) __nanosleep(2000);
+  while (globaltimer() < d) __nanosleep(2000);
 }
 
 // Turn newly published ring entries into publication words (one warp). The ring tail is
