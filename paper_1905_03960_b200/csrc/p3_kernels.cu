@@ -106,6 +106,18 @@ __device__ __forceinline__ void tma_load_1d(void* sdst, const void* gsrc, uint32
                "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
                : "memory");
 }
+// TMA bulk store shared -> global (any global address: a peer's memory over NVLink too)
+__device__ __forceinline__ void tma_store_1d(void* gdst, const void* ssrc, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(smem_u32(ssrc)),
+               "r"(bytes)
+               : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void tma_store_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void tma_store_wait_all() {
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
 __device__ __forceinline__ uint64_t globaltimer() {
   uint64_t t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -1647,11 +1659,21 @@ __global__ void __launch_bounds__(512, 1) k_comm(const __grid_constant__ CommArg
       if (d.flags & ST_EXIT) break;
       const uint64_t tm = tid == 0 ? globaltimer() : 0;
       const Job& j = slots[d.b];
-      if (d.flags & ST_DIRECT) {
+      const bool bulk_push = a.tma_store && j.kind == JOB_PUSH && !j.bf16 && !(d.flags & ST_DIRECT);
+      if (bulk_push) {
+        // the staged gradient tile goes out as one TMA bulk store (over NVLink to the
+        // owner's receive slot); the stage is released once the engine has read it
+        if (tid == 0) {
+          tma_store_1d(j.dst[0] + d.e0, stage_mem + (size_t)sidx * P3_STAGE_BYTES, d.n * 4u);
+          tma_store_wait_read();
+        }
+      } else if (d.flags & ST_DIRECT) {
         move_range(a, j, d.e0, d.n, &rptrs, tid, ncons);
       } else {
         consume_tile(a, j, d, stage_mem + (size_t)sidx * P3_STAGE_BYTES, tid, ncons);
       }
+      if ((d.flags & ST_LAST) && tid == 0 && a.tma_store && j.kind == JOB_PUSH)
+        tma_store_wait_all();  // every bulk store of the job complete before its signal
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty_bar[sidx]);
       if (tid == 0) t_move += globaltimer() - tm;
