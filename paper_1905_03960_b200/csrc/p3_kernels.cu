@@ -1188,7 +1188,7 @@ __device__ __forceinline__ bool job_tma_ok(const Job& j) {
 template <int NW, bool BF, bool MOM>
 __device__ __forceinline__ void consume_reduce(const uint8_t* st, uint32_t pitch, uint32_t n4, uint32_t e4,
                                                float* const* dstp, float* vp, int own, const UpdCoef& c,
-                                               uint32_t tid, uint32_t nthr) {
+                                               uint32_t tid, uint32_t nthr, bool tosmem = false) {
   float4* dst[NW];
 #pragma unroll
   for (int q = 0; q < NW; ++q) dst[q] = reinterpret_cast<float4*>(dstp[q]) + e4;
@@ -1215,6 +1215,11 @@ __device__ __forceinline__ void consume_reduce(const uint8_t* st, uint32_t pitch
     }
     float4 vv = MOM ? tv[k] : make_float4(0.f, 0.f, 0.f, 0.f);
     const float4 r = sgd4(tp[k], acc, c, MOM ? &vv : nullptr);
+    if (tosmem) {  // results back into the stage (p and v tiles), stored by TMA afterwards
+      const_cast<float4*>(tp)[k] = r;
+      if (MOM) const_cast<float4*>(tv)[k] = vv;
+      continue;
+    }
     if (MOM) v[k] = vv;
 #pragma unroll
     for (int q = 0; q < NW; ++q) dst[q][k] = r;
@@ -1222,7 +1227,7 @@ __device__ __forceinline__ void consume_reduce(const uint8_t* st, uint32_t pitch
 }
 
 __device__ void consume_tile(const CommArgs& a, const Job& j, const StageDesc& d, const uint8_t* st, uint32_t tid,
-                             uint32_t nthr) {
+                             uint32_t nthr, bool tosmem = false) {
   const uint32_t n4 = d.n / 4, e4 = d.e0 / 4, pitch = d.tile * 4;
   if (j.kind == JOB_PUSH) {
     const float4* t0 = reinterpret_cast<const float4*>(st);
@@ -1244,11 +1249,11 @@ __device__ void consume_tile(const CommArgs& a, const Job& j, const StageDesc& d
 #define P3_CONSUME(K)                                                                                   \
   case K:                                                                                               \
     if (bf) {                                                                                           \
-      if (mom) consume_reduce<K, true, true>(st, pitch, n4, e4, dst, v, own, c, tid, nthr);             \
-      else consume_reduce<K, true, false>(st, pitch, n4, e4, dst, v, own, c, tid, nthr);                \
+      if (mom) consume_reduce<K, true, true>(st, pitch, n4, e4, dst, v, own, c, tid, nthr, tosmem);     \
+      else consume_reduce<K, true, false>(st, pitch, n4, e4, dst, v, own, c, tid, nthr, tosmem);        \
     } else {                                                                                            \
-      if (mom) consume_reduce<K, false, true>(st, pitch, n4, e4, dst, v, own, c, tid, nthr);            \
-      else consume_reduce<K, false, false>(st, pitch, n4, e4, dst, v, own, c, tid, nthr);               \
+      if (mom) consume_reduce<K, false, true>(st, pitch, n4, e4, dst, v, own, c, tid, nthr, tosmem);    \
+      else consume_reduce<K, false, false>(st, pitch, n4, e4, dst, v, own, c, tid, nthr, tosmem);       \
     }                                                                                                   \
     return;
   switch (N) {
@@ -1669,10 +1674,23 @@ __global__ void __launch_bounds__(512, 1) k_comm(const __grid_constant__ CommArg
         }
       } else if (d.flags & ST_DIRECT) {
         move_range(a, j, d.e0, d.n, &rptrs, tid, ncons);
+      } else if (a.tma_store_red && j.kind == JOB_REDUCE && j.n <= 8) {
+        // results go back into the stage, then one TMA bulk store per replica (and the
+        // momentum) — NVLink for the remote ones
+        uint8_t* st = stage_mem + (size_t)sidx * P3_STAGE_BYTES;
+        consume_tile(a, j, d, st, tid, ncons, true);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        bar_sync(BAR_RANGE, ncons);
+        if (tid == 0) {
+          const uint32_t pitch = d.tile * 4;
+          for (uint32_t q = 0; q < j.n; ++q) tma_store_1d(j.dst[q] + d.e0, st + j.n * pitch, d.n * 4u);
+          if (j.v) tma_store_1d(j.v + d.e0, st + (j.n + 1) * pitch, d.n * 4u);
+          tma_store_wait_read();
+        }
       } else {
         consume_tile(a, j, d, stage_mem + (size_t)sidx * P3_STAGE_BYTES, tid, ncons);
       }
-      if ((d.flags & ST_LAST) && tid == 0 && a.tma_store && j.kind == JOB_PUSH)
+      if ((d.flags & ST_LAST) && tid == 0 && (a.tma_store || a.tma_store_red))
         tma_store_wait_all();  // every bulk store of the job complete before its signal
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty_bar[sidx]);
