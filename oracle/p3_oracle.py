@@ -165,6 +165,25 @@ def replay_params(counts: list[int], seed: int, world: int, iterations: int, lr:
     return params
 
 
+def replay_params_momentum(counts: list[int], seed: int, world: int, iterations: int, lr: float, mu: float,
+                           distinct: bool = True) -> list[np.ndarray]:
+    """replay_params with heavy-ball momentum (extension; the reference has plain SGD):
+    g = rank-ordered fp32 sum / N; v = fp32(mu * v) + g; p = p - fp32(lr * v) — each
+    operation rounded to fp32 separately, as the kernel does (no FMA)."""
+    params = [np.zeros(c, dtype=np.float32) for c in counts]
+    vel = [np.zeros(c, dtype=np.float32) for c in counts]
+    n, lr32, mu32 = np.float32(world), np.float32(lr), np.float32(mu)
+    for k in range(iterations):
+        for layer, c in enumerate(counts):
+            acc = np.zeros(c, dtype=np.float32)
+            for r in range(world):
+                acc = acc + grad_block(rank_seed(seed, r, distinct), k, layer, 0, c)
+            g = acc / n
+            vel[layer] = mu32 * vel[layer] + g
+            params[layer] = params[layer] - lr32 * vel[layer]
+    return params
+
+
 def to_bf16(x: np.ndarray) -> np.ndarray:
     """fp32 -> bf16 -> fp32, round to nearest even (finite inputs): the declared lossy
     transport of the B200 path (not in the reference)."""
