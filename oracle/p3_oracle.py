@@ -166,8 +166,9 @@ def replay_params(counts: list[int], seed: int, world: int, iterations: int, lr:
 
 
 def replay_params_momentum(counts: list[int], seed: int, world: int, iterations: int, lr: float, mu: float,
-                           distinct: bool = True) -> list[np.ndarray]:
-    """replay_params with heavy-ball momentum (extension; the reference has plain SGD):
+                           distinct: bool = True, bf16: bool = False) -> list[np.ndarray]:
+    """replay_params with heavy-ball momentum (extension; the reference has plain SGD; with
+    ``bf16`` every contribution rounded to bf16 first, the declared bf16 push transport):
     g = rank-ordered fp32 sum / N; v = fp32(mu * v) + g; p = p - fp32(lr * v) — each
     operation rounded to fp32 separately, as the kernel does (no FMA)."""
     params = [np.zeros(c, dtype=np.float32) for c in counts]
@@ -177,7 +178,8 @@ def replay_params_momentum(counts: list[int], seed: int, world: int, iterations:
         for layer, c in enumerate(counts):
             acc = np.zeros(c, dtype=np.float32)
             for r in range(world):
-                acc = acc + grad_block(rank_seed(seed, r, distinct), k, layer, 0, c)
+                gr = grad_block(rank_seed(seed, r, distinct), k, layer, 0, c)
+                acc = acc + (to_bf16(gr) if bf16 else gr)
             g = acc / n
             vel[layer] = mu32 * vel[layer] + g
             params[layer] = params[layer] - lr32 * vel[layer]

@@ -431,8 +431,8 @@ def test_frame_queue_api(cuda):
         q.put_batch(frames(0)[:1] if len(frames(0)) > 1 else frames(0) + frames(1))
 
 
-@pytest.mark.parametrize("world", [2, 3, 4])
-def test_momentum_multi_rank_matches_oracle(cuda, world):
+@pytest.mark.parametrize("world,push", [(2, "fp32"), (3, "fp32"), (4, "fp32"), (2, "bf16"), (4, "bf16")])
+def test_momentum_multi_rank_matches_oracle(cuda, world, push):
     """Fused momentum at N>1 (owned-slot momentum buffers, TMA-staged v tiles), rank-distinct
     gradients, against the oracle's separately rounded fp32 restatement."""
     from paper_1905_03960_b200.model import builtin_profile
@@ -443,10 +443,10 @@ def test_momentum_multi_rank_matches_oracle(cuda, world):
     cfg = WorkerConfig(rank=0, mode="p3", world=world, iterations=iters, lr=lr, deadlock_timeout=30.0,
                        emulate_compute=False, comm_ctas=16, rank_distinct_grads=True)
     ctx = SyncContext(prof.param_counts(), world, list(range(world)), lr=lr, momentum=mu, comm_ctas=16,
-                      timeout_s=30.0, emulate_grads=True)
+                      timeout_s=30.0, emulate_grads=True, push_dtype=push)
     w = TrainingWorker(cfg, prof, ranks=list(range(world)), ctx=ctx)
     w.run()
     got = {f"{w.params_digest(li):016x}" for li in range(world)}
     w.close()
-    want = f"{O.digest(O.replay_params_momentum(prof.param_counts(), prof.seed, world, iters, lr, mu)):016x}"
+    want = f"{O.digest(O.replay_params_momentum(prof.param_counts(), prof.seed, world, iters, lr, mu, bf16=push == 'bf16')):016x}"
     assert got == {want}
