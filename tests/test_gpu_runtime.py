@@ -450,3 +450,18 @@ def test_momentum_multi_rank_matches_oracle(cuda, world, push):
     w.close()
     want = f"{O.digest(O.replay_params_momentum(prof.param_counts(), prof.seed, world, iters, lr, mu, bf16=push == 'bf16')):016x}"
     assert got == {want}
+
+
+@pytest.mark.parametrize("knob", ["P3_TMA=0", "P3_TMA_STORE=0", "P3_TMA_STORE_RED=1"])
+def test_alternative_mover_paths(cuda, golden, knob, monkeypatch):
+    """The experiment switches keep the results: direct loads instead of the TMA ring,
+    consumer stores instead of bulk stores for pushes, bulk stores for reduce results."""
+    from paper_1905_03960_b200.model import builtin_profile
+
+    name, val = knob.split("=")
+    monkeypatch.setenv(name, val)  # read once at context creation
+    want = {(d[0], d[1]): d[5] for d in golden["digests"] if d[4] == "distinct"}
+    w = run_emulated(builtin_profile("resnet50-like"), 2, 4, distinct=True)
+    digests = {f"{w.params_digest(li):016x}" for li in range(2)}
+    w.close()
+    assert digests == {want[("resnet50-like", 2)]}
