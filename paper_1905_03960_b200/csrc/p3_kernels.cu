@@ -25,6 +25,24 @@ namespace p3 {
 #define FULL_MASK 0xffffffffu
 #define P3_NONE 0xffffffffu
 
+// Protocol invariants, compiled in for the checked build (libp3_checked.so, -DP3_CHECKS):
+// a violated one prints where and traps, so the host sees a launch failure instead of wrong
+// values (compute-sanitizer is not available on the GPU pool).
+#ifdef P3_CHECKS
+#define P3_CHECK(cond)                                                                                  \
+  do {                                                                                                 \
+    if (!(cond)) {                                                                                     \
+      printf("P3_CHECK failed: %s (%s:%d) block %d thread %d\n", #cond, __FILE__, __LINE__, blockIdx.x, \
+             threadIdx.x);                                                                             \
+      __trap();                                                                                        \
+    }                                                                                                  \
+  } while (0)
+#else
+#define P3_CHECK(cond) \
+  do {                 \
+  } while (0)
+#endif
+
 // ------------------------------------------------------------------ PTX helpers
 
 __device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
@@ -925,6 +943,7 @@ __device__ uint32_t prepare_push(const CommArgs& a, uint32_t li, uint32_t g, uin
       if (o == r) {
         // the contribution stays in place (published to this rank by the acquire above)
         const uint32_t old = atom_add_relaxed_gpu(a.peers.arrivals[o] + opos, 1u);
+        P3_CHECK(old >= a.k * P.world && old < (a.k + 1) * P.world);
         red_add_relaxed_sys(a.peers.tally[o], 1u);
         if (old + 1 == (a.k + 1) * P.world) {  // the last arrival: the slice is complete
           red_add_relaxed_sys(a.peers.hint[o] + l, 1u);
@@ -942,6 +961,7 @@ __device__ uint32_t prepare_push(const CommArgs& a, uint32_t li, uint32_t g, uin
   if (lane == 0) {
     job->kind = JOB_PUSH;
     job->run = 1;
+    job->n = 1;  // one source (the slot keeps no stale rank count from a previous reduce)
     job->li = li;
     job->g = g;
     job->layer = l;
@@ -1300,6 +1320,7 @@ __device__ void signal_job(const CommArgs& a, const Job& j) {
   if (j.kind == JOB_PUSH) {
     // the last arriver completes the slice and tells the owner's scheduler (hint)
     const uint32_t old = atom_add_relaxed_sys(a.peers.arrivals[j.rank] + j.opos, 1u);
+    P3_CHECK(old >= a.k * P.world && old < (a.k + 1) * P.world);  // one push per rank and slice
     red_add_relaxed_sys(a.peers.tally[j.rank], 1u);
     if (old + 1 == (a.k + 1) * P.world) {
       red_add_relaxed_sys(a.peers.hint[j.rank] + j.layer, 1u);
@@ -1513,6 +1534,12 @@ __global__ void __launch_bounds__(512, 1) k_comm(const __grid_constant__ CommArg
       }
       backoff = 0;
       idle_since = 0;
+      if (lane == 0 && (kind == JOB_PUSH || kind == JOB_REDUCE)) {
+        P3_CHECK(g < a.plan.total_slices && pp.layer < a.plan.n_layers);
+        P3_CHECK(a.plan.slice_layer[g] == pp.layer);  // the pop's layer is the slice's layer
+        P3_CHECK(pp.run >= 1 && g + pp.run <= a.plan.layer_first[pp.layer] + a.plan.layer_nslices[pp.layer]);
+        P3_CHECK(kind == JOB_PUSH || a.plan.slice_owner[g] == a.loc[li].rank);  // reduce only what it owns
+      }
       if (kind == JOB_PUSH) {
         const uint32_t how = prepare_push(a, li, g, pp.layer, pp.word, nullptr);
         if (how == PUSH_DONE) continue;  // own slice, still waiting for peers: counted in place
@@ -1604,8 +1631,10 @@ __global__ void __launch_bounds__(512, 1) k_comm(const __grid_constant__ CommArg
           const bool tma = a.use_tma && job_tma_ok(j);
           const uint32_t tile = job_tile(j), main = tma ? (len & ~7u) : 0u;
           const uint32_t nsrc = job_sources(j);
+          P3_CHECK(j.n >= 1 && j.n <= P3_MAX_RANKS && len > 0);
           for (uint32_t e0 = 0; e0 < main; e0 += tile) {
             const uint32_t n = min(tile, main - e0);
+            P3_CHECK(n > 0 && n <= tile && (n & 7u) == 0);
             next_stage(sidx);
             StageDesc& d = sdesc[sidx];
             d.b = b;
@@ -1662,6 +1691,7 @@ __global__ void __launch_bounds__(512, 1) k_comm(const __grid_constant__ CommArg
       mbar_wait_bounded(&full_bar[sidx], (it / P3_STAGES) & 1u, a);
       const StageDesc d = sdesc[sidx];
       if (d.flags & ST_EXIT) break;
+      P3_CHECK(d.b < 2);
       const uint64_t tm = tid == 0 ? globaltimer() : 0;
       const Job& j = slots[d.b];
       const bool bulk_push = a.tma_store && j.kind == JOB_PUSH && !j.bf16 && !(d.flags & ST_DIRECT);
