@@ -2,7 +2,8 @@
 //
 //   K1 k_gradgen       gradient_block / _materialize          hashing.py:55-63, worker.py:166-171
 //   K4 k_shard_update  ShardState.aggregate_and_update        server.py:55-68
-//   K3 k_comm          persistent per-iteration comm kernel:
+//   K3 k_comm          the comm kernel (DRAIN launches during the backward pass, one FINISH
+//                      launch per iteration), warp-specialised, TMA-staged:
 //        worker role   FrameQueue.poll + _priority_sender     queues.py:52-62, worker.py:184-190
 //        server role   ShardState.on_push/aggregate/bcast     server.py:36-88, 208-226
 //        apply role    on_bcast -> flags[layer]               worker.py:241-269 (remote stores +
@@ -10,7 +11,8 @@
 //   k_queue_pop        one FrameQueue.poll on the device queue (scripted tick replay)
 //   k_sleep            TrainingWorker._emulate                worker.py:299-310
 //
-// All traffic is bandwidth-bound streaming: 16-byte vector loads/stores, no tensor cores.
+// All traffic is bandwidth-bound streaming (TMA bulk copies through shared memory, 16-byte
+// vector stores), no tensor cores.
 // Floating point follows the reference's numpy fp32 semantics exactly: the sum is taken in
 // ascending rank order starting from +0.0, then divided by N, then p - lr*g with the multiply
 // and the subtract rounded separately (explicit _rn intrinsics: no FMA contraction).
@@ -837,7 +839,7 @@ __device__ __forceinline__ QueueView queue_of(const CommArgs& a, const LocalDev&
   return q;
 }
 
-// One job handed from the scheduler warp to the mover warps of a CTA.
+// One job handed from the scheduler warp to the producer / consumer warps of a CTA.
 #define JOB_NONE 0
 #define JOB_REDUCE 1
 #define JOB_PUSH 2
@@ -851,8 +853,8 @@ struct Job {
 };
 
 // Named barriers (0 is __syncthreads), per job slot b:
-//   FULL(b)  scheduler arrives, signaler + movers sync      (slot b holds a job)
-//   DONE(b)  movers arrive, signaler syncs                  (the job's data has moved)
+//   FULL(b)  scheduler arrives, producer + signaler sync    (slot b holds a job)
+//   DONE(b)  consumers arrive, signaler syncs               (the job's data has moved)
 //   EMPTY(b) signaler arrives, scheduler syncs              (slot b may be refilled)
 #define BAR_FULL(b) (1 + (b))
 #define BAR_DONE(b) (3 + (b))
@@ -916,10 +918,10 @@ __device__ void ingest(const LocalDev& L, uint32_t sched) {
 }
 
 // Scheduler side of a push. With job == nullptr, classify the popped slice: a remote
-// owner needs the movers (PUSH_REMOTE); for a local owner the contribution stays in place
+// owner needs a push job (PUSH_REMOTE); for a local owner the contribution stays in place
 // and only the arrival is counted here — and when that arrival completes the slice the
 // scheduler claims its reduction at once (PUSH_REDUCE) instead of leaving it to a later
-// server pick. With a slot: fill it for the movers, who store the slice into the owner's
+// server pick. With a slot: fill it for the producer / consumers, who store the slice into the owner's
 // receive slot over NVLink.
 #define PUSH_DONE 0
 #define PUSH_REMOTE 1
@@ -1307,14 +1309,14 @@ __device__ void consume_tile(const CommArgs& a, const Job& j, const StageDesc& d
   }
 }
 
-// Signaler (one thread, after the movers' barrier): publish the job's completion with
+// Signaler (one thread, after the consumers' barrier): publish the job's completion with
 // release semantics at system scope when a peer lives on another GPU. Push: count the
 // arrival at the owner (and the owner's layer hint when it completes the slice). Reduce:
 // bump every replica's done[layer] (the forward gate, worker.py:262-269).
 __device__ void signal_job(const CommArgs& a, const Job& j) {
   const PlanDev& P = a.plan;
   const LocalDev& L = a.loc[j.li];
-  // one fence releases every store the movers made (ordered before it by the DONE barrier);
+  // one fence releases every store the consumers made (ordered before it by the DONE barrier);
   // the counter updates after it are plain relaxed reductions (fire and forget)
   if (a.remote) fence_acq_rel_sys(); else fence_acq_rel_gpu();
   if (j.kind == JOB_PUSH) {
@@ -1362,13 +1364,15 @@ __device__ uint32_t take_stash(Stash* st, Popped* out) {
   return g;
 }
 
-// Comm kernel. Warp 0 of every CTA is the scheduler, warp 1 the signaler, warps 2.. the
-// movers; two job slots in shared memory.
+// Comm kernel. Warp 0 of every CTA is the scheduler, warp 1 the signaler, warp 2 the TMA
+// producer, warps 3.. the consumers; two job slots and a 3-stage ring in shared memory.
 //   scheduler: pick the next job — server work first (a reduced slice unblocks the next
 //   forward pass), then the most urgent published slice of the local worker queues — and
-//   prepare its pointers while the movers still run the previous job;
-//   movers: move the data of the job in the current slot, then go straight to the next;
-//   signaler: once the movers are done with a slot, fence and publish the completion
+//   prepare its pointers while the previous job is still moving;
+//   producer: cut the job into tiles and stream its sources into the ring (cp.async.bulk),
+//   running ahead into the next job;
+//   consumers: compute / store each staged tile (push tiles leave as TMA bulk stores);
+//   signaler: once a job's last tile is done, fence and publish the completion
 //   (arrival / done counters), then release the slot to the scheduler.
 // The queue is re-read for every pick, so a layer published while the kernel runs
 // preempts less urgent slices at slice granularity. DRAIN launches (one per published
@@ -1733,7 +1737,7 @@ __global__ void __launch_bounds__(512, 1) k_comm(const __grid_constant__ CommArg
 
 // With lazy module loading (CUDA_MODULE_LOADING=LAZY, the CUDA 12 default) the first launch
 // of a kernel loads it, and loading waits for the kernels already running on the device.
-// A persistent comm kernel waits for work of the compute streams, so every kernel those
+// A comm kernel that waited for work of the compute streams would block them, so every kernel those
 // streams may launch must be loaded before the comm kernel starts: query them all here.
 int preload_kernels() {
   if (cudaFuncSetAttribute(k_comm, cudaFuncAttributeMaxDynamicSharedMemorySize, P3_STAGES * P3_STAGE_BYTES) !=
