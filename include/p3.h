@@ -113,7 +113,7 @@ int p3_emulate_compute(uint64_t duration_us, void* stream);
 
 /* The device slice queue driven one operation at a time (FrameQueue, queues.py:20-75).
  * Used for tick-replay parity against the reference simulator; the same __device__ pop
- * routine runs inside the persistent comm kernel. */
+ * routine runs inside the comm kernel. */
 typedef struct p3_queue p3_queue_t;
 int p3_queue_create(const uint32_t* layer_nslices, uint32_t n_layers, uint32_t sched,
                     p3_queue_t** out);
@@ -182,8 +182,9 @@ typedef struct p3_config {
   uint32_t sched;                      /* P3_SCHED_PRIORITY (p3) or P3_SCHED_FIFO */
   float lr;                            /* RunConfig.lr (cli.py:69) */
   float momentum;                      /* 0 == the reference's plain SGD */
-  uint32_t comm_ctas;                  /* CTAs of the persistent comm kernel */
-  uint32_t comm_threads;               /* threads per comm CTA (multiple of 32) */
+  uint32_t comm_ctas;                  /* CTAs of each DRAIN launch of the comm kernel */
+  uint32_t comm_threads;               /* threads per comm CTA (multiple of 32 in [128, 512]:
+                                          scheduler, signaler, TMA producer, consumers) */
   double timeout_s;                    /* device spin deadline (deadlock_timeout) */
   uint32_t trace_cap;                  /* trace records per local rank (0 = off) */
   uint32_t emulate_grads;              /* allocate a gradient arena for gradgen mode */
@@ -296,7 +297,7 @@ int p3_counters(p3_ctx_t* ctx, uint32_t local_idx, uint64_t* bytes_in, uint64_t*
 /* Diagnostics snapshot of a local rank (deadlock dumps, worker.py:291-297): 5 arrays of
  * n_layers u32 — ready tag, claim cursor, server claims, completed-hint, done counter —
  * then the per-iteration counters (pushed, reduced, exited CTAs, jobs; then 4 u64 ns totals:
- * scheduler pick, scheduler slot wait, movers, signaler), the last phase word of the
+ * scheduler pick, scheduler slot wait, consumers, signaler), the last phase word of the
  * first 512 comm CTAs, and per slice the arrival counter and server claim tag. Copied on a private stream (never blocks on the
  * compute or comm streams). */
 int p3_debug_snapshot(p3_ctx_t* ctx, uint32_t local_idx, uint32_t* out, uint64_t cap,
