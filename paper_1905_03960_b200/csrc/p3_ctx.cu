@@ -113,7 +113,7 @@ struct p3_ctx {
   // P3_TMA=0 (direct loads instead of the TMA stage ring), P3_PUSH_SPLIT=n, P3_SRV_FILTER=n,
   // P3_TRACE_CTA=1 (trace records carry CTA indices; CTA start / exit records)
   struct {
-    uint32_t use_tma = 1, push_split = 0, srv_filter = 0, trace_cta = 0, srv_reserve = 0, tma_store = 1, tma_store_red = 0;
+    uint32_t use_tma = 1, push_split = 0, srv_filter = 0, trace_cta = 0, srv_reserve = 0, tma_store = 1, tma_store_red = 0, pop_relax = 0;
   } knobs;
   std::vector<uint32_t> own_total;
   std::vector<uint64_t> own_stride;
@@ -301,6 +301,7 @@ int p3_ctx_create(const p3_config_t* cfg, p3_ctx_t** out) {
     c->knobs.trace_cta = getenv("P3_TRACE_CTA") != nullptr;
     c->knobs.srv_reserve = env_u32("P3_SRV_RESERVE", 0);
     c->knobs.tma_store = env_u32("P3_TMA_STORE", 1);
+    c->knobs.pop_relax = env_u32("P3_POP_RELAX", 0);  // 0: the config's
     c->knobs.tma_store_red = env_u32("P3_TMA_STORE_RED", 0);
   }
   std::string perr;
@@ -638,7 +639,8 @@ static CommArgs comm_args(p3_ctx* c, uint32_t mode, uint32_t ctas) {
   // the launch's concurrent consumers (its CTAs) unless configured lower
   // (measured, tools/sync_sweep.py, ResNet-50 N=1 sync-only: C=8 2.2 TB/s, C=148 3.4 TB/s —
   // 148 schedulers racing for the same few one-slice layers lose an atomic round trip per try)
-  a.pop_relax = std::min<uint32_t>(ctas, c->cfg.pop_relax ? c->cfg.pop_relax : ctas);
+  const uint32_t relax_cfg = c->knobs.pop_relax ? c->knobs.pop_relax : c->cfg.pop_relax;
+  a.pop_relax = std::min<uint32_t>(ctas, relax_cfg ? relax_cfg : ctas);
   if (c->cfg.throttle_bps > 0) {
     a.ns_per_byte = (float)(8e9 / c->cfg.throttle_bps);
     a.burst_ns = (unsigned long long)((double)c->cfg.throttle_burst * 8e9 / c->cfg.throttle_bps);
