@@ -131,3 +131,12 @@ def test_graft_entry_importable():
     import py_compile
 
     py_compile.compile(str(HEADER.parents[1] / "bench.py"), doraise=True)
+
+
+def test_tools_parse():
+    """The measurement tools behind DESIGN.md / profiles/ stay syntactically valid."""
+    import ast
+    from pathlib import Path
+
+    for f in sorted((Path(__file__).resolve().parents[1] / "tools").glob("*.py")):
+        ast.parse(f.read_text(), filename=str(f))
