@@ -274,9 +274,9 @@ int p3_ctx_create(const p3_config_t* cfg, p3_ctx_t** out) {
   if (cfg->n_layers < 1 || !cfg->layer_counts) return fail(nullptr, P3_EUSAGE, "profile needs at least one layer");
   if (cfg->plan_mode != P3_PLAN_P3 && cfg->plan_mode != P3_PLAN_BASELINE) return fail(nullptr, P3_EUSAGE, "bad plan_mode");
   if (cfg->throttle_bps < 0) return fail(nullptr, P3_EUSAGE, "throttle rate must be >= 0 (0 disables shaping)");
-  if (cfg->comm_threads < 128 || cfg->comm_threads > 512 || cfg->comm_threads % 32)
+  if (cfg->comm_threads < 128 || cfg->comm_threads > P3_COMM_MAX_THREADS || cfg->comm_threads % 32)
     return fail(nullptr, P3_EUSAGE,
-                "comm_threads must be a multiple of 32 in [128, 512] (scheduler + signaler + producer + consumer warps)");
+                "comm_threads must be a multiple of 32 in [128, " + std::to_string(P3_COMM_MAX_THREADS) + "] (scheduler + signaler + producer + consumer warps)");
   if (cfg->comm_ctas < 1) return fail(nullptr, P3_EUSAGE, "comm_ctas must be >= 1");
   for (uint32_t i = 0; i < cfg->n_local; ++i)
     if (cfg->local_ranks[i] >= cfg->world) return fail(nullptr, P3_EUSAGE, "local rank out of range");

@@ -8,6 +8,9 @@
 
 #include "../../include/p3.h"
 
+#ifndef P3_COMM_MAX_THREADS
+#define P3_COMM_MAX_THREADS 512  // comm CTA size bound (launch bounds: 126 registers at 512)
+#endif
 #define P3_MAX_LOCAL 8      // ranks one process hosts (1 per GPU; up to 8 when emulating)
 #define P3_SIDE_STREAMS 4   // comm streams DRAIN launches rotate over
 #define P3_DBG_CTAS 512

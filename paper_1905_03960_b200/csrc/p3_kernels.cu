@@ -1380,7 +1380,7 @@ __device__ uint32_t take_stash(Stash* st, Popped* out) {
 // gradients would hold SMs that the compute producing them may need (co-residency-bound
 // library kernels, lazy module loading). The FINISH launch of an iteration ends once every
 // local slice is pushed and every owned slice reduced; it waits only for peers' pushes.
-__global__ void __launch_bounds__(512, 1) k_comm(const __grid_constant__ CommArgs a) {
+__global__ void __launch_bounds__(P3_COMM_MAX_THREADS, 1) k_comm(const __grid_constant__ CommArgs a) {
   __shared__ Job slots[2];  // double-buffered: the scheduler fills one while the other is moved
   __shared__ StageDesc sdesc[P3_STAGES];
   __shared__ __align__(8) uint64_t full_bar[P3_STAGES], empty_bar[P3_STAGES];
