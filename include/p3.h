@@ -46,9 +46,20 @@ extern "C" {
 /* Maximum ranks (workers == servers) in one NVSwitch domain handled by one context. */
 #define P3_MAX_RANKS 16
 
-/* Trace events (the Frame msg types that cross the link, proto.py:26-32). */
-#define P3_EV_PUSH 0  /* worker popped a slice and stored it into the owner's slot */
-#define P3_EV_BCAST 1 /* owner reduced + updated a slice and broadcast it */
+/* Trace events. PUSH / BCAST are the Frame msg types that cross the link (proto.py:26-32);
+ * PUBLISH, COMPLETE and PICK record the queue operations around them, so a live run can be
+ * replayed through FrameQueue (queues.py:44-62): PUBLISH = put_batch of a layer (worker.py:
+ * 173-182), PUSH = the sender's poll (worker.py:184-190), COMPLETE = the last on_push of a
+ * slice (server.py:36-53), PICK = the server consumer's poll of a complete slice
+ * (server.py:208-226). */
+#define P3_EV_PUSH 0     /* worker popped a slice (claim) and stored it into the owner's slot;
+                            t0_ns = start of the pop's queue snapshot, t_ns = after the claim */
+#define P3_EV_BCAST 1    /* owner reduced + updated a slice and broadcast it */
+#define P3_EV_PUBLISH 2  /* a layer's publication word became visible to the pops (ingest);
+                            slice = the publish sequence number (FIFO key) */
+#define P3_EV_COMPLETE 3 /* the last push of an owned slice arrived; rank = owner */
+#define P3_EV_PICK 4     /* owner claimed a complete slice for reduce + broadcast; t0_ns = start
+                            of the pick's scan, t_ns = after the claim */
 
 /* One row of a SlicePlan (plan.py:30-45: SliceKey + Slice). */
 typedef struct p3_slice {
@@ -63,6 +74,8 @@ typedef struct p3_slice {
 /* One device trace record; the wire header fields of proto.py:20-21 minus the codec. */
 typedef struct p3_trace_rec {
   uint64_t t_ns;      /* %globaltimer at the event */
+  uint64_t t0_ns;     /* PUSH / PICK: %globaltimer before the queue snapshot the claim came
+                         from (0 for other events) */
   uint32_t iteration; /* Frame.iteration */
   uint32_t layer;     /* Frame.layer_index (== priority) */
   uint32_t slice;     /* Frame.slice_index */
@@ -214,6 +227,10 @@ typedef struct p3_config {
   const uint32_t* gate_groups;         /* optional per-layer forward-gate group id (layers of
                                           one module gated together); NULL = one group per
                                           layer. Ids must be 0..G-1 */
+  uint32_t drain_streams;              /* side streams DRAIN launches rotate over (0: 4). With 1,
+                                          comm_ctas = finish_ctas = 1 and pop_relax = 1 there is
+                                          one consumer at a time: the strict FrameQueue order
+                                          (queues.py:52-62), checked by trace replay */
 } p3_config_t;
 
 /* Builds the plan, allocates per-local-rank arenas (parameters W zero-initialised like

@@ -238,6 +238,63 @@ class HeapQueue:
         return len(self._h)
 
 
+# Live-trace replay (the transmission-order contract of SPEC.md:435 on a recorded run).
+# Trace events, in device append order: (event, iteration, layer, slice, t_ns, t0_ns) with the
+# codes of include/p3.h (PUSH 0, BCAST 1, PUBLISH 2, COMPLETE 3, PICK 4).
+EV_PUSH, EV_BCAST, EV_PUBLISH, EV_COMPLETE, EV_PICK = 0, 1, 2, 3, 4
+
+
+def replay_live(events, nslices: list[int], priority_mode: bool = True) -> tuple[list, list]:
+    """Feed one rank's recorded publish / pop interleaving of one iteration through the
+    FrameQueue order: PUBLISH = put_batch of every slice of the layer (worker.py:173-182,
+    queues.py:44-50; FIFO arrival = the publish sequence number), PUSH = poll (queues.py:
+    52-62). Returns (expected pops, recorded pops) as (layer, slice) lists; with a single
+    consumer they must be equal."""
+    heap: list = []
+    expect, got = [], []
+    for ev, _it, layer, sl, _t, _t0 in events:
+        if ev == EV_PUBLISH:
+            for s in range(nslices[layer]):
+                key = (layer, layer, s) if priority_mode else ()
+                heapq.heappush(heap, (key, (sl, s), (layer, s)))
+        elif ev == EV_PUSH:
+            got.append((layer, sl))
+            expect.append(heapq.heappop(heap)[2] if heap else None)
+    return expect, got
+
+
+def relaxation(events, avail_event: int, take_event: int, owner: int | None = None) -> int:
+    """Largest number of distinct layers more urgent than a claimed slice's layer that certainly
+    held an available slice at the claim: made available (avail_event record) before the
+    claim's queue snapshot started (t0) and claimed (own snapshot start) after the claim
+    completed (t). A strict FrameQueue consumer gives 0; C consumers popping at once give < C
+    (bounded relaxation of queues.py:52-62). avail/take = PUBLISH/PUSH for one worker's
+    outbox (availability per layer), COMPLETE/PICK for one server's inbox (availability per
+    slice; records carry the owner as a 7th field, selected by ``owner``)."""
+    avail: dict = {}
+    claims = []
+    for rec in events:
+        ev, _it, layer, sl, t, t0 = rec[:6]
+        if owner is not None and len(rec) > 6 and rec[6] != owner:
+            continue
+        if ev == avail_event:
+            key = layer if avail_event == EV_PUBLISH else (layer, sl)
+            avail[key] = min(avail.get(key, t), t)
+        elif ev == take_event:
+            claims.append((layer, sl, t, t0))
+    worst = 0
+    for layer, sl, t, t0 in claims:
+        ahead = set()
+        for l2, s2, t2, t02 in claims:
+            if l2 >= layer or t02 <= t:
+                continue
+            ta = avail.get(l2) if avail_event == EV_PUBLISH else avail.get((l2, s2))
+            if ta is not None and ta < t0:
+                ahead.add(l2)
+        worst = max(worst, len(ahead))
+    return worst
+
+
 # ------------------------------------------------------------------ sim.py (tick model)
 
 

@@ -27,6 +27,9 @@ P3_MAX_RANKS = 16
 P3_IPC_BYTES = 64
 P3_EV_PUSH = 0
 P3_EV_BCAST = 1
+P3_EV_PUBLISH = 2
+P3_EV_COMPLETE = 3
+P3_EV_PICK = 4
 
 LIB_PATH = Path(__file__).resolve().parent / "libp3.so"
 
@@ -45,6 +48,7 @@ class SliceRow(ctypes.Structure):
 class TraceRec(ctypes.Structure):
     _fields_ = [
         ("t_ns", ctypes.c_uint64),
+        ("t0_ns", ctypes.c_uint64),
         ("iteration", ctypes.c_uint32),
         ("layer", ctypes.c_uint32),
         ("slice", ctypes.c_uint32),
@@ -97,6 +101,7 @@ class Config(ctypes.Structure):
         ("pop_multi", ctypes.c_uint32),
         ("push_bf16", ctypes.c_uint32),
         ("gate_groups", ctypes.POINTER(ctypes.c_uint32)),
+        ("drain_streams", ctypes.c_uint32),
     ]
 
 

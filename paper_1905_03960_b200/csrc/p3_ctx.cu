@@ -153,6 +153,10 @@ struct p3_ctx {
   uint64_t pub_pending[P3_MAX_LOCAL]{};
   cudaStream_t pend_stream[P3_MAX_LOCAL]{};  // may be the legacy default stream (NULL)
   bool pend_valid[P3_MAX_LOCAL]{};           // pend_stream holds a publishing stream
+  // every stream that published in the open iteration (the FINISH launch comes after all)
+  std::vector<cudaStream_t> pub_streams[P3_MAX_LOCAL];
+  cudaEvent_t switch_ev[P3_MAX_LOCAL]{};     // orders a new publishing stream after the previous one
+  uint32_t n_side = P3_SIDE_STREAMS;         // side streams DRAIN launches rotate over
   bool comm_pending = false;
   uint64_t synced_iterations = 0;
   std::string err;
@@ -278,6 +282,8 @@ int p3_ctx_create(const p3_config_t* cfg, p3_ctx_t** out) {
     return fail(nullptr, P3_EUSAGE,
                 "comm_threads must be a multiple of 32 in [128, " + std::to_string(P3_COMM_MAX_THREADS) + "] (scheduler + signaler + producer + consumer warps)");
   if (cfg->comm_ctas < 1) return fail(nullptr, P3_EUSAGE, "comm_ctas must be >= 1");
+  if (cfg->drain_streams > P3_SIDE_STREAMS)
+    return fail(nullptr, P3_EUSAGE, "drain_streams must be in [0, " + std::to_string(P3_SIDE_STREAMS) + "]");
   for (uint32_t i = 0; i < cfg->n_local; ++i)
     if (cfg->local_ranks[i] >= cfg->world) return fail(nullptr, P3_EUSAGE, "local rank out of range");
   if (!driver().ok) return fail(nullptr, P3_ECUDA, "CUDA driver stream memory operations unavailable");
@@ -290,6 +296,7 @@ int p3_ctx_create(const p3_config_t* cfg, p3_ctx_t** out) {
   c->cfg.gate_groups = nullptr;  // consumed below, not retained
   c->L = cfg->n_layers;
   c->N = cfg->world;
+  c->n_side = cfg->drain_streams ? cfg->drain_streams : P3_SIDE_STREAMS;
   {
     auto env_u32 = [](const char* name, uint32_t dflt) {
       const char* e = getenv(name);
@@ -508,8 +515,10 @@ int p3_ctx_create(const p3_config_t* cfg, p3_ctx_t** out) {
     }
   }
   e = cudaEventCreateWithFlags(&c->comm_done, cudaEventDisableTiming);
-  for (uint32_t i = 0; i < cfg->n_local && e == cudaSuccess; ++i)
+  for (uint32_t i = 0; i < cfg->n_local && e == cudaSuccess; ++i) {
     e = cudaEventCreateWithFlags(&c->ready_ev[i], cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->switch_ev[i], cudaEventDisableTiming);
+  }
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->iter_ev, cudaEventDisableTiming);
   {
     int lo = 0, hi = 0;
@@ -549,8 +558,10 @@ int p3_ctx_destroy(p3_ctx_t* c) {
     if (c->side[j]) cudaStreamDestroy(c->side[j]);
     if (c->side_ev[j]) cudaEventDestroy(c->side_ev[j]);
   }
-  for (uint32_t i = 0; i < P3_MAX_LOCAL; ++i)
+  for (uint32_t i = 0; i < P3_MAX_LOCAL; ++i) {
     if (c->ready_ev[i]) cudaEventDestroy(c->ready_ev[i]);
+    if (c->switch_ev[i]) cudaEventDestroy(c->switch_ev[i]);
+  }
   if (c->poll_stream) cudaStreamDestroy(c->poll_stream);
   delete c;
   return P3_OK;
@@ -665,7 +676,7 @@ static int flush_publications(p3_ctx* c, uint32_t li) {
 // after the per-iteration reset on the main comm stream; the FINISH launch on the main comm
 // stream comes after all of them.
 static int launch_drain(p3_ctx* c, int li) {
-  const uint32_t j = c->side_next++ % P3_SIDE_STREAMS;
+  const uint32_t j = c->side_next++ % c->n_side;
   cudaStream_t s = c->side[j];
   if (!(c->side_used & (1u << j))) {  // first launch of the iteration here: after the reset
     CK(cudaStreamWaitEvent(s, c->iter_ev, 0));
@@ -688,8 +699,11 @@ int p3_iteration_begin(p3_ctx_t* c, uint64_t k, void* stream) {
     if (!c->peers.W[r]) return fail(c, P3_EUSAGE, "peer arenas not opened (call p3_ctx_open_peers)");
   cudaStream_t s = (cudaStream_t)stream;
   const LocalLayout& ll = c->local_layout;
-  for (uint32_t i = 0; i < c->cfg.n_local; ++i)
+  for (uint32_t i = 0; i < c->cfg.n_local; ++i) {
     CK(cudaMemsetAsync(static_cast<char*>(c->local_arena[i]) + ll.iter_begin, 0, ll.iter_end - ll.iter_begin, s));
+    c->pend_valid[i] = false;  // (everything of the previous iteration was flushed at its end)
+    c->pub_streams[i].clear();
+  }
   CK(cudaEventRecord(c->iter_ev, s));  // side streams wait for it when they get a DRAIN launch
   c->side_used = 0;
   c->comm_stream = s;
@@ -706,8 +720,10 @@ int p3_iteration_end(p3_ctx_t* c, uint64_t k) {
     if (!c->pend_valid[i]) continue;
     int rc = flush_publications(c, i);
     if (rc) return rc;
-    CK(cudaEventRecord(c->ready_ev[i], c->pend_stream[i]));
-    CK(cudaStreamWaitEvent(c->comm_stream, c->ready_ev[i], 0));
+    for (cudaStream_t ps : c->pub_streams[i]) {
+      CK(cudaEventRecord(c->ready_ev[i], ps));
+      CK(cudaStreamWaitEvent(c->comm_stream, c->ready_ev[i], 0));
+    }
     c->published[i] = 0;
   }
   for (int j = 0; j < P3_SIDE_STREAMS; ++j) {  // only the side streams used this iteration
@@ -750,6 +766,12 @@ int p3_layer_ready(p3_ctx_t* c, uint32_t li, uint32_t layer, uint64_t k, const f
         return fail(c, P3_ETIMEOUT, "publication ring full: the comm kernels stopped ingesting");
       std::this_thread::sleep_for(std::chrono::microseconds(20));
     }
+    if (c->pend_valid[li] && c->pend_stream[li] != (cudaStream_t)stream) {
+      // A new publishing stream: the ring tail it advances also exposes the entries queued
+      // from the previous stream, so it must be ordered after that stream's producing work.
+      CK(cudaEventRecord(c->switch_ev[li], c->pend_stream[li]));
+      CK(cudaStreamWaitEvent((cudaStream_t)stream, c->switch_ev[li], 0));
+    }
     PubEntry& e = c->ring_host[li][c->ring_tail[li] % D.ring_cap];
     e.layer = layer;
     e.key = c->fifo_seq[li]++;
@@ -757,6 +779,8 @@ int p3_layer_ready(p3_ctx_t* c, uint32_t li, uint32_t layer, uint64_t k, const f
     c->ring_tail[li]++;
     c->pend_stream[li] = (cudaStream_t)stream;
     c->pend_valid[li] = true;
+    if (std::find(c->pub_streams[li].begin(), c->pub_streams[li].end(), (cudaStream_t)stream) == c->pub_streams[li].end())
+      c->pub_streams[li].push_back((cudaStream_t)stream);
     c->published[li] += 4ull * c->counts[layer];
     c->pub_pending[li] += 4ull * c->counts[layer];
     if (c->pub_pending[li] >= c->cfg.pub_batch_bytes) {

@@ -392,6 +392,25 @@ __global__ void k_sleep(uint64_t ns) {
   while (globaltimer() - t0 < ns) __nanosleep(1000);
 }
 
+// ------------------------------------------------------------------ trace ring
+
+__device__ __forceinline__ void trace_append(const LocalDev& L, uint32_t k, uint32_t layer, uint32_t slice,
+                                             uint32_t rank, uint32_t ev, uint64_t t0 = 0) {
+  if (!L.trace_cap) return;
+  const unsigned long long idx = atomicAdd(L.trace_n, 1ull);
+  if (idx < L.trace_cap) {
+    p3_trace_rec_t r;
+    r.t_ns = globaltimer();
+    r.t0_ns = t0;
+    r.iteration = k;
+    r.layer = layer;
+    r.slice = slice;
+    r.rank = (uint16_t)rank;
+    r.event = (uint16_t)ev;
+    L.trace[idx] = r;
+  }
+}
+
 // ------------------------------------------------------------------ device slice queue
 
 // The outbox of one worker: per layer a publication word (iteration tag in the top 16 bits,
@@ -413,6 +432,10 @@ struct QueueView {
 };
 
 __device__ void ingest(const LocalDev& L, uint32_t sched);
+__device__ __forceinline__ uint64_t globaltimer_lane0() {
+  uint64_t t = (threadIdx.x & 31) == 0 ? globaltimer() : 0ull;
+  return __shfl_sync(0xffffffffu, (unsigned long long)t, 0);
+}
 
 // Publication word: iteration tag (16 bits) above the 48-bit gradient pointer, written by one
 // 64-bit stream memory write, so the tag and the pointer become visible together.
@@ -440,6 +463,7 @@ struct Stash {
   uint32_t run[P3_MULTI];
   uint32_t layer[P3_MULTI];
   uint64_t word[P3_MULTI];
+  uint64_t t0[P3_MULTI];
 };
 
 // What a pop hands to the caller besides the slice id: the slice's layer and the layer's
@@ -449,6 +473,7 @@ struct Popped {
   uint32_t run;
   uint32_t layer;
   uint64_t word;
+  uint64_t t0;  // %globaltimer before the queue snapshot the claim came from (trace)
 };
 
 __device__ uint32_t warp_pop(const QueueView& q, uint32_t tag, uint32_t* dbg = nullptr, uint32_t want = 1,
@@ -458,6 +483,7 @@ __device__ uint32_t warp_pop(const QueueView& q, uint32_t tag, uint32_t* dbg = n
     constexpr uint32_t CH = 8;  // chunks of 32 layers examined per memory round trip
     for (uint32_t group = 0, attempt = 0; group < q.n_layers; ++attempt) {
       // all loads of the group issued before any is used: one round trip, not 2*CH
+      const uint64_t t_snap = globaltimer_lane0();  // (trace: before this snapshot's loads)
       uint64_t w[CH];
       uint32_t cur[CH], ns[CH];
       // the ring check rides on the same round trip as the first group's loads
@@ -539,6 +565,7 @@ __device__ uint32_t warp_pop(const QueueView& q, uint32_t tag, uint32_t* dbg = n
               out->run = __shfl_sync(FULL_MASK, won ? min(want, my_ns - s) : 0u, j0);
               out->layer = l;
               out->word = __shfl_sync(FULL_MASK, (unsigned long long)my_w, j0);
+              out->t0 = t_snap;
             }
             return g0;
           }
@@ -587,6 +614,7 @@ __device__ uint32_t warp_pop(const QueueView& q, uint32_t tag, uint32_t* dbg = n
               stash->run[idx] = my_run;
               stash->layer[idx] = l;
               stash->word[idx] = my_w;
+              stash->t0[idx] = t_snap;
             }
             __syncwarp();
             if (lane == 0 && stash) stash->n += __popc(wm) - 1u;
@@ -595,6 +623,7 @@ __device__ uint32_t warp_pop(const QueueView& q, uint32_t tag, uint32_t* dbg = n
               out->run = __shfl_sync(FULL_MASK, my_run, j0);
               out->layer = group + 32 * c + j0;
               out->word = __shfl_sync(FULL_MASK, (unsigned long long)my_w, j0);
+              out->t0 = t_snap;
             }
             return __shfl_sync(FULL_MASK, my_g, j0);
           }
@@ -609,10 +638,12 @@ __device__ uint32_t warp_pop(const QueueView& q, uint32_t tag, uint32_t* dbg = n
   if (q.ring) ingest(*q.ring, q.sched);
   for (uint32_t retry = 0;; ++retry) {
     if (dbg && lane == 0) *(volatile uint32_t*)dbg = (6u << 20) | (retry & 0xfffff);
+    const uint64_t t_snap = globaltimer_lane0();
     uint32_t best_key = P3_NONE, best_l = P3_NONE;
     uint64_t best_w = 0;
     for (uint32_t l = lane; l < q.n_layers; l += 32) {
-      const uint64_t w = ld_relaxed_gpu64(q.pub + l);
+      // acquire: the layer's publish sequence (fifo_key) was stored before its word (ingest)
+      const uint64_t w = ld_acquire_gpu64(q.pub + l);
       if (!pub_ready(w, tag)) continue;
       if (ld_relaxed_gpu(q.cursor + l) >= q.nslices[l]) continue;
       const uint32_t key = ld_relaxed_gpu(q.fifo_key + l);
@@ -642,6 +673,7 @@ __device__ uint32_t warp_pop(const QueueView& q, uint32_t tag, uint32_t* dbg = n
         out->run = min(want, q.nslices[best_l] - s);
         out->layer = best_l;
         out->word = best_w;
+        out->t0 = t_snap;
       }
       return q.first[best_l] + s;
     }
@@ -700,6 +732,7 @@ __device__ uint32_t warp_server_pick(const CommArgs& a, const LocalDev& L, uint3
   // takes one candidate — the (blockIdx + attempt)-th of the most urgent ones, spreading the
   // consumers like the pops do — and a miss rescans.
   for (uint32_t attempt = 0; attempt < 4; ++attempt) {
+    const uint64_t t_snap = globaltimer_lane0();  // (trace: before this scan's loads)
     uint32_t ncand = 0, tl = P3_NONE, t_start = 0, t_cnt = 0;
     for (uint32_t group = 0; group < nl && tl == P3_NONE; group += 32 * CH) {
       uint32_t oc[CH], hv[CH], tk[CH], lo[CH];
@@ -775,6 +808,7 @@ __device__ uint32_t warp_server_pick(const CommArgs& a, const LocalDev& L, uint3
           if (won) {
             atomicAdd(L.srv_taken + l, 1u);
             atomicAdd(&L.it->reduced, 1u);
+            if (L.trace_cap) trace_append(L, k, l, gj - P.layer_first[l], o, P3_EV_PICK, t_snap);
           }
         }
         won = __shfl_sync(FULL_MASK, won, 0);
@@ -786,22 +820,6 @@ __device__ uint32_t warp_server_pick(const CommArgs& a, const LocalDev& L, uint3
     }
   }
   return P3_NONE;
-}
-
-__device__ __forceinline__ void trace_append(const LocalDev& L, uint32_t k, uint32_t layer, uint32_t slice,
-                                             uint32_t rank, uint32_t ev) {
-  if (!L.trace_cap) return;
-  const unsigned long long idx = atomicAdd(L.trace_n, 1ull);
-  if (idx < L.trace_cap) {
-    p3_trace_rec_t r;
-    r.t_ns = globaltimer();
-    r.iteration = k;
-    r.layer = layer;
-    r.slice = slice;
-    r.rank = (uint16_t)rank;
-    r.event = (uint16_t)ev;
-    L.trace[idx] = r;
-  }
 }
 
 __device__ void cta_copy(float* dst, const float* src, uint32_t n, uint32_t tid, uint32_t nthr) {
@@ -910,8 +928,18 @@ __device__ void ingest(const LocalDev& L, uint32_t sched) {
   for (uint32_t i = lo + lane; (int32_t)(hi - i) > 0; i += 32) {
     const volatile PubEntry* e = L.ring + (i % L.ring_cap);
     const uint32_t layer = e->layer;
-    if (sched == P3_SCHED_FIFO) L.fifo_key[layer] = e->key;
-    *(volatile unsigned long long*)(L.pub + layer) = e->word;
+    const uint32_t key = e->key;
+    const unsigned long long word = e->word;
+    if (sched == P3_SCHED_FIFO) {
+      // the publish sequence is visible before the word (FIFO pops load the word with acquire)
+      *(volatile uint32_t*)(L.fifo_key + layer) = key;
+      __threadfence();
+    }
+    *(volatile unsigned long long*)(L.pub + layer) = word;
+    if (L.trace_cap) {  // PUBLISH (put_batch) once the word is visible to every pop
+      __threadfence();
+      trace_append(L, (uint32_t)(word >> 48) - 1u, layer, key, L.rank, P3_EV_PUBLISH);
+    }
   }
   __syncwarp();
   if (lane == 0) *(volatile uint32_t*)L.ingested_host = hi;  // host may reuse the entries
@@ -926,7 +954,8 @@ __device__ void ingest(const LocalDev& L, uint32_t sched) {
 #define PUSH_DONE 0
 #define PUSH_REMOTE 1
 #define PUSH_REDUCE 2
-__device__ uint32_t prepare_push(const CommArgs& a, uint32_t li, uint32_t g, uint32_t l, uint64_t w, Job* job) {
+__device__ uint32_t prepare_push(const CommArgs& a, uint32_t li, uint32_t g, uint32_t l, uint64_t w, Job* job,
+                                 uint64_t t0 = 0) {
   const PlanDev& P = a.plan;
   const LocalDev& L = a.loc[li];
   const uint32_t r = L.rank;
@@ -941,7 +970,7 @@ __device__ uint32_t prepare_push(const CommArgs& a, uint32_t li, uint32_t g, uin
       // the pop read the publication word relaxed: this fence makes it an acquire, so the
       // gradient is visible from here on (ingest released it)
       fence_acq_rel_gpu();
-      if (L.trace_cap) trace_append(L, a.k, l, g - P.layer_first[l], a.trace_cta ? blockIdx.x : r, P3_EV_PUSH);
+      if (L.trace_cap) trace_append(L, a.k, l, g - P.layer_first[l], a.trace_cta ? blockIdx.x : r, P3_EV_PUSH, t0);
       if (o == r) {
         // the contribution stays in place (published to this rank by the acquire above)
         const uint32_t old = atom_add_relaxed_gpu(a.peers.arrivals[o] + opos, 1u);
@@ -949,10 +978,20 @@ __device__ uint32_t prepare_push(const CommArgs& a, uint32_t li, uint32_t g, uin
         red_add_relaxed_sys(a.peers.tally[o], 1u);
         if (old + 1 == (a.k + 1) * P.world) {  // the last arrival: the slice is complete
           red_add_relaxed_sys(a.peers.hint[o] + l, 1u);
-          red_add_relaxed_sys(a.peers.tally[o] + 1, 1u);
-          if (atomicCAS(L.claim + opos, a.k, a.k + 1) == a.k) {
+          const uint32_t done_before = atom_add_relaxed_sys(a.peers.tally[o] + 1, 1u);
+          if (L.trace_cap) {  // COMPLETE once the completion is visible to every server pick
+            __threadfence();
+            trace_append(L, a.k, l, g - P.layer_first[l], o, P3_EV_COMPLETE);
+          }
+          // Claim the reduction right here only when no other completed owned slice waits
+          // (else the server picks take them in priority order, this one included). The pick
+          // time is taken before the backlog is read.
+          const uint64_t tc = L.trace_cap ? globaltimer() : 0ull;
+          const uint32_t backlog = done_before + 1u - a.k * P.own_total[o] - ld_relaxed_gpu(&L.it->reduced);
+          if ((int32_t)backlog <= 1 && atomicCAS(L.claim + opos, a.k, a.k + 1) == a.k) {
             atomicAdd(L.srv_taken + l, 1u);
             atomicAdd(&L.it->reduced, 1u);
+            if (L.trace_cap) trace_append(L, a.k, l, g - P.layer_first[l], o, P3_EV_PICK, tc);
             verdict = PUSH_REDUCE;
           }
         }
@@ -1327,6 +1366,10 @@ __device__ void signal_job(const CommArgs& a, const Job& j) {
     if (old + 1 == (a.k + 1) * P.world) {
       red_add_relaxed_sys(a.peers.hint[j.rank] + j.layer, 1u);
       red_add_relaxed_sys(a.peers.tally[j.rank] + 1, 1u);
+      if (L.trace_cap) {  // COMPLETE once the completion is visible to the owner's picks
+        fence_acq_rel_sys();
+        trace_append(L, a.k, j.layer, j.g - P.layer_first[j.layer], j.rank, P3_EV_COMPLETE);
+      }
     }
     atomicAdd(L.bytes + 1, (j.bf16 ? 2ull : 4ull) * j.len);
   } else {
@@ -1350,6 +1393,7 @@ __device__ uint32_t take_stash(Stash* st, Popped* out) {
   out->run = st->run[0];
   out->layer = st->layer[0];
   out->word = st->word[0];
+  out->t0 = st->t0[0];
   __syncwarp();
   if (lane == 0) {
     for (uint32_t i = 1; i < st->n; ++i) {
@@ -1357,6 +1401,7 @@ __device__ uint32_t take_stash(Stash* st, Popped* out) {
       st->run[i - 1] = st->run[i];
       st->layer[i - 1] = st->layer[i];
       st->word[i - 1] = st->word[i];
+      st->t0[i - 1] = st->t0[i];
     }
     st->n -= 1;
   }
@@ -1398,8 +1443,8 @@ __global__ void __launch_bounds__(P3_COMM_MAX_THREADS, 1) k_comm(const __grid_co
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  if (a.trace_cta && threadIdx.x == 0)  // diagnostics: CTA start (event 2)
-    trace_append(a.loc[0], a.k, 0, 0, blockIdx.x, 2);
+  if (a.trace_cta && threadIdx.x == 0)  // diagnostics: CTA start (event 16)
+    trace_append(a.loc[0], a.k, 0, 0, blockIdx.x, 16);
   if (warp == 0) {
     uint32_t* phase = (lane == 0 && blockIdx.x < P3_DBG_CTAS) ? a.loc[0].cta_phase + blockIdx.x : nullptr;
     const uint64_t t0 = globaltimer();
@@ -1420,6 +1465,7 @@ __global__ void __launch_bounds__(P3_COMM_MAX_THREADS, 1) k_comm(const __grid_co
       pp.run = 1;
       pp.layer = 0;
       pp.word = 0;
+      pp.t0 = 0;
       if (a.plan.world == 1) {
         // single rank: a popped slice is complete the moment it is popped (the owner's own
         // contribution is read in place), so the pop claims the reduction directly — no
@@ -1439,7 +1485,7 @@ __global__ void __launch_bounds__(P3_COMM_MAX_THREADS, 1) k_comm(const __grid_co
             if (L.trace_cap)
               for (uint32_t i = 0; i < pp.run; ++i)
                 trace_append(L, a.k, pp.layer, g + i - a.plan.layer_first[pp.layer], a.trace_cta ? blockIdx.x : L.rank,
-                             P3_EV_PUSH);
+                             P3_EV_PUSH, pp.t0);
           }
           kind = JOB_REDUCE;
         }
@@ -1545,7 +1591,7 @@ __global__ void __launch_bounds__(P3_COMM_MAX_THREADS, 1) k_comm(const __grid_co
         P3_CHECK(kind == JOB_PUSH || a.plan.slice_owner[g] == a.loc[li].rank);  // reduce only what it owns
       }
       if (kind == JOB_PUSH) {
-        const uint32_t how = prepare_push(a, li, g, pp.layer, pp.word, nullptr);
+        const uint32_t how = prepare_push(a, li, g, pp.layer, pp.word, nullptr, pp.t0);
         if (how == PUSH_DONE) continue;  // own slice, still waiting for peers: counted in place
         if (how == PUSH_REDUCE) kind = JOB_REDUCE;  // own slice completed it: reduce right away
       }
@@ -1580,7 +1626,7 @@ __global__ void __launch_bounds__(P3_COMM_MAX_THREADS, 1) k_comm(const __grid_co
       if (a.mode == P3_COMM_FINISH) atomicAdd(&stats->exited, 1u);
     }
     if (phase) *(volatile uint32_t*)phase = (a.k << 24) | (5u << 20);
-    if (a.trace_cta && lane == 0) trace_append(a.loc[0], a.k, 0, 0, blockIdx.x, 3);  // diagnostics: scheduler exit
+    if (a.trace_cta && lane == 0) trace_append(a.loc[0], a.k, 0, 0, blockIdx.x, 17);  // diagnostics: scheduler exit
   } else if (warp == 1) {
     // signaler: in job order, once the consumers are done with a job, fence and publish
     uint64_t t_sig = 0;

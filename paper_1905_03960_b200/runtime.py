@@ -42,7 +42,8 @@ class TraceEvent:
     layer: int
     slice: int
     rank: int
-    event: int  # _lib.P3_EV_PUSH / P3_EV_BCAST
+    event: int  # _lib.P3_EV_PUSH / BCAST / PUBLISH / COMPLETE / PICK
+    t0_ns: int = 0  # PUSH / PICK: before the queue snapshot the claim came from
 
 
 def plan_fingerprint(layer_counts, world, max_slice, plan_mode, big_threshold, rng_seed, priority_mode, lr, momentum,
@@ -114,6 +115,7 @@ class SyncContext:
         pop_run: int = 0,
         pop_multi: int = 0,
         push_dtype: str = "fp32",
+        drain_streams: int = 0,
     ) -> None:
         import torch
 
@@ -166,6 +168,8 @@ class SyncContext:
         cfg.trace_cap = trace_cap
         cfg.emulate_grads = 1 if emulate_grads else 0
         cfg.drain_bytes = drain_bytes
+        cfg.drain_streams = drain_streams
+        self.strict = comm_ctas == 1 and (finish_ctas or comm_ctas) == 1 and pop_relax == 1 and drain_streams == 1
         h = ctypes.c_void_p()
         _lib.check(self.lib.p3_ctx_create(ctypes.byref(cfg), ctypes.byref(h)), what="p3_ctx_create")
         self._h = h
@@ -256,7 +260,7 @@ class SyncContext:
             return []
         recs = (_lib.TraceRec * n.value)()
         self._check(self.lib.p3_trace_read(self._h, li, recs, n.value, ctypes.byref(n)), "p3_trace_read")
-        return [TraceEvent(r.t_ns, r.iteration, r.layer, r.slice, r.rank, r.event) for r in recs[: n.value]]
+        return [TraceEvent(r.t_ns, r.iteration, r.layer, r.slice, r.rank, r.event, r.t0_ns) for r in recs[: n.value]]
 
     def debug_snapshot(self, li: int = 0) -> dict:
         n = ctypes.c_uint64()
@@ -331,6 +335,11 @@ class WorkerConfig:
     big_threshold: int = 1_000_000     # baseline plan (cli.py:68)
     seed: int = 0                      # baseline plan placement seed (cli.py:74)
     push_dtype: str = "fp32"           # "bf16": declared lossy transport of pushes
+    finish_ctas: int = 0               # CTAs of the FINISH launch (0: comm_ctas)
+    pop_relax: int = 0                 # bounded pop relaxation (0: the launch's CTA count)
+    drain_streams: int = 0             # side streams of DRAIN launches (0: 4)
+    strict_order: bool = False         # one consumer at a time: 1 CTA per launch, 1 DRAIN stream,
+                                       # strict FrameQueue order (the reference's single sender)
 
 
 def rank_seed(seed: int, rank: int, distinct: bool) -> int:
@@ -374,7 +383,7 @@ class TrainingWorker:
             max_slice=config.max_slice,
             lr=config.lr,
             priority_mode=config.mode == P3_MODE,
-            comm_ctas=config.comm_ctas,
+            comm_ctas=1 if config.strict_order else config.comm_ctas,
             comm_threads=config.comm_threads,
             timeout_s=config.deadlock_timeout,
             trace_cap=config.trace_cap,
@@ -385,6 +394,9 @@ class TrainingWorker:
             throttle_bps=config.throttle_rate or 0.0,
             throttle_burst=config.throttle_burst,
             push_dtype=config.push_dtype,
+            finish_ctas=1 if config.strict_order else config.finish_ctas,
+            pop_relax=1 if config.strict_order else config.pop_relax,
+            drain_streams=1 if config.strict_order else config.drain_streams,
         )
         self.comm_stream = torch.cuda.Stream()
         self.streams = [torch.cuda.Stream() for _ in self.ranks]

@@ -157,3 +157,33 @@ def test_bf16_rounding_matches_torch():
                         np.array([0.0, -0.0, 1.0, 1.00390625, 1.01171875, 65504.0, 3.4e38])]).astype(np.float32)
     want = torch.from_numpy(x).to(torch.bfloat16).to(torch.float32).numpy()
     assert O.to_bf16(x).tobytes() == want.tobytes()
+
+
+def test_replay_live_and_relaxation():
+    # the live-trace checkers used by tests/test_gpu_live_order.py, on hand-made traces:
+    # PUBLISH = put_batch of a layer, PUSH = poll (queues.py:44-62)
+    P, U = O.EV_PUBLISH, O.EV_PUSH
+    nsl = [2, 1, 3]
+    ev = [(P, 0, 2, 0, 10, 0), (U, 0, 2, 0, 11, 10), (P, 0, 0, 1, 12, 0), (U, 0, 0, 0, 13, 12),
+          (U, 0, 0, 1, 14, 13), (P, 0, 1, 2, 15, 0), (U, 0, 1, 0, 16, 15), (U, 0, 2, 1, 17, 16),
+          (U, 0, 2, 2, 18, 17)]
+    expect, got = O.replay_live(ev, nsl, priority_mode=True)
+    assert got == expect
+    assert O.relaxation(ev, P, U) == 0
+    # a pop that passes over a layer published before its snapshot and popped after it
+    bad = [(P, 0, 2, 0, 10, 0), (P, 0, 0, 1, 11, 0), (U, 0, 2, 0, 20, 12), (U, 0, 0, 0, 22, 21),
+           (U, 0, 0, 1, 23, 22), (U, 0, 2, 1, 24, 23), (U, 0, 2, 2, 25, 24)]
+    e2, g2 = O.replay_live(bad, nsl, priority_mode=True)
+    assert g2 != e2 and e2[0] == (0, 0)
+    assert O.relaxation(bad, P, U) == 1
+    # FIFO: arrival = publish sequence (slice field of PUBLISH)
+    fifo = [(P, 0, 2, 0, 10, 0), (P, 0, 0, 1, 11, 0), (U, 0, 2, 0, 12, 11), (U, 0, 2, 1, 13, 12),
+            (U, 0, 2, 2, 14, 13), (U, 0, 0, 0, 15, 14), (U, 0, 0, 1, 16, 15)]
+    e3, g3 = O.replay_live(fifo, nsl, priority_mode=False)
+    assert g3 == e3
+    # server inbox: COMPLETE / PICK per slice, filtered by owner
+    C, K = O.EV_COMPLETE, O.EV_PICK
+    srv = [(C, 0, 1, 0, 5, 0, 0), (C, 0, 0, 0, 6, 0, 0), (K, 0, 1, 0, 9, 7, 0), (K, 0, 0, 0, 12, 10, 0),
+           (C, 0, 0, 1, 6, 0, 1), (K, 0, 2, 0, 3, 1, 1)]
+    assert O.relaxation(srv, C, K, owner=0) == 1
+    assert O.relaxation(srv, C, K, owner=1) == 0
