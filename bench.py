@@ -313,11 +313,11 @@ def run_ours(args):
     # --- P3: device-resident inputs
     model = build(args, rank)
     ddp = P3DataParallel(model, lr=args.lr, max_slice=args.max_slice, comm_ctas=args.comm_ctas)
-    launches0 = ddp.ctx.launches()
+    launches0 = ddp.launches()
     ms, clocks = time_training(args, world, rank, ddp, x, y, args.steps, args.warmup)
     value = args.steps * batch * world / (ms / 1000.0)
     # comm kernel launches (DRAIN per layer + FINISH per iteration) of the timed steps
-    gpu_launches = (ddp.ctx.launches() - launches0) * args.steps // (args.steps + args.warmup)
+    gpu_launches = (ddp.launches() - launches0) * args.steps // (args.steps + args.warmup)
 
     # --- e2e through the public API: pinned host batch copied in, loss copied out, every step
     e2e_value, h2d = None, 0

@@ -60,6 +60,10 @@ extern "C" {
 #define P3_EV_COMPLETE 3 /* the last push of an owned slice arrived; rank = owner */
 #define P3_EV_PICK 4     /* owner claimed a complete slice for reduce + broadcast; t0_ns = start
                             of the pick's scan, t_ns = after the claim */
+#define P3_EV_ITER_START 5 /* p3_trace_mark: a rank's forward pass of `iteration` starts
+                              (IterationRecord.start, worker.py:312-313) */
+#define P3_EV_SYNCED 6     /* p3_trace_mark: every layer of `iteration` synced on that rank
+                              (sync_end_times, worker.py:265-268) */
 
 /* One row of a SlicePlan (plan.py:30-45: SliceKey + Slice). */
 typedef struct p3_slice {
@@ -304,6 +308,11 @@ int p3_sync_all(p3_ctx_t* ctx, uint64_t iteration, double timeout_s);
 int p3_trace_read(p3_ctx_t* ctx, uint32_t local_idx, p3_trace_rec_t* out, uint64_t cap,
                   uint64_t* n_out);
 int p3_trace_clear(p3_ctx_t* ctx);
+
+/* Append a stream-ordered record (P3_EV_ITER_START / P3_EV_SYNCED) with the device clock to
+ * a local rank's trace: the iteration timeline of the reference worker (worker.py:312-368)
+ * on the same %globaltimer clock as the queue records. One 1-thread kernel on `stream`. */
+int p3_trace_mark(p3_ctx_t* ctx, uint32_t local_idx, uint64_t iteration, uint32_t event, void* stream);
 
 /* Comm kernel launches issued by this context so far (DRAIN + FINISH). */
 int p3_comm_launches(p3_ctx_t* ctx, uint64_t* n);

@@ -30,6 +30,8 @@ P3_EV_BCAST = 1
 P3_EV_PUBLISH = 2
 P3_EV_COMPLETE = 3
 P3_EV_PICK = 4
+P3_EV_ITER_START = 5
+P3_EV_SYNCED = 6
 
 LIB_PATH = Path(__file__).resolve().parent / "libp3.so"
 
@@ -142,6 +144,7 @@ SIGNATURES = {
     "p3_sync_all": (ctypes.c_int, [_P, _U64, ctypes.c_double]),
     "p3_trace_read": (ctypes.c_int, [_P, _U32, ctypes.POINTER(TraceRec), _U64, _PU64]),
     "p3_trace_clear": (ctypes.c_int, [_P]),
+    "p3_trace_mark": (ctypes.c_int, [_P, _U32, _U64, _U32, _P]),
     "p3_counters": (ctypes.c_int, [_P, _U32, _PU64, _PU64]),
     "p3_debug_snapshot": (ctypes.c_int, [_P, _U32, _PU32, _U64, _PU64]),
     "p3_last_error": (ctypes.c_char_p, [_P]),

@@ -925,6 +925,14 @@ int p3_trace_clear(p3_ctx_t* c) {
   return P3_OK;
 }
 
+int p3_trace_mark(p3_ctx_t* c, uint32_t li, uint64_t k, uint32_t ev, void* stream) {
+  int rc = check_local(c, li);
+  if (rc) return rc;
+  if (ev != P3_EV_ITER_START && ev != P3_EV_SYNCED) return fail(c, P3_EUSAGE, "mark event must be ITER_START or SYNCED");
+  if (launch_mark(c->loc[li], (uint32_t)k, ev, stream) != P3_OK) return cuda_fail(c, cudaGetLastError(), "mark launch");
+  return P3_OK;
+}
+
 int p3_comm_launches(p3_ctx_t* c, uint64_t* n) {
   if (!c || !n) return fail(c, P3_EUSAGE, "null argument");
   *n = c->launches;

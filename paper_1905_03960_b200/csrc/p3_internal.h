@@ -143,6 +143,7 @@ int preload_kernels();
 int launch_comm(const CommArgs& a, uint32_t ctas, uint32_t threads, void* stream);
 int launch_gradgen(uint64_t seed, uint64_t iteration, uint64_t layer, uint64_t start, uint64_t count,
                    float* out, void* stream);
+int launch_mark(const LocalDev& L, uint32_t k, uint32_t ev, void* stream);
 int launch_queue_pop(const uint32_t* nslices, const uint32_t* first, const uint64_t* pub,
                      const uint32_t* fifo_key, uint32_t* cursor, uint32_t n_layers, uint32_t sched,
                      uint32_t tag, uint32_t* result, void* stream);

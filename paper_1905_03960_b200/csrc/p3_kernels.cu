@@ -1781,6 +1781,16 @@ __global__ void __launch_bounds__(P3_COMM_MAX_THREADS, 1) k_comm(const __grid_co
   }
 }
 
+// p3_trace_mark: one stream-ordered trace record (iteration start / synced) on the device clock.
+__global__ void k_mark(const LocalDev L, uint32_t k, uint32_t ev) {
+  if (threadIdx.x == 0) trace_append(L, k, 0, 0, L.rank, ev);
+}
+
+int launch_mark(const LocalDev& L, uint32_t k, uint32_t ev, void* stream) {
+  k_mark<<<1, 32, 0, (cudaStream_t)stream>>>(L, k, ev);
+  return cudaGetLastError() == cudaSuccess ? P3_OK : P3_ECUDA;
+}
+
 // With lazy module loading (CUDA_MODULE_LOADING=LAZY, the CUDA 12 default) the first launch
 // of a kernel loads it, and loading waits for the kernels already running on the device.
 // A comm kernel that waited for work of the compute streams would block them, so every kernel those
@@ -1791,7 +1801,7 @@ int preload_kernels() {
     return P3_ECUDA;
   cudaFuncAttributes fa;
   const void* fns[] = {(const void*)k_comm, (const void*)k_gradgen, (const void*)k_sleep,
-                       (const void*)k_shard_update, (const void*)k_queue_pop};
+                       (const void*)k_shard_update, (const void*)k_queue_pop, (const void*)k_mark};
   for (const void* f : fns)
     if (cudaFuncGetAttributes(&fa, f) != cudaSuccess) return P3_ECUDA;
   return P3_OK;
