@@ -141,6 +141,21 @@ int p3_queue_put_layer(p3_queue_t* q, uint32_t layer, uint32_t iteration);
 int p3_queue_poll(p3_queue_t* q, uint32_t* layer, uint32_t* slice);
 int p3_queue_destroy(p3_queue_t* q);
 
+/* ------------------------------------------------------------- host frame queue */
+
+/* FrameQueue ordering (queues.py:16-62) for frames that stay on the host (wire path beyond
+ * the NVSwitch domain): a heap of opaque handles keyed (priority, layer, slice, arrival) in
+ * priority mode, arrival in FIFO mode. Callers serialise access. put_batch takes n keys as
+ * 3 u64 each (priority, layer, slice; ignored in FIFO mode). poll returns P3_ETIMEOUT when
+ * empty; snapshot lists the handles in dequeue order. */
+typedef struct p3_fq p3_fq_t;
+int p3_fq_create(uint32_t priority_mode, p3_fq_t** out);
+int p3_fq_put_batch(p3_fq_t* q, const uint64_t* keys3, const uint64_t* handles, uint64_t n);
+int p3_fq_poll(p3_fq_t* q, uint64_t* handle);
+uint64_t p3_fq_size(p3_fq_t* q);
+int p3_fq_snapshot(p3_fq_t* q, uint64_t* handles, uint64_t cap, uint64_t* n_out);
+int p3_fq_destroy(p3_fq_t* q);
+
 /* ------------------------------------------------------------- schedule model (host) */
 
 /* sim.py:26-34: policies and resources of the discrete-event model. */

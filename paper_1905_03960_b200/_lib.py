@@ -144,6 +144,12 @@ SIGNATURES = {
     "p3_sync_all": (ctypes.c_int, [_P, _U64, ctypes.c_double]),
     "p3_trace_read": (ctypes.c_int, [_P, _U32, ctypes.POINTER(TraceRec), _U64, _PU64]),
     "p3_trace_clear": (ctypes.c_int, [_P]),
+    "p3_fq_create": (ctypes.c_int, [_U32, ctypes.POINTER(_P)]),
+    "p3_fq_put_batch": (ctypes.c_int, [_P, _PU64, _PU64, _U64]),
+    "p3_fq_poll": (ctypes.c_int, [_P, _PU64]),
+    "p3_fq_size": (_U64, [_P]),
+    "p3_fq_snapshot": (ctypes.c_int, [_P, _PU64, _U64, _PU64]),
+    "p3_fq_destroy": (ctypes.c_int, [_P]),
     "p3_trace_mark": (ctypes.c_int, [_P, _U32, _U64, _U32, _P]),
     "p3_counters": (ctypes.c_int, [_P, _U32, _PU64, _PU64]),
     "p3_debug_snapshot": (ctypes.c_int, [_P, _U32, _PU32, _U64, _PU64]),

@@ -4,9 +4,11 @@
 //   p3_plan_baseline  <- make_baseline_plan  plan.py:122-164
 //   p3_splitmix64_*   <- hashing.py:24-35
 //   p3_fnv1a64        <- hashing.py:79-83
+//   p3_fq_*           <- FrameQueue ordering (queues.py:16-62) for host-resident frames
 #include "p3_internal.h"
 
 #include <cstring>
+#include <queue>
 
 namespace p3 {
 
@@ -116,6 +118,77 @@ int p3_plan_baseline(const uint64_t* counts, uint32_t n_layers, uint32_t num_ser
   if (rc == P3_OK) rc = emit(rows, out, cap, n_out, &err);
   if (rc != P3_OK) p3::set_thread_error(err);
   return rc;
+}
+
+// ------------------------------------------------------------ host frame queue
+
+// FrameQueue order for frames that live on the host (the wire path beyond one NVSwitch
+// domain, tests): a min-heap of (priority, layer, slice, arrival) in priority mode, of
+// arrival alone in FIFO mode (queues.py:16-17, 34-38). Frames themselves stay with the
+// caller; the heap orders opaque handles. Not thread-safe: the caller serialises (the
+// Python FrameQueue holds its condition lock around every call, which also makes a batch
+// atomic, queues.py:44-50). The GPU path never uses it: there the comm kernel pops the
+// device slice queue.
+struct p3_fq {
+  struct Ent {
+    uint64_t p, l, s, seq, h;
+    bool operator>(const Ent& o) const {
+      if (p != o.p) return p > o.p;
+      if (l != o.l) return l > o.l;
+      if (s != o.s) return s > o.s;
+      return seq > o.seq;
+    }
+  };
+  bool priority = true;
+  uint64_t seq = 0;
+  std::priority_queue<Ent, std::vector<Ent>, std::greater<Ent>> heap;
+};
+
+int p3_fq_create(uint32_t priority_mode, p3_fq_t** out) {
+  if (!out) return P3_EUSAGE;
+  p3_fq* q = new p3_fq();
+  q->priority = priority_mode != 0;
+  *out = q;
+  return P3_OK;
+}
+
+int p3_fq_put_batch(p3_fq_t* q, const uint64_t* keys3, const uint64_t* handles, uint64_t n) {
+  if (!q || (n && (!keys3 || !handles))) return P3_EUSAGE;
+  for (uint64_t i = 0; i < n; ++i) {
+    p3_fq::Ent e{0, 0, 0, q->seq++, handles[i]};
+    if (q->priority) {
+      e.p = keys3[3 * i];
+      e.l = keys3[3 * i + 1];
+      e.s = keys3[3 * i + 2];
+    }
+    q->heap.push(e);
+  }
+  return P3_OK;
+}
+
+int p3_fq_poll(p3_fq_t* q, uint64_t* handle) {
+  if (!q || !handle) return P3_EUSAGE;
+  if (q->heap.empty()) return P3_ETIMEOUT;
+  *handle = q->heap.top().h;
+  q->heap.pop();
+  return P3_OK;
+}
+
+uint64_t p3_fq_size(p3_fq_t* q) { return q ? (uint64_t)q->heap.size() : 0; }
+
+int p3_fq_snapshot(p3_fq_t* q, uint64_t* handles, uint64_t cap, uint64_t* n_out) {
+  if (!q || !n_out) return P3_EUSAGE;
+  *n_out = q->heap.size();
+  if (!handles) return P3_OK;
+  if (cap < q->heap.size()) return P3_EUSAGE;
+  auto copy = q->heap;  // queued frames in dequeue order (queues.py:69-71)
+  for (uint64_t i = 0; !copy.empty(); ++i, copy.pop()) handles[i] = copy.top().h;
+  return P3_OK;
+}
+
+int p3_fq_destroy(p3_fq_t* q) {
+  delete q;
+  return P3_OK;
 }
 
 }  // extern "C"

@@ -1,11 +1,16 @@
-"""The device slice queue (worker outbox) and the deadlock error.
+"""Slice queues: the device slice queue of the comm kernel, and FrameQueue for host frames.
 
 ``FrameQueue`` in the reference (``pkg/src/p3sync/queues.py:20-75``) is a host heap of
-frames keyed by ``priority_sort_key``. Here the outbox lives in device memory and is
-consumed by the persistent comm kernel: per layer an iteration tag, a publish sequence
-and a claim cursor; a pop returns the lowest ready layer's next slice (priority mode) or
-the earliest-published layer's next slice (FIFO mode). ``DeviceSliceQueue`` drives that
-same ``warp_pop`` routine one operation at a time (scripted replay / tests).
+frames keyed by ``priority_sort_key``. On the GPU path the outbox lives in device memory
+and is consumed by the comm kernel: per layer an iteration tag, a publish sequence and a
+claim cursor; a pop returns the lowest ready layer's next slice (priority mode) or the
+earliest-published layer's next slice (FIFO mode). ``DeviceSliceQueue`` drives that same
+``warp_pop`` routine one operation at a time (scripted replay / tests).
+
+``FrameQueue`` keeps the reference's API and semantics for frames that stay on the host
+(the wire path beyond one NVSwitch domain, host tooling): blocking ``poll`` with deadlock
+timeout, atomic ``put_batch``, close-then-drain, ``snapshot``. Its ordering lives in
+libp3's native heap (``p3_fq_*``); the GPU path never goes through it.
 """
 
 from __future__ import annotations
@@ -14,11 +19,16 @@ import ctypes
 import threading
 
 from . import _lib
-from .plan import SliceKey
+from .plan import SliceKey, priority_sort_key
 
 
 class DeadlockError(RuntimeError):
     """A blocking wait exceeded its deadline (queues.py:12-13)."""
+
+
+def frame_order_key(frame) -> tuple[int, int, int]:
+    """The total order of queued frames (queues.py:16-17): (priority, layer, slice)."""
+    return priority_sort_key(frame.priority, SliceKey(frame.layer_index, frame.slice_index))
 
 
 class DeviceSliceQueue:
@@ -58,72 +68,55 @@ class DeviceSliceQueue:
 
 
 class FrameQueue:
-    """FrameQueue (queues.py:20-75) with the device slice queue underneath.
+    """Blocking producer/consumer queue of host frames (queues.py:20-75): in priority mode a
+    poll returns the minimum of ``frame_order_key`` among the queued frames (arrival breaks
+    ties), in FIFO mode the earliest arrival; a batch put is atomic; after ``close`` polls
+    drain what is left, then return None."""
 
-    ``put_batch`` takes the frames of ONE layer — every slice of it, which is how the worker
-    enqueues a layer (worker.py:173-182) and what makes the batch atomic on the device: one
-    publication word; ``poll`` is the device pop (priority mode: lowest layer, ascending
-    slice; FIFO mode: publish order), blocking up to ``timeout`` and raising DeadlockError
-    when nothing arrives, None once closed and drained. The device keeps keys; the frames
-    (descriptors, worker.py:152-164) stay on the host. A layer must be drained before it is
-    queued again (the device holds one batch per layer).
-    """
-
-    def __init__(self, priority_mode: bool = True, slices_per_layer: list[int] | None = None) -> None:
-        if slices_per_layer is None:
-            raise ValueError("slices_per_layer (slices of each layer, from the slice plan) is required")
+    def __init__(self, priority_mode: bool = True) -> None:
         self.priority_mode = priority_mode
-        self._n = list(slices_per_layer)
-        self._q = DeviceSliceQueue(self._n, priority_mode)
-        self._frames: dict[tuple[int, int], object] = {}
-        self._remaining = [0] * len(self._n)
+        self._lib = _lib.load()
+        h = ctypes.c_void_p()
+        _lib.check(self._lib.p3_fq_create(1 if priority_mode else 0, ctypes.byref(h)), what="p3_fq_create")
+        self._h = h
+        self._frames: dict[int, object] = {}
+        self._next = 0
         self._closed = False
         self._cond = threading.Condition()
-
-    @classmethod
-    def for_plan(cls, plan, priority_mode: bool = True) -> "FrameQueue":
-        n = [0] * (max((s.key.layer_index for s in plan.slices), default=-1) + 1)
-        for s in plan.slices:
-            n[s.key.layer_index] += 1
-        return cls(priority_mode, n)
 
     def put(self, frame) -> None:
         self.put_batch([frame])
 
     def put_batch(self, frames) -> None:
         frames = list(frames)
-        if not frames:
-            return
-        layer = frames[0].layer_index
-        if any(f.layer_index != layer for f in frames) or not 0 <= layer < len(self._n):
-            raise ValueError("a batch holds the slices of one layer of the plan")
-        if sorted(f.slice_index for f in frames) != list(range(self._n[layer])):
-            raise ValueError(f"layer {layer}: a batch holds every one of its {self._n[layer]} slices")
-        if self.priority_mode and any(f.priority != layer for f in frames):
-            raise ValueError("priority mode orders by layer: priority must equal the layer index (plan.py:112)")
+        n = len(frames)
+        keys = (ctypes.c_uint64 * (3 * n))()
+        handles = (ctypes.c_uint64 * n)()
+        if self.priority_mode:
+            for i, f in enumerate(frames):
+                keys[3 * i : 3 * i + 3] = frame_order_key(f)
         with self._cond:
             if self._closed:
                 raise RuntimeError("queue is closed")
-            if self._remaining[layer]:
-                raise ValueError(f"layer {layer} is still queued")
-            for f in frames:
-                self._frames[(layer, f.slice_index)] = f
-            self._remaining[layer] = len(frames)
-            self._q.put_layer(layer, 0)
+            for i, f in enumerate(frames):
+                handles[i] = self._next + i
+                self._frames[self._next + i] = f
+            self._next += n
+            _lib.check(self._lib.p3_fq_put_batch(self._h, keys, handles, n), what="p3_fq_put_batch")
             self._cond.notify_all()
 
     def poll(self, timeout: float | None = None):
+        """Next frame; blocks while empty; None once closed and drained; DeadlockError when
+        nothing arrives within ``timeout`` seconds."""
+        out = ctypes.c_uint64()
         with self._cond:
-            while True:
-                if any(self._remaining):
-                    key = self._q.poll()
-                    if key is not None:
-                        self._remaining[key.layer_index] -= 1
-                        return self._frames.pop((key.layer_index, key.slice_index))
-                if self._closed:
-                    return None
+            while not self._frames and not self._closed:
                 if not self._cond.wait(timeout):
-                    raise DeadlockError(f"queue poll stalled for {timeout}s ({len(self)} queued)")
+                    raise DeadlockError(f"queue poll stalled for {timeout}s ({len(self._frames)} queued)")
+            if not self._frames:
+                return None
+            _lib.check(self._lib.p3_fq_poll(self._h, ctypes.byref(out)), what="p3_fq_poll")
+            return self._frames.pop(int(out.value))
 
     def close(self) -> None:
         with self._cond:
@@ -131,8 +124,22 @@ class FrameQueue:
             self._cond.notify_all()
 
     def snapshot(self) -> list:
+        """Queued frames in dequeue order."""
         with self._cond:
-            return list(self._frames.values())
+            n = ctypes.c_uint64()
+            _lib.check(self._lib.p3_fq_snapshot(self._h, None, 0, ctypes.byref(n)), what="p3_fq_snapshot")
+            buf = (ctypes.c_uint64 * max(1, n.value))()
+            _lib.check(self._lib.p3_fq_snapshot(self._h, buf, n.value, ctypes.byref(n)), what="p3_fq_snapshot")
+            return [self._frames[int(buf[i])] for i in range(n.value)]
 
     def __len__(self) -> int:
-        return sum(self._remaining)
+        with self._cond:
+            return len(self._frames)
+
+    def __del__(self):  # pragma: no cover - best effort
+        try:
+            if getattr(self, "_h", None):
+                self._lib.p3_fq_destroy(self._h)
+                self._h = None
+        except Exception:
+            pass

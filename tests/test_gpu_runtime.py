@@ -391,50 +391,6 @@ def test_real_shapes_match_oracle(cuda, model, world, iters):
     assert got == {want}
 
 
-def test_frame_queue_api(cuda):
-    """FrameQueue (queues.py:20-75 API) over the device queue: atomic layer batches, priority
-    and FIFO order, blocking poll with DeadlockError, close -> drain -> None."""
-    import threading
-    import time
-
-    from paper_1905_03960_b200.plan import make_p3_plan
-    from paper_1905_03960_b200.model import builtin_profile
-    from paper_1905_03960_b200.proto import Frame, MsgType
-    from paper_1905_03960_b200.queues import DeadlockError, FrameQueue
-
-    plan = make_p3_plan(builtin_profile("vgg19-like"), 2)
-    def frames(layer):
-        return [Frame(MsgType.PUSH, s.priority, 0, 0, s.key.layer_index, s.key.slice_index, s.offset)
-                for s in plan.slices_of_layer(layer)]
-    L = 1 + max(s.key.layer_index for s in plan.slices)
-    for prio in (True, False):
-        q = FrameQueue.for_plan(plan, priority_mode=prio)
-        order = [L - 1 - i for i in range(L)]  # backward order, as the worker enqueues
-        for l in order:
-            q.put_batch(frames(l))
-        got = [q.poll(1.0) for _ in range(len(plan.slices))]
-        keys = [(f.layer_index, f.slice_index) for f in got]
-        if prio:
-            assert keys == sorted(keys)
-        else:
-            assert [k[0] for k in keys] == [l for l in order for _ in plan.slices_of_layer(l)]
-        assert len(q) == 0
-        with pytest.raises(DeadlockError):
-            q.poll(0.05)
-        q.put_batch(frames(3))
-        with pytest.raises(ValueError):
-            q.put_batch(frames(3))  # still queued
-        threading.Timer(0.1, q.close).start()
-        assert q.poll(1.0).layer_index == 3
-        t0 = time.monotonic()
-        assert q.poll(2.0) is None and time.monotonic() - t0 < 1.5
-        with pytest.raises(RuntimeError):
-            q.put_batch(frames(4))
-    q = FrameQueue.for_plan(plan)
-    with pytest.raises(ValueError):
-        q.put_batch(frames(0)[:1] if len(frames(0)) > 1 else frames(0) + frames(1))
-
-
 @pytest.mark.parametrize("world,push", [(2, "fp32"), (3, "fp32"), (4, "fp32"), (2, "bf16"), (4, "bf16")])
 def test_momentum_multi_rank_matches_oracle(cuda, world, push):
     """Fused momentum at N>1 (owned-slot momentum buffers, TMA-staged v tiles), rank-distinct
