@@ -89,6 +89,43 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(rows)}
 
 
+class NvlinkCounters:
+    """NVLink data bytes sent / received by this GPU (NVML field values THROUGHPUT_DATA_TX/RX,
+    KiB, summed over the links), read around a measured phase: the traffic of the transfers."""
+
+    FIELDS = (138, 139)  # NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX / _RX
+
+    def __init__(self, device_index: int) -> None:
+        self.ok = False
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self._nvml = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self.links = [l for l in range(18) if self._link_up(l)]
+            self.ok = bool(self.links)
+        except Exception:  # noqa: BLE001 - no NVML / no NVLink: traffic stays null
+            self.ok = False
+
+    def _link_up(self, link: int) -> bool:
+        try:
+            return bool(self._nvml.nvmlDeviceGetNvLinkState(self.h, link))
+        except Exception:  # noqa: BLE001
+            return False
+
+    def read(self) -> tuple[int, int] | None:
+        if not self.ok:
+            return None
+        ids = [(f, l) for f in self.FIELDS for l in self.links]
+        vals = self._nvml.nvmlDeviceGetFieldValues(self.h, ids)
+        tot = [0, 0]
+        for (f, _), v in zip(ids, vals):
+            if v.nvmlReturn == 0:
+                tot[self.FIELDS.index(f)] += int(v.value.ullVal)
+        return tot[0] * 1024, tot[1] * 1024
+
+
 def dist_setup(args):
     import torch
     import torch.distributed as dist
@@ -207,7 +244,12 @@ def sync_only_roofline(args, world, rank, counts):
     stream.synchronize()
     times = []
     reps = args.sync_reps
+    nvl = NvlinkCounters(torch.cuda.current_device()) if world > 1 else None
+    nvl0 = None
     for k in range(reps + 2):
+        if k == 2 and nvl is not None:
+            torch.cuda.synchronize()
+            nvl0 = nvl.read()
         with torch.cuda.stream(stream):
             flush.fill_(k & 0xFF)
         for l in range(len(counts)):  # published before the iteration opens: no DRAIN launches
@@ -229,16 +271,98 @@ def sync_only_roofline(args, world, rank, counts):
         stream.synchronize()
         if k >= 2:
             times.append(max_over_ranks(s.elapsed_time(e), world))
+    traffic = None
+    if nvl0 is not None:
+        nvl1 = nvl.read()
+        if nvl1 is not None:  # NVLink TX bytes per launch (the all-reduce that aligns the ranks: 4 B)
+            traffic = {"tx_bytes_per_launch": (nvl1[0] - nvl0[0]) / reps, "rx_bytes_per_launch": (nvl1[1] - nvl0[1]) / reps,
+                       "source": "NVML NVLink THROUGHPUT_DATA_TX/RX counters around the timed launches"}
     ctx.close()
-    return statistics.mean(times), ctas
+    return statistics.mean(times), ctas, traffic
+
+
+def training_sync_profile(args, world, rank, x, y, steps=4, warmup=3):
+    """The comm kernel inside training, from its device trace (a traced P3DataParallel run of
+    `steps` steps): per iteration, the bytes this rank moved over its link and when — how much
+    of the sync overlapped the backward pass (before the last publication) and the exposed
+    tail after it, with that tail's throughput (the FINISH phase of the shipped launch policy)."""
+    import torch
+
+    from paper_1905_03960_b200 import _lib
+    from paper_1905_03960_b200.ddp import P3DataParallel
+    from paper_1905_03960_b200.torch_models import loss_fn
+
+    model = build(args, rank)
+    P = sum(p.numel() for p in model.parameters())
+    d = P3DataParallel(model, lr=args.lr, max_slice=args.max_slice, comm_ctas=args.comm_ctas,
+                       trace_cap=(steps + warmup + 1) * 8 * (P // args.max_slice + 400))
+    for _ in range(warmup + steps):
+        loss_fn(args.model, d, x, y).backward()
+    d.synchronize()
+    torch.cuda.synchronize()
+    tr = d.ctx.trace(0)
+    plan_counts = d.ctx.layer_counts
+    from paper_1905_03960_b200.model import LayerSpec, ModelProfile
+    from paper_1905_03960_b200.plan import make_p3_plan
+
+    plan = make_p3_plan(ModelProfile("m", 0, tuple(LayerSpec(i, "t", c, 0, 0) for i, c in enumerate(plan_counts))),
+                        world, args.max_slice)
+    rows = []
+    for k in range(warmup, warmup + steps):
+        ev = [e for e in tr if e.iteration == k]
+        pubs = [e.t_ns for e in ev if e.event == _lib.P3_EV_PUBLISH]
+        moves = [e for e in ev if e.event in (_lib.P3_EV_PUSH, _lib.P3_EV_BCAST)]
+        if not pubs or not moves:
+            continue
+        t_last = max(pubs)
+        # N > 1: this rank's NVLink egress — pushes of slices it does not own + (N-1) broadcast
+        # copies of owned ones; N = 1: the update's HBM bytes (read g, read p, write p)
+        own = {(s.key.layer_index, s.key.slice_index): s for s in plan.slices}
+        egress_before = egress_after = 0
+        for e in moves:
+            sl = own[(e.layer, e.slice)]
+            if world == 1:
+                nb = 12 * sl.length if e.event == _lib.P3_EV_BCAST else 0
+            elif e.event == _lib.P3_EV_PUSH and sl.server != rank:
+                nb = 4 * sl.length
+            elif e.event == _lib.P3_EV_BCAST:
+                nb = 4 * sl.length * (world - 1)
+            else:
+                continue
+            if e.t_ns <= t_last:
+                egress_before += nb
+            else:
+                egress_after += nb
+        t_end = max(e.t_ns for e in moves)
+        rows.append((egress_before, egress_after, (t_end - t_last) / 1e6))
+    d.close()
+    if not rows:
+        return None
+    eb = statistics.mean(r[0] for r in rows)
+    ea = statistics.mean(r[1] for r in rows)
+    tail_ms = statistics.mean(r[2] for r in rows)
+    return {
+        "bytes_per_iteration": eb + ea,
+        "bytes": "NVLink egress of this rank" if world > 1 else "HBM bytes of the update (12 B/param)",
+        "overlapped_fraction": eb / (eb + ea) if eb + ea else None,
+        "exposed_tail_ms": tail_ms,
+        "tail_GBps": ea / (tail_ms * 1e-3) / 1e9 if tail_ms > 0 and ea else None,
+        "steps": len(rows),
+        "how": "device trace of a P3DataParallel training run: PUBLISH / PUSH / BCAST records on %globaltimer; "
+               "egress = pushes of slices owned elsewhere + (N-1) broadcast copies of owned slices",
+    }
 
 
 def cpu_reference(counts, world, batch, steps, warmup, seconds_budget=20.0):
-    """The reference P3 iteration on host cores (oracle port), bounded sample."""
+    """The reference's P3 sync iteration on host cores, bounded sample: the reference's own
+    code from baseline/_ref (kind "reference": FrameQueue, GradGen, ShardState) when it is
+    installed, else the numpy restatement (kind "port")."""
     sys.path.insert(0, str(REPO / "oracle"))
+    import ref_p3
     from cpu_p3 import CpuP3
 
-    cpu = CpuP3(counts, world)
+    kind = "reference" if ref_p3.available() else "port"
+    cpu = ref_p3.RefP3(counts, world) if kind == "reference" else CpuP3(counts, world)
     n_slices = len(cpu.rows)
     dt, frac = cpu.time_iteration(0, sample_slices=min(n_slices, 32))  # calibrate
     per_iter = dt / frac
@@ -257,10 +381,12 @@ def cpu_reference(counts, world, batch, steps, warmup, seconds_budget=20.0):
         "value": batch * world / iter_s,
         "unit": "samples/sec",
         "cores": cpu.threads,
-        "kind": "port",
+        "kind": kind,
         "sample": f"{sample} of {n_slices} slices per step (priority pop order), {steps} steps, scaled to a full "
                   f"iteration; sync path only (GradGen materialise + rank-ordered aggregate + SGD + replica apply), "
-                  f"compute excluded",
+                  f"compute excluded; " + ("the reference's own p3sync objects (baseline/_ref)" if kind == "reference"
+                                           else "numpy restatement (oracle/cpu_p3.py)") +
+                  f"; {cpu.threads} threads of nproc {os.cpu_count()}",
         "seconds_per_iteration": iter_s,
     }
 
@@ -282,6 +408,9 @@ def run_reference(args):
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic (GradGen gradients)",
         "config": {"workload": f"{args.model} P3 sync path, {world} ranks, {args.max_slice}-param slices",
                    "global_batch": batch * world, "max_slice": args.max_slice},
+        "note": "the reference computes no model (its compute is emulated by sleeps, worker.py:299-310): this is its "
+                "sync path per iteration at the model's shapes, converted with the training batch; compare it with "
+                "our line's sync_path (same work on the GPU), not with the training value",
         "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
         "e2e": {"value": cb["value"], "unit": "samples/sec", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
@@ -362,8 +491,13 @@ def run_ours(args):
             torch.cuda.empty_cache()
         throttled["p3_vs_layerwise"] = throttled["p3"] / throttled["layerwise_fifo"]
 
+    # --- the comm kernel inside training (device trace): overlap and exposed tail
+    train_sync = training_sync_profile(args, world, rank, x, y) if not args.skip_sync else None
+    torch.cuda.empty_cache()
+
     # --- slice-sync kernel roofline
-    sync_ms, ctas = sync_only_roofline(args, world, rank, counts) if not args.skip_sync else (float("nan"), 0)
+    sync_ms, ctas, nvl_traffic = (sync_only_roofline(args, world, rank, counts) if not args.skip_sync
+                                  else (float("nan"), 0, None))
     peaks = json.loads((REPO / "MEASURED_PEAKS.json").read_text()) if (REPO / "MEASURED_PEAKS.json").exists() else {}
     if world == 1:
         alg = 12 * P  # read G + read W + write W per element (SURVEY §8(d), K4 with N=1)
@@ -379,11 +513,15 @@ def run_ours(args):
     # capture (profiles/ncu_traffic.json), when one exists for this model and world size
     traffic = None
     tf = REPO / "profiles" / "ncu_traffic.json"
-    if tf.exists():
+    if tf.exists() and world == 1:
         t = json.loads(tf.read_text()).get(args.model)
         if t and t["world"] == world and t["max_slice"] == args.max_slice:
             traffic = t["dram_bytes_read"] + t["dram_bytes_write"]
-    roof.update({"frac": roof["achieved"] / peak, "traffic": traffic, "kernel": "k_comm (K3 push + K4 reduce/SGD/bcast)",
+    if world > 1 and nvl_traffic is not None:  # NVLink bytes actually sent per launch (NVML counters)
+        traffic = nvl_traffic["tx_bytes_per_launch"]
+        roof["traffic_detail"] = nvl_traffic
+    roof.update({"frac": roof["achieved"] / peak, "traffic": traffic,
+                 "kernel": "k_comm (K3 push + K4 reduce/SGD/bcast)" + (", SWEEP mode" if world == 1 else ""),
                  "algorithmic_bytes_per_launch": alg, "launch_ms": sync_ms, "ctas": ctas,
                  "measured_in": "sync-only phase: all layers' gradients in HBM and published, one launch per "
                                 "iteration over the whole GPU, L2 flushed (256 MB write) between launches"})
@@ -391,9 +529,19 @@ def run_ours(args):
     out = None
     if rank == 0:
         cpu = None
-        if world == 1 and not args.skip_cpu:
+        if not args.skip_cpu:
             cb = cpu_reference(counts, world, batch, 3, 1)
             cpu = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        # like-for-like: the same sync work per iteration (every slice of the model through
+        # aggregate + SGD + replica apply) on the GPU (sync-only launch) and on the host cores
+        gpu_sync = batch * world / (sync_ms * 1e-3) if sync_ms == sync_ms else None
+        sync_path = {"gpu_samples_per_s": gpu_sync, "gpu_ms_per_iteration": sync_ms,
+                     "cpu_samples_per_s": cpu["value"] if cpu else None,
+                     "cpu_ms_per_iteration": 1000.0 * batch * world / cpu["value"] if cpu else None,
+                     "gpu_over_cpu": gpu_sync / cpu["value"] if (cpu and gpu_sync) else None,
+                     "what": "one iteration of the P3 sync path at the model's shapes (aggregate in rank order + SGD "
+                             "+ apply to every replica; the CPU side also materialises GradGen gradients) — the "
+                             "reference arm measures this; the training value above adds the model's compute"}
         out = {
             "metric": METRIC, "value": value, "unit": "samples/sec", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
@@ -401,7 +549,16 @@ def run_ours(args):
             "data": "synthetic (random-init weights, N(0,1) bf16 images / uniform labels)",
             "config": {"workload": f"{args.model} bf16-autocast training, P3 sliced priority sync",
                        "model": args.model, "per_gpu_batch": batch, "global_batch": batch * world,
-                       "max_slice": args.max_slice, "comm_ctas": args.comm_ctas, "parallelism": f"dp{world}",
+                       "max_slice": args.max_slice,
+                       "comm_launches": (f"{args.comm_ctas}-CTA DRAIN launches during the backward pass + one "
+                                         f"{args.comm_ctas}-CTA FINISH launch per step" if world > 1 else
+                                         f"one {torch.cuda.get_device_properties(0).multi_processor_count}-CTA FINISH "
+                                         "launch per step (SWEEP mode: nothing to overlap at N=1)"),
+                       "pop_order": ("bounded relaxation: each pop among the C most urgent available layers, C = CTAs "
+                                     "of its launch; strict FrameQueue order is the strict_order mode (tests)"
+                                     if world > 1 else "guided chunk claims of the priority-ordered element space, "
+                                     "in order (bounded by the concurrent CTAs)"),
+                       "parallelism": f"dp{world}",
                        "model_compute": "bf16 autocast (fp32 master parameters)",
                        "params": P, "tensors": len(counts), "l2": "activations >> 126 MB L2 each step"},
             "e2e": {"value": e2e_value, "unit": "samples/sec", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 4}
@@ -411,6 +568,8 @@ def run_ours(args):
             "throttled": throttled,
             "roofline": roof,
             "slice_sync": {"ms": sync_ms, "GBps_per_gpu": roof["achieved"], "bound": roof["bound"]},
+            "sync_path": sync_path,
+            "training_sync": train_sync,
             "cpu_baseline": cpu,
             "clocks": clocks,
             "gpu_launches": gpu_launches,

@@ -64,6 +64,11 @@ extern "C" {
                               (IterationRecord.start, worker.py:312-313) */
 #define P3_EV_SYNCED 6     /* p3_trace_mark: every layer of `iteration` synced on that rank
                               (sync_end_times, worker.py:265-268) */
+#define P3_EV_NOTIFY 7     /* notify mode: owner told rank `rank` that slice (layer, slice) is
+                              updated (server.py:227-239) */
+#define P3_EV_PULL 8       /* notify mode: this rank asked owner `rank` for the slice
+                              (worker.py:226-239); the answer is a BCAST record at the owner
+                              with rank = the requester */
 
 /* One row of a SlicePlan (plan.py:30-45: SliceKey + Slice). */
 typedef struct p3_slice {
@@ -250,6 +255,12 @@ typedef struct p3_config {
                                           comm_ctas = finish_ctas = 1 and pop_relax = 1 there is
                                           one consumer at a time: the strict FrameQueue order
                                           (queues.py:52-62), checked by trace replay */
+  uint32_t notify_pull;                /* N > 1, the baseline's protocol (server.py:227-247,
+                                          worker.py:226-239): the owner updates only its own
+                                          replica and NOTIFYs the other ranks; each replica
+                                          queues a PULL behind its pushes and the owner answers
+                                          it with the slice (one more round trip than P3's
+                                          broadcast) */
 } p3_config_t;
 
 /* Builds the plan, allocates per-local-rank arenas (parameters W zero-initialised like
@@ -314,6 +325,18 @@ int p3_wait_layer(p3_ctx_t* ctx, uint32_t local_idx, uint32_t layer, uint64_t it
  * for forward pass `iteration` — one stream memory wait for a whole module. */
 int p3_wait_group(p3_ctx_t* ctx, uint32_t local_idx, uint32_t group, uint64_t iteration,
                   void* stream);
+
+/* TrainingWorker.on_bcast (worker.py:241-269) for a BCAST frame that arrived on the host
+ * (the wire path beyond the NVSwitch domain): copy `n` fp32 values of slice (layer, slice)
+ * into the local replica W at the slice's offset and count the slice towards the layer's
+ * forward gate (done[layer], its gate group) — stream-ordered on `stream`. `n` must equal the
+ * slice length (P3_EPROTOCOL otherwise). Iteration / duplicate checks are the caller's. */
+int p3_apply_slice(p3_ctx_t* ctx, uint32_t local_idx, uint32_t layer, uint32_t slice, const float* values_host,
+                   uint64_t n, void* stream);
+
+/* flags[layer] of the reference worker (worker.py:74-75): the forward pass whose parameters
+ * layer `layer` of a local rank holds = done[layer] / slices of the layer (device read). */
+int p3_layer_flag(p3_ctx_t* ctx, uint32_t local_idx, uint32_t layer, uint64_t* iteration);
 
 /* TrainingWorker._wait_all (worker.py:287-289) + error check: block the host until the
  * comm kernels finished and every local layer reached `iteration`, or timeout. */

@@ -32,6 +32,8 @@ P3_EV_COMPLETE = 3
 P3_EV_PICK = 4
 P3_EV_ITER_START = 5
 P3_EV_SYNCED = 6
+P3_EV_NOTIFY = 7
+P3_EV_PULL = 8
 
 LIB_PATH = Path(__file__).resolve().parent / "libp3.so"
 
@@ -104,6 +106,7 @@ class Config(ctypes.Structure):
         ("push_bf16", ctypes.c_uint32),
         ("gate_groups", ctypes.POINTER(ctypes.c_uint32)),
         ("drain_streams", ctypes.c_uint32),
+        ("notify_pull", ctypes.c_uint32),
     ]
 
 
@@ -144,6 +147,8 @@ SIGNATURES = {
     "p3_sync_all": (ctypes.c_int, [_P, _U64, ctypes.c_double]),
     "p3_trace_read": (ctypes.c_int, [_P, _U32, ctypes.POINTER(TraceRec), _U64, _PU64]),
     "p3_trace_clear": (ctypes.c_int, [_P]),
+    "p3_apply_slice": (ctypes.c_int, [_P, _U32, _U32, _U32, _P, _U64, _P]),
+    "p3_layer_flag": (ctypes.c_int, [_P, _U32, _U32, _PU64]),
     "p3_fq_create": (ctypes.c_int, [_U32, ctypes.POINTER(_P)]),
     "p3_fq_put_batch": (ctypes.c_int, [_P, _PU64, _PU64, _U64]),
     "p3_fq_poll": (ctypes.c_int, [_P, _PU64]),

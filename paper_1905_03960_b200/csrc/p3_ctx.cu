@@ -90,14 +90,14 @@ using namespace p3;
 
 // Peer-visible arena of one rank: W | R | arrivals | hint | done (256-byte aligned parts).
 struct PeerLayout {
-  uint64_t w, r, arrivals, hint, tally, done, gdone, bytes;
+  uint64_t w, r, arrivals, hint, tally, done, gdone, ntf_tail, ntf_ring, pull_tail, pull_ring, bytes;
 };
 
 // Local arena of one rank. The per-iteration part (cursor | srv_lo | srv_taken | it) is
 // contiguous so one memset resets it before each launch.
 struct LocalLayout {
-  uint64_t pub, fifo_key, claim, iter_begin, cursor, srv_lo, srv_taken, it, iter_end, V, bytes,
-      trace_n, trace, cta_phase, vclock, pubseq, ingested, total;
+  uint64_t pub, fifo_key, claim, iter_begin, cursor, srv_lo, srv_taken, it, sweep, slice_elems, pcount, iter_end, V,
+      bytes, trace_n, trace, cta_phase, vclock, pubseq, ingested, heads, total;
 };
 
 struct p3_ctx {
@@ -113,7 +113,8 @@ struct p3_ctx {
   // P3_TMA=0 (direct loads instead of the TMA stage ring), P3_PUSH_SPLIT=n, P3_SRV_FILTER=n,
   // P3_TRACE_CTA=1 (trace records carry CTA indices; CTA start / exit records)
   struct {
-    uint32_t use_tma = 1, push_split = 0, srv_filter = 0, trace_cta = 0, srv_reserve = 0, tma_store = 1, tma_store_red = 0, pop_relax = 0;
+    uint32_t use_tma = 1, push_split = 0, srv_filter = 0, trace_cta = 0, srv_reserve = 0, tma_store = 1, tma_store_red = 0, pop_relax = 0,
+             no_sweep = 0;
   } knobs;
   std::vector<uint32_t> own_total;
   std::vector<uint64_t> own_stride;
@@ -197,6 +198,15 @@ PeerLayout peer_layout_of(const p3_ctx* c, uint32_t rank) {
   o = align_up(o + (uint64_t)c->L * 4, 256);
   p.gdone = o;
   o = align_up(o + (uint64_t)c->G * 4, 256);
+  const bool ring = c->cfg.notify_pull && c->N > 1;
+  p.ntf_tail = o;
+  o = align_up(o + 4, 256);
+  p.ntf_ring = o;
+  o = align_up(o + (ring ? (uint64_t)c->S * 8 : 8), 256);
+  p.pull_tail = o;
+  o = align_up(o + 4, 256);
+  p.pull_ring = o;
+  o = align_up(o + (ring ? (uint64_t)c->S * (c->N - 1) * 8 : 8), 256);
   p.bytes = o;
   return p;
 }
@@ -216,6 +226,9 @@ LocalLayout local_layout_of(const p3_ctx* c, uint64_t v_elems) {
   take(q.srv_lo, c->L * 4ull);
   take(q.srv_taken, c->L * 4ull);
   take(q.it, sizeof(IterState));
+  take(q.sweep, 8);
+  take(q.slice_elems, c->S * 4ull);
+  take(q.pcount, 8);
   q.iter_end = o;
   take(q.V, v_elems * 4);
   take(q.bytes, 16);
@@ -225,6 +238,7 @@ LocalLayout local_layout_of(const p3_ctx* c, uint64_t v_elems) {
   take(q.vclock, 8);
   take(q.pubseq, 4);
   take(q.ingested, 4);
+  take(q.heads, 8);
   q.total = o;
   return q;
 }
@@ -238,6 +252,10 @@ void set_peer_pointers(p3_ctx* c, uint32_t rank, char* base) {
   c->peers.tally[rank] = reinterpret_cast<uint32_t*>(base + p.tally);
   c->peers.done[rank] = reinterpret_cast<uint32_t*>(base + p.done);
   c->peers.gdone[rank] = reinterpret_cast<uint32_t*>(base + p.gdone);
+  c->peers.ntf_tail[rank] = reinterpret_cast<uint32_t*>(base + p.ntf_tail);
+  c->peers.ntf_ring[rank] = reinterpret_cast<unsigned long long*>(base + p.ntf_ring);
+  c->peers.pull_tail[rank] = reinterpret_cast<uint32_t*>(base + p.pull_tail);
+  c->peers.pull_ring[rank] = reinterpret_cast<unsigned long long*>(base + p.pull_ring);
 }
 
 int check_local(p3_ctx* c, uint32_t li) {
@@ -310,6 +328,7 @@ int p3_ctx_create(const p3_config_t* cfg, p3_ctx_t** out) {
     c->knobs.tma_store = env_u32("P3_TMA_STORE", 1);
     c->knobs.pop_relax = env_u32("P3_POP_RELAX", 0);  // 0: the config's
     c->knobs.tma_store_red = env_u32("P3_TMA_STORE_RED", 0);
+    c->knobs.no_sweep = env_u32("P3_NO_SWEEP", 0);  // single rank: slice pops in the FINISH launch
   }
   std::string perr;
   int rc = cfg->plan_mode == P3_PLAN_P3
@@ -421,6 +440,10 @@ int p3_ctx_create(const p3_config_t* cfg, p3_ctx_t** out) {
   std::vector<uint32_t> own_base(N, 0);
   for (uint32_t o = 1; o < N; ++o) own_base[o] = own_base[o - 1] + c->own_total[o - 1];
   const size_t o_ob = put(own_base.data(), N * 4ull);
+  std::vector<uint64_t> pstart(L + 1, 0);
+  for (uint32_t l = 0; l < L; ++l) pstart[l + 1] = pstart[l] + align_up(c->counts[l], 8);
+  const size_t o_ps = put(pstart.data(), (L + 1) * 8ull);
+  const size_t o_lc = put(c->counts.data(), L * 8ull);
   bool rr = true;
   for (uint32_t g = 0; g < S && rr; ++g) rr = slice_owner[g] == g % N;
   cudaError_t e = cudaMalloc(&c->d_plan, blob.size());
@@ -453,6 +476,8 @@ int p3_ctx_create(const p3_config_t* cfg, p3_ctx_t** out) {
   P.own_stride = reinterpret_cast<const uint64_t*>(pb + o_ost);
   P.layer_group = reinterpret_cast<const uint32_t*>(pb + o_lg);
   P.own_base = reinterpret_cast<const uint32_t*>(pb + o_ob);
+  P.layer_pstart = reinterpret_cast<const uint64_t*>(pb + o_ps);
+  P.layer_count = reinterpret_cast<const uint64_t*>(pb + o_lc);
   P.rr_owner = rr ? 1u : 0u;
 
   // ---- per-rank arenas
@@ -496,6 +521,11 @@ int p3_ctx_create(const p3_config_t* cfg, p3_ctx_t** out) {
     D.vclock = reinterpret_cast<unsigned long long*>(lb + ll.vclock);
     D.pubseq = reinterpret_cast<uint32_t*>(lb + ll.pubseq);
     D.ingested = reinterpret_cast<uint32_t*>(lb + ll.ingested);
+    D.sweep = reinterpret_cast<unsigned long long*>(lb + ll.sweep);
+    D.slice_elems = reinterpret_cast<uint32_t*>(lb + ll.slice_elems);
+    D.pcount = reinterpret_cast<uint32_t*>(lb + ll.pcount);
+    D.ntf_head = reinterpret_cast<uint32_t*>(lb + ll.heads);
+    D.pull_head = D.ntf_head + 1;
     D.ring_cap = 4 * L + 64;
     if (e == cudaSuccess)
       e = cudaHostAlloc((void**)&c->ring_host[i], D.ring_cap * sizeof(PubEntry) + 256, cudaHostAllocMapped);
@@ -639,6 +669,9 @@ static CommArgs comm_args(p3_ctx* c, uint32_t mode, uint32_t ctas) {
                              : std::max<uint32_t>(1, std::min<uint32_t>(8, c->S / std::max<uint32_t>(1, 4 * ctas)));
   a.pop_multi = std::max<uint32_t>(1, std::min<uint32_t>(4, c->cfg.pop_multi ? c->cfg.pop_multi : 1));
   a.push_bf16 = c->cfg.push_bf16 ? 1u : 0u;
+  a.notify = c->cfg.notify_pull && c->N > 1 ? 1u : 0u;
+  a.ntf_cap = c->S;
+  a.pull_cap = c->S * (c->N > 1 ? c->N - 1 : 1);
   a.trace_cta = c->knobs.trace_cta;
   a.push_split = c->knobs.push_split;
   a.srv_filter = c->knobs.srv_filter;
@@ -732,7 +765,12 @@ int p3_iteration_end(p3_ctx_t* c, uint64_t k) {
     CK(cudaStreamWaitEvent(c->comm_stream, c->side_ev[j], 0));
   }
   const uint32_t ctas = c->cfg.finish_ctas ? c->cfg.finish_ctas : c->cfg.comm_ctas;
-  if (launch_comm(comm_args(c, P3_COMM_FINISH, ctas), ctas, c->cfg.comm_threads, c->comm_stream) != P3_OK)
+  // Single rank, no DRAIN launch this iteration and bounded relaxation allowed: the FINISH
+  // launch is the only consumer and every layer is published, so it sweeps the priority-
+  // ordered element space in guided chunks (perfect balance over the CTAs, claims in order).
+  const bool sweep = c->N == 1 && c->side_used == 0 && c->cfg.pop_relax != 1 && !c->knobs.no_sweep;
+  if (launch_comm(comm_args(c, sweep ? P3_COMM_SWEEP : P3_COMM_FINISH, ctas), ctas, c->cfg.comm_threads,
+                  c->comm_stream) != P3_OK)
     return cuda_fail(c, cudaGetLastError(), "comm kernel launch");
   c->launches++;
   CK(cudaEventRecord(c->comm_done, c->comm_stream));
@@ -843,6 +881,35 @@ int p3_wait_group(p3_ctx_t* c, uint32_t li, uint32_t group, uint64_t k, void* st
   uint32_t* flag = c->peers.gdone[c->cfg.local_ranks[li]] + group;
   CUresult r = driver().wait32((CUstream)stream, (CUdeviceptr)flag, target, CU_STREAM_WAIT_VALUE_GEQ);
   if (r != CUDA_SUCCESS) return fail(c, P3_ECUDA, "cuStreamWaitValue32 failed (code " + std::to_string(r) + ")");
+  return P3_OK;
+}
+
+int p3_apply_slice(p3_ctx_t* c, uint32_t li, uint32_t layer, uint32_t slice, const float* values, uint64_t n,
+                   void* stream) {
+  int rc = check_local(c, li);
+  if (rc) return rc;
+  if (layer >= c->L || slice >= c->layer_nslices[layer]) return fail(c, P3_EPROTOCOL, "BCAST for unknown slice");
+  const p3_slice_t& r = c->plan[c->layer_first[layer] + slice];
+  if (n != r.length)
+    return fail(c, P3_EPROTOCOL, "slice payload holds " + std::to_string(n) + " values, expected " +
+                                     std::to_string(r.length));
+  if (!values) return fail(c, P3_EUSAGE, "null payload");
+  const uint32_t rank = c->cfg.local_ranks[li];
+  float* dst = c->peers.W[rank] + c->layer_woff[layer] + r.offset;
+  CK(cudaMemcpyAsync(dst, values, n * 4, cudaMemcpyHostToDevice, (cudaStream_t)stream));
+  if (launch_bump(c->peers.done[rank] + layer, c->peers.gdone[rank] + c->layer_group[layer], 1, stream) != P3_OK)
+    return cuda_fail(c, cudaGetLastError(), "gate counter update");
+  return P3_OK;
+}
+
+int p3_layer_flag(p3_ctx_t* c, uint32_t li, uint32_t layer, uint64_t* iteration) {
+  int rc = check_local(c, li);
+  if (rc) return rc;
+  if (layer >= c->L || !iteration) return fail(c, P3_EUSAGE, "layer out of range");
+  uint32_t d = 0;
+  CK(cudaMemcpyAsync(&d, c->peers.done[c->cfg.local_ranks[li]] + layer, 4, cudaMemcpyDeviceToHost, c->poll_stream));
+  CK(cudaStreamSynchronize(c->poll_stream));
+  *iteration = d / c->layer_nslices[layer];
   return P3_OK;
 }
 

@@ -16,6 +16,8 @@
 #define P3_DBG_CTAS 512
 #define P3_COMM_DRAIN 0   // exit as soon as nothing is poppable or reducible
 #define P3_COMM_FINISH 1  // exit when the iteration's local work is complete
+#define P3_COMM_SWEEP 2   // single rank, every layer published, no other consumer: claim chunks of
+                          // the priority-ordered element space (guided sizes) until it is covered
 
 namespace p3 {
 
@@ -52,6 +54,9 @@ struct PlanDev {
   const uint64_t* own_stride;     // [world] R block stride (padded owned elements)
   const uint32_t* layer_group;    // [L] forward-gate group of the layer
   const uint32_t* own_base;       // [world] first own_list position of each owner
+  const uint64_t* layer_pstart;   // [L+1] start of each layer in the padded flat element space
+                                  // (layers in priority order, each padded to a multiple of 8)
+  const uint64_t* layer_count;    // [L] parameters of each layer
 };
 
 // Peer-visible state of every rank (pointers valid in this process: local or IPC-mapped).
@@ -63,6 +68,12 @@ struct PeersDev {
   uint32_t* tally[P3_MAX_RANKS];     // [2] pushes arrived, owned slices completed (monotone)
   uint32_t* done[P3_MAX_RANKS];      // [L] slices of a layer broadcast into W (monotone)
   uint32_t* gdone[P3_MAX_RANKS];     // [G] slices of a gate group broadcast into W (monotone)
+  // notify mode: NOTIFY ring of each rank (entries ((k+1) << 32) | slice, appended by owners)
+  // and PULL ring of each owner (entries ((k+1) << 40) | (requester << 32) | slice)
+  uint32_t* ntf_tail[P3_MAX_RANKS];
+  unsigned long long* ntf_ring[P3_MAX_RANKS];
+  uint32_t* pull_tail[P3_MAX_RANKS];
+  unsigned long long* pull_ring[P3_MAX_RANKS];
 };
 
 // Per-iteration scratch of one local rank; zeroed before each comm launch.
@@ -107,6 +118,11 @@ struct LocalDev {
   uint32_t* pubseq;            // ring entries published (stream memory write, monotone)
   uint32_t* ingested;          // ring entries turned into publication words (monotone)
   uint32_t* ingested_host;     // host-mapped mirror of `ingested` (host back-pressure)
+  unsigned long long* sweep;   // SWEEP: next unclaimed position of the padded flat space (per iteration)
+  uint32_t* slice_elems;       // [S] SWEEP: elements of each slice updated so far (per iteration)
+  uint32_t* ntf_head;          // notify mode: NOTIFY entries consumed (monotone)
+  uint32_t* pull_head;         // notify mode: PULL requests answered or claimed (monotone)
+  uint32_t* pcount;            // [2] notify mode, per iteration: PULLs sent, PULLs answered
 };
 
 struct CommArgs {
@@ -125,6 +141,8 @@ struct CommArgs {
   uint32_t pop_relax; // a pop may take any of this many most urgent layers (1: strict)
   uint32_t pop_multi; // candidate layers claimed per round of pop atomics
   uint32_t push_bf16; // pushes travel as bf16
+  uint32_t notify;    // notify mode (P3 config notify_pull, N > 1)
+  uint32_t ntf_cap, pull_cap;  // ring entries
   uint32_t push_split; // every push_split-th CTA prefers pushes over server work (0: none)
   uint32_t srv_filter; // server picks: only srv_filter x (ready slices) consumers look (0: all)
   uint32_t srv_reserve; // N > 1: every srv_reserve-th CTA does server work only (0: none)
@@ -144,6 +162,7 @@ int launch_comm(const CommArgs& a, uint32_t ctas, uint32_t threads, void* stream
 int launch_gradgen(uint64_t seed, uint64_t iteration, uint64_t layer, uint64_t start, uint64_t count,
                    float* out, void* stream);
 int launch_mark(const LocalDev& L, uint32_t k, uint32_t ev, void* stream);
+int launch_bump(uint32_t* done, uint32_t* gdone, uint32_t v, void* stream);
 int launch_queue_pop(const uint32_t* nslices, const uint32_t* first, const uint64_t* pub,
                      const uint32_t* fifo_key, uint32_t* cursor, uint32_t n_layers, uint32_t sched,
                      uint32_t tag, uint32_t* result, void* stream);

@@ -862,8 +862,14 @@ __device__ __forceinline__ QueueView queue_of(const CommArgs& a, const LocalDev&
 #define JOB_REDUCE 1
 #define JOB_PUSH 2
 #define JOB_EXIT 3
+#define JOB_ANSWER 4  // scheduler only: becomes a PUSH-shaped slot with `answer` set
 struct Job {
   uint32_t kind, li, g, layer, opos, rank, len, n, aligned, run;  // opos: position in the owner's list
+  uint32_t ndst;    // REDUCE: replicas written (dst[0..ndst)): N, or 1 when peers pull (notify mode)
+  uint32_t answer;  // PUSH-shaped copy of an updated slice to a peer that pulled it (notify mode)
+  uint32_t piece;  // SWEEP: the job updates elements [e0, e0 + len) of layer `layer` (slices
+                   // complete when all their elements are done, counted per element)
+  uint32_t e0;
   uint32_t bf16;  // pushes travel as bf16 (declared lossy mode); own = index of the fp32 source
   const float* src[P3_MAX_RANKS];  // PUSH: src[0]; REDUCE: contributions in rank order
   float* dst[P3_MAX_RANKS];        // PUSH: dst[0]; REDUCE: replicas, dst[0] = owner's master
@@ -874,10 +880,14 @@ struct Job {
 //   FULL(b)  scheduler arrives, producer + signaler sync    (slot b holds a job)
 //   DONE(b)  consumers arrive, signaler syncs               (the job's data has moved)
 //   EMPTY(b) signaler arrives, scheduler syncs              (slot b may be refilled)
+#ifndef P3_SLOTS
+#define P3_SLOTS 4  // job slots: the scheduler prepares up to P3_SLOTS - 1 jobs ahead of the movers
+#endif
 #define BAR_FULL(b) (1 + (b))
-#define BAR_DONE(b) (3 + (b))
-#define BAR_EMPTY(b) (5 + (b))
-#define BAR_RANGE 7  // consumers among themselves (direct-path scratch)
+#define BAR_DONE(b) (1 + P3_SLOTS + (b))
+#define BAR_EMPTY(b) (1 + 2 * P3_SLOTS + (b))
+#define BAR_RANGE (1 + 3 * P3_SLOTS)  // consumers among themselves (direct-path scratch)
+static_assert(BAR_RANGE <= 15, "16 named barriers per CTA");
 __device__ __forceinline__ void bar_sync(uint32_t id, uint32_t n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
@@ -1001,6 +1011,9 @@ __device__ uint32_t prepare_push(const CommArgs& a, uint32_t li, uint32_t g, uin
   }
   if (lane == 0) {
     job->kind = JOB_PUSH;
+    job->piece = 0;
+    job->ndst = 1;
+    job->answer = 0;
     job->run = 1;
     job->n = 1;  // one source (the slot keeps no stale rank count from a previous reduce)
     job->li = li;
@@ -1059,6 +1072,9 @@ __device__ void prepare_reduce(const CommArgs& a, uint32_t li, uint32_t g, uint3
   for (int off = 16; off; off >>= 1) len += __shfl_xor_sync(FULL_MASK, len, off);
   if (q == 0) {
     job->kind = JOB_REDUCE;
+    job->piece = 0;
+    job->ndst = a.notify ? 1u : N;  // notify mode: peers pull the update (server.py:227-247)
+    job->answer = 0;
     job->li = li;
     job->g = g;
     job->layer = l;
@@ -1070,6 +1086,59 @@ __device__ void prepare_reduce(const CommArgs& a, uint32_t li, uint32_t g, uint3
     job->bf16 = a.push_bf16 ? 1u + o : 0u;  // 1 + index of the owner's own (fp32) contribution
     job->aligned = ((al | (uintptr_t)v) & 15) == 0;
   }
+}
+
+// SWEEP (single rank): elements [e0, e0 + len) of layer l (momentum: inside slice g).
+__device__ void prepare_piece(const CommArgs& a, uint32_t l, uint64_t w, uint32_t e0, uint32_t len, uint32_t g,
+                              Job* job) {
+  const PlanDev& P = a.plan;
+  const LocalDev& L = a.loc[0];
+  if ((threadIdx.x & 31) == 0) {
+    const float* src = pub_ptr(w) + e0;
+    float* dst = a.peers.W[L.rank] + P.layer_woff[l] + e0;
+    float* v = L.V ? L.V + P.slice_slot[g] + (e0 - P.slice_off[g]) : nullptr;
+    job->kind = JOB_REDUCE;
+    job->piece = 1;
+    job->ndst = 1;
+    job->answer = 0;
+    job->e0 = e0;
+    job->li = 0;
+    job->g = g;
+    job->layer = l;
+    job->rank = L.rank;
+    job->run = 1;
+    job->len = len;
+    job->n = 1;
+    job->src[0] = src;
+    job->dst[0] = dst;
+    job->v = v;
+    job->bf16 = a.push_bf16 ? 1u : 0u;
+    job->aligned = (((uintptr_t)src | (uintptr_t)dst | (uintptr_t)v) & 15) == 0;
+  }
+}
+
+// Largest layer l with layer_pstart[l] <= pos (one warp; a 32-ary search: one round trip per
+// factor of 32 layers).
+__device__ uint32_t find_layer(const PlanDev& P, uint64_t pos) {
+  const uint32_t lane = threadIdx.x & 31;
+  uint32_t lo = 0, hi = P.n_layers;
+  while (hi - lo > 1) {
+    const uint32_t step = (hi - lo + 31) / 32;
+    const uint32_t idx = lo + lane * step;
+    const bool le = idx < hi && P.layer_pstart[idx] <= pos;
+    const uint32_t m = __ballot_sync(FULL_MASK, le);
+    lo = lo + (31 - __clz(m)) * step;
+    hi = min(hi, lo + step);
+  }
+  return lo;
+}
+
+// Slice of layer l holding element e: slices are equal-sized except the last (make_p3_plan
+// and make_baseline_plan both cut that way).
+__device__ __forceinline__ uint32_t slice_at(const PlanDev& P, uint32_t l, uint64_t e) {
+  const uint32_t first = P.layer_first[l], ns = P.layer_nslices[l];
+  const uint64_t unit = P.slice_len[first];
+  return first + (uint32_t)min(e / unit, (uint64_t)(ns - 1));
 }
 
 // bf16 transport (declared lossy mode): each rank's contribution is rounded to bf16 (round
@@ -1201,9 +1270,9 @@ __device__ void move_range(const CommArgs& a, const Job& j, uint32_t e0, uint32_
   bar_sync(BAR_RANGE, nthr);
   float* v = j.v ? j.v + e0 : nullptr;
   if (bf)
-    cta_update_bf16(ptrs->dst, (int)j.n, ptrs->src, (int)j.n, own, v, n, make_coef(j.n, a.lr, a.momentum), tid, nthr);
+    cta_update_bf16(ptrs->dst, (int)j.ndst, ptrs->src, (int)j.n, own, v, n, make_coef(j.n, a.lr, a.momentum), tid, nthr);
   else
-    cta_update_generic(ptrs->dst[0], ptrs->dst, (int)j.n, ptrs->src, (int)j.n, v, n, j.aligned != 0,
+    cta_update_generic(ptrs->dst[0], ptrs->dst, (int)j.ndst, ptrs->src, (int)j.n, v, n, j.aligned != 0,
                        make_coef(j.n, a.lr, a.momentum), tid, nthr);
   bar_sync(BAR_RANGE, nthr);  // the scratch may be rewritten by the next range
 }
@@ -1249,7 +1318,7 @@ __device__ __forceinline__ bool job_tma_ok(const Job& j) {
 template <int NW, bool BF, bool MOM>
 __device__ __forceinline__ void consume_reduce(const uint8_t* st, uint32_t pitch, uint32_t n4, uint32_t e4,
                                                float* const* dstp, float* vp, int own, const UpdCoef& c,
-                                               uint32_t tid, uint32_t nthr, bool tosmem = false) {
+                                               uint32_t tid, uint32_t nthr, bool tosmem, int ndst) {
   float4* dst[NW];
 #pragma unroll
   for (int q = 0; q < NW; ++q) dst[q] = reinterpret_cast<float4*>(dstp[q]) + e4;
@@ -1283,7 +1352,8 @@ __device__ __forceinline__ void consume_reduce(const uint8_t* st, uint32_t pitch
     }
     if (MOM) v[k] = vv;
 #pragma unroll
-    for (int q = 0; q < NW; ++q) dst[q][k] = r;
+    for (int q = 0; q < NW; ++q)
+      if (q < ndst) dst[q][k] = r;
   }
 }
 
@@ -1302,6 +1372,7 @@ __device__ void consume_tile(const CommArgs& a, const Job& j, const StageDesc& d
     return;
   }
   const uint32_t N = j.n;
+  const int nd = (int)j.ndst;
   const bool bf = j.bf16 != 0, mom = j.v != nullptr;
   const int own = bf ? (int)j.bf16 - 1 : -1;
   const UpdCoef c = make_coef(N, a.lr, a.momentum);
@@ -1310,11 +1381,11 @@ __device__ void consume_tile(const CommArgs& a, const Job& j, const StageDesc& d
 #define P3_CONSUME(K)                                                                                   \
   case K:                                                                                               \
     if (bf) {                                                                                           \
-      if (mom) consume_reduce<K, true, true>(st, pitch, n4, e4, dst, v, own, c, tid, nthr, tosmem);     \
-      else consume_reduce<K, true, false>(st, pitch, n4, e4, dst, v, own, c, tid, nthr, tosmem);        \
+      if (mom) consume_reduce<K, true, true>(st, pitch, n4, e4, dst, v, own, c, tid, nthr, tosmem, nd);     \
+      else consume_reduce<K, true, false>(st, pitch, n4, e4, dst, v, own, c, tid, nthr, tosmem, nd);        \
     } else {                                                                                            \
-      if (mom) consume_reduce<K, false, true>(st, pitch, n4, e4, dst, v, own, c, tid, nthr, tosmem);    \
-      else consume_reduce<K, false, false>(st, pitch, n4, e4, dst, v, own, c, tid, nthr, tosmem);       \
+      if (mom) consume_reduce<K, false, true>(st, pitch, n4, e4, dst, v, own, c, tid, nthr, tosmem, nd);    \
+      else consume_reduce<K, false, false>(st, pitch, n4, e4, dst, v, own, c, tid, nthr, tosmem, nd);       \
     }                                                                                                   \
     return;
   switch (N) {
@@ -1344,7 +1415,7 @@ __device__ void consume_tile(const CommArgs& a, const Job& j, const StageDesc& d
     float4 vv = mom ? reinterpret_cast<const float4*>(st + (N + 1) * pitch)[k] : make_float4(0.f, 0.f, 0.f, 0.f);
     const float4 r = sgd4(reinterpret_cast<const float4*>(st + N * pitch)[k], acc, c, mom ? &vv : nullptr);
     if (mom) reinterpret_cast<float4*>(v)[e4 + k] = vv;
-    for (uint32_t q = 0; q < N; ++q) reinterpret_cast<float4*>(dst[q])[e4 + k] = r;
+    for (int q = 0; q < nd; ++q) reinterpret_cast<float4*>(dst[q])[e4 + k] = r;
   }
 }
 
@@ -1358,7 +1429,15 @@ __device__ void signal_job(const CommArgs& a, const Job& j) {
   // one fence releases every store the consumers made (ordered before it by the DONE barrier);
   // the counter updates after it are plain relaxed reductions (fire and forget)
   if (a.remote) fence_acq_rel_sys(); else fence_acq_rel_gpu();
-  if (j.kind == JOB_PUSH) {
+  if (j.kind == JOB_PUSH && j.answer) {
+    // notify mode: the pulled slice is in the requester's replica (the BCAST answer of
+    // server.py:240-247; on_bcast, worker.py:241-269)
+    red_add_relaxed_sys(a.peers.done[j.rank] + j.layer, 1u);
+    red_add_relaxed_sys(a.peers.gdone[j.rank] + P.layer_group[j.layer], 1u);
+    atomicAdd(L.pcount + 1, 1u);
+    atomicAdd(L.bytes + 1, 4ull * j.len);
+    if (L.trace_cap) trace_append(L, a.k, j.layer, j.g - P.layer_first[j.layer], j.rank, P3_EV_BCAST);
+  } else if (j.kind == JOB_PUSH) {
     // the last arriver completes the slice and tells the owner's scheduler (hint)
     const uint32_t old = atom_add_relaxed_sys(a.peers.arrivals[j.rank] + j.opos, 1u);
     P3_CHECK(old >= a.k * P.world && old < (a.k + 1) * P.world);  // one push per rank and slice
@@ -1372,6 +1451,38 @@ __device__ void signal_job(const CommArgs& a, const Job& j) {
       }
     }
     atomicAdd(L.bytes + 1, (j.bf16 ? 2ull : 4ull) * j.len);
+  } else if (j.piece) {
+    // SWEEP: a slice is complete when all its elements are (pieces possibly from several CTAs)
+    const uint64_t e1 = (uint64_t)j.e0 + j.len;
+    const uint32_t g1 = slice_at(P, j.layer, e1 - 1);
+    for (uint32_t g = slice_at(P, j.layer, j.e0); g <= g1; ++g) {
+      const uint64_t so = P.slice_off[g], se = so + P.slice_len[g];
+      const uint32_t part = (uint32_t)(min(e1, se) - max((uint64_t)j.e0, so));
+      const uint32_t old = atomicAdd(L.slice_elems + g, part);
+      if (old + part == P.slice_len[g]) {
+        fence_acq_rel_gpu();  // acquire the other pieces' releases before releasing the gate
+        red_add_relaxed_sys(a.peers.done[L.rank] + j.layer, 1u);
+        red_add_relaxed_sys(a.peers.gdone[L.rank] + P.layer_group[j.layer], 1u);
+        atomicAdd(&L.it->reduced, 1u);
+        if (L.trace_cap) trace_append(L, a.k, j.layer, g - P.layer_first[j.layer], L.rank, P3_EV_BCAST);
+      }
+    }
+  } else if (a.notify) {
+    // notify mode: the owner's replica holds the update; NOTIFY every other rank, which will
+    // PULL it (server.py:227-239)
+    const uint32_t grp = P.layer_group[j.layer];
+    red_add_relaxed_sys(a.peers.done[j.rank] + j.layer, j.run);
+    red_add_relaxed_sys(a.peers.gdone[j.rank] + grp, j.run);
+    for (uint32_t q = 0; q < j.n; ++q) {
+      if (q == j.rank) continue;
+      for (uint32_t i = 0; i < j.run; ++i) {
+        const uint32_t pos = atom_add_relaxed_sys(a.peers.ntf_tail[q], 1u);
+        *(volatile unsigned long long*)(a.peers.ntf_ring[q] + pos % a.ntf_cap) =
+            ((unsigned long long)(a.k + 1) << 32) | (j.g + i);
+        if (L.trace_cap) trace_append(L, a.k, j.layer, j.g + i - P.layer_first[j.layer], q, P3_EV_NOTIFY);
+      }
+    }
+    atomicAdd(L.bytes + 0, (j.bf16 ? 2ull : 4ull) * j.len * (j.n - 1));  // pushes received
   } else {
     const uint32_t grp = P.layer_group[j.layer];
     for (uint32_t q = 0; q < j.n; ++q) {
@@ -1409,6 +1520,92 @@ __device__ uint32_t take_stash(Stash* st, Popped* out) {
   return g;
 }
 
+// Notify mode, owner side: claim the next PULL request of this rank's pull ring (one warp;
+// lane 0 decides). Returns the slice and the requester, or P3_NONE.
+__device__ uint32_t warp_answer_pick(const CommArgs& a, const LocalDev& L, uint32_t* layer, uint32_t* requester) {
+  const uint32_t lane = threadIdx.x & 31;
+  uint32_t g = P3_NONE, q = 0;
+  if (lane == 0) {
+    const uint32_t o = L.rank;
+    const uint32_t h = ld_relaxed_gpu(L.pull_head), t = ld_relaxed_sys(a.peers.pull_tail[o]);
+    if ((int32_t)(t - h) > 0 && atomicCAS(L.pull_head, h, h + 1) == h) {
+      const volatile unsigned long long* e = a.peers.pull_ring[o] + h % a.pull_cap;
+      unsigned long long v = *e;
+      const uint64_t t0 = globaltimer();
+      while ((uint32_t)(v >> 40) != ((a.k + 1) & 0xffffffu)) {  // reserved, entry still on its way
+        if (globaltimer() - t0 > a.timeout_ns) break;
+        __nanosleep(64);
+        v = *e;
+      }
+      fence_acq_rel_sys();  // acquire: the request came after the NOTIFY of the updated slice
+      q = (uint32_t)(v >> 32) & 0xffu;
+      g = (uint32_t)v;
+    }
+  }
+  g = __shfl_sync(FULL_MASK, g, 0);
+  q = __shfl_sync(FULL_MASK, q, 0);
+  if (g != P3_NONE) {
+    *layer = a.plan.slice_layer[g];
+    *requester = q;
+  }
+  return g;
+}
+
+// Notify mode, worker side: turn the next NOTIFY of this rank into a PULL request queued at
+// the slice's owner (worker.py:226-239). Returns whether one was sent.
+__device__ bool warp_issue_pull(const CommArgs& a, const LocalDev& L) {
+  const uint32_t lane = threadIdx.x & 31;
+  uint32_t sent = 0;
+  if (lane == 0) {
+    const uint32_t r = L.rank;
+    const uint32_t h = ld_relaxed_gpu(L.ntf_head), t = ld_relaxed_sys(a.peers.ntf_tail[r]);
+    if ((int32_t)(t - h) > 0 && atomicCAS(L.ntf_head, h, h + 1) == h) {
+      const volatile unsigned long long* e = a.peers.ntf_ring[r] + h % a.ntf_cap;
+      unsigned long long v = *e;
+      const uint64_t t0 = globaltimer();
+      while ((uint32_t)(v >> 32) != a.k + 1) {
+        if (globaltimer() - t0 > a.timeout_ns) break;
+        __nanosleep(64);
+        v = *e;
+      }
+      const uint32_t g = (uint32_t)v;
+      const uint32_t o = a.plan.slice_owner[g];
+      const uint32_t pos = atom_add_relaxed_sys(a.peers.pull_tail[o], 1u);
+      *(volatile unsigned long long*)(a.peers.pull_ring[o] + pos % a.pull_cap) =
+          ((unsigned long long)((a.k + 1) & 0xffffffu) << 40) | ((unsigned long long)r << 32) | g;
+      atomicAdd(L.pcount, 1u);
+      const uint32_t l = a.plan.slice_layer[g];
+      if (L.trace_cap) trace_append(L, a.k, l, g - a.plan.layer_first[l], o, P3_EV_PULL);
+      sent = 1;
+    }
+  }
+  return __shfl_sync(FULL_MASK, sent, 0) != 0;
+}
+
+// Notify mode: the answer to a PULL — the owner's updated slice copied into the requester's
+// replica (a push-shaped job: TMA-staged, bulk-stored over NVLink).
+__device__ void prepare_answer(const CommArgs& a, uint32_t li, uint32_t g, uint32_t l, uint32_t q, Job* job) {
+  const PlanDev& P = a.plan;
+  const LocalDev& L = a.loc[li];
+  if ((threadIdx.x & 31) == 0) {
+    const uint64_t woff = P.layer_woff[l] + P.slice_off[g];
+    job->kind = JOB_PUSH;
+    job->answer = 1;
+    job->piece = 0;
+    job->ndst = 1;
+    job->run = 1;
+    job->n = 1;
+    job->li = li;
+    job->g = g;
+    job->layer = l;
+    job->rank = q;
+    job->len = P.slice_len[g];
+    job->bf16 = 0;
+    job->src[0] = a.peers.W[L.rank] + woff;
+    job->dst[0] = a.peers.W[q] + woff;
+  }
+}
+
 // Comm kernel. Warp 0 of every CTA is the scheduler, warp 1 the signaler, warp 2 the TMA
 // producer, warps 3.. the consumers; two job slots and a 3-stage ring in shared memory.
 //   scheduler: pick the next job — server work first (a reduced slice unblocks the next
@@ -1426,7 +1623,7 @@ __device__ uint32_t take_stash(Stash* st, Popped* out) {
 // library kernels, lazy module loading). The FINISH launch of an iteration ends once every
 // local slice is pushed and every owned slice reduced; it waits only for peers' pushes.
 __global__ void __launch_bounds__(P3_COMM_MAX_THREADS, 1) k_comm(const __grid_constant__ CommArgs a) {
-  __shared__ Job slots[2];  // double-buffered: the scheduler fills one while the other is moved
+  __shared__ Job slots[P3_SLOTS];  // a ring: the scheduler fills ahead while earlier jobs move
   __shared__ StageDesc sdesc[P3_STAGES];
   __shared__ __align__(8) uint64_t full_bar[P3_STAGES], empty_bar[P3_STAGES];
   __shared__ RangePtrs rptrs;
@@ -1455,8 +1652,15 @@ __global__ void __launch_bounds__(P3_COMM_MAX_THREADS, 1) k_comm(const __grid_co
     __shared__ uint32_t stash_li;
     if (lane == 0) stash.n = 0;
     __syncwarp();
-    bool pending[2] = {false, false};
+    bool pending[P3_SLOTS];
+#pragma unroll
+    for (uint32_t i = 0; i < P3_SLOTS; ++i) pending[i] = false;
     bool pops_done = false;  // FINISH, N > 1: every local slice claimed (see the pop phase)
+    // SWEEP: the claimed chunk's unprocessed part, the next claim's size, a window of 32
+    // layers' metadata (lane j: layer sw_w0 + j) and the current job's piece
+    uint64_t sw_lo = 0, sw_hi = 0, sw_t0 = 0, sw_size = 0;
+    uint32_t sw_w0 = P3_NONE, sw_l = 0, sw_off = 0, sw_len = 0, sw_g = 0;
+    uint64_t w_ps = 0, w_pe = 0, w_word = 0, w_cnt = 0;
     for (uint32_t iter = 0;; ++iter) {
       if (phase) *(volatile uint32_t*)phase = (a.k << 24) | (1u << 20) | (iter & 0xfffff);
       const uint64_t tp = globaltimer();
@@ -1466,7 +1670,85 @@ __global__ void __launch_bounds__(P3_COMM_MAX_THREADS, 1) k_comm(const __grid_co
       pp.layer = 0;
       pp.word = 0;
       pp.t0 = 0;
-      if (a.plan.world == 1) {
+      if (a.mode == P3_COMM_SWEEP) {
+        // Single rank with every layer published: claim the next chunk of the priority-ordered
+        // element space (layers in order, each padded to a multiple of 8 elements) — guided
+        // size: 1/(2 x CTAs) of what is left, 4K..64K elements — and update it layer piece by
+        // layer piece. Claims follow the FrameQueue order at element granularity and the CTAs
+        // finish within one small chunk of each other.
+        const PlanDev& P = a.plan;
+        const LocalDev& L = a.loc[0];
+        const uint64_t total = P.layer_pstart[P.n_layers];
+        while (kind == JOB_NONE) {
+          if (sw_lo >= sw_hi) {
+            unsigned long long lo = 0;
+            const uint64_t tc = globaltimer_lane0();
+            if (lane == 0) {
+              // guided by what is left NOW (a size fixed at the previous claim would hand the
+              // last large chunk to one late CTA)
+              const uint64_t seen = ld_relaxed_gpu64(reinterpret_cast<const uint64_t*>(L.sweep));
+              sw_size = min(max((seen < total ? total - seen : 0ull) / (2ull * gridDim.x), 4096ull), 65536ull) & ~7ull;
+              lo = atomicAdd(L.sweep, (unsigned long long)sw_size);
+            }
+            lo = __shfl_sync(FULL_MASK, lo, 0);
+            sw_size = __shfl_sync(FULL_MASK, sw_size, 0);
+            if (lo >= total) {
+              kind = JOB_EXIT;
+              break;
+            }
+            sw_lo = lo;
+            sw_hi = min((uint64_t)(lo + sw_size), total);
+            sw_t0 = tc;
+          }
+          // the layer holding sw_lo: from the window of 32 layers, reloaded when it moves on
+          const bool in_win = sw_w0 != P3_NONE && __shfl_sync(FULL_MASK, w_ps, 0) <= sw_lo &&
+                              sw_lo < __shfl_sync(FULL_MASK, w_pe, 31);
+          if (!in_win) {
+            sw_w0 = find_layer(P, sw_lo);
+            const uint32_t l = sw_w0 + lane;
+            const bool in = l < P.n_layers;
+            w_ps = in ? P.layer_pstart[l] : ~0ull;
+            w_pe = in ? P.layer_pstart[l + 1] : ~0ull;
+            w_cnt = in ? P.layer_count[l] : 0ull;
+            w_word = in ? ld_relaxed_gpu64(L.pub + l) : 0ull;
+          }
+          const uint32_t j = 31 - __clz(__ballot_sync(FULL_MASK, w_ps <= sw_lo));
+          sw_l = sw_w0 + j;
+          const uint64_t ps = __shfl_sync(FULL_MASK, w_ps, j), pe = __shfl_sync(FULL_MASK, w_pe, j);
+          uint64_t word = __shfl_sync(FULL_MASK, w_word, j);
+          const uint64_t count = __shfl_sync(FULL_MASK, w_cnt, j);
+          const uint64_t e0 = sw_lo - ps;
+          uint64_t e1 = min(min(sw_hi, pe) - ps, count);
+          sw_g = L.V && e0 < count ? slice_at(P, sw_l, e0) : 0u;
+          if (L.V && e0 < count) e1 = min(e1, P.slice_off[sw_g] + P.slice_len[sw_g]);  // V slots are per slice
+          sw_lo = (e1 < count && e1 > e0) ? ps + e1 : min(sw_hi, pe);
+          if (e1 <= e0) continue;  // (the chunk starts in the layer's padding)
+          if (!pub_ready(word, a.k + 1)) {  // gradient pointer not yet ingested from the ring
+            for (uint32_t spin = 0; !pub_ready(word, a.k + 1); ++spin) {
+              ingest(L, a.sched);  // (the iteration's entries are all in before this launch)
+              if (spin > 4) __nanosleep(256);
+              word = ld_relaxed_gpu64(L.pub + sw_l);
+            }
+            if (lane == j) w_word = word;
+          }
+          if (lane == 0) fence_acq_rel_gpu();  // acquire of the gradient (ingest released it)
+          __syncwarp();
+          pp.layer = sw_l;
+          pp.word = word;
+          g = sw_g;  // (momentum: the slice holding the piece; otherwise unused)
+          sw_off = (uint32_t)e0;
+          sw_len = (uint32_t)(e1 - e0);
+          if (L.trace_cap && lane == 0) {  // the pops: slices whose first element this claim takes
+            const uint32_t first = P.layer_first[sw_l];
+            for (uint32_t g2 = slice_at(P, sw_l, e0); g2 <= slice_at(P, sw_l, e1 - 1); ++g2)
+              if (P.slice_off[g2] >= e0) {
+                atomicAdd(&L.it->pushed, 1u);
+                trace_append(L, a.k, sw_l, g2 - first, L.rank, P3_EV_PUSH, sw_t0);
+              }
+          }
+          kind = JOB_REDUCE;
+        }
+      } else if (a.plan.world == 1) {
         // single rank: a popped slice is complete the moment it is popped (the owner's own
         // contribution is read in place), so the pop claims the reduction directly — no
         // arrival counting, no server role — and takes up to pop_run consecutive slices of
@@ -1494,12 +1776,19 @@ __global__ void __launch_bounds__(P3_COMM_MAX_THREADS, 1) k_comm(const __grid_co
       // progress, like the reference's server and sender threads: `push_split` > 0 makes
       // every push_split-th CTA look for pushes first, the others for server work first.
       const bool push_first = a.push_split && (blockIdx.x % a.push_split) == a.push_split - 1;
+      uint32_t ans_q = 0;
+      bool pulled = false;
       for (uint32_t round = 0; round < 2 && kind == JOB_NONE && a.plan.world > 1; ++round) {
         if ((round == 0) != push_first) {
           for (uint32_t t = 0; t < a.n_local && kind == JOB_NONE; ++t) {
             li = (blockIdx.x + t) % a.n_local;
             g = warp_server_pick(a, a.loc[li], &pp.layer, phase);
             if (g != P3_NONE) kind = JOB_REDUCE;
+          }
+          for (uint32_t t = 0; t < a.n_local && kind == JOB_NONE && a.notify; ++t) {
+            li = (blockIdx.x + t) % a.n_local;
+            g = warp_answer_pick(a, a.loc[li], &pp.layer, &ans_q);
+            if (g != P3_NONE) kind = JOB_ANSWER;
           }
         } else {
           if (stash.n) {
@@ -1521,6 +1810,9 @@ __global__ void __launch_bounds__(P3_COMM_MAX_THREADS, 1) k_comm(const __grid_co
               kind = JOB_PUSH;
             }
           }
+          // notify mode: PULLs wait behind the pushes (the baseline's per-server FIFO outbox)
+          for (uint32_t t = 0; t < a.n_local && kind == JOB_NONE && a.notify; ++t)
+            pulled |= warp_issue_pull(a, a.loc[(blockIdx.x + t) % a.n_local]);
           if (kind == JOB_NONE && !pops_done && a.mode == P3_COMM_FINISH) {
             // FINISH runs after every publication of the iteration: once every local slice
             // is claimed there is nothing left to pop — idle picks then only poll the server
@@ -1533,6 +1825,7 @@ __global__ void __launch_bounds__(P3_COMM_MAX_THREADS, 1) k_comm(const __grid_co
           }
         }
       }
+      if (kind == JOB_NONE && pulled) continue;  // progress (requests sent): look again at once
       if (kind == JOB_NONE) {
         // decided by lane 0 and broadcast: a per-lane decision could split the warp
         uint32_t verdict = 0;  // 0 keep looking, 1 leave, 2 timed out
@@ -1554,8 +1847,12 @@ __global__ void __launch_bounds__(P3_COMM_MAX_THREADS, 1) k_comm(const __grid_co
             bool fin = true;
             for (uint32_t t = 0; t < a.n_local; ++t) {
               const LocalDev& L = a.loc[t];
+              const uint32_t own = a.plan.own_total[L.rank];
               fin = fin && ld_relaxed_gpu(&L.it->pushed) >= a.plan.total_slices &&
-                    ld_relaxed_gpu(&L.it->reduced) >= a.plan.own_total[L.rank];
+                    ld_relaxed_gpu(&L.it->reduced) >= own;
+              if (a.notify)  // every NOTIFY pulled, every PULL of an owned slice answered
+                fin = fin && ld_relaxed_gpu(L.pcount) >= a.plan.total_slices - own &&
+                      ld_relaxed_gpu(L.pcount + 1) >= own * (a.plan.world - 1);
             }
             verdict = (fin || ld_relaxed_gpu(a.err) != 0) ? 1u : (globaltimer() - t0 > a.timeout_ns ? 2u : 0u);
           }
@@ -1584,7 +1881,7 @@ __global__ void __launch_bounds__(P3_COMM_MAX_THREADS, 1) k_comm(const __grid_co
       }
       backoff = 0;
       idle_since = 0;
-      if (lane == 0 && (kind == JOB_PUSH || kind == JOB_REDUCE)) {
+      if (lane == 0 && (kind == JOB_PUSH || kind == JOB_REDUCE) && a.mode != P3_COMM_SWEEP) {
         P3_CHECK(g < a.plan.total_slices && pp.layer < a.plan.n_layers);
         P3_CHECK(a.plan.slice_layer[g] == pp.layer);  // the pop's layer is the slice's layer
         P3_CHECK(pp.run >= 1 && g + pp.run <= a.plan.layer_first[pp.layer] + a.plan.layer_nslices[pp.layer]);
@@ -1595,9 +1892,12 @@ __global__ void __launch_bounds__(P3_COMM_MAX_THREADS, 1) k_comm(const __grid_co
         if (how == PUSH_DONE) continue;  // own slice, still waiting for peers: counted in place
         if (how == PUSH_REDUCE) kind = JOB_REDUCE;  // own slice completed it: reduce right away
       }
-      if (kind == JOB_PUSH || kind == JOB_REDUCE) {  // egress bytes of this job on the rank's link
+      if ((kind == JOB_PUSH || kind == JOB_REDUCE || kind == JOB_ANSWER) && a.ns_per_byte != 0.f &&
+          a.plan.world > 1) {
+        // egress bytes of this job on the rank's link (K7): a push, an answer to a PULL, or the
+        // N-1 broadcast copies of a reduce (none in notify mode: the peers pull)
         const uint64_t bytes = (kind == JOB_PUSH && a.push_bf16 ? 2ull : 4ull) * a.plan.slice_len[g] *
-                               (kind == JOB_PUSH ? 1u : a.plan.world - 1u);
+                               (kind == JOB_REDUCE ? (a.notify ? 0u : a.plan.world - 1u) : 1u);
         if (lane == 0) pace(a, a.loc[li], bytes);
         __syncwarp();
       }
@@ -1606,10 +1906,17 @@ __global__ void __launch_bounds__(P3_COMM_MAX_THREADS, 1) k_comm(const __grid_co
       if (pending[b]) bar_sync(BAR_EMPTY(b), 64);  // the signaler released this slot
       if (kind == JOB_PUSH) {
         prepare_push(a, li, g, pp.layer, pp.word, &slots[b]);
+      } else if (kind == JOB_ANSWER) {
+        prepare_answer(a, li, g, pp.layer, ans_q, &slots[b]);
+      } else if (kind == JOB_REDUCE && a.mode == P3_COMM_SWEEP) {
+        prepare_piece(a, pp.layer, pp.word, sw_off, sw_len, sw_g, &slots[b]);
       } else if (kind == JOB_REDUCE) {
         prepare_reduce(a, li, g, pp.layer, pp.word, &slots[b], pp.run);
       } else {
-        if (pending[b ^ 1]) bar_sync(BAR_EMPTY(b ^ 1), 64);  // leave every barrier balanced
+        for (uint32_t i = 1; i < P3_SLOTS; ++i) {  // leave every barrier balanced
+          const uint32_t bi = (b + i) % P3_SLOTS;
+          if (pending[bi]) bar_sync(BAR_EMPTY(bi), 64);
+        }
         if (lane == 0) slots[b].kind = JOB_EXIT;
       }
       t_wait += globaltimer() - tw;
@@ -1617,7 +1924,7 @@ __global__ void __launch_bounds__(P3_COMM_MAX_THREADS, 1) k_comm(const __grid_co
       bar_arrive(BAR_FULL(b), 96);  // producer + signaler wait on it
       if (kind == JOB_EXIT) break;
       pending[b] = true;
-      b ^= 1;
+      b = (b + 1) % P3_SLOTS;
       if (lane == 0) atomicAdd(&stats->jobs, 1u);
     }
     if (lane == 0) {
@@ -1630,7 +1937,7 @@ __global__ void __launch_bounds__(P3_COMM_MAX_THREADS, 1) k_comm(const __grid_co
   } else if (warp == 1) {
     // signaler: in job order, once the consumers are done with a job, fence and publish
     uint64_t t_sig = 0;
-    for (uint32_t b = 0;; b ^= 1) {
+    for (uint32_t b = 0;; b = (b + 1) % P3_SLOTS) {
       bar_sync(BAR_FULL(b), 96);
       const Job& j = slots[b];
       if (j.kind == JOB_EXIT) break;
@@ -1646,6 +1953,10 @@ __global__ void __launch_bounds__(P3_COMM_MAX_THREADS, 1) k_comm(const __grid_co
       mine.n = j.n;
       mine.run = j.run;
       mine.bf16 = j.bf16;
+      mine.piece = j.piece;
+      mine.ndst = j.ndst;
+      mine.answer = j.answer;
+      mine.e0 = j.e0;
       __syncwarp();
       bar_arrive(BAR_EMPTY(b), 64);
       if (lane == 0) {
@@ -1664,7 +1975,7 @@ __global__ void __launch_bounds__(P3_COMM_MAX_THREADS, 1) k_comm(const __grid_co
       if (it >= P3_STAGES) mbar_wait_bounded(&empty_bar[sidx], ((it / P3_STAGES) - 1) & 1u, a);
       ++it;
     };
-    for (uint32_t b = 0;; b ^= 1) {
+    for (uint32_t b = 0;; b = (b + 1) % P3_SLOTS) {
       bar_sync(BAR_FULL(b), 96);
       const Job& j = slots[b];
       if (lane == 0) {
@@ -1741,7 +2052,7 @@ __global__ void __launch_bounds__(P3_COMM_MAX_THREADS, 1) k_comm(const __grid_co
       mbar_wait_bounded(&full_bar[sidx], (it / P3_STAGES) & 1u, a);
       const StageDesc d = sdesc[sidx];
       if (d.flags & ST_EXIT) break;
-      P3_CHECK(d.b < 2);
+      P3_CHECK(d.b < P3_SLOTS);
       const uint64_t tm = tid == 0 ? globaltimer() : 0;
       const Job& j = slots[d.b];
       const bool bulk_push = a.tma_store && j.kind == JOB_PUSH && !j.bf16 && !(d.flags & ST_DIRECT);
@@ -1763,7 +2074,7 @@ __global__ void __launch_bounds__(P3_COMM_MAX_THREADS, 1) k_comm(const __grid_co
         bar_sync(BAR_RANGE, ncons);
         if (tid == 0) {
           const uint32_t pitch = d.tile * 4;
-          for (uint32_t q = 0; q < j.n; ++q) tma_store_1d(j.dst[q] + d.e0, st + j.n * pitch, d.n * 4u);
+          for (uint32_t q = 0; q < j.ndst; ++q) tma_store_1d(j.dst[q] + d.e0, st + j.n * pitch, d.n * 4u);
           if (j.v) tma_store_1d(j.v + d.e0, st + (j.n + 1) * pitch, d.n * 4u);
           tma_store_wait_read();
         }
@@ -1786,6 +2097,21 @@ __global__ void k_mark(const LocalDev L, uint32_t k, uint32_t ev) {
   if (threadIdx.x == 0) trace_append(L, k, 0, 0, L.rank, ev);
 }
 
+// p3_apply_slice: count a host-applied slice towards its layer's and gate group's forward gate
+// (system-scope release: the values copied before it on the stream are visible first).
+__global__ void k_bump(uint32_t* done, uint32_t* gdone, uint32_t v) {
+  if (threadIdx.x == 0) {
+    fence_acq_rel_sys();
+    red_add_relaxed_sys(done, v);
+    red_add_relaxed_sys(gdone, v);
+  }
+}
+
+int launch_bump(uint32_t* done, uint32_t* gdone, uint32_t v, void* stream) {
+  k_bump<<<1, 32, 0, (cudaStream_t)stream>>>(done, gdone, v);
+  return cudaGetLastError() == cudaSuccess ? P3_OK : P3_ECUDA;
+}
+
 int launch_mark(const LocalDev& L, uint32_t k, uint32_t ev, void* stream) {
   k_mark<<<1, 32, 0, (cudaStream_t)stream>>>(L, k, ev);
   return cudaGetLastError() == cudaSuccess ? P3_OK : P3_ECUDA;
@@ -1801,7 +2127,7 @@ int preload_kernels() {
     return P3_ECUDA;
   cudaFuncAttributes fa;
   const void* fns[] = {(const void*)k_comm, (const void*)k_gradgen, (const void*)k_sleep,
-                       (const void*)k_shard_update, (const void*)k_queue_pop, (const void*)k_mark};
+                       (const void*)k_shard_update, (const void*)k_queue_pop, (const void*)k_mark, (const void*)k_bump};
   for (const void* f : fns)
     if (cudaFuncGetAttributes(&fa, f) != cudaSuccess) return P3_ECUDA;
   return P3_OK;

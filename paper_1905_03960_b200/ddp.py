@@ -265,6 +265,7 @@ class P3DataParallel(_HookedDataParallel):
         big_threshold: int = 1_000_000,
         order: str = "forward",
         local_world: P3LocalWorld | None = None,
+        notify_pull: bool | None = None,
     ) -> None:
         super().__init__(module, order)
         self.lr = lr
@@ -299,6 +300,7 @@ class P3DataParallel(_HookedDataParallel):
             plan_mode=plan_mode, throttle_bps=throttle_bps, throttle_burst=throttle_burst,
             big_threshold=big_threshold, pub_batch_bytes=pub_batch_bytes, drain_linger_us=drain_linger_us,
             finish_ctas=finish_ctas, push_dtype=push_dtype,
+            notify_pull=(plan_mode == "baseline") if notify_pull is None else notify_pull,
         )
         self.ctx: SyncContext | None = None
         self.comm_stream = None

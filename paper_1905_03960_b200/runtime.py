@@ -47,12 +47,12 @@ class TraceEvent:
 
 
 def plan_fingerprint(layer_counts, world, max_slice, plan_mode, big_threshold, rng_seed, priority_mode, lr, momentum,
-                     push_dtype) -> str:
+                     push_dtype, notify_pull=False) -> str:
     """What every rank of one sync group must agree on: the plan (layer sizes, world, slice
     size, placement), the discipline and the update rule. Ranks that disagree would wait on
     each other forever (a slice one rank never pushes), so ``connect`` refuses them."""
     key = repr((list(map(int, layer_counts)), int(world), int(max_slice), plan_mode, int(big_threshold), int(rng_seed),
-                bool(priority_mode), float(lr), float(momentum), push_dtype))
+                bool(priority_mode), float(lr), float(momentum), push_dtype, bool(notify_pull)))
     return f"{fnv1a64(key.encode()):016x}"
 
 
@@ -116,6 +116,7 @@ class SyncContext:
         pop_multi: int = 0,
         push_dtype: str = "fp32",
         drain_streams: int = 0,
+        notify_pull: bool = False,
     ) -> None:
         import torch
 
@@ -169,6 +170,7 @@ class SyncContext:
         cfg.emulate_grads = 1 if emulate_grads else 0
         cfg.drain_bytes = drain_bytes
         cfg.drain_streams = drain_streams
+        cfg.notify_pull = 1 if notify_pull else 0
         self.strict = comm_ctas == 1 and (finish_ctas or comm_ctas) == 1 and pop_relax == 1 and drain_streams == 1
         h = ctypes.c_void_p()
         _lib.check(self.lib.p3_ctx_create(ctypes.byref(cfg), ctypes.byref(h)), what="p3_ctx_create")
@@ -181,7 +183,7 @@ class SyncContext:
         self.arena_elems = self.layer_offsets[-1] + self.layer_counts[-1]
         self.plan_mode = plan_mode
         self.fingerprint = plan_fingerprint(self.layer_counts, world, max_slice, plan_mode, big_threshold, rng_seed,
-                                            priority_mode, lr, momentum, push_dtype)
+                                            priority_mode, lr, momentum, push_dtype, notify_pull)
 
     # ------------------------------------------------------------------ plumbing
     def _check(self, rc: int, what: str) -> None:
@@ -315,23 +317,28 @@ class SyncContext:
 
 @dataclass
 class WorkerConfig:
-    """Worker settings (worker.py:25-36); ``servers`` is replaced by the world size."""
+    """Worker settings (worker.py:39-50). ``servers`` keeps the reference's meaning — the
+    parameter servers a worker pushes to, one per rank (cli.py:81-82) — given as the peer
+    list or just its length; ``world`` is that count. The fields after ``sample_period_ms``
+    configure the device path."""
 
     rank: int
     mode: str
-    world: int
-    iterations: int
+    servers: object = None             # list of peers (host, port) / GPUs, or their count
+    iterations: int = 1
     lr: float = 0.1
     batch_size: int = 32
-    max_slice: int = DEFAULT_MAX_SLICE
+    throttle_rate: float | None = None  # bit/s per rank egress (worker.py:46); None = full NVLink
+    throttle_burst: int = 50 * 1024
     deadlock_timeout: float = 60.0
+    sample_period_ms: int = 10
+    world: int = 0                      # = number of servers (derived from ``servers``)
+    max_slice: int = DEFAULT_MAX_SLICE
     emulate_compute: bool = True
     comm_ctas: int = 16
     comm_threads: int = 512
     trace_cap: int = 0
     rank_distinct_grads: bool = False
-    throttle_rate: float | None = None  # bit/s per rank egress (worker.py:33); None = full NVLink
-    throttle_burst: int = 50 * 1024
     big_threshold: int = 1_000_000     # baseline plan (cli.py:68)
     seed: int = 0                      # baseline plan placement seed (cli.py:74)
     push_dtype: str = "fp32"           # "bf16": declared lossy transport of pushes
@@ -340,6 +347,21 @@ class WorkerConfig:
     drain_streams: int = 0             # side streams of DRAIN launches (0: 4)
     strict_order: bool = False         # one consumer at a time: 1 CTA per launch, 1 DRAIN stream,
                                        # strict FrameQueue order (the reference's single sender)
+    notify_pull: bool | None = None    # owners NOTIFY, replicas PULL (None: in baseline mode, as the
+                                       # reference's baseline does, server.py:227-247)
+
+    def __post_init__(self) -> None:
+        n = None if self.servers is None else (self.servers if isinstance(self.servers, int) else len(self.servers))
+        if self.world == 0:
+            if n is None:
+                raise ValueError("WorkerConfig needs servers (or world)")
+            self.world = n
+        elif n is None:
+            self.servers = self.world
+        elif n != self.world:
+            raise ValueError(f"{n} servers but world={self.world}")
+        if not 0 <= self.rank < self.world:
+            raise ValueError(f"rank {self.rank} outside [0, {self.world})")
 
 
 def rank_seed(seed: int, rank: int, distinct: bool) -> int:
@@ -362,20 +384,36 @@ class TrainingWorker:
     a DRAIN launch of the comm kernel, and the iteration ends with a FINISH launch.
     """
 
-    def __init__(self, config: WorkerConfig, profile: ModelProfile, ranks: list[int] | None = None, ctx: SyncContext | None = None) -> None:
+    def __init__(self, config: WorkerConfig, profile: ModelProfile, plan=None, ranks: list[int] | None = None,
+                 ctx: SyncContext | None = None) -> None:
         import torch
 
+        if plan is not None and not hasattr(plan, "slices"):  # (round-1 call form: ranks third)
+            plan, ranks = None, plan
         if config.mode not in (P3_MODE, BASELINE_MODE):
             raise ValueError(f"mode must be {P3_MODE!r} or {BASELINE_MODE!r}, not {config.mode!r}")
+        if plan is not None and plan.mode != config.mode:
+            raise ValueError(f"plan mode {plan.mode!r} != worker mode {config.mode!r}")  # worker.py:65-67
         self.cfg = config
         self.profile = profile
         self.ranks = list(ranks) if ranks is not None else [config.rank]
         # p3: sliced plan + priority queue; baseline: KVStore placement + FIFO (the reference's
-        # two modes, worker.py:84-93, plan.py:94-164)
+        # two modes, worker.py:84-93, plan.py:94-164). The device builds its plan from the
+        # same inputs; a caller's plan must be that plan.
+        if plan is not None and config.mode == P3_MODE:
+            multi = [s.length for s in plan.slices if s.key.slice_index == 0 and len(plan.slices_of_layer(s.key.layer_index)) > 1]
+            if multi:
+                config.max_slice = max(multi)
         if config.mode == P3_MODE:
             self.plan = make_p3_plan(profile, config.world, config.max_slice)
         else:
             self.plan = make_baseline_plan(profile, config.world, config.big_threshold, config.seed)
+        if plan is not None:
+            from .plan import PlanError, plan_to_csv
+
+            if plan_to_csv(plan) != plan_to_csv(self.plan):
+                raise PlanError("the plan differs from the one the device builds for this profile, server count, "
+                                "slice size and placement (make_p3_plan / make_baseline_plan)")
         self.ctx = ctx or SyncContext(
             profile.param_counts(),
             config.world,
@@ -397,11 +435,15 @@ class TrainingWorker:
             finish_ctas=1 if config.strict_order else config.finish_ctas,
             pop_relax=1 if config.strict_order else config.pop_relax,
             drain_streams=1 if config.strict_order else config.drain_streams,
+            notify_pull=(config.mode == BASELINE_MODE) if config.notify_pull is None else config.notify_pull,
         )
         self.comm_stream = torch.cuda.Stream()
         self.streams = [torch.cuda.Stream() for _ in self.ranks]
+        self.mark_stream = torch.cuda.Stream()
         self.iterations_done = 0
         self.iter_events: list = []
+        self._nslices = [len(self.plan.slices_of_layer(l.index)) for l in profile.layers]
+        self._recv_seen: dict = {}
 
     def run_iteration(self, k: int) -> None:
         import torch
@@ -409,10 +451,13 @@ class TrainingWorker:
         lib = self.ctx.lib
         ctx = self.ctx
         ctx.iteration_begin(k, self.comm_stream)
+        marks = ctx.trace_cap > 0
         for li, rank in enumerate(self.ranks):
             s = self.streams[li]
             sh = _lib.stream_handle(s)
             seed = rank_seed(self.profile.seed, rank, self.cfg.rank_distinct_grads)
+            if marks:  # IterationRecord.start (worker.py:312-313) on the device clock
+                ctx._check(lib.p3_trace_mark(ctx.handle, li, k, _lib.P3_EV_ITER_START, sh), "p3_trace_mark")
             for layer in self.profile.layers:
                 ctx._check(lib.p3_wait_layer(ctx.handle, li, layer.index, k, sh), "p3_wait_layer")
                 if self.cfg.emulate_compute and layer.fwd_time:
@@ -427,7 +472,62 @@ class TrainingWorker:
                 ctx._check(lib.p3_gradgen_layer(ctx.handle, li, seed & 0xFFFFFFFFFFFFFFFF, k, layer.index, sh), "p3_gradgen_layer")
                 ctx._check(lib.p3_layer_ready(ctx.handle, li, layer.index, k, None, sh), "p3_layer_ready")
         ctx.iteration_end(k)
+        if marks:  # sync_end (worker.py:265-268): every layer of the rank holds iteration k+1
+            mh = _lib.stream_handle(self.mark_stream)
+            for li in range(len(self.ranks)):
+                for layer in self.profile.layers:
+                    ctx._check(lib.p3_wait_layer(ctx.handle, li, layer.index, k + 1, mh), "p3_wait_layer")
+                ctx._check(lib.p3_trace_mark(ctx.handle, li, k, _lib.P3_EV_SYNCED, mh), "p3_trace_mark")
         self.iterations_done = k + 1
+
+    # -- the reference worker's public entry points -----------------------------------
+
+    def enqueue_layer(self, layer_index: int, iteration: int, li: int = 0, grad=None, stream=None) -> None:
+        """TrainingWorker.enqueue_layer (worker.py:173-182): publish every slice of the layer for
+        ``iteration`` atomically. Emulate mode (``grad`` None) first materialises the rank's
+        GradGen gradient (K1, worker.py:166-171) on ``stream``; the iteration must be open
+        (``ctx.iteration_begin``) for the comm kernel to pick it up."""
+        s = stream if stream is not None else self.streams[li]
+        if grad is None:
+            seed = rank_seed(self.profile.seed, self.ranks[li], self.cfg.rank_distinct_grads)
+            self.ctx.gradgen_layer(li, seed & 0xFFFFFFFFFFFFFFFF, iteration, layer_index, s)
+        self.ctx.layer_ready(li, layer_index, iteration, grad, s)
+
+    def flag(self, layer_index: int, li: int = 0) -> int:
+        """flags[layer] (worker.py:74-75): the forward pass whose parameters the layer holds."""
+        it = ctypes.c_uint64()
+        self.ctx._check(self.ctx.lib.p3_layer_flag(self.ctx.handle, li, layer_index, ctypes.byref(it)), "p3_layer_flag")
+        return int(it.value)
+
+    def on_bcast(self, frame, li: int = 0) -> None:
+        """TrainingWorker.on_bcast (worker.py:241-269) for a BCAST frame that reached the host
+        (the wire path beyond the NVSwitch domain): same checks and ProtocolErrors, then the
+        slice goes into the device replica and counts towards the layer's forward gate."""
+        from .proto import ProtocolError
+
+        key = SliceKey(frame.layer_index, frame.slice_index)
+        layer = key.layer_index
+        if not 0 <= layer < len(self._nslices) or not 0 <= key.slice_index < self._nslices[layer]:
+            raise ProtocolError(f"BCAST for unknown key {key}")
+        held = self.flag(layer, li)
+        if frame.iteration != held:
+            raise ProtocolError(f"layer {layer}: BCAST for iteration {frame.iteration}, "
+                                f"worker holds parameters of iteration {held}")
+        seen = self._recv_seen.setdefault((li, layer, held), set())
+        if key in seen:
+            raise ProtocolError(f"duplicate BCAST slice {key} at iteration {frame.iteration}")
+        values = np.ascontiguousarray(frame.payload_f32(), dtype=np.float32)
+        sl = self.plan.slices_of_layer(layer)[key.slice_index]
+        if len(values) != sl.length:
+            raise ProtocolError(f"slice {key}: payload holds {len(values)} values, expected {sl.length}")
+        stream = self.streams[li]
+        self.ctx._check(self.ctx.lib.p3_apply_slice(self.ctx.handle, li, layer, key.slice_index,
+                                                    values.ctypes.data_as(ctypes.c_void_p), len(values),
+                                                    _lib.stream_handle(stream)), "p3_apply_slice")
+        stream.synchronize()  # the host payload buffer may be released after return
+        seen.add(key)
+        if len(seen) == self._nslices[layer]:
+            del self._recv_seen[(li, layer, held)]
 
     def run(self) -> None:
         for k in range(self.cfg.iterations):

@@ -86,7 +86,8 @@ def main():
         cfg = WorkerConfig(rank=rank, mode="baseline", world=world, iterations=10, deadlock_timeout=60.0,
                            emulate_compute=False, comm_ctas=8, big_threshold=100_000)
         ctx = SyncContext(prof.param_counts(), world, [rank], lr=cfg.lr, comm_ctas=8, timeout_s=60.0,
-                          emulate_grads=True, plan_mode="baseline", priority_mode=False, big_threshold=100_000)
+                          emulate_grads=True, plan_mode="baseline", priority_mode=False, big_threshold=100_000,
+                          notify_pull=True)  # the reference baseline's NOTIFY -> PULL round trip
         hs = [None] * world
         dist.all_gather_object(hs, ctx.ipc_handle(0))
         ctx.open_peers(hs)
@@ -131,6 +132,41 @@ def main():
     out["torch_layerwise_close"] = all(torch.allclose(a, b, atol=1e-5) for a, b in zip(mod2.parameters(), ref.parameters()))
     ddp.close()
     lw.close()
+
+    # torch mode on real shapes with DIFFERENT data on every rank: after every step each
+    # replica must hold p - lr * ((g_0 + ... + g_{N-1}) / N), the rank-ordered fp32 sum of the
+    # ranks' own autograd gradients (gathered here), separately rounded (server.py:55-68)
+    from paper_1905_03960_b200.torch_models import build_model, loss_fn, synthetic_batch
+
+    for name, batch in (("resnet50", 8), ("seq2seq", 8)):
+        torch.manual_seed(7)
+        m = build_model(name).cuda()
+        if name == "resnet50":
+            m = m.to(memory_format=torch.channels_last)
+        d = P3DataParallel(m, lr=lr, comm_ctas=8, timeout_s=60.0)
+        names = [n for n, p in m.named_parameters() if p.requires_grad]
+        exact, differs = True, False
+        for it in range(3):
+            old = {n: p.detach().clone() for n, p in m.named_parameters() if p.requires_grad}
+            x, y = synthetic_batch(name, batch, seed=1000 * it + rank)
+            loss_fn(name, d, x, y).backward()
+            grads = {n: p.grad.detach().clone() for n, p in m.named_parameters() if p.requires_grad}
+            d.synchronize()
+            torch.cuda.synchronize()
+            params = dict(m.named_parameters())
+            for n in names:
+                gs = [torch.empty_like(grads[n]) for _ in range(world)]
+                dist.all_gather(gs, grads[n].contiguous())
+                acc = torch.zeros_like(old[n])
+                for r in range(world):
+                    acc = acc + gs[r].view_as(acc)
+                want = old[n] - (acc / torch.full_like(acc, world)).mul(lr)
+                exact &= bool(torch.equal(params[n].detach(), want))
+                differs |= not torch.equal(gs[0], gs[-1])
+        out[f"torch_p3_distinct_{name}"] = exact and differs
+        d.close()
+        del d, m
+        torch.cuda.empty_cache()
     out_dir = os.environ.get("P3_MP_OUT")
     if out_dir:
         Path(out_dir, f"rank{rank}.json").write_text(json.dumps(out))

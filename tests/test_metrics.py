@@ -40,3 +40,41 @@ def test_sampler_monotone():
     ts = [x.t_ms for x in smp.samples]
     assert len(ts) >= 5 and ts == sorted(ts)
     assert all(b.bytes_in >= a.bytes_in for a, b in zip(smp.samples, smp.samples[1:]))
+
+
+def test_samples_and_timeline_from_device_trace():
+    # link bytes from trace records: pushes of slices owned elsewhere leave the pusher and
+    # enter the owner; a broadcast leaves the owner N-1 times and enters every other rank
+    from dataclasses import dataclass
+
+    from paper_1905_03960_b200.metrics import iteration_timeline, link_bytes, samples_from_trace
+    from paper_1905_03960_b200.model import LayerSpec, ModelProfile
+    from paper_1905_03960_b200.plan import make_p3_plan
+
+    @dataclass
+    class R:
+        t_ns: int
+        iteration: int
+        layer: int
+        slice: int
+        rank: int
+        event: int
+
+    plan = make_p3_plan(ModelProfile("m", 0, (LayerSpec(0, "a", 10, 0, 0), LayerSpec(1, "b", 30, 0, 0))), 2, 20)
+    owner = {(s.key.layer_index, s.key.slice_index): s.server for s in plan.slices}
+    assert owner == {(0, 0): 0, (1, 0): 1, (1, 1): 0}
+    ms = 1_000_000
+    traces = {
+        0: [R(0, 0, 0, 0, 0, 5), R(1 * ms, 0, 1, 0, 0, 0), R(2 * ms, 0, 0, 0, 0, 0), R(12 * ms, 0, 0, 0, 0, 1),
+            R(15 * ms, 0, 1, 1, 0, 1), R(31 * ms, 0, 0, 0, 0, 6)],
+        1: [R(0, 0, 0, 0, 1, 5), R(3 * ms, 0, 0, 0, 1, 0), R(4 * ms, 0, 1, 1, 1, 0), R(25 * ms, 0, 1, 0, 1, 1),
+            R(30 * ms, 0, 0, 0, 1, 6)],
+    }
+    rows = link_bytes(traces, plan, 0)
+    assert sum(r[2] for r in rows) == 4 * 20 + 4 * 10 + 4 * 10  # push (1,0) + bcasts of (0,0), (1,1)
+    assert sum(r[1] for r in rows) == 4 * 10 + 4 * 10 + 4 * 20  # push of (0,0), (1,1) from rank 1 + bcast (1,0)
+    smp = samples_from_trace(traces, plan, 0, 0, 31 * ms)
+    assert [s.t_ms for s in smp] == [0, 10, 20, 30, 40]
+    assert smp[-1].bytes_out == 160 and smp[1].bytes_out == 80 and smp[2].bytes_out == 160
+    walls, starts = iteration_timeline(traces[0], 0)
+    assert walls == [31.0] and starts == [0.0]

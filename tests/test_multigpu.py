@@ -36,3 +36,5 @@ def test_multiprocess_parity(world, tmp_path):
             assert got == want, (r["rank"], k, got, want)
         assert r["torch_p3_exact"], r
         assert r["torch_layerwise_close"], r
+        assert r["torch_p3_distinct_resnet50"], r
+        assert r["torch_p3_distinct_seq2seq"], r

@@ -52,8 +52,8 @@ def main():
         ctx.sync_all(k + 1, 30.0)
         st.synchronize()
         tr_all = [r for r in ctx.trace(0) if r.iteration == k]
-        starts_ev = [r.t_ns for r in tr_all if r.event == 2]
-        exits_ev = [r.t_ns for r in tr_all if r.event == 3]
+        starts_ev = [r.t_ns for r in tr_all if r.event == 16]
+        exits_ev = [r.t_ns for r in tr_all if r.event == 17]
         tr = [r for r in tr_all if r.event in (0, 1)]
         picks = sorted(r.t_ns for r in tr if r.event == 0)
         sig = sorted((r.t_ns, lens[first[r.layer] + r.slice]) for r in tr if r.event == 1)
