@@ -114,7 +114,7 @@ struct p3_ctx {
   // P3_TRACE_CTA=1 (trace records carry CTA indices; CTA start / exit records)
   struct {
     uint32_t use_tma = 1, push_split = 0, srv_filter = 0, trace_cta = 0, srv_reserve = 0, tma_store = 1, tma_store_red = 0, pop_relax = 0,
-             no_sweep = 0;
+             sweep = 0, sweep_div = 2, sweep_min = 4096, sweep_max = 65536;
   } knobs;
   std::vector<uint32_t> own_total;
   std::vector<uint64_t> own_stride;
@@ -328,7 +328,12 @@ int p3_ctx_create(const p3_config_t* cfg, p3_ctx_t** out) {
     c->knobs.tma_store = env_u32("P3_TMA_STORE", 1);
     c->knobs.pop_relax = env_u32("P3_POP_RELAX", 0);  // 0: the config's
     c->knobs.tma_store_red = env_u32("P3_TMA_STORE_RED", 0);
-    c->knobs.no_sweep = env_u32("P3_NO_SWEEP", 0);  // single rank: slice pops in the FINISH launch
+    // single rank: the FINISH launch sweeps guided chunks of the element space instead of
+    // popping slices (measured slower than the slice pops so far: off by default)
+    c->knobs.sweep = env_u32("P3_SWEEP", 0);
+    c->knobs.sweep_div = std::max<uint32_t>(1, env_u32("P3_SWEEP_DIV", 2));
+    c->knobs.sweep_min = env_u32("P3_SWEEP_MIN", 4096) & ~7u;
+    c->knobs.sweep_max = std::max<uint32_t>(c->knobs.sweep_min, env_u32("P3_SWEEP_MAX", 65536) & ~7u);
   }
   std::string perr;
   int rc = cfg->plan_mode == P3_PLAN_P3
@@ -671,6 +676,9 @@ static CommArgs comm_args(p3_ctx* c, uint32_t mode, uint32_t ctas) {
   a.push_bf16 = c->cfg.push_bf16 ? 1u : 0u;
   a.notify = c->cfg.notify_pull && c->N > 1 ? 1u : 0u;
   a.ntf_cap = c->S;
+  a.sweep_div = c->knobs.sweep_div;
+  a.sweep_min = std::max<uint32_t>(8, c->knobs.sweep_min);
+  a.sweep_max = c->knobs.sweep_max;
   a.pull_cap = c->S * (c->N > 1 ? c->N - 1 : 1);
   a.trace_cta = c->knobs.trace_cta;
   a.push_split = c->knobs.push_split;
@@ -768,7 +776,7 @@ int p3_iteration_end(p3_ctx_t* c, uint64_t k) {
   // Single rank, no DRAIN launch this iteration and bounded relaxation allowed: the FINISH
   // launch is the only consumer and every layer is published, so it sweeps the priority-
   // ordered element space in guided chunks (perfect balance over the CTAs, claims in order).
-  const bool sweep = c->N == 1 && c->side_used == 0 && c->cfg.pop_relax != 1 && !c->knobs.no_sweep;
+  const bool sweep = c->N == 1 && c->side_used == 0 && c->cfg.pop_relax != 1 && c->knobs.sweep;
   if (launch_comm(comm_args(c, sweep ? P3_COMM_SWEEP : P3_COMM_FINISH, ctas), ctas, c->cfg.comm_threads,
                   c->comm_stream) != P3_OK)
     return cuda_fail(c, cudaGetLastError(), "comm kernel launch");

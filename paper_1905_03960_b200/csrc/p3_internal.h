@@ -143,6 +143,7 @@ struct CommArgs {
   uint32_t push_bf16; // pushes travel as bf16
   uint32_t notify;    // notify mode (P3 config notify_pull, N > 1)
   uint32_t ntf_cap, pull_cap;  // ring entries
+  uint32_t sweep_div, sweep_min, sweep_max;  // SWEEP chunk: remaining / (div x CTAs) in [min, max]
   uint32_t push_split; // every push_split-th CTA prefers pushes over server work (0: none)
   uint32_t srv_filter; // server picks: only srv_filter x (ready slices) consumers look (0: all)
   uint32_t srv_reserve; // N > 1: every srv_reserve-th CTA does server work only (0: none)

@@ -881,7 +881,8 @@ struct Job {
 //   DONE(b)  consumers arrive, signaler syncs               (the job's data has moved)
 //   EMPTY(b) signaler arrives, scheduler syncs              (slot b may be refilled)
 #ifndef P3_SLOTS
-#define P3_SLOTS 4  // job slots: the scheduler prepares up to P3_SLOTS - 1 jobs ahead of the movers
+#define P3_SLOTS 2  // job slots: the scheduler prepares up to P3_SLOTS - 1 jobs ahead of the movers
+                    // (measured: 4 slots hold more claims per CTA and lose the tail balance)
 #endif
 #define BAR_FULL(b) (1 + (b))
 #define BAR_DONE(b) (1 + P3_SLOTS + (b))
@@ -1687,7 +1688,9 @@ __global__ void __launch_bounds__(P3_COMM_MAX_THREADS, 1) k_comm(const __grid_co
               // guided by what is left NOW (a size fixed at the previous claim would hand the
               // last large chunk to one late CTA)
               const uint64_t seen = ld_relaxed_gpu64(reinterpret_cast<const uint64_t*>(L.sweep));
-              sw_size = min(max((seen < total ? total - seen : 0ull) / (2ull * gridDim.x), 4096ull), 65536ull) & ~7ull;
+              const unsigned long long rem = seen < total ? total - seen : 0ull;
+              sw_size = min(max(rem / ((unsigned long long)a.sweep_div * gridDim.x), (unsigned long long)a.sweep_min),
+                            (unsigned long long)a.sweep_max) & ~7ull;
               lo = atomicAdd(L.sweep, (unsigned long long)sw_size);
             }
             lo = __shfl_sync(FULL_MASK, lo, 0);

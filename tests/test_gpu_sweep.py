@@ -5,11 +5,18 @@ Bit-exact against the oracle's ShardState replay (server.py:55-68) with words wr
 directly (sync-only phase) or through the publication ring (training: no DRAIN launch at
 N=1), odd slice sizes, momentum, and every slice popped once per iteration in claim order."""
 
+import os
+
 import pytest
 
 import p3_oracle as O
 
 pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(autouse=True)
+def _sweep_on(monkeypatch):
+    monkeypatch.setenv("P3_SWEEP", "1")  # read by p3_ctx_create
 
 COUNTS = [5, 1023, 70_001, 9, 200_000, 64, 64, 2_359_296, 1000, 2_048_000]
 
