@@ -93,7 +93,7 @@ class NvlinkCounters:
     """NVLink data bytes sent / received by this GPU (NVML field values THROUGHPUT_DATA_TX/RX,
     KiB, summed over the links), read around a measured phase: the traffic of the transfers."""
 
-    FIELDS = (138, 139)  # NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX / _RX
+    FIELDS = (138, 139)  # NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX / _RX (KiB)
 
     def __init__(self, device_index: int) -> None:
         self.ok = False
@@ -245,11 +245,12 @@ def sync_only_roofline(args, world, rank, counts):
     times = []
     reps = args.sync_reps
     nvl = NvlinkCounters(torch.cuda.current_device()) if world > 1 else None
-    nvl0 = None
+    nvl0 = dev0 = None
     for k in range(reps + 2):
         if k == 2 and nvl is not None:
             torch.cuda.synchronize()
             nvl0 = nvl.read()
+            dev0 = ctx.counters(0)
         with torch.cuda.stream(stream):
             flush.fill_(k & 0xFF)
         for l in range(len(counts)):  # published before the iteration opens: no DRAIN launches
@@ -272,11 +273,19 @@ def sync_only_roofline(args, world, rank, counts):
         if k >= 2:
             times.append(max_over_ranks(s.elapsed_time(e), world))
     traffic = None
-    if nvl0 is not None:
-        nvl1 = nvl.read()
-        if nvl1 is not None:  # NVLink TX bytes per launch (the all-reduce that aligns the ranks: 4 B)
-            traffic = {"tx_bytes_per_launch": (nvl1[0] - nvl0[0]) / reps, "rx_bytes_per_launch": (nvl1[1] - nvl0[1]) / reps,
-                       "source": "NVML NVLink THROUGHPUT_DATA_TX/RX counters around the timed launches"}
+    if dev0 is not None:
+        nvl1, dev1 = nvl.read(), ctx.counters(0)
+        traffic = {"device_counted_out_bytes_per_launch": (dev1[1] - dev0[1]) / reps,
+                   "device_counted_in_bytes_per_launch": (dev1[0] - dev0[0]) / reps,
+                   "device_counted": "the comm kernel's own byte counters (p3_counters: payload it stored over "
+                                     "NVLink / received), per timed launch"}
+        if nvl1 is not None and nvl0 is not None and nvl1[0] > nvl0[0]:
+            traffic.update({"nvlink_tx_bytes_per_launch": (nvl1[0] - nvl0[0]) / reps,
+                            "nvlink_rx_bytes_per_launch": (nvl1[1] - nvl0[1]) / reps})
+        else:  # NVML returns NOT_SUPPORTED for every NVLink counter field on this pool
+            traffic["nvlink_hw_counters"] = ("unavailable: NVML NVLink throughput/count fields return NOT_SUPPORTED "
+                                             "here (profiles/r02/nvml_nvlink_probe.txt); ncu cannot replay a "
+                                             "cross-rank kernel")
     ctx.close()
     return statistics.mean(times), ctas, traffic
 
@@ -517,8 +526,8 @@ def run_ours(args):
         t = json.loads(tf.read_text()).get(args.model)
         if t and t["world"] == world and t["max_slice"] == args.max_slice:
             traffic = t["dram_bytes_read"] + t["dram_bytes_write"]
-    if world > 1 and nvl_traffic is not None:  # NVLink bytes actually sent per launch (NVML counters)
-        traffic = nvl_traffic["tx_bytes_per_launch"]
+    if world > 1 and nvl_traffic is not None:  # hardware NVLink bytes when NVML has them, else null
+        traffic = nvl_traffic.get("nvlink_tx_bytes_per_launch")
         roof["traffic_detail"] = nvl_traffic
     roof.update({"frac": roof["achieved"] / peak, "traffic": traffic,
                  "kernel": "k_comm (K3 push + K4 reduce/SGD/bcast)" + (", SWEEP mode" if world == 1 else ""),
