@@ -489,8 +489,10 @@ def run_ours(args):
     if world > 1 and args.throttle_gbps > 0:
         throttled = {"gbps": args.throttle_gbps, "burst_bytes": 50 * 1024}
         for arm, kw in (("p3", {}), ("layerwise_fifo", {"plan_mode": "baseline", "priority_mode": False}),
-                        ("p3_bf16_push", {"push_dtype": "bf16"})):
+                        ("p3_bf16_push", {"push_dtype": "bf16"}), ("p3_bf16_params", {})):
             model = build(args, rank)
+            if arm == "p3_bf16_params":  # bf16 parameters: bf16 replicas on the wire, fp32 masters
+                model = model.bfloat16()
             d = P3DataParallel(model, lr=args.lr, max_slice=args.max_slice, comm_ctas=4, pub_batch_bytes=0,
                                throttle_bps=args.throttle_gbps * 1e9, **kw)
             ms_t, _ = time_training(args, world, rank, d, x, y, max(5, args.steps), 3)
@@ -530,7 +532,7 @@ def run_ours(args):
         traffic = nvl_traffic.get("nvlink_tx_bytes_per_launch")
         roof["traffic_detail"] = nvl_traffic
     roof.update({"frac": roof["achieved"] / peak, "traffic": traffic,
-                 "kernel": "k_comm (K3 push + K4 reduce/SGD/bcast)" + (", SWEEP mode" if world == 1 else ""),
+                 "kernel": "k_comm (K3 push + K4 reduce/SGD/bcast)",
                  "algorithmic_bytes_per_launch": alg, "launch_ms": sync_ms, "ctas": ctas,
                  "measured_in": "sync-only phase: all layers' gradients in HBM and published, one launch per "
                                 "iteration over the whole GPU, L2 flushed (256 MB write) between launches"})

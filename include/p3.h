@@ -261,6 +261,14 @@ typedef struct p3_config {
                                           queues a PULL behind its pushes and the owner answers
                                           it with the slice (one more round trip than P3's
                                           broadcast) */
+  uint32_t param_bf16;                 /* declared bf16 replicas: the model's parameters and
+                                          gradients are bf16 (W holds bf16); each owner keeps an
+                                          fp32 master of its slices. Pushes carry the bf16
+                                          gradients, the owner sums them in fp32 in rank order,
+                                          updates the fp32 master (same arithmetic as the fp32
+                                          path) and broadcasts bf16(master), round to nearest
+                                          even. Call p3_master_init once the replica holds the
+                                          initial parameters. */
 } p3_config_t;
 
 /* Builds the plan, allocates per-local-rank arenas (parameters W zero-initialised like
@@ -279,6 +287,10 @@ int p3_ctx_open_peers(p3_ctx_t* ctx, const void* handles);
  * it (layers are 16-byte aligned). TrainingWorker.params, worker.py:72. */
 int p3_ctx_params(p3_ctx_t* ctx, uint32_t local_idx, float** params_dev);
 int p3_ctx_layer_offset(p3_ctx_t* ctx, uint32_t layer, uint64_t* elem_offset);
+/* param_bf16: initialise the fp32 master of the local rank's owned slices from its (bf16)
+ * replica W — once, after the initial parameters were written into W (stream-ordered). */
+int p3_master_init(p3_ctx_t* ctx, uint32_t local_idx, void* stream);
+
 /* Device pointer of the local rank's gradient arena (emulate_grads only). */
 int p3_ctx_grads(p3_ctx_t* ctx, uint32_t local_idx, float** grads_dev);
 

@@ -107,6 +107,7 @@ class Config(ctypes.Structure):
         ("gate_groups", ctypes.POINTER(ctypes.c_uint32)),
         ("drain_streams", ctypes.c_uint32),
         ("notify_pull", ctypes.c_uint32),
+        ("param_bf16", ctypes.c_uint32),
     ]
 
 
@@ -148,6 +149,7 @@ SIGNATURES = {
     "p3_trace_read": (ctypes.c_int, [_P, _U32, ctypes.POINTER(TraceRec), _U64, _PU64]),
     "p3_trace_clear": (ctypes.c_int, [_P]),
     "p3_apply_slice": (ctypes.c_int, [_P, _U32, _U32, _U32, _P, _U64, _P]),
+    "p3_master_init": (ctypes.c_int, [_P, _U32, _P]),
     "p3_layer_flag": (ctypes.c_int, [_P, _U32, _U32, _PU64]),
     "p3_fq_create": (ctypes.c_int, [_U32, ctypes.POINTER(_P)]),
     "p3_fq_put_batch": (ctypes.c_int, [_P, _PU64, _PU64, _U64]),
@@ -174,14 +176,17 @@ def load() -> ctypes.CDLL:
     global _lib
     if _lib is not None:
         return _lib
-    path = Path(os.environ.get("P3_LIB", LIB_PATH))
+    path = Path(os.environ.get("P3_LIB") or LIB_PATH)
     if not path.exists():
         raise RuntimeError(
             f"{path} is missing: build the sm_100a extension first "
             "(python -c 'import __graft_entry__ as g; g.build()')"
         )
     lib = ctypes.CDLL(str(path))
+    variant = bool(os.environ.get("P3_LIB"))  # an experiment build (older variants may lack newer entries)
     for name, (res, args) in SIGNATURES.items():
+        if variant and not hasattr(lib, name):
+            continue
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args

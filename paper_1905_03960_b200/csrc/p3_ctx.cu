@@ -96,8 +96,8 @@ struct PeerLayout {
 // Local arena of one rank. The per-iteration part (cursor | srv_lo | srv_taken | it) is
 // contiguous so one memset resets it before each launch.
 struct LocalLayout {
-  uint64_t pub, fifo_key, claim, iter_begin, cursor, srv_lo, srv_taken, it, sweep, slice_elems, pcount, iter_end, V,
-      bytes, trace_n, trace, cta_phase, vclock, pubseq, ingested, heads, total;
+  uint64_t pub, fifo_key, claim, iter_begin, cursor, srv_lo, srv_taken, it, pcount, iter_end, V,
+      M, bytes, trace_n, trace, cta_phase, vclock, pubseq, ingested, heads, total;
 };
 
 struct p3_ctx {
@@ -113,8 +113,7 @@ struct p3_ctx {
   // P3_TMA=0 (direct loads instead of the TMA stage ring), P3_PUSH_SPLIT=n, P3_SRV_FILTER=n,
   // P3_TRACE_CTA=1 (trace records carry CTA indices; CTA start / exit records)
   struct {
-    uint32_t use_tma = 1, push_split = 0, srv_filter = 0, trace_cta = 0, srv_reserve = 0, tma_store = 1, tma_store_red = 0, pop_relax = 0,
-             sweep = 0, sweep_div = 2, sweep_min = 4096, sweep_max = 65536;
+    uint32_t use_tma = 1, push_split = 0, srv_filter = 0, trace_cta = 0, srv_reserve = 0, tma_store = 1, tma_store_red = 0, pop_relax = 0;
   } knobs;
   std::vector<uint32_t> own_total;
   std::vector<uint64_t> own_stride;
@@ -185,7 +184,7 @@ PeerLayout peer_layout_of(const p3_ctx* c, uint32_t rank) {
   PeerLayout p;
   uint64_t o = 0;
   p.w = o;
-  o = align_up(o + c->w_elems * 4, 256);
+  o = align_up(o + c->w_elems * (c->cfg.param_bf16 ? 2 : 4), 256);
   p.r = o;
   o = align_up(o + (uint64_t)c->N * c->own_stride[rank] * 4, 256);
   p.arrivals = o;
@@ -211,7 +210,7 @@ PeerLayout peer_layout_of(const p3_ctx* c, uint32_t rank) {
   return p;
 }
 
-LocalLayout local_layout_of(const p3_ctx* c, uint64_t v_elems) {
+LocalLayout local_layout_of(const p3_ctx* c, uint64_t v_elems, uint64_t m_elems) {
   LocalLayout q;
   uint64_t o = 0;
   auto take = [&](uint64_t& field, uint64_t bytes) {
@@ -226,11 +225,10 @@ LocalLayout local_layout_of(const p3_ctx* c, uint64_t v_elems) {
   take(q.srv_lo, c->L * 4ull);
   take(q.srv_taken, c->L * 4ull);
   take(q.it, sizeof(IterState));
-  take(q.sweep, 8);
-  take(q.slice_elems, c->S * 4ull);
   take(q.pcount, 8);
   q.iter_end = o;
   take(q.V, v_elems * 4);
+  take(q.M, m_elems * 4);
   take(q.bytes, 16);
   take(q.trace_n, 8);
   take(q.trace, (uint64_t)c->cfg.trace_cap * sizeof(p3_trace_rec_t));
@@ -300,6 +298,8 @@ int p3_ctx_create(const p3_config_t* cfg, p3_ctx_t** out) {
     return fail(nullptr, P3_EUSAGE,
                 "comm_threads must be a multiple of 32 in [128, " + std::to_string(P3_COMM_MAX_THREADS) + "] (scheduler + signaler + producer + consumer warps)");
   if (cfg->comm_ctas < 1) return fail(nullptr, P3_EUSAGE, "comm_ctas must be >= 1");
+  if (cfg->param_bf16 && (cfg->push_bf16 || cfg->emulate_grads))
+    return fail(nullptr, P3_EUSAGE, "param_bf16 takes bf16 gradients from the model (no push_bf16, no emulate_grads)");
   if (cfg->drain_streams > P3_SIDE_STREAMS)
     return fail(nullptr, P3_EUSAGE, "drain_streams must be in [0, " + std::to_string(P3_SIDE_STREAMS) + "]");
   for (uint32_t i = 0; i < cfg->n_local; ++i)
@@ -328,12 +328,6 @@ int p3_ctx_create(const p3_config_t* cfg, p3_ctx_t** out) {
     c->knobs.tma_store = env_u32("P3_TMA_STORE", 1);
     c->knobs.pop_relax = env_u32("P3_POP_RELAX", 0);  // 0: the config's
     c->knobs.tma_store_red = env_u32("P3_TMA_STORE_RED", 0);
-    // single rank: the FINISH launch sweeps guided chunks of the element space instead of
-    // popping slices (measured slower than the slice pops so far: off by default)
-    c->knobs.sweep = env_u32("P3_SWEEP", 0);
-    c->knobs.sweep_div = std::max<uint32_t>(1, env_u32("P3_SWEEP_DIV", 2));
-    c->knobs.sweep_min = env_u32("P3_SWEEP_MIN", 4096) & ~7u;
-    c->knobs.sweep_max = std::max<uint32_t>(c->knobs.sweep_min, env_u32("P3_SWEEP_MAX", 65536) & ~7u);
   }
   std::string perr;
   int rc = cfg->plan_mode == P3_PLAN_P3
@@ -445,10 +439,6 @@ int p3_ctx_create(const p3_config_t* cfg, p3_ctx_t** out) {
   std::vector<uint32_t> own_base(N, 0);
   for (uint32_t o = 1; o < N; ++o) own_base[o] = own_base[o - 1] + c->own_total[o - 1];
   const size_t o_ob = put(own_base.data(), N * 4ull);
-  std::vector<uint64_t> pstart(L + 1, 0);
-  for (uint32_t l = 0; l < L; ++l) pstart[l + 1] = pstart[l] + align_up(c->counts[l], 8);
-  const size_t o_ps = put(pstart.data(), (L + 1) * 8ull);
-  const size_t o_lc = put(c->counts.data(), L * 8ull);
   bool rr = true;
   for (uint32_t g = 0; g < S && rr; ++g) rr = slice_owner[g] == g % N;
   cudaError_t e = cudaMalloc(&c->d_plan, blob.size());
@@ -481,8 +471,6 @@ int p3_ctx_create(const p3_config_t* cfg, p3_ctx_t** out) {
   P.own_stride = reinterpret_cast<const uint64_t*>(pb + o_ost);
   P.layer_group = reinterpret_cast<const uint32_t*>(pb + o_lg);
   P.own_base = reinterpret_cast<const uint32_t*>(pb + o_ob);
-  P.layer_pstart = reinterpret_cast<const uint64_t*>(pb + o_ps);
-  P.layer_count = reinterpret_cast<const uint64_t*>(pb + o_lc);
   P.rr_owner = rr ? 1u : 0u;
 
   // ---- per-rank arenas
@@ -493,7 +481,8 @@ int p3_ctx_create(const p3_config_t* cfg, p3_ctx_t** out) {
     e = cudaMalloc(&c->peer_arena[i], pl.bytes);
     if (e == cudaSuccess) e = cudaMemset(c->peer_arena[i], 0, pl.bytes);
     const uint64_t v_elems = cfg->momentum != 0.f ? c->own_stride[rank] : 0;
-    LocalLayout ll = local_layout_of(c, v_elems);
+    const uint64_t m_elems = cfg->param_bf16 ? c->own_stride[rank] : 0;
+    LocalLayout ll = local_layout_of(c, v_elems, m_elems);
     c->local_layout = ll;
     if (e == cudaSuccess) e = cudaMalloc(&c->local_arena[i], ll.total);
     if (e == cudaSuccess) e = cudaMemset(c->local_arena[i], 0, ll.total);
@@ -519,6 +508,7 @@ int p3_ctx_create(const p3_config_t* cfg, p3_ctx_t** out) {
     D.srv_taken = reinterpret_cast<uint32_t*>(lb + ll.srv_taken);
     D.it = reinterpret_cast<IterState*>(lb + ll.it);
     D.V = v_elems ? reinterpret_cast<float*>(lb + ll.V) : nullptr;
+    D.M = m_elems ? reinterpret_cast<float*>(lb + ll.M) : nullptr;
     D.bytes = reinterpret_cast<unsigned long long*>(lb + ll.bytes);
     D.trace_n = reinterpret_cast<unsigned long long*>(lb + ll.trace_n);
     D.trace = reinterpret_cast<p3_trace_rec_t*>(lb + ll.trace);
@@ -526,8 +516,6 @@ int p3_ctx_create(const p3_config_t* cfg, p3_ctx_t** out) {
     D.vclock = reinterpret_cast<unsigned long long*>(lb + ll.vclock);
     D.pubseq = reinterpret_cast<uint32_t*>(lb + ll.pubseq);
     D.ingested = reinterpret_cast<uint32_t*>(lb + ll.ingested);
-    D.sweep = reinterpret_cast<unsigned long long*>(lb + ll.sweep);
-    D.slice_elems = reinterpret_cast<uint32_t*>(lb + ll.slice_elems);
     D.pcount = reinterpret_cast<uint32_t*>(lb + ll.pcount);
     D.ntf_head = reinterpret_cast<uint32_t*>(lb + ll.heads);
     D.pull_head = D.ntf_head + 1;
@@ -637,6 +625,19 @@ int p3_ctx_params(p3_ctx_t* c, uint32_t li, float** params) {
   return P3_OK;
 }
 
+static CommArgs comm_args(p3_ctx* c, uint32_t mode, uint32_t ctas);
+
+int p3_master_init(p3_ctx_t* c, uint32_t li, void* stream) {
+  int rc = check_local(c, li);
+  if (rc) return rc;
+  if (!c->cfg.param_bf16) return fail(c, P3_EUSAGE, "p3_master_init needs param_bf16");
+  CommArgs a = comm_args(c, P3_COMM_FINISH, 1);
+  a.loc[0] = c->loc[li];
+  a.n_local = 1;
+  if (launch_master_init(a, stream) != P3_OK) return cuda_fail(c, cudaGetLastError(), "master init launch");
+  return P3_OK;
+}
+
 int p3_ctx_grads(p3_ctx_t* c, uint32_t li, float** grads) {
   int rc = check_local(c, li);
   if (rc) return rc;
@@ -674,11 +675,9 @@ static CommArgs comm_args(p3_ctx* c, uint32_t mode, uint32_t ctas) {
                              : std::max<uint32_t>(1, std::min<uint32_t>(8, c->S / std::max<uint32_t>(1, 4 * ctas)));
   a.pop_multi = std::max<uint32_t>(1, std::min<uint32_t>(4, c->cfg.pop_multi ? c->cfg.pop_multi : 1));
   a.push_bf16 = c->cfg.push_bf16 ? 1u : 0u;
+  a.pb16 = c->cfg.param_bf16 ? 1u : 0u;
   a.notify = c->cfg.notify_pull && c->N > 1 ? 1u : 0u;
   a.ntf_cap = c->S;
-  a.sweep_div = c->knobs.sweep_div;
-  a.sweep_min = std::max<uint32_t>(8, c->knobs.sweep_min);
-  a.sweep_max = c->knobs.sweep_max;
   a.pull_cap = c->S * (c->N > 1 ? c->N - 1 : 1);
   a.trace_cta = c->knobs.trace_cta;
   a.push_split = c->knobs.push_split;
@@ -773,12 +772,7 @@ int p3_iteration_end(p3_ctx_t* c, uint64_t k) {
     CK(cudaStreamWaitEvent(c->comm_stream, c->side_ev[j], 0));
   }
   const uint32_t ctas = c->cfg.finish_ctas ? c->cfg.finish_ctas : c->cfg.comm_ctas;
-  // Single rank, no DRAIN launch this iteration and bounded relaxation allowed: the FINISH
-  // launch is the only consumer and every layer is published, so it sweeps the priority-
-  // ordered element space in guided chunks (perfect balance over the CTAs, claims in order).
-  const bool sweep = c->N == 1 && c->side_used == 0 && c->cfg.pop_relax != 1 && c->knobs.sweep;
-  if (launch_comm(comm_args(c, sweep ? P3_COMM_SWEEP : P3_COMM_FINISH, ctas), ctas, c->cfg.comm_threads,
-                  c->comm_stream) != P3_OK)
+  if (launch_comm(comm_args(c, P3_COMM_FINISH, ctas), ctas, c->cfg.comm_threads, c->comm_stream) != P3_OK)
     return cuda_fail(c, cudaGetLastError(), "comm kernel launch");
   c->launches++;
   CK(cudaEventRecord(c->comm_done, c->comm_stream));
@@ -903,8 +897,21 @@ int p3_apply_slice(p3_ctx_t* c, uint32_t li, uint32_t layer, uint32_t slice, con
                                      std::to_string(r.length));
   if (!values) return fail(c, P3_EUSAGE, "null payload");
   const uint32_t rank = c->cfg.local_ranks[li];
-  float* dst = c->peers.W[rank] + c->layer_woff[layer] + r.offset;
-  CK(cudaMemcpyAsync(dst, values, n * 4, cudaMemcpyHostToDevice, (cudaStream_t)stream));
+  const uint64_t e = c->layer_woff[layer] + r.offset;
+  if (c->cfg.param_bf16) {  // the replica holds bf16: round to nearest even on the host
+    std::vector<uint16_t> h(n);
+    for (uint64_t i = 0; i < n; ++i) {
+      uint32_t x;
+      std::memcpy(&x, values + i, 4);
+      h[i] = (x & 0x7fffffffu) > 0x7f800000u ? (uint16_t)((x >> 16) | 0x40u)
+                                             : (uint16_t)((x + 0x7fffu + ((x >> 16) & 1u)) >> 16);
+    }
+    CK(cudaMemcpyAsync(reinterpret_cast<uint16_t*>(c->peers.W[rank]) + e, h.data(), n * 2, cudaMemcpyHostToDevice,
+                       (cudaStream_t)stream));
+    CK(cudaStreamSynchronize((cudaStream_t)stream));  // (h is released on return)
+  } else {
+    CK(cudaMemcpyAsync(c->peers.W[rank] + e, values, n * 4, cudaMemcpyHostToDevice, (cudaStream_t)stream));
+  }
   if (launch_bump(c->peers.done[rank] + layer, c->peers.gdone[rank] + c->layer_group[layer], 1, stream) != P3_OK)
     return cuda_fail(c, cudaGetLastError(), "gate counter update");
   return P3_OK;

@@ -16,8 +16,6 @@
 #define P3_DBG_CTAS 512
 #define P3_COMM_DRAIN 0   // exit as soon as nothing is poppable or reducible
 #define P3_COMM_FINISH 1  // exit when the iteration's local work is complete
-#define P3_COMM_SWEEP 2   // single rank, every layer published, no other consumer: claim chunks of
-                          // the priority-ordered element space (guided sizes) until it is covered
 
 namespace p3 {
 
@@ -54,9 +52,6 @@ struct PlanDev {
   const uint64_t* own_stride;     // [world] R block stride (padded owned elements)
   const uint32_t* layer_group;    // [L] forward-gate group of the layer
   const uint32_t* own_base;       // [world] first own_list position of each owner
-  const uint64_t* layer_pstart;   // [L+1] start of each layer in the padded flat element space
-                                  // (layers in priority order, each padded to a multiple of 8)
-  const uint64_t* layer_count;    // [L] parameters of each layer
 };
 
 // Peer-visible state of every rank (pointers valid in this process: local or IPC-mapped).
@@ -108,6 +103,7 @@ struct LocalDev {
   uint32_t* srv_taken;  // [L] owned slices claimed (per iteration)
   IterState* it;        // per iteration
   float* V;             // momentum of owned elements [own_stride] (may be null)
+  float* M;             // param_bf16: fp32 master of owned elements [own_stride] (else null)
   unsigned long long* bytes;  // [2] in, out
   unsigned long long* trace_n;
   p3_trace_rec_t* trace;
@@ -118,8 +114,6 @@ struct LocalDev {
   uint32_t* pubseq;            // ring entries published (stream memory write, monotone)
   uint32_t* ingested;          // ring entries turned into publication words (monotone)
   uint32_t* ingested_host;     // host-mapped mirror of `ingested` (host back-pressure)
-  unsigned long long* sweep;   // SWEEP: next unclaimed position of the padded flat space (per iteration)
-  uint32_t* slice_elems;       // [S] SWEEP: elements of each slice updated so far (per iteration)
   uint32_t* ntf_head;          // notify mode: NOTIFY entries consumed (monotone)
   uint32_t* pull_head;         // notify mode: PULL requests answered or claimed (monotone)
   uint32_t* pcount;            // [2] notify mode, per iteration: PULLs sent, PULLs answered
@@ -142,8 +136,8 @@ struct CommArgs {
   uint32_t pop_multi; // candidate layers claimed per round of pop atomics
   uint32_t push_bf16; // pushes travel as bf16
   uint32_t notify;    // notify mode (P3 config notify_pull, N > 1)
+  uint32_t pb16;      // param_bf16: bf16 replicas / gradients, fp32 masters
   uint32_t ntf_cap, pull_cap;  // ring entries
-  uint32_t sweep_div, sweep_min, sweep_max;  // SWEEP chunk: remaining / (div x CTAs) in [min, max]
   uint32_t push_split; // every push_split-th CTA prefers pushes over server work (0: none)
   uint32_t srv_filter; // server picks: only srv_filter x (ready slices) consumers look (0: all)
   uint32_t srv_reserve; // N > 1: every srv_reserve-th CTA does server work only (0: none)
@@ -164,6 +158,7 @@ int launch_gradgen(uint64_t seed, uint64_t iteration, uint64_t layer, uint64_t s
                    float* out, void* stream);
 int launch_mark(const LocalDev& L, uint32_t k, uint32_t ev, void* stream);
 int launch_bump(uint32_t* done, uint32_t* gdone, uint32_t v, void* stream);
+int launch_master_init(const CommArgs& a, void* stream);
 int launch_queue_pop(const uint32_t* nslices, const uint32_t* first, const uint64_t* pub,
                      const uint32_t* fifo_key, uint32_t* cursor, uint32_t n_layers, uint32_t sched,
                      uint32_t tag, uint32_t* result, void* stream);

@@ -143,6 +143,23 @@ __device__ __forceinline__ uint64_t globaltimer() {
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
+// P3_COLD: functions off the N=1 hot loop (N>1 server role, notify mode, K7, the trace) may be
+// compiled out of line so the scheduler's inlined code stays small (experiment switch).
+#ifndef P3_COLD
+#define P3_COLD
+#endif
+// P3_TRACE=0 compiles the device trace out (experiment switch; the tests need it on).
+#ifndef P3_TRACE
+#define P3_TRACE 1
+#endif
+
+// Diagnostics clock of the per-job time totals (t_pick / t_slot_wait / t_move / t_signal in
+// the debug snapshot): %globaltimer reads are not free, so they compile out with P3_STATS=0.
+#ifndef P3_STATS
+#define P3_STATS 1
+#endif
+__device__ __forceinline__ uint64_t stat_clock() { return P3_STATS ? globaltimer() : 0ull; }
+
 // Bounded mbarrier wait: every wait of the stage pipeline ends within the iteration timeout
 // (the scheduler posts EXIT by then), so one that outlives it is a protocol bug — trap (the
 // host sees a launch failure) rather than hang the GPU.
@@ -396,7 +413,7 @@ __global__ void k_sleep(uint64_t ns) {
 
 __device__ __forceinline__ void trace_append(const LocalDev& L, uint32_t k, uint32_t layer, uint32_t slice,
                                              uint32_t rank, uint32_t ev, uint64_t t0 = 0) {
-  if (!L.trace_cap) return;
+  if (!P3_TRACE || !L.trace_cap) return;
   const unsigned long long idx = atomicAdd(L.trace_n, 1ull);
   if (idx < L.trace_cap) {
     p3_trace_rec_t r;
@@ -483,7 +500,8 @@ __device__ uint32_t warp_pop(const QueueView& q, uint32_t tag, uint32_t* dbg = n
     constexpr uint32_t CH = 8;  // chunks of 32 layers examined per memory round trip
     for (uint32_t group = 0, attempt = 0; group < q.n_layers; ++attempt) {
       // all loads of the group issued before any is used: one round trip, not 2*CH
-      const uint64_t t_snap = globaltimer_lane0();  // (trace: before this snapshot's loads)
+      // (trace only: the time before this snapshot's loads; %globaltimer is not free)
+      const uint64_t t_snap = P3_TRACE && q.ring && q.ring->trace_cap ? globaltimer_lane0() : 0ull;
       uint64_t w[CH];
       uint32_t cur[CH], ns[CH];
       // the ring check rides on the same round trip as the first group's loads
@@ -638,7 +656,7 @@ __device__ uint32_t warp_pop(const QueueView& q, uint32_t tag, uint32_t* dbg = n
   if (q.ring) ingest(*q.ring, q.sched);
   for (uint32_t retry = 0;; ++retry) {
     if (dbg && lane == 0) *(volatile uint32_t*)dbg = (6u << 20) | (retry & 0xfffff);
-    const uint64_t t_snap = globaltimer_lane0();
+    const uint64_t t_snap = q.ring && q.ring->trace_cap ? globaltimer_lane0() : 0ull;
     uint32_t best_key = P3_NONE, best_l = P3_NONE;
     uint64_t best_w = 0;
     for (uint32_t l = lane; l < q.n_layers; l += 32) {
@@ -703,7 +721,7 @@ int launch_queue_pop(const uint32_t* nslices, const uint32_t* first, const uint6
 // ends here), one to scan 256 layers, one for a window of 32 owned slices (arrivals and
 // claims are indexed by the slice's position in the owner's list, so no indirection), one
 // claim.
-__device__ uint32_t warp_server_pick(const CommArgs& a, const LocalDev& L, uint32_t* layer_out,
+__device__ P3_COLD uint32_t warp_server_pick(const CommArgs& a, const LocalDev& L, uint32_t* layer_out,
                                      uint32_t* dbg = nullptr) {
   const uint32_t lane = threadIdx.x & 31;
   const PlanDev& P = a.plan;
@@ -732,7 +750,7 @@ __device__ uint32_t warp_server_pick(const CommArgs& a, const LocalDev& L, uint3
   // takes one candidate — the (blockIdx + attempt)-th of the most urgent ones, spreading the
   // consumers like the pops do — and a miss rescans.
   for (uint32_t attempt = 0; attempt < 4; ++attempt) {
-    const uint64_t t_snap = globaltimer_lane0();  // (trace: before this scan's loads)
+    const uint64_t t_snap = L.trace_cap ? globaltimer_lane0() : 0ull;  // (trace: before this scan's loads)
     uint32_t ncand = 0, tl = P3_NONE, t_start = 0, t_cnt = 0;
     for (uint32_t group = 0; group < nl && tl == P3_NONE; group += 32 * CH) {
       uint32_t oc[CH], hv[CH], tk[CH], lo[CH];
@@ -866,10 +884,9 @@ __device__ __forceinline__ QueueView queue_of(const CommArgs& a, const LocalDev&
 struct Job {
   uint32_t kind, li, g, layer, opos, rank, len, n, aligned, run;  // opos: position in the owner's list
   uint32_t ndst;    // REDUCE: replicas written (dst[0..ndst)): N, or 1 when peers pull (notify mode)
+  uint32_t pb16;    // REDUCE, param_bf16: bf16 contributions, fp32 master m, bf16 replicas
+  float* m;         // REDUCE, param_bf16: the owner's fp32 master of the slice
   uint32_t answer;  // PUSH-shaped copy of an updated slice to a peer that pulled it (notify mode)
-  uint32_t piece;  // SWEEP: the job updates elements [e0, e0 + len) of layer `layer` (slices
-                   // complete when all their elements are done, counted per element)
-  uint32_t e0;
   uint32_t bf16;  // pushes travel as bf16 (declared lossy mode); own = index of the fp32 source
   const float* src[P3_MAX_RANKS];  // PUSH: src[0]; REDUCE: contributions in rank order
   float* dst[P3_MAX_RANKS];        // PUSH: dst[0]; REDUCE: replicas, dst[0] = owner's master
@@ -901,7 +918,7 @@ __device__ __forceinline__ void bar_arrive(uint32_t id, uint32_t n) {
 // wait until they are all taken — the reference's consume() returns at that point. As a
 // virtual clock V (the time the bucket has paid for): a grant moves it to
 // max(V, now - burst) + bytes/rate and may proceed once now >= V'.
-__device__ void pace(const CommArgs& a, const LocalDev& L, uint64_t bytes) {
+__device__ P3_COLD void pace(const CommArgs& a, const LocalDev& L, uint64_t bytes) {
   if (a.ns_per_byte == 0.f || bytes == 0) return;
   const unsigned long long cost = (unsigned long long)((double)bytes * a.ns_per_byte);
   const unsigned long long now = globaltimer();
@@ -1012,9 +1029,9 @@ __device__ uint32_t prepare_push(const CommArgs& a, uint32_t li, uint32_t g, uin
   }
   if (lane == 0) {
     job->kind = JOB_PUSH;
-    job->piece = 0;
     job->ndst = 1;
     job->answer = 0;
+    job->pb16 = 0;
     job->run = 1;
     job->n = 1;  // one source (the slot keeps no stale rank count from a previous reduce)
     job->li = li;
@@ -1023,11 +1040,17 @@ __device__ uint32_t prepare_push(const CommArgs& a, uint32_t li, uint32_t g, uin
     job->opos = opos;
     job->rank = o;
     job->len = P.slice_len[g];
-    job->src[0] = pub_ptr(w) + P.slice_off[g];
-    job->bf16 = a.push_bf16;
     const uint64_t ri = (uint64_t)r * P.own_stride[o] + P.slice_slot[g];
-    job->dst[0] = a.push_bf16 ? reinterpret_cast<float*>(reinterpret_cast<__nv_bfloat16*>(a.peers.R[o]) + ri)
-                              : a.peers.R[o] + ri;
+    if (a.pb16) {  // bf16 gradient copied as is into a bf16 receive slot (2-byte elements)
+      job->src[0] = reinterpret_cast<const float*>(reinterpret_cast<const __nv_bfloat16*>(pub_ptr(w)) + P.slice_off[g]);
+      job->bf16 = 2;
+      job->dst[0] = reinterpret_cast<float*>(reinterpret_cast<__nv_bfloat16*>(a.peers.R[o]) + ri);
+    } else {
+      job->src[0] = pub_ptr(w) + P.slice_off[g];
+      job->bf16 = a.push_bf16;
+      job->dst[0] = a.push_bf16 ? reinterpret_cast<float*>(reinterpret_cast<__nv_bfloat16*>(a.peers.R[o]) + ri)
+                                : a.peers.R[o] + ri;
+    }
   }
   return PUSH_REMOTE;
 }
@@ -1058,22 +1081,26 @@ __device__ void prepare_reduce(const CommArgs& a, uint32_t li, uint32_t g, uint3
   uintptr_t al = 0;
   if (q < N) {
     const uint64_t ri = (uint64_t)q * stride + slot;
-    const float* rsrc = a.push_bf16 ? reinterpret_cast<const float*>(reinterpret_cast<__nv_bfloat16*>(a.peers.R[o]) + ri)
-                                    : a.peers.R[o] + ri;
-    const float* src = q == o ? pub_ptr(w) + soff : rsrc;
-    float* dst = a.peers.W[q] + woff;
+    const bool b16 = a.push_bf16 || a.pb16;  // receive slots hold bf16
+    const float* rsrc = b16 ? reinterpret_cast<const float*>(reinterpret_cast<__nv_bfloat16*>(a.peers.R[o]) + ri)
+                            : a.peers.R[o] + ri;
+    const float* own = a.pb16 ? reinterpret_cast<const float*>(reinterpret_cast<const __nv_bfloat16*>(pub_ptr(w)) + soff)
+                              : pub_ptr(w) + soff;
+    const float* src = q == o ? own : rsrc;
+    float* dst = a.pb16 ? reinterpret_cast<float*>(reinterpret_cast<__nv_bfloat16*>(a.peers.W[q]) + woff)
+                        : a.peers.W[q] + woff;
     job->src[q] = src;
     job->dst[q == o ? 0 : (q < o ? q + 1 : q)] = dst;
     al = (uintptr_t)src | (uintptr_t)dst;
   }
   float* v = L.V ? L.V + slot : nullptr;
+  float* m = L.M ? L.M + slot : nullptr;
 #pragma unroll
   for (int off = 16; off; off >>= 1) al |= __shfl_xor_sync(FULL_MASK, (unsigned long long)al, off);
 #pragma unroll
   for (int off = 16; off; off >>= 1) len += __shfl_xor_sync(FULL_MASK, len, off);
   if (q == 0) {
     job->kind = JOB_REDUCE;
-    job->piece = 0;
     job->ndst = a.notify ? 1u : N;  // notify mode: peers pull the update (server.py:227-247)
     job->answer = 0;
     job->li = li;
@@ -1084,62 +1111,11 @@ __device__ void prepare_reduce(const CommArgs& a, uint32_t li, uint32_t g, uint3
     job->len = len;
     job->n = N;
     job->v = v;
+    job->m = m;
+    job->pb16 = a.pb16;
     job->bf16 = a.push_bf16 ? 1u + o : 0u;  // 1 + index of the owner's own (fp32) contribution
-    job->aligned = ((al | (uintptr_t)v) & 15) == 0;
+    job->aligned = ((al | (uintptr_t)v | (uintptr_t)m) & 15) == 0;
   }
-}
-
-// SWEEP (single rank): elements [e0, e0 + len) of layer l (momentum: inside slice g).
-__device__ void prepare_piece(const CommArgs& a, uint32_t l, uint64_t w, uint32_t e0, uint32_t len, uint32_t g,
-                              Job* job) {
-  const PlanDev& P = a.plan;
-  const LocalDev& L = a.loc[0];
-  if ((threadIdx.x & 31) == 0) {
-    const float* src = pub_ptr(w) + e0;
-    float* dst = a.peers.W[L.rank] + P.layer_woff[l] + e0;
-    float* v = L.V ? L.V + P.slice_slot[g] + (e0 - P.slice_off[g]) : nullptr;
-    job->kind = JOB_REDUCE;
-    job->piece = 1;
-    job->ndst = 1;
-    job->answer = 0;
-    job->e0 = e0;
-    job->li = 0;
-    job->g = g;
-    job->layer = l;
-    job->rank = L.rank;
-    job->run = 1;
-    job->len = len;
-    job->n = 1;
-    job->src[0] = src;
-    job->dst[0] = dst;
-    job->v = v;
-    job->bf16 = a.push_bf16 ? 1u : 0u;
-    job->aligned = (((uintptr_t)src | (uintptr_t)dst | (uintptr_t)v) & 15) == 0;
-  }
-}
-
-// Largest layer l with layer_pstart[l] <= pos (one warp; a 32-ary search: one round trip per
-// factor of 32 layers).
-__device__ uint32_t find_layer(const PlanDev& P, uint64_t pos) {
-  const uint32_t lane = threadIdx.x & 31;
-  uint32_t lo = 0, hi = P.n_layers;
-  while (hi - lo > 1) {
-    const uint32_t step = (hi - lo + 31) / 32;
-    const uint32_t idx = lo + lane * step;
-    const bool le = idx < hi && P.layer_pstart[idx] <= pos;
-    const uint32_t m = __ballot_sync(FULL_MASK, le);
-    lo = lo + (31 - __clz(m)) * step;
-    hi = min(hi, lo + step);
-  }
-  return lo;
-}
-
-// Slice of layer l holding element e: slices are equal-sized except the last (make_p3_plan
-// and make_baseline_plan both cut that way).
-__device__ __forceinline__ uint32_t slice_at(const PlanDev& P, uint32_t l, uint64_t e) {
-  const uint32_t first = P.layer_first[l], ns = P.layer_nslices[l];
-  const uint64_t unit = P.slice_len[first];
-  return first + (uint32_t)min(e / unit, (uint64_t)(ns - 1));
 }
 
 // bf16 transport (declared lossy mode): each rank's contribution is rounded to bf16 (round
@@ -1251,9 +1227,15 @@ struct RangePtrs {
   const float* src[P3_MAX_RANKS];
   float* dst[P3_MAX_RANKS];
 };
+__device__ __noinline__ void move_range_pb16(const CommArgs& a, const Job& j, uint32_t e0, uint32_t n, uint32_t tid,
+                                             uint32_t nthr);
 __device__ void move_range(const CommArgs& a, const Job& j, uint32_t e0, uint32_t n, RangePtrs* ptrs, uint32_t tid,
                            uint32_t nthr) {
   const bool bf = j.bf16 != 0;
+  if (j.pb16 || (j.kind == JOB_PUSH && j.bf16 == 2)) {
+    move_range_pb16(a, j, e0, n, tid, nthr);
+    return;
+  }
   if (j.kind == JOB_PUSH) {
     if (bf)
       cta_copy_to_bf16(reinterpret_cast<__nv_bfloat16*>(j.dst[0]) + e0, j.src[0] + e0, n, tid, nthr);
@@ -1307,8 +1289,8 @@ __device__ __forceinline__ uint32_t job_tile(const Job& j) {
 // 16-byte aligned sources (TMA requirement; bf16 receive slots at 2-byte pitch)
 __device__ __forceinline__ bool job_tma_ok(const Job& j) {
   if (j.kind == JOB_PUSH)  // and the vector stores of the consumers (float4, or 4 x bf16)
-    return ((uintptr_t)j.src[0] & 15) == 0 && ((uintptr_t)j.dst[0] & (j.bf16 ? 7 : 15)) == 0;
-  uintptr_t al = (uintptr_t)j.dst[0] | (uintptr_t)j.v;
+    return ((uintptr_t)j.src[0] & 15) == 0 && ((uintptr_t)j.dst[0] & (j.bf16 == 1 ? 7 : 15)) == 0;
+  uintptr_t al = (uintptr_t)j.dst[0] | (uintptr_t)j.v | (uintptr_t)j.m;
   for (uint32_t q = 0; q < j.n; ++q) al |= (uintptr_t)j.src[q];
   return (al & 15) == 0 && j.aligned;
 }
@@ -1358,12 +1340,63 @@ __device__ __forceinline__ void consume_reduce(const uint8_t* st, uint32_t pitch
   }
 }
 
+// param_bf16 reduce of one staged tile: the N bf16 contributions summed in fp32 in ascending
+// rank order, the fp32 master updated (the same sgd4 as the fp32 path) and stored, and every
+// replica written as bf16(master), round to nearest even. Out of line: an opt-in mode.
+__device__ __noinline__ void consume_reduce_pb16(const CommArgs& a, const Job& j, const StageDesc& d,
+                                                 const uint8_t* st, uint32_t tid, uint32_t nthr) {
+  const uint32_t N = j.n, n4 = d.n / 4, e4 = d.e0 / 4, pitch = d.tile * 4;
+  const UpdCoef c = make_coef(N, a.lr, a.momentum);
+  const float4* tp = reinterpret_cast<const float4*>(st + N * pitch);
+  const float4* tv = reinterpret_cast<const float4*>(st + (N + 1) * pitch);
+  float4* m = reinterpret_cast<float4*>(j.m) + e4;
+  float4* v = j.v ? reinterpret_cast<float4*>(j.v) + e4 : nullptr;
+  for (uint32_t k = tid; k < n4; k += nthr) {
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (uint32_t q = 0; q < N; ++q) {
+      const float4 x = from_bf16x4(reinterpret_cast<const uint2*>(st + q * pitch)[k]);
+      acc.x = __fadd_rn(acc.x, x.x);
+      acc.y = __fadd_rn(acc.y, x.y);
+      acc.z = __fadd_rn(acc.z, x.z);
+      acc.w = __fadd_rn(acc.w, x.w);
+    }
+    float4 vv = v ? tv[k] : make_float4(0.f, 0.f, 0.f, 0.f);
+    const float4 r = sgd4(tp[k], acc, c, v ? &vv : nullptr);
+    if (v) v[k] = vv;
+    m[k] = r;
+    const uint2 h = to_bf16x4(r);
+    for (uint32_t q = 0; q < j.ndst; ++q) reinterpret_cast<uint2*>(j.dst[q])[e4 + k] = h;
+  }
+}
+
+__device__ __noinline__ void move_range_pb16(const CommArgs& a, const Job& j, uint32_t e0, uint32_t n, uint32_t tid,
+                                             uint32_t nthr) {
+  const UpdCoef c = make_coef(j.n, a.lr, a.momentum);
+  for (uint32_t i = e0 + tid; i < e0 + n; i += nthr) {
+    if (j.kind == JOB_PUSH) {  // bf16 copy
+      reinterpret_cast<__nv_bfloat16*>(j.dst[0])[i] = reinterpret_cast<const __nv_bfloat16*>(j.src[0])[i];
+      continue;
+    }
+    float acc = 0.f;
+    for (uint32_t q = 0; q < j.n; ++q)
+      acc = __fadd_rn(acc, __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(j.src[q])[i]));
+    const float p = sgd_step(j.m[i], acc, c, j.v ? j.v + i : nullptr);
+    j.m[i] = p;
+    const __nv_bfloat16 h = __float2bfloat16_rn(p);
+    for (uint32_t q = 0; q < j.ndst; ++q) reinterpret_cast<__nv_bfloat16*>(j.dst[q])[i] = h;
+  }
+}
+
+template <bool ONE>
 __device__ void consume_tile(const CommArgs& a, const Job& j, const StageDesc& d, const uint8_t* st, uint32_t tid,
                              uint32_t nthr, bool tosmem = false) {
   const uint32_t n4 = d.n / 4, e4 = d.e0 / 4, pitch = d.tile * 4;
   if (j.kind == JOB_PUSH) {
     const float4* t0 = reinterpret_cast<const float4*>(st);
-    if (j.bf16) {
+    if (j.bf16 == 2) {  // bf16 copy: 8 bf16 per 16 bytes
+      float4* out = reinterpret_cast<float4*>(reinterpret_cast<__nv_bfloat16*>(j.dst[0]) + d.e0);
+      for (uint32_t k = tid; k < d.n / 8; k += nthr) out[k] = t0[k];
+    } else if (j.bf16) {
       uint2* out = reinterpret_cast<uint2*>(j.dst[0]) + e4;  // 4 bf16 per 8 bytes
       for (uint32_t k = tid; k < n4; k += nthr) out[k] = to_bf16x4(t0[k]);
     } else {
@@ -1372,7 +1405,11 @@ __device__ void consume_tile(const CommArgs& a, const Job& j, const StageDesc& d
     }
     return;
   }
-  const uint32_t N = j.n;
+  if (!ONE && j.pb16) {
+    consume_reduce_pb16(a, j, d, st, tid, nthr);
+    return;
+  }
+  const uint32_t N = ONE ? 1u : j.n;
   const int nd = (int)j.ndst;
   const bool bf = j.bf16 != 0, mom = j.v != nullptr;
   const int own = bf ? (int)j.bf16 - 1 : -1;
@@ -1389,10 +1426,14 @@ __device__ void consume_tile(const CommArgs& a, const Job& j, const StageDesc& d
       else consume_reduce<K, false, false>(st, pitch, n4, e4, dst, v, own, c, tid, nthr, tosmem, nd);       \
     }                                                                                                   \
     return;
-  switch (N) {
-    P3_CONSUME(1) P3_CONSUME(2) P3_CONSUME(3) P3_CONSUME(4) P3_CONSUME(5) P3_CONSUME(6) P3_CONSUME(7)
-    P3_CONSUME(8)
-    default: break;
+  if (ONE) {
+    switch (N) { P3_CONSUME(1) default: break; }
+  } else {
+    switch (N) {
+      P3_CONSUME(1) P3_CONSUME(2) P3_CONSUME(3) P3_CONSUME(4) P3_CONSUME(5) P3_CONSUME(6) P3_CONSUME(7)
+      P3_CONSUME(8)
+      default: break;
+    }
   }
 #undef P3_CONSUME
   // more than 8 ranks: runtime rank loop
@@ -1424,7 +1465,7 @@ __device__ void consume_tile(const CommArgs& a, const Job& j, const StageDesc& d
 // release semantics at system scope when a peer lives on another GPU. Push: count the
 // arrival at the owner (and the owner's layer hint when it completes the slice). Reduce:
 // bump every replica's done[layer] (the forward gate, worker.py:262-269).
-__device__ void signal_job(const CommArgs& a, const Job& j) {
+__device__ P3_COLD void signal_job(const CommArgs& a, const Job& j) {
   const PlanDev& P = a.plan;
   const LocalDev& L = a.loc[j.li];
   // one fence releases every store the consumers made (ordered before it by the DONE barrier);
@@ -1436,7 +1477,7 @@ __device__ void signal_job(const CommArgs& a, const Job& j) {
     red_add_relaxed_sys(a.peers.done[j.rank] + j.layer, 1u);
     red_add_relaxed_sys(a.peers.gdone[j.rank] + P.layer_group[j.layer], 1u);
     atomicAdd(L.pcount + 1, 1u);
-    atomicAdd(L.bytes + 1, 4ull * j.len);
+    atomicAdd(L.bytes + 1, (j.bf16 == 2 ? 2ull : 4ull) * j.len);
     if (L.trace_cap) trace_append(L, a.k, j.layer, j.g - P.layer_first[j.layer], j.rank, P3_EV_BCAST);
   } else if (j.kind == JOB_PUSH) {
     // the last arriver completes the slice and tells the owner's scheduler (hint)
@@ -1452,22 +1493,6 @@ __device__ void signal_job(const CommArgs& a, const Job& j) {
       }
     }
     atomicAdd(L.bytes + 1, (j.bf16 ? 2ull : 4ull) * j.len);
-  } else if (j.piece) {
-    // SWEEP: a slice is complete when all its elements are (pieces possibly from several CTAs)
-    const uint64_t e1 = (uint64_t)j.e0 + j.len;
-    const uint32_t g1 = slice_at(P, j.layer, e1 - 1);
-    for (uint32_t g = slice_at(P, j.layer, j.e0); g <= g1; ++g) {
-      const uint64_t so = P.slice_off[g], se = so + P.slice_len[g];
-      const uint32_t part = (uint32_t)(min(e1, se) - max((uint64_t)j.e0, so));
-      const uint32_t old = atomicAdd(L.slice_elems + g, part);
-      if (old + part == P.slice_len[g]) {
-        fence_acq_rel_gpu();  // acquire the other pieces' releases before releasing the gate
-        red_add_relaxed_sys(a.peers.done[L.rank] + j.layer, 1u);
-        red_add_relaxed_sys(a.peers.gdone[L.rank] + P.layer_group[j.layer], 1u);
-        atomicAdd(&L.it->reduced, 1u);
-        if (L.trace_cap) trace_append(L, a.k, j.layer, g - P.layer_first[j.layer], L.rank, P3_EV_BCAST);
-      }
-    }
   } else if (a.notify) {
     // notify mode: the owner's replica holds the update; NOTIFY every other rank, which will
     // PULL it (server.py:227-239)
@@ -1483,15 +1508,15 @@ __device__ void signal_job(const CommArgs& a, const Job& j) {
         if (L.trace_cap) trace_append(L, a.k, j.layer, j.g + i - P.layer_first[j.layer], q, P3_EV_NOTIFY);
       }
     }
-    atomicAdd(L.bytes + 0, (j.bf16 ? 2ull : 4ull) * j.len * (j.n - 1));  // pushes received
+    atomicAdd(L.bytes + 0, (j.bf16 || j.pb16 ? 2ull : 4ull) * j.len * (j.n - 1));  // pushes received
   } else {
     const uint32_t grp = P.layer_group[j.layer];
     for (uint32_t q = 0; q < j.n; ++q) {
       red_add_relaxed_sys(a.peers.done[q] + j.layer, j.run);
       red_add_relaxed_sys(a.peers.gdone[q] + grp, j.run);
     }
-    atomicAdd(L.bytes + 0, (j.bf16 ? 2ull : 4ull) * j.len * (j.n - 1));  // pushes received
-    atomicAdd(L.bytes + 1, 4ull * j.len * (j.n - 1));  // broadcasts sent
+    atomicAdd(L.bytes + 0, (j.bf16 || j.pb16 ? 2ull : 4ull) * j.len * (j.n - 1));  // pushes received
+    atomicAdd(L.bytes + 1, (j.pb16 ? 2ull : 4ull) * j.len * (j.n - 1));  // broadcasts sent
     if (L.trace_cap)
       for (uint32_t i = 0; i < j.run; ++i)
         trace_append(L, a.k, j.layer, j.g + i - P.layer_first[j.layer], a.trace_cta ? blockIdx.x : j.rank, P3_EV_BCAST);
@@ -1523,7 +1548,7 @@ __device__ uint32_t take_stash(Stash* st, Popped* out) {
 
 // Notify mode, owner side: claim the next PULL request of this rank's pull ring (one warp;
 // lane 0 decides). Returns the slice and the requester, or P3_NONE.
-__device__ uint32_t warp_answer_pick(const CommArgs& a, const LocalDev& L, uint32_t* layer, uint32_t* requester) {
+__device__ P3_COLD uint32_t warp_answer_pick(const CommArgs& a, const LocalDev& L, uint32_t* layer, uint32_t* requester) {
   const uint32_t lane = threadIdx.x & 31;
   uint32_t g = P3_NONE, q = 0;
   if (lane == 0) {
@@ -1554,7 +1579,7 @@ __device__ uint32_t warp_answer_pick(const CommArgs& a, const LocalDev& L, uint3
 
 // Notify mode, worker side: turn the next NOTIFY of this rank into a PULL request queued at
 // the slice's owner (worker.py:226-239). Returns whether one was sent.
-__device__ bool warp_issue_pull(const CommArgs& a, const LocalDev& L) {
+__device__ P3_COLD bool warp_issue_pull(const CommArgs& a, const LocalDev& L) {
   const uint32_t lane = threadIdx.x & 31;
   uint32_t sent = 0;
   if (lane == 0) {
@@ -1585,14 +1610,14 @@ __device__ bool warp_issue_pull(const CommArgs& a, const LocalDev& L) {
 
 // Notify mode: the answer to a PULL — the owner's updated slice copied into the requester's
 // replica (a push-shaped job: TMA-staged, bulk-stored over NVLink).
-__device__ void prepare_answer(const CommArgs& a, uint32_t li, uint32_t g, uint32_t l, uint32_t q, Job* job) {
+__device__ P3_COLD void prepare_answer(const CommArgs& a, uint32_t li, uint32_t g, uint32_t l, uint32_t q, Job* job) {
   const PlanDev& P = a.plan;
   const LocalDev& L = a.loc[li];
   if ((threadIdx.x & 31) == 0) {
     const uint64_t woff = P.layer_woff[l] + P.slice_off[g];
     job->kind = JOB_PUSH;
     job->answer = 1;
-    job->piece = 0;
+    job->pb16 = 0;
     job->ndst = 1;
     job->run = 1;
     job->n = 1;
@@ -1601,9 +1626,15 @@ __device__ void prepare_answer(const CommArgs& a, uint32_t li, uint32_t g, uint3
     job->layer = l;
     job->rank = q;
     job->len = P.slice_len[g];
-    job->bf16 = 0;
-    job->src[0] = a.peers.W[L.rank] + woff;
-    job->dst[0] = a.peers.W[q] + woff;
+    if (a.pb16) {  // bf16 replicas: a 2-byte copy
+      job->bf16 = 2;
+      job->src[0] = reinterpret_cast<const float*>(reinterpret_cast<const __nv_bfloat16*>(a.peers.W[L.rank]) + woff);
+      job->dst[0] = reinterpret_cast<float*>(reinterpret_cast<__nv_bfloat16*>(a.peers.W[q]) + woff);
+    } else {
+      job->bf16 = 0;
+      job->src[0] = a.peers.W[L.rank] + woff;
+      job->dst[0] = a.peers.W[q] + woff;
+    }
   }
 }
 
@@ -1623,6 +1654,10 @@ __device__ void prepare_answer(const CommArgs& a, uint32_t li, uint32_t g, uint3
 // gradients would hold SMs that the compute producing them may need (co-residency-bound
 // library kernels, lazy module loading). The FINISH launch of an iteration ends once every
 // local slice is pushed and every owned slice reduced; it waits only for peers' pushes.
+// ONE: the single-rank instantiation (no peers, no server role, fp32 replicas): the N>1,
+// notify and bf16-replica paths are compiled out, so the scheduler and movers run a smaller
+// kernel (measured: the general kernel is ~5% slower at N=1 than this one).
+template <bool ONE>
 __global__ void __launch_bounds__(P3_COMM_MAX_THREADS, 1) k_comm(const __grid_constant__ CommArgs a) {
   __shared__ Job slots[P3_SLOTS];  // a ring: the scheduler fills ahead while earlier jobs move
   __shared__ StageDesc sdesc[P3_STAGES];
@@ -1657,101 +1692,16 @@ __global__ void __launch_bounds__(P3_COMM_MAX_THREADS, 1) k_comm(const __grid_co
 #pragma unroll
     for (uint32_t i = 0; i < P3_SLOTS; ++i) pending[i] = false;
     bool pops_done = false;  // FINISH, N > 1: every local slice claimed (see the pop phase)
-    // SWEEP: the claimed chunk's unprocessed part, the next claim's size, a window of 32
-    // layers' metadata (lane j: layer sw_w0 + j) and the current job's piece
-    uint64_t sw_lo = 0, sw_hi = 0, sw_t0 = 0, sw_size = 0;
-    uint32_t sw_w0 = P3_NONE, sw_l = 0, sw_off = 0, sw_len = 0, sw_g = 0;
-    uint64_t w_ps = 0, w_pe = 0, w_word = 0, w_cnt = 0;
     for (uint32_t iter = 0;; ++iter) {
       if (phase) *(volatile uint32_t*)phase = (a.k << 24) | (1u << 20) | (iter & 0xfffff);
-      const uint64_t tp = globaltimer();
+      const uint64_t tp = stat_clock();
       uint32_t kind = JOB_NONE, li = 0, g = P3_NONE;
       Popped pp;
       pp.run = 1;
       pp.layer = 0;
       pp.word = 0;
       pp.t0 = 0;
-      if (a.mode == P3_COMM_SWEEP) {
-        // Single rank with every layer published: claim the next chunk of the priority-ordered
-        // element space (layers in order, each padded to a multiple of 8 elements) — guided
-        // size: 1/(2 x CTAs) of what is left, 4K..64K elements — and update it layer piece by
-        // layer piece. Claims follow the FrameQueue order at element granularity and the CTAs
-        // finish within one small chunk of each other.
-        const PlanDev& P = a.plan;
-        const LocalDev& L = a.loc[0];
-        const uint64_t total = P.layer_pstart[P.n_layers];
-        while (kind == JOB_NONE) {
-          if (sw_lo >= sw_hi) {
-            unsigned long long lo = 0;
-            const uint64_t tc = globaltimer_lane0();
-            if (lane == 0) {
-              // guided by what is left NOW (a size fixed at the previous claim would hand the
-              // last large chunk to one late CTA)
-              const uint64_t seen = ld_relaxed_gpu64(reinterpret_cast<const uint64_t*>(L.sweep));
-              const unsigned long long rem = seen < total ? total - seen : 0ull;
-              sw_size = min(max(rem / ((unsigned long long)a.sweep_div * gridDim.x), (unsigned long long)a.sweep_min),
-                            (unsigned long long)a.sweep_max) & ~7ull;
-              lo = atomicAdd(L.sweep, (unsigned long long)sw_size);
-            }
-            lo = __shfl_sync(FULL_MASK, lo, 0);
-            sw_size = __shfl_sync(FULL_MASK, sw_size, 0);
-            if (lo >= total) {
-              kind = JOB_EXIT;
-              break;
-            }
-            sw_lo = lo;
-            sw_hi = min((uint64_t)(lo + sw_size), total);
-            sw_t0 = tc;
-          }
-          // the layer holding sw_lo: from the window of 32 layers, reloaded when it moves on
-          const bool in_win = sw_w0 != P3_NONE && __shfl_sync(FULL_MASK, w_ps, 0) <= sw_lo &&
-                              sw_lo < __shfl_sync(FULL_MASK, w_pe, 31);
-          if (!in_win) {
-            sw_w0 = find_layer(P, sw_lo);
-            const uint32_t l = sw_w0 + lane;
-            const bool in = l < P.n_layers;
-            w_ps = in ? P.layer_pstart[l] : ~0ull;
-            w_pe = in ? P.layer_pstart[l + 1] : ~0ull;
-            w_cnt = in ? P.layer_count[l] : 0ull;
-            w_word = in ? ld_relaxed_gpu64(L.pub + l) : 0ull;
-          }
-          const uint32_t j = 31 - __clz(__ballot_sync(FULL_MASK, w_ps <= sw_lo));
-          sw_l = sw_w0 + j;
-          const uint64_t ps = __shfl_sync(FULL_MASK, w_ps, j), pe = __shfl_sync(FULL_MASK, w_pe, j);
-          uint64_t word = __shfl_sync(FULL_MASK, w_word, j);
-          const uint64_t count = __shfl_sync(FULL_MASK, w_cnt, j);
-          const uint64_t e0 = sw_lo - ps;
-          uint64_t e1 = min(min(sw_hi, pe) - ps, count);
-          sw_g = L.V && e0 < count ? slice_at(P, sw_l, e0) : 0u;
-          if (L.V && e0 < count) e1 = min(e1, P.slice_off[sw_g] + P.slice_len[sw_g]);  // V slots are per slice
-          sw_lo = (e1 < count && e1 > e0) ? ps + e1 : min(sw_hi, pe);
-          if (e1 <= e0) continue;  // (the chunk starts in the layer's padding)
-          if (!pub_ready(word, a.k + 1)) {  // gradient pointer not yet ingested from the ring
-            for (uint32_t spin = 0; !pub_ready(word, a.k + 1); ++spin) {
-              ingest(L, a.sched);  // (the iteration's entries are all in before this launch)
-              if (spin > 4) __nanosleep(256);
-              word = ld_relaxed_gpu64(L.pub + sw_l);
-            }
-            if (lane == j) w_word = word;
-          }
-          if (lane == 0) fence_acq_rel_gpu();  // acquire of the gradient (ingest released it)
-          __syncwarp();
-          pp.layer = sw_l;
-          pp.word = word;
-          g = sw_g;  // (momentum: the slice holding the piece; otherwise unused)
-          sw_off = (uint32_t)e0;
-          sw_len = (uint32_t)(e1 - e0);
-          if (L.trace_cap && lane == 0) {  // the pops: slices whose first element this claim takes
-            const uint32_t first = P.layer_first[sw_l];
-            for (uint32_t g2 = slice_at(P, sw_l, e0); g2 <= slice_at(P, sw_l, e1 - 1); ++g2)
-              if (P.slice_off[g2] >= e0) {
-                atomicAdd(&L.it->pushed, 1u);
-                trace_append(L, a.k, sw_l, g2 - first, L.rank, P3_EV_PUSH, sw_t0);
-              }
-          }
-          kind = JOB_REDUCE;
-        }
-      } else if (a.plan.world == 1) {
+      if (ONE || a.plan.world == 1) {
         // single rank: a popped slice is complete the moment it is popped (the owner's own
         // contribution is read in place), so the pop claims the reduction directly — no
         // arrival counting, no server role — and takes up to pop_run consecutive slices of
@@ -1760,7 +1710,7 @@ __global__ void __launch_bounds__(P3_COMM_MAX_THREADS, 1) k_comm(const __grid_co
         if (stash.n) {
           g = take_stash(&stash, &pp);
         } else {
-          g = warp_pop(queue_of(a, L), a.k + 1, phase, L.V ? 1u : a.pop_run, &pp, &stash);
+          g = warp_pop(queue_of(a, L), a.k + 1, phase, (L.V || L.M) ? 1u : a.pop_run, &pp, &stash);
         }
         if (g != P3_NONE) {
           if (lane == 0) {
@@ -1781,7 +1731,7 @@ __global__ void __launch_bounds__(P3_COMM_MAX_THREADS, 1) k_comm(const __grid_co
       const bool push_first = a.push_split && (blockIdx.x % a.push_split) == a.push_split - 1;
       uint32_t ans_q = 0;
       bool pulled = false;
-      for (uint32_t round = 0; round < 2 && kind == JOB_NONE && a.plan.world > 1; ++round) {
+      for (uint32_t round = 0; round < 2 && kind == JOB_NONE && !ONE && a.plan.world > 1; ++round) {
         if ((round == 0) != push_first) {
           for (uint32_t t = 0; t < a.n_local && kind == JOB_NONE; ++t) {
             li = (blockIdx.x + t) % a.n_local;
@@ -1828,12 +1778,14 @@ __global__ void __launch_bounds__(P3_COMM_MAX_THREADS, 1) k_comm(const __grid_co
           }
         }
       }
-      if (kind == JOB_NONE && pulled) continue;  // progress (requests sent): look again at once
+      if (!ONE && kind == JOB_NONE && pulled) continue;  // progress (requests sent): look again at once
       if (kind == JOB_NONE) {
         // decided by lane 0 and broadcast: a per-lane decision could split the warp
         uint32_t verdict = 0;  // 0 keep looking, 1 leave, 2 timed out
         if (lane == 0) {
-          if (a.mode == P3_COMM_DRAIN) {
+          if (a.mode == P3_COMM_DRAIN && ONE) {
+            verdict = 1;  // single rank: nothing arrives from peers
+          } else if (a.mode == P3_COMM_DRAIN) {
             // Nothing to do. Linger (bounded) while some owned slice has part of its pushes:
             // the rest come from peers' comm kernels, never from this rank's compute, and
             // reducing it now keeps it off the post-backward tail.
@@ -1853,7 +1805,7 @@ __global__ void __launch_bounds__(P3_COMM_MAX_THREADS, 1) k_comm(const __grid_co
               const uint32_t own = a.plan.own_total[L.rank];
               fin = fin && ld_relaxed_gpu(&L.it->pushed) >= a.plan.total_slices &&
                     ld_relaxed_gpu(&L.it->reduced) >= own;
-              if (a.notify)  // every NOTIFY pulled, every PULL of an owned slice answered
+              if (!ONE && a.notify)  // every NOTIFY pulled, every PULL of an owned slice answered
                 fin = fin && ld_relaxed_gpu(L.pcount) >= a.plan.total_slices - own &&
                       ld_relaxed_gpu(L.pcount + 1) >= own * (a.plan.world - 1);
             }
@@ -1884,7 +1836,7 @@ __global__ void __launch_bounds__(P3_COMM_MAX_THREADS, 1) k_comm(const __grid_co
       }
       backoff = 0;
       idle_since = 0;
-      if (lane == 0 && (kind == JOB_PUSH || kind == JOB_REDUCE) && a.mode != P3_COMM_SWEEP) {
+      if (lane == 0 && (kind == JOB_PUSH || kind == JOB_REDUCE)) {
         P3_CHECK(g < a.plan.total_slices && pp.layer < a.plan.n_layers);
         P3_CHECK(a.plan.slice_layer[g] == pp.layer);  // the pop's layer is the slice's layer
         P3_CHECK(pp.run >= 1 && g + pp.run <= a.plan.layer_first[pp.layer] + a.plan.layer_nslices[pp.layer]);
@@ -1895,24 +1847,23 @@ __global__ void __launch_bounds__(P3_COMM_MAX_THREADS, 1) k_comm(const __grid_co
         if (how == PUSH_DONE) continue;  // own slice, still waiting for peers: counted in place
         if (how == PUSH_REDUCE) kind = JOB_REDUCE;  // own slice completed it: reduce right away
       }
-      if ((kind == JOB_PUSH || kind == JOB_REDUCE || kind == JOB_ANSWER) && a.ns_per_byte != 0.f &&
+      if (!ONE && (kind == JOB_PUSH || kind == JOB_REDUCE || kind == JOB_ANSWER) && a.ns_per_byte != 0.f &&
           a.plan.world > 1) {
         // egress bytes of this job on the rank's link (K7): a push, an answer to a PULL, or the
         // N-1 broadcast copies of a reduce (none in notify mode: the peers pull)
-        const uint64_t bytes = (kind == JOB_PUSH && a.push_bf16 ? 2ull : 4ull) * a.plan.slice_len[g] *
+        const bool two = a.pb16 || (kind == JOB_PUSH && a.push_bf16);  // 2-byte elements on the link
+        const uint64_t bytes = (two ? 2ull : 4ull) * a.plan.slice_len[g] *
                                (kind == JOB_REDUCE ? (a.notify ? 0u : a.plan.world - 1u) : 1u);
         if (lane == 0) pace(a, a.loc[li], bytes);
         __syncwarp();
       }
-      const uint64_t tw = globaltimer();
+      const uint64_t tw = stat_clock();
       t_pick += tw - tp;
       if (pending[b]) bar_sync(BAR_EMPTY(b), 64);  // the signaler released this slot
       if (kind == JOB_PUSH) {
         prepare_push(a, li, g, pp.layer, pp.word, &slots[b]);
       } else if (kind == JOB_ANSWER) {
         prepare_answer(a, li, g, pp.layer, ans_q, &slots[b]);
-      } else if (kind == JOB_REDUCE && a.mode == P3_COMM_SWEEP) {
-        prepare_piece(a, pp.layer, pp.word, sw_off, sw_len, sw_g, &slots[b]);
       } else if (kind == JOB_REDUCE) {
         prepare_reduce(a, li, g, pp.layer, pp.word, &slots[b], pp.run);
       } else {
@@ -1922,7 +1873,7 @@ __global__ void __launch_bounds__(P3_COMM_MAX_THREADS, 1) k_comm(const __grid_co
         }
         if (lane == 0) slots[b].kind = JOB_EXIT;
       }
-      t_wait += globaltimer() - tw;
+      t_wait += stat_clock() - tw;
       __syncwarp();
       bar_arrive(BAR_FULL(b), 96);  // producer + signaler wait on it
       if (kind == JOB_EXIT) break;
@@ -1956,16 +1907,26 @@ __global__ void __launch_bounds__(P3_COMM_MAX_THREADS, 1) k_comm(const __grid_co
       mine.n = j.n;
       mine.run = j.run;
       mine.bf16 = j.bf16;
-      mine.piece = j.piece;
       mine.ndst = j.ndst;
       mine.answer = j.answer;
-      mine.e0 = j.e0;
+      mine.pb16 = j.pb16;
       __syncwarp();
       bar_arrive(BAR_EMPTY(b), 64);
       if (lane == 0) {
-        const uint64_t ts = globaltimer();
-        signal_job(a, mine);
-        t_sig += globaltimer() - ts;
+        const uint64_t ts = stat_clock();
+        if (ONE) {  // single rank: the update is in the replica; open its gate
+          const PlanDev& P = a.plan;
+          const LocalDev& L = a.loc[0];
+          fence_acq_rel_gpu();
+          red_add_relaxed_sys(a.peers.done[L.rank] + mine.layer, mine.run);
+          red_add_relaxed_sys(a.peers.gdone[L.rank] + P.layer_group[mine.layer], mine.run);
+          if (L.trace_cap)
+            for (uint32_t i = 0; i < mine.run; ++i)
+              trace_append(L, a.k, mine.layer, mine.g + i - P.layer_first[mine.layer], L.rank, P3_EV_BCAST);
+        } else {
+          signal_job(a, mine);
+        }
+        t_sig += stat_clock() - ts;
       }
       __syncwarp();
     }
@@ -2009,7 +1970,8 @@ __global__ void __launch_bounds__(P3_COMM_MAX_THREADS, 1) k_comm(const __grid_co
             uint8_t* st = stage_mem + (size_t)sidx * P3_STAGE_BYTES;
             uint32_t bytes = 0;
             for (uint32_t q = 0; q < nsrc; ++q) {
-              const bool half = j.bf16 && j.kind == JOB_REDUCE && q < j.n && (int)q != (int)j.bf16 - 1;
+              const bool half = j.kind == JOB_PUSH ? j.bf16 == 2
+                                                   : q < j.n && (j.pb16 || (j.bf16 && (int)q != (int)j.bf16 - 1));
               bytes += n * (half ? 2u : 4u);
             }
             mbar_arrive_expect_tx(&full_bar[sidx], bytes);
@@ -2017,14 +1979,16 @@ __global__ void __launch_bounds__(P3_COMM_MAX_THREADS, 1) k_comm(const __grid_co
               const void* g;
               uint32_t esz = 4;
               if (j.kind == JOB_PUSH) {
-                g = j.src[0] + e0;
+                esz = j.bf16 == 2 ? 2u : 4u;  // (2: a bf16 copy)
+                g = j.bf16 == 2 ? (const void*)(reinterpret_cast<const __nv_bfloat16*>(j.src[0]) + e0)
+                                : (const void*)(j.src[0] + e0);
               } else if (q < j.n) {
-                const bool half = j.bf16 && (int)q != (int)j.bf16 - 1;
+                const bool half = j.pb16 || (j.bf16 && (int)q != (int)j.bf16 - 1);
                 esz = half ? 2u : 4u;
                 g = half ? (const void*)(reinterpret_cast<const __nv_bfloat16*>(j.src[q]) + e0)
                          : (const void*)(j.src[q] + e0);
               } else if (q == j.n) {
-                g = j.dst[0] + e0;  // master copy p
+                g = j.pb16 ? j.m + e0 : j.dst[0] + e0;  // master copy p
               } else {
                 g = j.v + e0;
               }
@@ -2056,23 +2020,27 @@ __global__ void __launch_bounds__(P3_COMM_MAX_THREADS, 1) k_comm(const __grid_co
       const StageDesc d = sdesc[sidx];
       if (d.flags & ST_EXIT) break;
       P3_CHECK(d.b < P3_SLOTS);
-      const uint64_t tm = tid == 0 ? globaltimer() : 0;
+      const uint64_t tm = tid == 0 ? stat_clock() : 0;
       const Job& j = slots[d.b];
-      const bool bulk_push = a.tma_store && j.kind == JOB_PUSH && !j.bf16 && !(d.flags & ST_DIRECT);
+      const bool bulk_push = a.tma_store && j.kind == JOB_PUSH && j.bf16 != 1 && !(d.flags & ST_DIRECT);
       if (bulk_push) {
         // the staged gradient tile goes out as one TMA bulk store (over NVLink to the
         // owner's receive slot); the stage is released once the engine has read it
         if (tid == 0) {
-          tma_store_1d(j.dst[0] + d.e0, stage_mem + (size_t)sidx * P3_STAGE_BYTES, d.n * 4u);
+          if (j.bf16 == 2)  // bf16 copy (param_bf16 push / answer)
+            tma_store_1d(reinterpret_cast<__nv_bfloat16*>(j.dst[0]) + d.e0, stage_mem + (size_t)sidx * P3_STAGE_BYTES,
+                         d.n * 2u);
+          else
+            tma_store_1d(j.dst[0] + d.e0, stage_mem + (size_t)sidx * P3_STAGE_BYTES, d.n * 4u);
           tma_store_wait_read();
         }
       } else if (d.flags & ST_DIRECT) {
         move_range(a, j, d.e0, d.n, &rptrs, tid, ncons);
-      } else if (a.tma_store_red && j.kind == JOB_REDUCE && j.n <= 8) {
+      } else if (a.tma_store_red && j.kind == JOB_REDUCE && j.n <= 8 && !j.pb16) {
         // results go back into the stage, then one TMA bulk store per replica (and the
         // momentum) — NVLink for the remote ones
         uint8_t* st = stage_mem + (size_t)sidx * P3_STAGE_BYTES;
-        consume_tile(a, j, d, st, tid, ncons, true);
+        consume_tile<ONE>(a, j, d, st, tid, ncons, true);
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         bar_sync(BAR_RANGE, ncons);
         if (tid == 0) {
@@ -2082,13 +2050,13 @@ __global__ void __launch_bounds__(P3_COMM_MAX_THREADS, 1) k_comm(const __grid_co
           tma_store_wait_read();
         }
       } else {
-        consume_tile(a, j, d, stage_mem + (size_t)sidx * P3_STAGE_BYTES, tid, ncons);
+        consume_tile<ONE>(a, j, d, stage_mem + (size_t)sidx * P3_STAGE_BYTES, tid, ncons);
       }
       if ((d.flags & ST_LAST) && tid == 0 && (a.tma_store || a.tma_store_red))
         tma_store_wait_all();  // every bulk store of the job complete before its signal
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty_bar[sidx]);
-      if (tid == 0) t_move += globaltimer() - tm;
+      if (tid == 0) t_move += stat_clock() - tm;
       if (d.flags & ST_LAST) bar_arrive(BAR_DONE(d.b), ncons + 32);
     }
     if (tid == 0) atomicAdd(&stats->t_move, (unsigned long long)t_move);
@@ -2110,6 +2078,25 @@ __global__ void k_bump(uint32_t* done, uint32_t* gdone, uint32_t v) {
   }
 }
 
+// param_bf16: the fp32 master of every owned slice from the (bf16) replica, once at start.
+__global__ void k_master_init(const __grid_constant__ CommArgs a) {
+  const PlanDev& P = a.plan;
+  const LocalDev& L = a.loc[0];
+  const uint32_t o = L.rank, base = P.own_base[o];
+  for (uint32_t i = blockIdx.x; i < P.own_total[o]; i += gridDim.x) {
+    const uint32_t g = P.own_list[base + i];
+    const __nv_bfloat16* w = reinterpret_cast<const __nv_bfloat16*>(a.peers.W[o]) + P.layer_woff[P.slice_layer[g]] +
+                             P.slice_off[g];
+    float* m = L.M + P.slice_slot[g];
+    for (uint32_t e = threadIdx.x; e < P.slice_len[g]; e += blockDim.x) m[e] = __bfloat162float(w[e]);
+  }
+}
+
+int launch_master_init(const CommArgs& a, void* stream) {
+  k_master_init<<<296, 256, 0, (cudaStream_t)stream>>>(a);
+  return cudaGetLastError() == cudaSuccess ? P3_OK : P3_ECUDA;
+}
+
 int launch_bump(uint32_t* done, uint32_t* gdone, uint32_t v, void* stream) {
   k_bump<<<1, 32, 0, (cudaStream_t)stream>>>(done, gdone, v);
   return cudaGetLastError() == cudaSuccess ? P3_OK : P3_ECUDA;
@@ -2125,19 +2112,25 @@ int launch_mark(const LocalDev& L, uint32_t k, uint32_t ev, void* stream) {
 // A comm kernel that waited for work of the compute streams would block them, so every kernel those
 // streams may launch must be loaded before the comm kernel starts: query them all here.
 int preload_kernels() {
-  if (cudaFuncSetAttribute(k_comm, cudaFuncAttributeMaxDynamicSharedMemorySize, P3_STAGES * P3_STAGE_BYTES) !=
-      cudaSuccess)
+  if (cudaFuncSetAttribute(k_comm<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, P3_STAGES * P3_STAGE_BYTES) !=
+          cudaSuccess ||
+      cudaFuncSetAttribute(k_comm<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, P3_STAGES * P3_STAGE_BYTES) !=
+          cudaSuccess)
     return P3_ECUDA;
   cudaFuncAttributes fa;
-  const void* fns[] = {(const void*)k_comm, (const void*)k_gradgen, (const void*)k_sleep,
-                       (const void*)k_shard_update, (const void*)k_queue_pop, (const void*)k_mark, (const void*)k_bump};
+  const void* fns[] = {(const void*)k_comm<false>, (const void*)k_comm<true>, (const void*)k_gradgen, (const void*)k_sleep,
+                       (const void*)k_shard_update, (const void*)k_queue_pop, (const void*)k_mark, (const void*)k_bump,
+                       (const void*)k_master_init};
   for (const void* f : fns)
     if (cudaFuncGetAttributes(&fa, f) != cudaSuccess) return P3_ECUDA;
   return P3_OK;
 }
 
 int launch_comm(const CommArgs& a, uint32_t ctas, uint32_t threads, void* stream) {
-  k_comm<<<ctas, threads, P3_STAGES * P3_STAGE_BYTES, (cudaStream_t)stream>>>(a);
+  if (a.plan.world == 1 && !a.pb16)
+    k_comm<true><<<ctas, threads, P3_STAGES * P3_STAGE_BYTES, (cudaStream_t)stream>>>(a);
+  else
+    k_comm<false><<<ctas, threads, P3_STAGES * P3_STAGE_BYTES, (cudaStream_t)stream>>>(a);
   return cudaGetLastError() == cudaSuccess ? P3_OK : P3_ECUDA;
 }
 

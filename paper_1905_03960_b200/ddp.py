@@ -268,6 +268,11 @@ class P3DataParallel(_HookedDataParallel):
         notify_pull: bool | None = None,
     ) -> None:
         super().__init__(module, order)
+        dtypes = {p.dtype for p in self.params}
+        if dtypes - {torch.float32, torch.bfloat16} or len(dtypes) > 1:
+            raise ValueError(f"parameters must be all float32 or all bfloat16 (have {sorted(map(str, dtypes))})")
+        # bf16 parameters: bf16 replicas and gradients on the wire, fp32 masters at the owners
+        self.param_dtype = "bf16" if dtypes == {torch.bfloat16} else "fp32"
         self.lr = lr
         self.lw = local_world
         if local_world is not None:
@@ -301,6 +306,7 @@ class P3DataParallel(_HookedDataParallel):
             big_threshold=big_threshold, pub_batch_bytes=pub_batch_bytes, drain_linger_us=drain_linger_us,
             finish_ctas=finish_ctas, push_dtype=push_dtype,
             notify_pull=(plan_mode == "baseline") if notify_pull is None else notify_pull,
+            param_dtype=self.param_dtype,
         )
         self.ctx: SyncContext | None = None
         self.comm_stream = None
@@ -351,6 +357,8 @@ class P3DataParallel(_HookedDataParallel):
                     view = flat.as_strided(p.shape, p.stride())
                 view.copy_(p.data)
                 p.data = view
+        if self.param_dtype == "bf16":  # the owners' fp32 masters start from the replica's values
+            self.ctx.master_init(self.li, torch.cuda.current_stream())
         torch.cuda.synchronize()
         if self.world > 1 and lw is None:
             dist.barrier()
@@ -381,7 +389,7 @@ class P3DataParallel(_HookedDataParallel):
 
     def _publish(self, l: int, grad) -> None:
         p = self.params[l]
-        if grad.dtype != torch.float32 or grad.stride() != p.stride():
+        if grad.dtype != p.dtype or grad.stride() != p.stride():
             grad = _relayout(grad, p)
             p.grad = grad
         self.ctx.layer_ready(self.li, l, self.k, grad)
@@ -446,7 +454,7 @@ def _dense(t: torch.Tensor) -> bool:
 
 
 def _relayout(grad: torch.Tensor, p: torch.Tensor) -> torch.Tensor:
-    out = torch.empty_strided(p.shape, p.stride(), dtype=torch.float32, device=p.device)
+    out = torch.empty_strided(p.shape, p.stride(), dtype=p.dtype, device=p.device)
     out.copy_(grad)
     return out
 

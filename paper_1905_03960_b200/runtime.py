@@ -30,8 +30,8 @@ from .plan import BASELINE_MODE, P3_MODE, DEFAULT_MAX_SLICE, SliceKey, make_base
 class _DeviceArray:
     """Zero-copy __cuda_array_interface__ view so torch can alias libp3-owned memory."""
 
-    def __init__(self, ptr: int, n: int, owner) -> None:
-        self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<f4", "data": (ptr, False), "version": 2}
+    def __init__(self, ptr: int, n: int, owner, typestr: str = "<f4") -> None:
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": typestr, "data": (ptr, False), "version": 2}
         self._owner = owner
 
 
@@ -47,12 +47,12 @@ class TraceEvent:
 
 
 def plan_fingerprint(layer_counts, world, max_slice, plan_mode, big_threshold, rng_seed, priority_mode, lr, momentum,
-                     push_dtype, notify_pull=False) -> str:
+                     push_dtype, notify_pull=False, param_dtype="fp32") -> str:
     """What every rank of one sync group must agree on: the plan (layer sizes, world, slice
     size, placement), the discipline and the update rule. Ranks that disagree would wait on
     each other forever (a slice one rank never pushes), so ``connect`` refuses them."""
     key = repr((list(map(int, layer_counts)), int(world), int(max_slice), plan_mode, int(big_threshold), int(rng_seed),
-                bool(priority_mode), float(lr), float(momentum), push_dtype, bool(notify_pull)))
+                bool(priority_mode), float(lr), float(momentum), push_dtype, bool(notify_pull), param_dtype))
     return f"{fnv1a64(key.encode()):016x}"
 
 
@@ -117,6 +117,7 @@ class SyncContext:
         push_dtype: str = "fp32",
         drain_streams: int = 0,
         notify_pull: bool = False,
+        param_dtype: str = "fp32",
     ) -> None:
         import torch
 
@@ -171,6 +172,10 @@ class SyncContext:
         cfg.drain_bytes = drain_bytes
         cfg.drain_streams = drain_streams
         cfg.notify_pull = 1 if notify_pull else 0
+        if param_dtype not in ("fp32", "bf16"):
+            raise ValueError("param_dtype must be 'fp32' or 'bf16'")
+        cfg.param_bf16 = 1 if param_dtype == "bf16" else 0
+        self.param_dtype = param_dtype
         self.strict = comm_ctas == 1 and (finish_ctas or comm_ctas) == 1 and pop_relax == 1 and drain_streams == 1
         h = ctypes.c_void_p()
         _lib.check(self.lib.p3_ctx_create(ctypes.byref(cfg), ctypes.byref(h)), what="p3_ctx_create")
@@ -183,7 +188,7 @@ class SyncContext:
         self.arena_elems = self.layer_offsets[-1] + self.layer_counts[-1]
         self.plan_mode = plan_mode
         self.fingerprint = plan_fingerprint(self.layer_counts, world, max_slice, plan_mode, big_threshold, rng_seed,
-                                            priority_mode, lr, momentum, push_dtype, notify_pull)
+                                            priority_mode, lr, momentum, push_dtype, notify_pull, param_dtype)
 
     # ------------------------------------------------------------------ plumbing
     def _check(self, rc: int, what: str) -> None:
@@ -199,10 +204,20 @@ class SyncContext:
         return int(p.value)
 
     def params_arena(self, li: int = 0):
-        """torch float32 view over the whole parameter replica W of local rank ``li``."""
+        """torch view (float32, or bfloat16 with param_dtype="bf16") over the whole parameter
+        replica W of local rank ``li``."""
         import torch
 
-        return torch.as_tensor(_DeviceArray(self._ptr(self.lib.p3_ctx_params, li), self.arena_elems, self), device="cuda")
+        ptr = self._ptr(self.lib.p3_ctx_params, li)
+        if self.param_dtype == "bf16":
+            raw = torch.as_tensor(_DeviceArray(ptr, self.arena_elems, self, "<i2"), device="cuda")
+            return raw.view(torch.bfloat16)
+        return torch.as_tensor(_DeviceArray(ptr, self.arena_elems, self), device="cuda")
+
+    def master_init(self, li: int = 0, stream=None) -> None:
+        """param_bf16: the owned slices' fp32 master from the replica (once, after the initial
+        parameters are in W)."""
+        self._check(self.lib.p3_master_init(self._h, li, _lib.stream_handle(stream)), "p3_master_init")
 
     def grads_arena(self, li: int = 0):
         import torch
@@ -293,7 +308,7 @@ class SyncContext:
         return int(a.value), int(b.value)
 
     def params_numpy(self, li: int = 0) -> list[np.ndarray]:
-        flat = self.params_arena(li).cpu().numpy()
+        flat = self.params_arena(li).float().cpu().numpy()
         return [flat[o : o + c].copy() for o, c in zip(self.layer_offsets, self.layer_counts)]
 
     def params_digest(self, li: int = 0) -> int:

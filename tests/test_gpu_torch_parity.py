@@ -151,3 +151,46 @@ def test_forward_order_priorities_and_tied_gate(cuda):
     for a, b in zip(mod.parameters(), ref.parameters()):
         assert torch.equal(a, b)
     ddp.close()
+
+
+@pytest.mark.parametrize("name,world,batch", [("mlp", 1, 16), ("mlp", 3, 16), ("resnet50", 2, 4)])
+def test_bf16_parameters_fp32_masters(cuda, name, world, batch):
+    """Declared bf16 replicas (param_dtype bf16, chosen from the model's bf16 parameters): bf16
+    gradients are pushed as they are, the owner sums them in fp32 in rank order, updates its
+    fp32 master with the fp32 path's arithmetic and broadcasts bf16(master) (round to nearest
+    even). Each replica must equal that, computed here with torch from the replicas' own bf16
+    gradients — bit for bit; no copy / cast kernels on the sync path (the gradients are
+    published in place)."""
+    import torch
+
+    from paper_1905_03960_b200.ddp import P3DataParallel, P3LocalWorld
+
+    lr = 0.05
+    models = [_model(name, 11).bfloat16() for _ in range(world)]
+    lw = P3LocalWorld(world, timeout_s=60.0) if world > 1 else None
+    reps = [P3DataParallel(m, lr=lr, local_world=lw, comm_ctas=8) for m in models]
+    assert reps[0].param_dtype == "bf16"
+    names = [n for n, p in models[0].named_parameters() if p.requires_grad]
+    master = {n: p.detach().float().clone() for n, p in models[0].named_parameters() if p.requires_grad}
+    for it in range(3):
+        grads = []
+        for r, (rep, m) in enumerate(zip(reps, models)):
+            x, y = _batch(name, batch, seed=500 * it + r)
+            if name == "resnet50":
+                x = x.bfloat16()
+            _loss(name, rep, x, y).backward()
+            grads.append({n: p.grad.detach().clone() for n, p in m.named_parameters() if p.requires_grad})
+        reps[0].synchronize()
+        torch.cuda.synchronize()
+        for n in names:
+            acc = torch.zeros_like(master[n])
+            for r in range(world):
+                acc = acc + grads[r][n].float()
+            master[n] = master[n] - (acc / torch.full_like(acc, world)).mul(lr)
+            want = master[n].bfloat16()
+            for r, m in enumerate(models):
+                got = dict(m.named_parameters())[n]
+                assert got.dtype == torch.bfloat16
+                assert torch.equal(got, want), f"{name} it {it} rank {r} {n}"
+    for rep in reps:
+        rep.close()
