@@ -503,7 +503,8 @@ def run_ours(args):
         throttled["p3_vs_layerwise"] = throttled["p3"] / throttled["layerwise_fifo"]
 
     # --- the comm kernel inside training (device trace): overlap and exposed tail
-    train_sync = training_sync_profile(args, world, rank, x, y) if not args.skip_sync else None
+    # (N>1 only: at N=1 the whole update is one FINISH launch after the backward pass)
+    train_sync = training_sync_profile(args, world, rank, x, y) if world > 1 and not args.skip_sync else None
     torch.cuda.empty_cache()
 
     # --- slice-sync kernel roofline

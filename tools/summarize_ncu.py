@@ -20,7 +20,7 @@ def launches(path):
            "| share | total us | launches | avg us | kernel |", "|---:|---:|---:|---:|---|"]
     for n, v in tot.most_common(20):
         out.append(f"| {v/T*100:.2f}% | {v:.1f} | {cnt[n]} | {v/cnt[n]:.2f} | `{n}` |")
-    mine = {n: v for n, v in tot.items() if n.startswith("p3::")}
+    mine = {n: v for n, v in tot.items() if "p3::" in n}
     out.append("")
     out.append("libp3 kernels: " + ", ".join(f"`{n}` {v/T*100:.2f}% ({cnt[n]} launches, avg {v/cnt[n]:.1f} us)" for n, v in mine.items()))
     return "\n".join(out)
