@@ -113,7 +113,8 @@ struct p3_ctx {
   // P3_TMA=0 (direct loads instead of the TMA stage ring), P3_PUSH_SPLIT=n, P3_SRV_FILTER=n,
   // P3_TRACE_CTA=1 (trace records carry CTA indices; CTA start / exit records)
   struct {
-    uint32_t use_tma = 1, push_split = 0, srv_filter = 0, trace_cta = 0, srv_reserve = 0, tma_store = 1, tma_store_red = 0, pop_relax = 0;
+    uint32_t use_tma = 1, push_split = 0, srv_filter = 0, trace_cta = 0, srv_reserve = 0, tma_store = 1, tma_store_red = 0, pop_relax = 0,
+             push_max = 2;
   } knobs;
   std::vector<uint32_t> own_total;
   std::vector<uint64_t> own_stride;
@@ -328,6 +329,7 @@ int p3_ctx_create(const p3_config_t* cfg, p3_ctx_t** out) {
     c->knobs.tma_store = env_u32("P3_TMA_STORE", 1);
     c->knobs.pop_relax = env_u32("P3_POP_RELAX", 0);  // 0: the config's
     c->knobs.tma_store_red = env_u32("P3_TMA_STORE_RED", 0);
+    c->knobs.push_max = env_u32("P3_PUSH_MAX", 2);
   }
   std::string perr;
   int rc = cfg->plan_mode == P3_PLAN_P3
@@ -686,6 +688,7 @@ static CommArgs comm_args(p3_ctx* c, uint32_t mode, uint32_t ctas) {
   a.srv_reserve = c->knobs.srv_reserve;
   a.tma_store = c->knobs.tma_store;
   a.tma_store_red = c->knobs.tma_store_red;
+  a.push_max = c->knobs.push_max;
   // bounded relaxation of the pop order: a pop takes one of the C most urgent slices, C =
   // the launch's concurrent consumers (its CTAs) unless configured lower
   // (measured, tools/sync_sweep.py, ResNet-50 N=1 sync-only: C=8 2.2 TB/s, C=148 3.4 TB/s —

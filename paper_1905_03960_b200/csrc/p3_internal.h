@@ -142,7 +142,8 @@ struct CommArgs {
   uint32_t srv_filter; // server picks: only srv_filter x (ready slices) consumers look (0: all)
   uint32_t srv_reserve; // N > 1: every srv_reserve-th CTA does server work only (0: none)
   uint32_t tma_store;  // fp32 push tiles leave shared memory as TMA bulk stores
-  uint32_t tma_store_red; // reduce results leave shared memory as TMA bulk stores
+  uint32_t tma_store_red; // reduce results leave shared memory as TMA bulk stores (1: all, 2: remote)
+  uint32_t push_max;  // FINISH: 1 = a CTA keeps at most one push in flight (the other slot for reduces)
   uint32_t use_tma;   // movers stage sources through shared memory with TMA (else direct loads)
   uint32_t trace_cta; // diagnostics (P3_TRACE_CTA=1): trace records carry the CTA index as `rank`
   float ns_per_byte;  // K7 link emulation (0: unthrottled)

@@ -1301,7 +1301,7 @@ __device__ __forceinline__ bool job_tma_ok(const Job& j) {
 template <int NW, bool BF, bool MOM>
 __device__ __forceinline__ void consume_reduce(const uint8_t* st, uint32_t pitch, uint32_t n4, uint32_t e4,
                                                float* const* dstp, float* vp, int own, const UpdCoef& c,
-                                               uint32_t tid, uint32_t nthr, bool tosmem, int ndst) {
+                                               uint32_t tid, uint32_t nthr, int tosmem, int ndst) {
   float4* dst[NW];
 #pragma unroll
   for (int q = 0; q < NW; ++q) dst[q] = reinterpret_cast<float4*>(dstp[q]) + e4;
@@ -1328,15 +1328,17 @@ __device__ __forceinline__ void consume_reduce(const uint8_t* st, uint32_t pitch
     }
     float4 vv = MOM ? tv[k] : make_float4(0.f, 0.f, 0.f, 0.f);
     const float4 r = sgd4(tp[k], acc, c, MOM ? &vv : nullptr);
-    if (tosmem) {  // results back into the stage (p and v tiles), stored by TMA afterwards
+    if (tosmem) {  // results back into the stage (p tile), stored by TMA afterwards
       const_cast<float4*>(tp)[k] = r;
-      if (MOM) const_cast<float4*>(tv)[k] = vv;
-      continue;
+      if (tosmem == 1) {  // every replica and v by TMA
+        if (MOM) const_cast<float4*>(tv)[k] = vv;
+        continue;
+      }
     }
     if (MOM) v[k] = vv;
 #pragma unroll
-    for (int q = 0; q < NW; ++q)
-      if (q < ndst) dst[q][k] = r;
+    for (int q = 0; q < NW; ++q)  // (tosmem 2: the local replica here, the remote ones by TMA)
+      if (q < ndst && (tosmem != 2 || q == 0)) dst[q][k] = r;
   }
 }
 
@@ -1389,7 +1391,7 @@ __device__ __noinline__ void move_range_pb16(const CommArgs& a, const Job& j, ui
 
 template <bool ONE>
 __device__ void consume_tile(const CommArgs& a, const Job& j, const StageDesc& d, const uint8_t* st, uint32_t tid,
-                             uint32_t nthr, bool tosmem = false) {
+                             uint32_t nthr, int tosmem = 0) {
   const uint32_t n4 = d.n / 4, e4 = d.e0 / 4, pitch = d.tile * 4;
   if (j.kind == JOB_PUSH) {
     const float4* t0 = reinterpret_cast<const float4*>(st);
@@ -1692,6 +1694,7 @@ __global__ void __launch_bounds__(P3_COMM_MAX_THREADS, 1) k_comm(const __grid_co
 #pragma unroll
     for (uint32_t i = 0; i < P3_SLOTS; ++i) pending[i] = false;
     bool pops_done = false;  // FINISH, N > 1: every local slice claimed (see the pop phase)
+    bool last_push = false;  // the most recently filled slot holds a push
     for (uint32_t iter = 0;; ++iter) {
       if (phase) *(volatile uint32_t*)phase = (a.k << 24) | (1u << 20) | (iter & 0xfffff);
       const uint64_t tp = stat_clock();
@@ -1752,7 +1755,9 @@ __global__ void __launch_bounds__(P3_COMM_MAX_THREADS, 1) k_comm(const __grid_co
           }
           // server-reserved CTAs (srv_reserve > 0: every srv_reserve-th CTA) never take pushes,
           // so a completed slice is reduced while the other CTAs' pipelines hold pushes
-          const bool reserved = a.srv_reserve && (blockIdx.x % a.srv_reserve) == 0;
+          const bool reserved = (a.srv_reserve && (blockIdx.x % a.srv_reserve) == 0) ||
+                                (a.push_max == 1 && a.mode == P3_COMM_FINISH && last_push && backoff < 512u &&
+                                 pending[(b + P3_SLOTS - 1) % P3_SLOTS]);  // (an idle scheduler pushes anyway)
           for (uint32_t t = 0; t < a.n_local && kind == JOB_NONE && !pops_done && !reserved; ++t) {
             li = (blockIdx.x + t) % a.n_local;
             g = warp_pop(queue_of(a, a.loc[li]), a.k + 1, phase, 1u, &pp, &stash);
@@ -1878,6 +1883,7 @@ __global__ void __launch_bounds__(P3_COMM_MAX_THREADS, 1) k_comm(const __grid_co
       bar_arrive(BAR_FULL(b), 96);  // producer + signaler wait on it
       if (kind == JOB_EXIT) break;
       pending[b] = true;
+      last_push = kind == JOB_PUSH || kind == JOB_ANSWER;
       b = (b + 1) % P3_SLOTS;
       if (lane == 0) atomicAdd(&stats->jobs, 1u);
     }
@@ -2036,17 +2042,20 @@ __global__ void __launch_bounds__(P3_COMM_MAX_THREADS, 1) k_comm(const __grid_co
         }
       } else if (d.flags & ST_DIRECT) {
         move_range(a, j, d.e0, d.n, &rptrs, tid, ncons);
-      } else if (a.tma_store_red && j.kind == JOB_REDUCE && j.n <= 8 && !j.pb16) {
-        // results go back into the stage, then one TMA bulk store per replica (and the
-        // momentum) — NVLink for the remote ones
+      } else if (!ONE && a.tma_store_red && j.kind == JOB_REDUCE && j.n <= 8 && !j.pb16 && j.bf16 == 0 &&
+                 (a.tma_store_red == 1 || j.ndst > 1)) {
+        // results go back into the stage, then TMA bulk stores: every replica and the momentum
+        // (tma_store_red 1), or only the remote replicas over NVLink while the consumers store
+        // the local one (2)
         uint8_t* st = stage_mem + (size_t)sidx * P3_STAGE_BYTES;
-        consume_tile<ONE>(a, j, d, st, tid, ncons, true);
+        const int mode = (int)a.tma_store_red;
+        consume_tile<ONE>(a, j, d, st, tid, ncons, mode);
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         bar_sync(BAR_RANGE, ncons);
         if (tid == 0) {
           const uint32_t pitch = d.tile * 4;
-          for (uint32_t q = 0; q < j.ndst; ++q) tma_store_1d(j.dst[q] + d.e0, st + j.n * pitch, d.n * 4u);
-          if (j.v) tma_store_1d(j.v + d.e0, st + (j.n + 1) * pitch, d.n * 4u);
+          for (uint32_t q = mode == 2 ? 1u : 0u; q < j.ndst; ++q) tma_store_1d(j.dst[q] + d.e0, st + j.n * pitch, d.n * 4u);
+          if (j.v && mode == 1) tma_store_1d(j.v + d.e0, st + (j.n + 1) * pitch, d.n * 4u);
           tma_store_wait_read();
         }
       } else {
