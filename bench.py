@@ -533,7 +533,9 @@ def run_ours(args):
         traffic = nvl_traffic.get("nvlink_tx_bytes_per_launch")
         roof["traffic_detail"] = nvl_traffic
     roof.update({"frac": roof["achieved"] / peak, "traffic": traffic,
-                 "kernel": "k_comm (K3 push + K4 reduce/SGD/bcast)",
+                 "kernel": ("k_update_stream (single-rank FINISH: the fused SGD update of every slice in "
+                            "priority order, one streaming pass)" if world == 1 and os.environ.get("P3_STREAM", "1") != "0"
+                            else "k_comm (K3 push + K4 reduce/SGD/bcast)"),
                  "algorithmic_bytes_per_launch": alg, "launch_ms": sync_ms, "ctas": ctas,
                  "measured_in": "sync-only phase: all layers' gradients in HBM and published, one launch per "
                                 "iteration over the whole GPU, L2 flushed (256 MB write) between launches"})

@@ -96,7 +96,7 @@ struct PeerLayout {
 // Local arena of one rank. The per-iteration part (cursor | srv_lo | srv_taken | it) is
 // contiguous so one memset resets it before each launch.
 struct LocalLayout {
-  uint64_t pub, fifo_key, claim, iter_begin, cursor, srv_lo, srv_taken, it, pcount, iter_end, V,
+  uint64_t pub, fifo_key, claim, iter_begin, cursor, srv_lo, srv_taken, it, pcount, slice_elems, stream_next, iter_end, V,
       M, bytes, trace_n, trace, cta_phase, vclock, pubseq, ingested, heads, total;
 };
 
@@ -114,7 +114,7 @@ struct p3_ctx {
   // P3_TRACE_CTA=1 (trace records carry CTA indices; CTA start / exit records)
   struct {
     uint32_t use_tma = 1, push_split = 0, srv_filter = 0, trace_cta = 0, srv_reserve = 0, tma_store = 1, tma_store_red = 0, pop_relax = 0,
-             push_max = 2;
+             push_max = 2, stream = 1;
   } knobs;
   std::vector<uint32_t> own_total;
   std::vector<uint64_t> own_stride;
@@ -227,6 +227,8 @@ LocalLayout local_layout_of(const p3_ctx* c, uint64_t v_elems, uint64_t m_elems)
   take(q.srv_taken, c->L * 4ull);
   take(q.it, sizeof(IterState));
   take(q.pcount, 8);
+  take(q.slice_elems, c->N == 1 ? c->S * 4ull : 4ull);
+  take(q.stream_next, 8);
   q.iter_end = o;
   take(q.V, v_elems * 4);
   take(q.M, m_elems * 4);
@@ -330,6 +332,7 @@ int p3_ctx_create(const p3_config_t* cfg, p3_ctx_t** out) {
     c->knobs.pop_relax = env_u32("P3_POP_RELAX", 0);  // 0: the config's
     c->knobs.tma_store_red = env_u32("P3_TMA_STORE_RED", 0);
     c->knobs.push_max = env_u32("P3_PUSH_MAX", 2);
+    c->knobs.stream = env_u32("P3_STREAM", 1);  // single rank: streaming FINISH (0: slice pops)
   }
   std::string perr;
   int rc = cfg->plan_mode == P3_PLAN_P3
@@ -441,6 +444,9 @@ int p3_ctx_create(const p3_config_t* cfg, p3_ctx_t** out) {
   std::vector<uint32_t> own_base(N, 0);
   for (uint32_t o = 1; o < N; ++o) own_base[o] = own_base[o - 1] + c->own_total[o - 1];
   const size_t o_ob = put(own_base.data(), N * 4ull);
+  std::vector<uint64_t> flat(L + 1, 0);
+  for (uint32_t l = 0; l < L; ++l) flat[l + 1] = flat[l] + align_up(c->counts[l], 8);
+  const size_t o_fl = put(flat.data(), (L + 1) * 8ull);
   bool rr = true;
   for (uint32_t g = 0; g < S && rr; ++g) rr = slice_owner[g] == g % N;
   cudaError_t e = cudaMalloc(&c->d_plan, blob.size());
@@ -473,6 +479,7 @@ int p3_ctx_create(const p3_config_t* cfg, p3_ctx_t** out) {
   P.own_stride = reinterpret_cast<const uint64_t*>(pb + o_ost);
   P.layer_group = reinterpret_cast<const uint32_t*>(pb + o_lg);
   P.own_base = reinterpret_cast<const uint32_t*>(pb + o_ob);
+  P.layer_flat = reinterpret_cast<const uint64_t*>(pb + o_fl);
   P.rr_owner = rr ? 1u : 0u;
 
   // ---- per-rank arenas
@@ -519,6 +526,8 @@ int p3_ctx_create(const p3_config_t* cfg, p3_ctx_t** out) {
     D.pubseq = reinterpret_cast<uint32_t*>(lb + ll.pubseq);
     D.ingested = reinterpret_cast<uint32_t*>(lb + ll.ingested);
     D.pcount = reinterpret_cast<uint32_t*>(lb + ll.pcount);
+    D.slice_elems = reinterpret_cast<uint32_t*>(lb + ll.slice_elems);
+    D.stream_next = reinterpret_cast<unsigned long long*>(lb + ll.stream_next);
     D.ntf_head = reinterpret_cast<uint32_t*>(lb + ll.heads);
     D.pull_head = D.ntf_head + 1;
     D.ring_cap = 4 * L + 64;
@@ -775,8 +784,19 @@ int p3_iteration_end(p3_ctx_t* c, uint64_t k) {
     CK(cudaStreamWaitEvent(c->comm_stream, c->side_ev[j], 0));
   }
   const uint32_t ctas = c->cfg.finish_ctas ? c->cfg.finish_ctas : c->cfg.comm_ctas;
-  if (launch_comm(comm_args(c, P3_COMM_FINISH, ctas), ctas, c->cfg.comm_threads, c->comm_stream) != P3_OK)
+  // Single rank, no DRAIN launch this iteration, relaxed order allowed: nothing to exchange and
+  // every layer published — the FINISH work is one priority-ordered streaming update of the
+  // whole parameter space (k_update_stream); otherwise the comm kernel.
+  const bool stream = c->N == 1 && c->side_used == 0 && c->cfg.pop_relax != 1 && !c->cfg.param_bf16 &&
+                      c->knobs.stream;
+  if (stream) {
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
+    if (launch_update_stream(comm_args(c, P3_COMM_FINISH, ctas), (uint32_t)sms, c->comm_stream) != P3_OK)
+      return cuda_fail(c, cudaGetLastError(), "update kernel launch");
+  } else if (launch_comm(comm_args(c, P3_COMM_FINISH, ctas), ctas, c->cfg.comm_threads, c->comm_stream) != P3_OK) {
     return cuda_fail(c, cudaGetLastError(), "comm kernel launch");
+  }
   c->launches++;
   CK(cudaEventRecord(c->comm_done, c->comm_stream));
   c->comm_pending = true;

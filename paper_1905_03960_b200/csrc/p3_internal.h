@@ -52,6 +52,8 @@ struct PlanDev {
   const uint64_t* own_stride;     // [world] R block stride (padded owned elements)
   const uint32_t* layer_group;    // [L] forward-gate group of the layer
   const uint32_t* own_base;       // [world] first own_list position of each owner
+  const uint64_t* layer_flat;     // [L+1] start of each layer in the single-rank streaming order
+                                  // (layers in priority order, each padded to 8 elements)
 };
 
 // Peer-visible state of every rank (pointers valid in this process: local or IPC-mapped).
@@ -117,6 +119,8 @@ struct LocalDev {
   uint32_t* ntf_head;          // notify mode: NOTIFY entries consumed (monotone)
   uint32_t* pull_head;         // notify mode: PULL requests answered or claimed (monotone)
   uint32_t* pcount;            // [2] notify mode, per iteration: PULLs sent, PULLs answered
+  uint32_t* slice_elems;       // [S] single-rank stream: elements of each slice updated (per iteration)
+  unsigned long long* stream_next;  // single-rank stream: next warp tile to claim (per iteration)
 };
 
 struct CommArgs {
@@ -155,6 +159,7 @@ struct CommArgs {
 // Launchers (p3_kernels.cu)
 int preload_kernels();
 int launch_comm(const CommArgs& a, uint32_t ctas, uint32_t threads, void* stream);
+int launch_update_stream(const CommArgs& a, uint32_t ctas, void* stream);
 int launch_gradgen(uint64_t seed, uint64_t iteration, uint64_t layer, uint64_t start, uint64_t count,
                    float* out, void* stream);
 int launch_mark(const LocalDev& L, uint32_t k, uint32_t ev, void* stream);

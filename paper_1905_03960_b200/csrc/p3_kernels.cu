@@ -2116,6 +2116,185 @@ int launch_mark(const LocalDev& L, uint32_t k, uint32_t ev, void* stream) {
   return cudaGetLastError() == cudaSuccess ? P3_OK : P3_ECUDA;
 }
 
+// ------------------------------------------------------------------ single-rank FINISH
+
+// With one rank there is nothing to exchange: once every layer is published (no DRAIN launch
+// ran, so the FINISH launch is the only consumer) the iteration's sync is the fused update
+// p -= lr * (0 + g) / 1 (server.py:55-68 with N = 1) of every slice, in priority order so the
+// next forward's gates open layer by layer. As one streaming kernel: tiles of P3_STREAM_TILE
+// elements of the priority-ordered element space (layers back to back, each padded to 8) go to
+// the CTAs round-robin, so round r of the grid covers the r-th stretch of the model; a tile is
+// cut at layer and slice ends, and a slice is complete when all its elements are (its gate
+// counters then advance, exactly as the comm kernel's broadcast signal does).
+#ifndef P3_STREAM_TILE
+#define P3_STREAM_TILE 4096u
+#endif
+#ifndef P3_STREAM_THREADS
+#define P3_STREAM_THREADS 512
+#endif
+#ifndef P3_STREAM_CTAS_PER_SM
+#define P3_STREAM_CTAS_PER_SM 1
+#endif
+#ifndef P3_STREAM_U
+#define P3_STREAM_U 4  // float4s of each stream in flight per lane (8: register spills)
+#endif
+
+// Largest l < n_layers with layer_flat[l] <= pos (one warp, 32-ary search).
+__device__ uint32_t warp_find_layer(const PlanDev& P, uint64_t pos) {
+  const uint32_t lane = threadIdx.x & 31;
+  uint32_t lo = 0, hi = P.n_layers;
+  while (hi - lo > 1) {
+    const uint32_t step = (hi - lo + 31) / 32;
+    const uint32_t idx = lo + lane * step;
+    const uint32_t m = __ballot_sync(FULL_MASK, idx < hi && P.layer_flat[idx] <= pos);
+    lo += (31 - __clz(m)) * step;
+    hi = min(hi, lo + step);
+  }
+  return lo;
+}
+
+// One warp updates elements [0, n) of a piece: g the gradient, p the replica (read, then
+// written), v the momentum; U float4s of each stream in flight per lane.
+template <bool MOM>
+__device__ __forceinline__ void warp_stream_piece(const float* __restrict__ g, float* __restrict__ p,
+                                                  float* __restrict__ v, uint32_t n, const UpdCoef& c, bool bf,
+                                                  uint32_t lane) {
+  constexpr int U = P3_STREAM_U;
+  uint32_t done = 0;
+  if ((((uintptr_t)g | (uintptr_t)p | (uintptr_t)v) & 15) == 0) {
+    const uint32_t n4 = n / 4;
+    const float4* g4 = reinterpret_cast<const float4*>(g);
+    float4* p4 = reinterpret_cast<float4*>(p);
+    float4* v4 = reinterpret_cast<float4*>(v);
+    for (uint32_t j = lane; j < n4; j += U * 32) {
+      float4 gg[U], pp[U], vv[MOM ? U : 1];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {  // every load of the round before any use
+        const uint32_t i = j + u * 32 < n4 ? j + u * 32 : j;
+        gg[u] = __ldcs(g4 + i);  // read once: evict first
+        pp[u] = __ldcg(p4 + i);
+        if (MOM) vv[MOM ? u : 0] = __ldcg(v4 + i);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const uint32_t i = j + u * 32;
+        if (i >= n4) continue;
+        float4 x = gg[u];
+        if (bf) x = make_float4(bf16_round(x.x), bf16_round(x.y), bf16_round(x.z), bf16_round(x.w));
+        // the rank-ordered sum from +0.0 of one contribution, then / 1, * lr, - (server.py:60-65)
+        const float4 acc = make_float4(__fadd_rn(0.f, x.x), __fadd_rn(0.f, x.y), __fadd_rn(0.f, x.z),
+                                       __fadd_rn(0.f, x.w));
+        const float4 r = sgd4(pp[u], acc, c, MOM ? &vv[MOM ? u : 0] : nullptr);
+        if (MOM) v4[i] = vv[MOM ? u : 0];
+        p4[i] = r;
+      }
+    }
+    done = 4 * n4;
+  }
+  for (uint32_t i = done + lane; i < n; i += 32) {
+    float x = __ldcs(g + i);
+    if (bf) x = bf16_round(x);
+    p[i] = sgd_step(__ldcg(p + i), __fadd_rn(0.f, x), c, MOM ? v + i : nullptr);
+  }
+}
+
+// Work units are warp tiles of the element space, claimed in order with one atomic (strict
+// priority order at tile granularity, balanced over all warps): P3_STREAM_TILE elements, and
+// P3_STREAM_TAIL-element tiles over the last stretch (the last wave stays short).
+#ifndef P3_STREAM_TAIL
+#define P3_STREAM_TAIL 256u
+#endif
+
+__global__ void __launch_bounds__(P3_STREAM_THREADS, P3_STREAM_CTAS_PER_SM)
+    k_update_stream(const __grid_constant__ CommArgs a) {
+  const PlanDev& P = a.plan;
+  const LocalDev& L = a.loc[0];
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t total = P.layer_flat[P.n_layers];
+  const uint64_t nwarps = (uint64_t)gridDim.x * (blockDim.x / 32);
+  // tiles [0, t1) are big, the rest small: the small ones cover ~2 per warp at the end
+  const uint64_t tail = min(total, nwarps * 2 * P3_STREAM_TAIL);
+  const uint64_t t1 = (total - tail) / P3_STREAM_TILE;
+  const uint64_t big_end = t1 * P3_STREAM_TILE;
+  const UpdCoef c = make_coef(1, a.lr, a.momentum);
+  float* const W = a.peers.W[L.rank];
+  uint32_t lc = P3_NONE;  // cached layer and its metadata (warp-uniform)
+  uint64_t lstart = 0, lnext = 0, count = 0, unit = 1, woff = 0, word = 0;
+  uint32_t first = 0, ns = 0, grp = 0;
+  for (;;) {
+    unsigned long long t = 0;
+    if (lane == 0) t = atomicAdd(L.stream_next, 1ull);
+    t = __shfl_sync(FULL_MASK, t, 0);
+    uint64_t pos = t < t1 ? t * P3_STREAM_TILE : big_end + (t - t1) * P3_STREAM_TAIL;
+    if (pos >= total) break;
+    const uint64_t end = min(pos + (t < t1 ? P3_STREAM_TILE : P3_STREAM_TAIL), total);
+    while (pos < end) {
+      if (lc == P3_NONE || pos < lstart || pos >= lnext) {  // the layer holding pos
+        lc = warp_find_layer(P, pos);
+        lstart = P.layer_flat[lc];
+        lnext = P.layer_flat[lc + 1];
+        first = P.layer_first[lc];
+        ns = P.layer_nslices[lc];
+        unit = P.slice_len[first];
+        count = P.slice_off[first + ns - 1] + P.slice_len[first + ns - 1];
+        woff = P.layer_woff[lc];
+        grp = P.layer_group[lc];
+        word = ld_relaxed_gpu64(L.pub + lc);
+        if (!pub_ready(word, a.k + 1)) {  // published before this launch; maybe not yet ingested
+          const uint64_t t0 = globaltimer();
+          while (!pub_ready(word, a.k + 1)) {
+            ingest(L, a.sched);
+            __nanosleep(128);
+            word = ld_relaxed_gpu64(L.pub + lc);
+            if (globaltimer() - t0 > a.timeout_ns) {
+              if (lane == 0) atomicCAS(a.err, 0u, (uint32_t)P3_ETIMEOUT);
+              return;
+            }
+          }
+        }
+        if (lane == 0) fence_acq_rel_gpu();  // acquire of the gradient (ingest released it)
+        __syncwarp();
+      }
+      const uint64_t e0 = pos - lstart;
+      if (e0 >= count) {  // the layer's padding
+        pos = min(lnext, end);
+        continue;
+      }
+      const uint32_t g = first + (uint32_t)min(e0 / unit, (uint64_t)(ns - 1));
+      const uint64_t soff = P.slice_off[g], send = soff + P.slice_len[g];
+      const uint64_t e1 = min(end - lstart, send);  // cut at the slice end (and the tile end)
+      float* v = L.V ? L.V + P.slice_slot[g] + (e0 - soff) : nullptr;
+      if (v)
+        warp_stream_piece<true>(pub_ptr(word) + e0, W + woff + e0, v, (uint32_t)(e1 - e0), c, a.push_bf16 != 0, lane);
+      else
+        warp_stream_piece<false>(pub_ptr(word) + e0, W + woff + e0, v, (uint32_t)(e1 - e0), c, a.push_bf16 != 0, lane);
+      __syncwarp();
+      if (lane == 0) {
+        if (e0 == soff) {  // the slice's first element: its pop
+          atomicAdd(&L.it->pushed, 1u);
+          if (L.trace_cap) trace_append(L, a.k, lc, g - first, L.rank, P3_EV_PUSH);
+        }
+        fence_acq_rel_gpu();  // release this piece (and acquire the other pieces' releases)
+        const uint32_t part = (uint32_t)(e1 - e0);
+        if (atomicAdd(L.slice_elems + g, part) + part == send - soff) {
+          fence_acq_rel_gpu();
+          red_add_relaxed_sys(a.peers.done[L.rank] + lc, 1u);
+          red_add_relaxed_sys(a.peers.gdone[L.rank] + grp, 1u);
+          atomicAdd(&L.it->reduced, 1u);
+          if (L.trace_cap) trace_append(L, a.k, lc, g - first, L.rank, P3_EV_BCAST);
+        }
+      }
+      __syncwarp();
+      pos = min(e1 >= count ? lnext : lstart + e1, end);
+    }
+  }
+}
+
+int launch_update_stream(const CommArgs& a, uint32_t sms, void* stream) {
+  k_update_stream<<<sms * P3_STREAM_CTAS_PER_SM, P3_STREAM_THREADS, 0, (cudaStream_t)stream>>>(a);
+  return cudaGetLastError() == cudaSuccess ? P3_OK : P3_ECUDA;
+}
+
 // With lazy module loading (CUDA_MODULE_LOADING=LAZY, the CUDA 12 default) the first launch
 // of a kernel loads it, and loading waits for the kernels already running on the device.
 // A comm kernel that waited for work of the compute streams would block them, so every kernel those
@@ -2129,7 +2308,7 @@ int preload_kernels() {
   cudaFuncAttributes fa;
   const void* fns[] = {(const void*)k_comm<false>, (const void*)k_comm<true>, (const void*)k_gradgen, (const void*)k_sleep,
                        (const void*)k_shard_update, (const void*)k_queue_pop, (const void*)k_mark, (const void*)k_bump,
-                       (const void*)k_master_init};
+                       (const void*)k_master_init, (const void*)k_update_stream};
   for (const void* f : fns)
     if (cudaFuncGetAttributes(&fa, f) != cudaSuccess) return P3_ECUDA;
   return P3_OK;
