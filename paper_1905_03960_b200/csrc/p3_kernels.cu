@@ -2202,7 +2202,10 @@ __device__ __forceinline__ void warp_stream_piece(const float* __restrict__ g, f
 // priority order at tile granularity, balanced over all warps): P3_STREAM_TILE elements, and
 // P3_STREAM_TAIL-element tiles over the last stretch (the last wave stays short).
 #ifndef P3_STREAM_TAIL
-#define P3_STREAM_TAIL 256u
+#define P3_STREAM_TAIL 1024u
+#endif
+#ifndef P3_STREAM_TAIL_TILES
+#define P3_STREAM_TAIL_TILES 2u  // tail tiles per warp
 #endif
 
 __global__ void __launch_bounds__(P3_STREAM_THREADS, P3_STREAM_CTAS_PER_SM)
@@ -2212,10 +2215,13 @@ __global__ void __launch_bounds__(P3_STREAM_THREADS, P3_STREAM_CTAS_PER_SM)
   const uint32_t lane = threadIdx.x & 31;
   const uint64_t total = P.layer_flat[P.n_layers];
   const uint64_t nwarps = (uint64_t)gridDim.x * (blockDim.x / 32);
-  // tiles [0, t1) are big, the rest small: the small ones cover ~2 per warp at the end
-  const uint64_t tail = min(total, nwarps * 2 * P3_STREAM_TAIL);
-  const uint64_t t1 = (total - tail) / P3_STREAM_TILE;
-  const uint64_t big_end = t1 * P3_STREAM_TILE;
+  // tiles [0, t1) are big, the rest small (P3_STREAM_TAIL_TILES per warp at the end); models of
+  // 32M+ parameters take tiles twice as big (measured: ResNet-50 / seq2seq / VGG-19 sweeps)
+  const uint64_t big = total >= (32ull << 20) ? 2ull * P3_STREAM_TILE : (uint64_t)P3_STREAM_TILE;
+  const uint64_t small = big * P3_STREAM_TAIL / P3_STREAM_TILE;
+  const uint64_t tail = min(total, nwarps * P3_STREAM_TAIL_TILES * small);
+  const uint64_t t1 = (total - tail) / big;
+  const uint64_t big_end = t1 * big;
   const UpdCoef c = make_coef(1, a.lr, a.momentum);
   float* const W = a.peers.W[L.rank];
   uint32_t lc = P3_NONE;  // cached layer and its metadata (warp-uniform)
@@ -2225,9 +2231,9 @@ __global__ void __launch_bounds__(P3_STREAM_THREADS, P3_STREAM_CTAS_PER_SM)
     unsigned long long t = 0;
     if (lane == 0) t = atomicAdd(L.stream_next, 1ull);
     t = __shfl_sync(FULL_MASK, t, 0);
-    uint64_t pos = t < t1 ? t * P3_STREAM_TILE : big_end + (t - t1) * P3_STREAM_TAIL;
+    uint64_t pos = t < t1 ? t * big : big_end + (t - t1) * small;
     if (pos >= total) break;
-    const uint64_t end = min(pos + (t < t1 ? P3_STREAM_TILE : P3_STREAM_TAIL), total);
+    const uint64_t end = min(pos + (t < t1 ? big : small), total);
     while (pos < end) {
       if (lc == P3_NONE || pos < lstart || pos >= lnext) {  // the layer holding pos
         lc = warp_find_layer(P, pos);
