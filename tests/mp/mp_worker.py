@@ -155,7 +155,7 @@ def main():
             torch.cuda.synchronize()
             params = dict(m.named_parameters())
             for n in names:
-                gs = [torch.empty_like(grads[n]) for _ in range(world)]
+                gs = [torch.empty(grads[n].shape, dtype=grads[n].dtype, device="cuda") for _ in range(world)]
                 dist.all_gather(gs, grads[n].contiguous())
                 acc = torch.zeros_like(old[n])
                 for r in range(world):
@@ -167,6 +167,34 @@ def main():
         d.close()
         del d, m
         torch.cuda.empty_cache()
+    # bf16 replicas (param_dtype bf16) over NVLink, different data per rank: each replica equals
+    # bf16(master), the fp32 master updated from the ranks' own bf16 gradients in rank order
+    torch.manual_seed(7)
+    m = build_model("resnet50").cuda().to(memory_format=torch.channels_last).bfloat16()
+    d = P3DataParallel(m, lr=lr, comm_ctas=8, timeout_s=60.0)
+    names = [n for n, p in m.named_parameters() if p.requires_grad]
+    master = {n: p.detach().float().clone() for n, p in m.named_parameters() if p.requires_grad}
+    exact, differs = d.param_dtype == "bf16", False
+    for it in range(2):
+        x, y = synthetic_batch("resnet50", 8, seed=2000 * it + rank)
+        loss_fn("resnet50", d, x, y).backward()
+        grads = {n: p.grad.detach().clone() for n, p in m.named_parameters() if p.requires_grad}
+        d.synchronize()
+        torch.cuda.synchronize()
+        params = dict(m.named_parameters())
+        for n in names:
+            gs = [torch.empty(grads[n].shape, dtype=grads[n].dtype, device="cuda") for _ in range(world)]
+            dist.all_gather(gs, grads[n].contiguous())
+            acc = torch.zeros_like(master[n])
+            for r in range(world):
+                acc = acc + gs[r].view_as(acc).float()
+            master[n] = master[n] - (acc / torch.full_like(acc, world)).mul(lr)
+            exact &= bool(torch.equal(params[n].detach(), master[n].bfloat16()))
+            differs |= not torch.equal(gs[0], gs[-1])
+    out["torch_p3_bf16_replicas"] = exact and differs
+    d.close()
+    del d, m
+    torch.cuda.empty_cache()
     out_dir = os.environ.get("P3_MP_OUT")
     if out_dir:
         Path(out_dir, f"rank{rank}.json").write_text(json.dumps(out))

@@ -38,3 +38,4 @@ def test_multiprocess_parity(world, tmp_path):
         assert r["torch_layerwise_close"], r
         assert r["torch_p3_distinct_resnet50"], r
         assert r["torch_p3_distinct_seq2seq"], r
+        assert r["torch_p3_bf16_replicas"], r

@@ -13,7 +13,7 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", int(os.environ["LOCAL_RANK"])))
     name = sys.argv[1]
-    B = int(sys.argv[2]) if len(sys.argv) > 2 else {"resnet50": 256, "vgg19": 128, "seq2seq": 128}[name]
+    B = (int(sys.argv[2]) if len(sys.argv) > 2 else 0) or {"resnet50": 256, "vgg19": 128, "seq2seq": 128}[name]
     slices = [int(v) for v in (sys.argv[3] if len(sys.argv) > 3 else "1000,10000,50000,100000,1000000").split(",")]
     rates = [float(v) for v in (sys.argv[4] if len(sys.argv) > 4 else "10,25,0").split(",")]
     x, y = synthetic_batch(name, B, seed=7 + rank)
