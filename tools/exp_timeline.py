@@ -75,6 +75,13 @@ def main():
                                      "last_signal_us": [q(ends, 0), q(ends, .1), q(ends, .5), q(ends, .9), q(ends, 1)],
                                      "elems_per_cta_M": [round(busy_elems[0] / 1e6, 3), round(busy_elems[len(busy_elems) // 2] / 1e6, 3), round(busy_elems[-1] / 1e6, 3)],
                                      "jobs_per_cta": [njobs[0], njobs[len(njobs) // 2], njobs[-1]]}), flush=True)
+            # SM-time accounting: the share of (CTAs x span) each CTA spends after its last signal
+            # (tail), and each CTA's element rate between its first pick and its last signal
+            span = max(ends) - min(starts)
+            tail = sum(max(ends) - max(t for t, ev, _ in v) for v in per.values()) / (len(per) * span)
+            rates = sorted(sum(n for _, ev, n in v if ev == 1) * 12 / max(1, (max(t for t, ev, _ in v) - min(t for t, ev, _ in v))) for v in per.values())
+            print("SMTIME", json.dumps({"span_us": round(span / 1e3, 1), "tail_share": round(tail, 3),
+                                        "GBps_per_cta_p10_p50_p90": [round(rates[int(f * (len(rates) - 1))], 1) for f in (.1, .5, .9)]}), flush=True)
             # the CTA that finished last: its job sequence
             last = max(per, key=lambda c: max(t for t, ev, _ in per[c]))
             print("LAST", [(round(t / 1e3, 1), ev, n) for t, ev, n in sorted(per[last])], flush=True)
