@@ -134,6 +134,17 @@ __device__ __forceinline__ void tma_store_1d(void* gdst, const void* ssrc, uint3
   asm volatile("cp.async.bulk.commit_group;" ::: "memory");
 }
 __device__ __forceinline__ void tma_store_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+// bulk store without its own commit (a stage's stores form one bulk group)
+__device__ __forceinline__ void tma_store_1d_nc(void* gdst, const void* ssrc, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(smem_u32(ssrc)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+// every bulk group but the most recent one has finished reading shared memory
+__device__ __forceinline__ void tma_store_wait_read_all_but_one() {
+  asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+}
 __device__ __forceinline__ void tma_store_wait_all() {
   asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   asm volatile("fence.proxy.async.global;" ::: "memory");
@@ -2017,29 +2028,43 @@ __global__ void __launch_bounds__(P3_COMM_MAX_THREADS, 1) k_comm(const __grid_co
       if (j.kind == JOB_EXIT) break;
     }
   } else {
-    // consumers: compute each stage from shared memory, release it, report finished jobs
+    // consumers: compute each stage from shared memory, release it, report finished jobs.
+    // A stage that leaves by TMA bulk store is released by the first consumer warp only once
+    // the engine has read it — deferred to the next bulk stage (wait for all groups but the
+    // newest), so the next tile computes while the store drains.
     const uint32_t tid = threadIdx.x - 96;
+    const bool w0 = warp == 3;  // the first consumer warp (tid 0 issues the bulk stores)
+    uint32_t pend = P3_NONE;    // (w0) stage whose release waits for its bulk store's read
     uint64_t t_move = 0;
     for (uint32_t it = 0;; ++it) {
       const uint32_t sidx = it % P3_STAGES;
       mbar_wait_bounded(&full_bar[sidx], (it / P3_STAGES) & 1u, a);
       const StageDesc d = sdesc[sidx];
-      if (d.flags & ST_EXIT) break;
+      if (d.flags & ST_EXIT) {
+        if (w0 && pend != P3_NONE) {
+          if (lane == 0) tma_store_wait_read();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&empty_bar[pend]);
+        }
+        break;
+      }
       P3_CHECK(d.b < P3_SLOTS);
       const uint64_t tm = tid == 0 ? stat_clock() : 0;
       const Job& j = slots[d.b];
       const bool bulk_push = a.tma_store && j.kind == JOB_PUSH && j.bf16 != 1 && !(d.flags & ST_DIRECT);
+      bool bulk = false;  // this stage leaves by TMA bulk store (one group)
       if (bulk_push) {
         // the staged gradient tile goes out as one TMA bulk store (over NVLink to the
-        // owner's receive slot); the stage is released once the engine has read it
+        // owner's receive slot)
         if (tid == 0) {
           if (j.bf16 == 2)  // bf16 copy (param_bf16 push / answer)
-            tma_store_1d(reinterpret_cast<__nv_bfloat16*>(j.dst[0]) + d.e0, stage_mem + (size_t)sidx * P3_STAGE_BYTES,
-                         d.n * 2u);
+            tma_store_1d_nc(reinterpret_cast<__nv_bfloat16*>(j.dst[0]) + d.e0,
+                            stage_mem + (size_t)sidx * P3_STAGE_BYTES, d.n * 2u);
           else
-            tma_store_1d(j.dst[0] + d.e0, stage_mem + (size_t)sidx * P3_STAGE_BYTES, d.n * 4u);
-          tma_store_wait_read();
+            tma_store_1d_nc(j.dst[0] + d.e0, stage_mem + (size_t)sidx * P3_STAGE_BYTES, d.n * 4u);
+          bulk_commit();
         }
+        bulk = true;
       } else if (d.flags & ST_DIRECT) {
         move_range(a, j, d.e0, d.n, &rptrs, tid, ncons);
       } else if (!ONE && a.tma_store_red && j.kind == JOB_REDUCE && j.n <= 8 && !j.pb16 && j.bf16 == 0 &&
@@ -2054,17 +2079,34 @@ __global__ void __launch_bounds__(P3_COMM_MAX_THREADS, 1) k_comm(const __grid_co
         bar_sync(BAR_RANGE, ncons);
         if (tid == 0) {
           const uint32_t pitch = d.tile * 4;
-          for (uint32_t q = mode == 2 ? 1u : 0u; q < j.ndst; ++q) tma_store_1d(j.dst[q] + d.e0, st + j.n * pitch, d.n * 4u);
-          if (j.v && mode == 1) tma_store_1d(j.v + d.e0, st + (j.n + 1) * pitch, d.n * 4u);
-          tma_store_wait_read();
+          for (uint32_t q = mode == 2 ? 1u : 0u; q < j.ndst; ++q) tma_store_1d_nc(j.dst[q] + d.e0, st + j.n * pitch, d.n * 4u);
+          if (j.v && mode == 1) tma_store_1d_nc(j.v + d.e0, st + (j.n + 1) * pitch, d.n * 4u);
+          bulk_commit();
         }
+        bulk = true;
       } else {
         consume_tile<ONE>(a, j, d, stage_mem + (size_t)sidx * P3_STAGE_BYTES, tid, ncons);
       }
-      if ((d.flags & ST_LAST) && tid == 0 && (a.tma_store || a.tma_store_red))
+      const bool last = (d.flags & ST_LAST) != 0;
+      if (last && tid == 0 && (a.tma_store || a.tma_store_red))
         tma_store_wait_all();  // every bulk store of the job complete before its signal
       __syncwarp();
-      if (lane == 0) mbar_arrive(&empty_bar[sidx]);
+      if (w0 && bulk && !last) {  // release the previous deferred stage, defer this one
+        if (pend != P3_NONE) {
+          if (lane == 0) tma_store_wait_read_all_but_one();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&empty_bar[pend]);
+        }
+        pend = sidx;
+      } else {
+        if (w0 && pend != P3_NONE) {
+          if (lane == 0 && !last) tma_store_wait_read();  // (at a job end the wait above covered it)
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&empty_bar[pend]);
+          pend = P3_NONE;
+        }
+        if (lane == 0) mbar_arrive(&empty_bar[sidx]);
+      }
       if (tid == 0) t_move += stat_clock() - tm;
       if (d.flags & ST_LAST) bar_arrive(BAR_DONE(d.b), ncons + 32);
     }
