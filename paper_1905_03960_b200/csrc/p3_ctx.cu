@@ -96,7 +96,7 @@ struct PeerLayout {
 // Local arena of one rank. The per-iteration part (cursor | srv_lo | srv_taken | it) is
 // contiguous so one memset resets it before each launch.
 struct LocalLayout {
-  uint64_t pub, fifo_key, claim, iter_begin, cursor, srv_lo, srv_taken, it, pcount, slice_elems, stream_next, iter_end, V,
+  uint64_t pub, fifo_key, claim, iter_begin, cursor, srv_lo, srv_taken, it, pcount, slice_elems, stream_next, piece, iter_end, V,
       M, bytes, trace_n, trace, cta_phase, vclock, pubseq, ingested, heads, total;
 };
 
@@ -114,7 +114,7 @@ struct p3_ctx {
   // P3_TRACE_CTA=1 (trace records carry CTA indices; CTA start / exit records)
   struct {
     uint32_t use_tma = 1, push_split = 0, srv_filter = 0, trace_cta = 0, srv_reserve = 0, tma_store = 1, tma_store_red = 0, pop_relax = 0,
-             push_max = 2, stream = 1;
+             push_max = 2, stream = 1, push_cap = 0, bcast_pull = 0, lazy_pick = 0, srv_piece = 0;
   } knobs;
   std::vector<uint32_t> own_total;
   std::vector<uint64_t> own_stride;
@@ -198,7 +198,7 @@ PeerLayout peer_layout_of(const p3_ctx* c, uint32_t rank) {
   o = align_up(o + (uint64_t)c->L * 4, 256);
   p.gdone = o;
   o = align_up(o + (uint64_t)c->G * 4, 256);
-  const bool ring = c->cfg.notify_pull && c->N > 1;
+  const bool ring = (c->cfg.notify_pull || c->knobs.bcast_pull) && c->N > 1;
   p.ntf_tail = o;
   o = align_up(o + 4, 256);
   p.ntf_ring = o;
@@ -229,6 +229,7 @@ LocalLayout local_layout_of(const p3_ctx* c, uint64_t v_elems, uint64_t m_elems)
   take(q.pcount, 8);
   take(q.slice_elems, c->N == 1 ? c->S * 4ull : 4ull);
   take(q.stream_next, 8);
+  take(q.piece, c->N > 1 ? c->S * 8ull : 8ull);
   q.iter_end = o;
   take(q.V, v_elems * 4);
   take(q.M, m_elems * 4);
@@ -332,6 +333,10 @@ int p3_ctx_create(const p3_config_t* cfg, p3_ctx_t** out) {
     c->knobs.pop_relax = env_u32("P3_POP_RELAX", 0);  // 0: the config's
     c->knobs.tma_store_red = env_u32("P3_TMA_STORE_RED", 0);
     c->knobs.push_max = env_u32("P3_PUSH_MAX", 2);
+    c->knobs.push_cap = env_u32("P3_PUSH_CAP", 0);
+    c->knobs.bcast_pull = env_u32("P3_BCAST_PULL", 0);
+    c->knobs.lazy_pick = env_u32("P3_LAZY_PICK", 0);
+    c->knobs.srv_piece = env_u32("P3_SRV_PIECE", 0) & ~7u;
     c->knobs.stream = env_u32("P3_STREAM", 1);  // single rank: streaming FINISH (0: slice pops)
   }
   std::string perr;
@@ -528,6 +533,8 @@ int p3_ctx_create(const p3_config_t* cfg, p3_ctx_t** out) {
     D.pcount = reinterpret_cast<uint32_t*>(lb + ll.pcount);
     D.slice_elems = reinterpret_cast<uint32_t*>(lb + ll.slice_elems);
     D.stream_next = reinterpret_cast<unsigned long long*>(lb + ll.stream_next);
+    D.piece_next = reinterpret_cast<uint32_t*>(lb + ll.piece);
+    D.piece_done = D.piece_next + (c->N > 1 ? c->S : 1u);
     D.ntf_head = reinterpret_cast<uint32_t*>(lb + ll.heads);
     D.pull_head = D.ntf_head + 1;
     D.ring_cap = 4 * L + 64;
@@ -687,7 +694,7 @@ static CommArgs comm_args(p3_ctx* c, uint32_t mode, uint32_t ctas) {
   a.pop_multi = std::max<uint32_t>(1, std::min<uint32_t>(4, c->cfg.pop_multi ? c->cfg.pop_multi : 1));
   a.push_bf16 = c->cfg.push_bf16 ? 1u : 0u;
   a.pb16 = c->cfg.param_bf16 ? 1u : 0u;
-  a.notify = c->cfg.notify_pull && c->N > 1 ? 1u : 0u;
+  a.notify = c->N < 2 ? 0u : c->cfg.notify_pull ? 1u : c->knobs.bcast_pull ? 2u : 0u;
   a.ntf_cap = c->S;
   a.pull_cap = c->S * (c->N > 1 ? c->N - 1 : 1);
   a.trace_cta = c->knobs.trace_cta;
@@ -698,6 +705,9 @@ static CommArgs comm_args(p3_ctx* c, uint32_t mode, uint32_t ctas) {
   a.tma_store = c->knobs.tma_store;
   a.tma_store_red = c->knobs.tma_store_red;
   a.push_max = c->knobs.push_max;
+  a.push_cap = c->knobs.push_cap;
+  a.lazy_pick = c->knobs.lazy_pick;
+  a.srv_piece = c->knobs.srv_piece;
   // bounded relaxation of the pop order: a pop takes one of the C most urgent slices, C =
   // the launch's concurrent consumers (its CTAs) unless configured lower
   // (measured, tools/sync_sweep.py, ResNet-50 N=1 sync-only: C=8 2.2 TB/s, C=148 3.4 TB/s —
@@ -1070,8 +1080,8 @@ int p3_debug_snapshot(p3_ctx_t* c, uint32_t li, uint32_t* out, uint64_t cap, uin
     CK(cudaMemcpyAsync(out + (uint64_t)a * c->L, src[a], c->L * 4ull, cudaMemcpyDeviceToHost, c->poll_stream));
   std::vector<uint64_t> pub(c->L);
   CK(cudaMemcpyAsync(pub.data(), D.pub, c->L * 8ull, cudaMemcpyDeviceToHost, c->poll_stream));
-  static_assert(sizeof(IterState) == 48, "IterState layout");
-  CK(cudaMemcpyAsync(out + 5ull * c->L, D.it, sizeof(IterState), cudaMemcpyDeviceToHost, c->poll_stream));
+  static_assert(sizeof(IterState) == 56, "IterState layout");
+  CK(cudaMemcpyAsync(out + 5ull * c->L, D.it, 48, cudaMemcpyDeviceToHost, c->poll_stream));  // (up to t_signal)
   CK(cudaMemcpyAsync(out + 5ull * c->L + 12, D.cta_phase, P3_DBG_CTAS * 4ull, cudaMemcpyDeviceToHost, c->poll_stream));
   uint32_t* tail = out + 5ull * c->L + 12 + P3_DBG_CTAS;
   CK(cudaMemcpyAsync(tail, c->peers.arrivals[rank], c->S * 4ull, cudaMemcpyDeviceToHost, c->poll_stream));

@@ -82,6 +82,8 @@ struct IterState {
   // time (ns, summed over CTAs) spent by the scheduler picking, the scheduler waiting for a
   // free slot, the movers moving data, the signaler publishing completions (diagnostics)
   unsigned long long t_pick, t_slot_wait, t_move, t_signal;
+  uint32_t push_live;  // remote pushes popped and not yet signalled (the push_cap gate)
+  uint32_t pad_;
 };
 
 // Local-only state of one rank hosted in this process.
@@ -121,6 +123,8 @@ struct LocalDev {
   uint32_t* pcount;            // [2] notify mode, per iteration: PULLs sent, PULLs answered
   uint32_t* slice_elems;       // [S] single-rank stream: elements of each slice updated (per iteration)
   unsigned long long* stream_next;  // single-rank stream: next warp tile to claim (per iteration)
+  uint32_t* piece_next;  // [S] by own-list position: server pieces claimed (srv_piece; per iteration)
+  uint32_t* piece_done;  // [S] by own-list position: server pieces signalled (per iteration)
 };
 
 struct CommArgs {
@@ -147,6 +151,11 @@ struct CommArgs {
   uint32_t srv_reserve; // N > 1: every srv_reserve-th CTA does server work only (0: none)
   uint32_t tma_store;  // fp32 push tiles leave shared memory as TMA bulk stores
   uint32_t tma_store_red; // reduce results leave shared memory as TMA bulk stores (1: all, 2: remote)
+  uint32_t push_cap;
+  uint32_t srv_piece;  // >0: a completed owned slice is reduced in pieces of this many elements
+                       // (multiple of 8), each claimed by whichever CTA is free
+  uint32_t lazy_pick;  // FINISH, N > 1: once every local slice is claimed, pick the next job only
+                       // when the CTA's movers are idle (no job bound to a busy CTA)  // >0: at most this many remote pushes of a rank in flight (pops wait)
   uint32_t push_max;  // FINISH: 1 = a CTA keeps at most one push in flight (the other slot for reduces)
   uint32_t use_tma;   // movers stage sources through shared memory with TMA (else direct loads)
   uint32_t trace_cta; // diagnostics (P3_TRACE_CTA=1): trace records carry the CTA index as `rank`

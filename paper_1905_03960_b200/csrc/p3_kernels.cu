@@ -499,6 +499,7 @@ struct Stash {
 // round trip through slice_layer[] / pub[].
 struct Popped {
   uint32_t run;
+  uint32_t piece;  // server pick with srv_piece: the piece of the slice claimed
   uint32_t layer;
   uint64_t word;
   uint64_t t0;  // %globaltimer before the queue snapshot the claim came from (trace)
@@ -733,7 +734,7 @@ int launch_queue_pop(const uint32_t* nslices, const uint32_t* first, const uint6
 // claims are indexed by the slice's position in the owner's list, so no indirection), one
 // claim.
 __device__ P3_COLD uint32_t warp_server_pick(const CommArgs& a, const LocalDev& L, uint32_t* layer_out,
-                                     uint32_t* dbg = nullptr) {
+                                     uint32_t* dbg = nullptr, uint32_t* piece_out = nullptr) {
   const uint32_t lane = threadIdx.x & 31;
   const PlanDev& P = a.plan;
   const uint32_t o = L.rank, nl = P.n_layers, k = a.k;
@@ -831,18 +832,33 @@ __device__ P3_COLD uint32_t warp_server_pick(const CommArgs& a, const LocalDev& 
         m &= ~(1u << jj);
         const uint32_t gj = __shfl_sync(FULL_MASK, g, jj);
         const uint32_t pj = lf + i0 + jj;
-        uint32_t won = 0;
+        uint32_t won = 0, piece = 0;
         if (lane == 0) {
-          won = atomicCAS(L.claim + pj, k, k + 1) == k;
-          if (won) {
+          if (a.srv_piece) {
+            // pieces: claim the next piece; the claim of the last one claims the slice
+            const uint32_t np = (P.slice_len[gj] + a.srv_piece - 1) / a.srv_piece;
+            piece = atomicAdd(L.piece_next + pj, 1u);
+            won = piece < np;
+            if (won && piece + 1 < np) {
+              if (L.trace_cap && piece == 0) trace_append(L, k, l, gj - P.layer_first[l], o, P3_EV_PICK, t_snap);
+              won = 2;  // a piece; the slice stays open for the other pieces
+            } else if (won) {
+              atomicExch(L.claim + pj, k + 1);
+            }
+          } else {
+            won = atomicCAS(L.claim + pj, k, k + 1) == k;
+          }
+          if (won == 1) {
             atomicAdd(L.srv_taken + l, 1u);
             atomicAdd(&L.it->reduced, 1u);
-            if (L.trace_cap) trace_append(L, k, l, gj - P.layer_first[l], o, P3_EV_PICK, t_snap);
+            if (L.trace_cap && (!a.srv_piece || piece == 0))
+              trace_append(L, k, l, gj - P.layer_first[l], o, P3_EV_PICK, t_snap);
           }
         }
         won = __shfl_sync(FULL_MASK, won, 0);
         if (won) {
           *layer_out = l;
+          if (piece_out) *piece_out = __shfl_sync(FULL_MASK, piece, 0);
           return gj;
         }
       }
@@ -892,12 +908,14 @@ __device__ __forceinline__ QueueView queue_of(const CommArgs& a, const LocalDev&
 #define JOB_PUSH 2
 #define JOB_EXIT 3
 #define JOB_ANSWER 4  // scheduler only: becomes a PUSH-shaped slot with `answer` set
+#define JOB_FETCH 5   // scheduler only (broadcast pull): a PUSH-shaped slot with `answer` = 2
 struct Job {
   uint32_t kind, li, g, layer, opos, rank, len, n, aligned, run;  // opos: position in the owner's list
   uint32_t ndst;    // REDUCE: replicas written (dst[0..ndst)): N, or 1 when peers pull (notify mode)
   uint32_t pb16;    // REDUCE, param_bf16: bf16 contributions, fp32 master m, bf16 replicas
   float* m;         // REDUCE, param_bf16: the owner's fp32 master of the slice
   uint32_t answer;  // PUSH-shaped copy of an updated slice to a peer that pulled it (notify mode)
+  uint32_t pieces;  // REDUCE: pieces the slice is reduced in (srv_piece; 1 = whole)
   uint32_t bf16;  // pushes travel as bf16 (declared lossy mode); own = index of the fp32 source
   const float* src[P3_MAX_RANKS];  // PUSH: src[0]; REDUCE: contributions in rank order
   float* dst[P3_MAX_RANKS];        // PUSH: dst[0]; REDUCE: replicas, dst[0] = owner's master
@@ -1027,7 +1045,7 @@ __device__ uint32_t prepare_push(const CommArgs& a, uint32_t li, uint32_t g, uin
           // time is taken before the backlog is read.
           const uint64_t tc = L.trace_cap ? globaltimer() : 0ull;
           const uint32_t backlog = done_before + 1u - a.k * P.own_total[o] - ld_relaxed_gpu(&L.it->reduced);
-          if ((int32_t)backlog <= 1 && atomicCAS(L.claim + opos, a.k, a.k + 1) == a.k) {
+          if (!a.srv_piece && (int32_t)backlog <= 1 && atomicCAS(L.claim + opos, a.k, a.k + 1) == a.k) {
             atomicAdd(L.srv_taken + l, 1u);
             atomicAdd(&L.it->reduced, 1u);
             if (L.trace_cap) trace_append(L, a.k, l, g - P.layer_first[l], o, P3_EV_PICK, tc);
@@ -1070,15 +1088,18 @@ __device__ uint32_t prepare_push(const CommArgs& a, uint32_t li, uint32_t g, uin
 // its gradient) and every replica to write, master first.
 // `w` is the layer's publication word when the caller already holds it (0: load it).
 __device__ void prepare_reduce(const CommArgs& a, uint32_t li, uint32_t g, uint32_t l, uint64_t w, Job* job,
-                               uint32_t run = 1) {
+                               uint32_t run = 1, uint32_t piece = 0) {
   const PlanDev& P = a.plan;
   const LocalDev& L = a.loc[li];
+  // srv_piece: elements [piece * srv_piece, +srv_piece) of the slice
   const uint32_t o = L.rank, N = P.world;
+  const bool pieces = a.srv_piece && N > 1;
+  const uint32_t pe0 = pieces ? piece * a.srv_piece : 0u;
   const uint32_t q = threadIdx.x & 31;
   // independent loads first (one round trip), then the acquire that orders the data reads
-  const uint64_t soff = P.slice_off[g];
+  const uint64_t soff = P.slice_off[g] + pe0;
   const uint64_t woff = P.layer_woff[l] + soff;
-  const uint64_t slot = P.slice_slot[g];
+  const uint64_t slot = P.slice_slot[g] + pe0;
   const uint32_t opos = N > 1 ? P.slice_opos[g] : 0u;
   const uint64_t stride = P.own_stride[o];
   uint32_t len = q < run ? P.slice_len[g + q] : 0u;  // consecutive slices: contiguous
@@ -1110,8 +1131,12 @@ __device__ void prepare_reduce(const CommArgs& a, uint32_t li, uint32_t g, uint3
   for (int off = 16; off; off >>= 1) al |= __shfl_xor_sync(FULL_MASK, (unsigned long long)al, off);
 #pragma unroll
   for (int off = 16; off; off >>= 1) len += __shfl_xor_sync(FULL_MASK, len, off);
+  const uint32_t np = pieces ? (len + a.srv_piece - 1) / a.srv_piece : 1u;
+  if (pieces) len = min(a.srv_piece, len - pe0);
   if (q == 0) {
     job->kind = JOB_REDUCE;
+    job->pieces = np;
+    job->opos = opos;
     job->ndst = a.notify ? 1u : N;  // notify mode: peers pull the update (server.py:227-247)
     job->answer = 0;
     job->li = li;
@@ -1492,11 +1517,14 @@ __device__ P3_COLD void signal_job(const CommArgs& a, const Job& j) {
     atomicAdd(L.pcount + 1, 1u);
     atomicAdd(L.bytes + 1, (j.bf16 == 2 ? 2ull : 4ull) * j.len);
     if (L.trace_cap) trace_append(L, a.k, j.layer, j.g - P.layer_first[j.layer], j.rank, P3_EV_BCAST);
-  } else if (j.kind == JOB_PUSH) {
+    return;
+  }
+  if (j.kind == JOB_PUSH) {
     // the last arriver completes the slice and tells the owner's scheduler (hint)
     const uint32_t old = atom_add_relaxed_sys(a.peers.arrivals[j.rank] + j.opos, 1u);
     P3_CHECK(old >= a.k * P.world && old < (a.k + 1) * P.world);  // one push per rank and slice
     red_add_relaxed_sys(a.peers.tally[j.rank], 1u);
+    if (a.push_cap) atomicSub(&a.loc[0].it->push_live, 1u);
     if (old + 1 == (a.k + 1) * P.world) {
       red_add_relaxed_sys(a.peers.hint[j.rank] + j.layer, 1u);
       red_add_relaxed_sys(a.peers.tally[j.rank] + 1, 1u);
@@ -1506,7 +1534,17 @@ __device__ P3_COLD void signal_job(const CommArgs& a, const Job& j) {
       }
     }
     atomicAdd(L.bytes + 1, (j.bf16 ? 2ull : 4ull) * j.len);
-  } else if (a.notify) {
+    return;
+  }
+  if (j.pieces > 1) {
+    // a piece of a slice reduced in pieces: only the last one to finish signals the slice,
+    // after acquiring the other pieces' releases
+    atomicAdd(L.bytes + 0, (j.bf16 || j.pb16 ? 2ull : 4ull) * j.len * (j.n - 1));
+    if (!a.notify) atomicAdd(L.bytes + 1, (j.pb16 ? 2ull : 4ull) * j.len * (j.n - 1));
+    if (atomicAdd(L.piece_done + j.opos, 1u) + 1 < j.pieces) return;
+    fence_acq_rel_sys();
+  }
+  if (a.notify) {
     // notify mode: the owner's replica holds the update; NOTIFY every other rank, which will
     // PULL it (server.py:227-239)
     const uint32_t grp = P.layer_group[j.layer];
@@ -1521,15 +1559,17 @@ __device__ P3_COLD void signal_job(const CommArgs& a, const Job& j) {
         if (L.trace_cap) trace_append(L, a.k, j.layer, j.g + i - P.layer_first[j.layer], q, P3_EV_NOTIFY);
       }
     }
-    atomicAdd(L.bytes + 0, (j.bf16 || j.pb16 ? 2ull : 4ull) * j.len * (j.n - 1));  // pushes received
+    if (j.pieces <= 1) atomicAdd(L.bytes + 0, (j.bf16 || j.pb16 ? 2ull : 4ull) * j.len * (j.n - 1));  // pushes received
   } else {
     const uint32_t grp = P.layer_group[j.layer];
     for (uint32_t q = 0; q < j.n; ++q) {
       red_add_relaxed_sys(a.peers.done[q] + j.layer, j.run);
       red_add_relaxed_sys(a.peers.gdone[q] + grp, j.run);
     }
-    atomicAdd(L.bytes + 0, (j.bf16 || j.pb16 ? 2ull : 4ull) * j.len * (j.n - 1));  // pushes received
-    atomicAdd(L.bytes + 1, (j.pb16 ? 2ull : 4ull) * j.len * (j.n - 1));  // broadcasts sent
+    if (j.pieces <= 1) {
+      atomicAdd(L.bytes + 0, (j.bf16 || j.pb16 ? 2ull : 4ull) * j.len * (j.n - 1));  // pushes received
+      atomicAdd(L.bytes + 1, (j.pb16 ? 2ull : 4ull) * j.len * (j.n - 1));  // broadcasts sent
+    }
     if (L.trace_cap)
       for (uint32_t i = 0; i < j.run; ++i)
         trace_append(L, a.k, j.layer, j.g + i - P.layer_first[j.layer], a.trace_cta ? blockIdx.x : j.rank, P3_EV_BCAST);
@@ -1621,15 +1661,49 @@ __device__ P3_COLD bool warp_issue_pull(const CommArgs& a, const LocalDev& L) {
   return __shfl_sync(FULL_MASK, sent, 0) != 0;
 }
 
+// Broadcast-pull mode (notify 2), worker side: take the next NOTIFY of this rank; the
+// scheduler turns it into a fetch of the owner's updated slice (one NVLink read, no request).
+__device__ P3_COLD uint32_t warp_take_notify(const CommArgs& a, const LocalDev& L, uint32_t* layer) {
+  const uint32_t lane = threadIdx.x & 31;
+  uint32_t g = P3_NONE;
+  if (lane == 0) {
+    const uint32_t r = L.rank;
+    const uint32_t h = ld_relaxed_gpu(L.ntf_head), t = ld_relaxed_sys(a.peers.ntf_tail[r]);
+    if ((int32_t)(t - h) > 0 && atomicCAS(L.ntf_head, h, h + 1) == h) {
+      const volatile unsigned long long* e = a.peers.ntf_ring[r] + h % a.ntf_cap;
+      unsigned long long v = *e;
+      const uint64_t t0 = globaltimer();
+      while ((uint32_t)(v >> 32) != a.k + 1) {  // reserved, entry still on its way
+        if (globaltimer() - t0 > a.timeout_ns) break;
+        __nanosleep(64);
+        v = *e;
+      }
+      fence_acq_rel_sys();  // acquire: the owner's replica stores came before its NOTIFY
+      g = (uint32_t)v;
+      if (L.trace_cap) {
+        const uint32_t l = a.plan.slice_layer[g];
+        trace_append(L, a.k, l, g - a.plan.layer_first[l], a.plan.slice_owner[g], P3_EV_PULL);
+      }
+    }
+  }
+  g = __shfl_sync(FULL_MASK, g, 0);
+  if (g != P3_NONE) *layer = a.plan.slice_layer[g];
+  return g;
+}
+
 // Notify mode: the answer to a PULL — the owner's updated slice copied into the requester's
 // replica (a push-shaped job: TMA-staged, bulk-stored over NVLink).
-__device__ P3_COLD void prepare_answer(const CommArgs& a, uint32_t li, uint32_t g, uint32_t l, uint32_t q, Job* job) {
+// Broadcast pull (fetch = true): the same copy run by the requester q itself, from the owner's
+// replica into its own.
+__device__ P3_COLD void prepare_answer(const CommArgs& a, uint32_t li, uint32_t g, uint32_t l, uint32_t q, Job* job,
+                                       bool fetch = false) {
   const PlanDev& P = a.plan;
   const LocalDev& L = a.loc[li];
   if ((threadIdx.x & 31) == 0) {
     const uint64_t woff = P.layer_woff[l] + P.slice_off[g];
+    const uint32_t from = fetch ? P.slice_owner[g] : L.rank;
     job->kind = JOB_PUSH;
-    job->answer = 1;
+    job->answer = fetch ? 2u : 1u;
     job->pb16 = 0;
     job->ndst = 1;
     job->run = 1;
@@ -1641,11 +1715,11 @@ __device__ P3_COLD void prepare_answer(const CommArgs& a, uint32_t li, uint32_t 
     job->len = P.slice_len[g];
     if (a.pb16) {  // bf16 replicas: a 2-byte copy
       job->bf16 = 2;
-      job->src[0] = reinterpret_cast<const float*>(reinterpret_cast<const __nv_bfloat16*>(a.peers.W[L.rank]) + woff);
+      job->src[0] = reinterpret_cast<const float*>(reinterpret_cast<const __nv_bfloat16*>(a.peers.W[from]) + woff);
       job->dst[0] = reinterpret_cast<float*>(reinterpret_cast<__nv_bfloat16*>(a.peers.W[q]) + woff);
     } else {
       job->bf16 = 0;
-      job->src[0] = a.peers.W[L.rank] + woff;
+      job->src[0] = a.peers.W[from] + woff;
       job->dst[0] = a.peers.W[q] + woff;
     }
   }
@@ -1712,6 +1786,7 @@ __global__ void __launch_bounds__(P3_COMM_MAX_THREADS, 1) k_comm(const __grid_co
       uint32_t kind = JOB_NONE, li = 0, g = P3_NONE;
       Popped pp;
       pp.run = 1;
+      pp.piece = 0;
       pp.layer = 0;
       pp.word = 0;
       pp.t0 = 0;
@@ -1743,33 +1818,61 @@ __global__ void __launch_bounds__(P3_COMM_MAX_THREADS, 1) k_comm(const __grid_co
       // progress, like the reference's server and sender threads: `push_split` > 0 makes
       // every push_split-th CTA look for pushes first, the others for server work first.
       const bool push_first = a.push_split && (blockIdx.x % a.push_split) == a.push_split - 1;
+      if (!ONE && a.lazy_pick && pops_done) {
+        // late binding: a job picked now would wait behind the one moving; with no pushes left,
+        // leave it to an idle CTA unless this one's movers are done too
+        const uint32_t pb = (b + P3_SLOTS - 1) % P3_SLOTS;
+        if (pending[pb]) {
+          bar_sync(BAR_EMPTY(pb), 64);
+          pending[pb] = false;
+        }
+      }
       uint32_t ans_q = 0;
-      bool pulled = false;
+      bool pulled = false, was_capped = false, token = false;
       for (uint32_t round = 0; round < 2 && kind == JOB_NONE && !ONE && a.plan.world > 1; ++round) {
         if ((round == 0) != push_first) {
           for (uint32_t t = 0; t < a.n_local && kind == JOB_NONE; ++t) {
             li = (blockIdx.x + t) % a.n_local;
-            g = warp_server_pick(a, a.loc[li], &pp.layer, phase);
+            g = warp_server_pick(a, a.loc[li], &pp.layer, phase, &pp.piece);
             if (g != P3_NONE) kind = JOB_REDUCE;
           }
-          for (uint32_t t = 0; t < a.n_local && kind == JOB_NONE && a.notify; ++t) {
+          for (uint32_t t = 0; t < a.n_local && kind == JOB_NONE && a.notify == 1; ++t) {
             li = (blockIdx.x + t) % a.n_local;
             g = warp_answer_pick(a, a.loc[li], &pp.layer, &ans_q);
             if (g != P3_NONE) kind = JOB_ANSWER;
           }
-        } else {
-          if (stash.n) {
-            li = stash_li;
-            g = take_stash(&stash, &pp);
-            if (lane == 0) atomicAdd(&a.loc[li].it->pushed, 1u);
-            kind = JOB_PUSH;
+          for (uint32_t t = 0; t < a.n_local && kind == JOB_NONE && a.notify == 2; ++t) {
+            li = (blockIdx.x + t) % a.n_local;
+            g = warp_take_notify(a, a.loc[li], &pp.layer);
+            if (g != P3_NONE) kind = JOB_FETCH;
           }
+        } else {
           // server-reserved CTAs (srv_reserve > 0: every srv_reserve-th CTA) never take pushes,
           // so a completed slice is reduced while the other CTAs' pipelines hold pushes
           const bool reserved = (a.srv_reserve && (blockIdx.x % a.srv_reserve) == 0) ||
                                 (a.push_max == 1 && a.mode == P3_COMM_FINISH && last_push && backoff < 512u &&
                                  pending[(b + P3_SLOTS - 1) % P3_SLOTS]);  // (an idle scheduler pushes anyway)
-          for (uint32_t t = 0; t < a.n_local && kind == JOB_NONE && !pops_done && !reserved; ++t) {
+          // push_cap: a pop takes one of push_cap tokens of the rank (returned by the push's
+          // signal, or at once when the pop yields no remote push), so the first pushes
+          // complete (and their reductions start) early instead of every CTA's pushes sharing
+          // the link at once
+          bool capped = false;
+          if (a.push_cap && (stash.n || (!pops_done && !reserved))) {
+            uint32_t ok = 0;
+            if (lane == 0) {
+              ok = atomicAdd(&a.loc[0].it->push_live, 1u) < a.push_cap;
+              if (!ok) atomicSub(&a.loc[0].it->push_live, 1u);
+            }
+            token = __shfl_sync(FULL_MASK, ok, 0) != 0;
+            capped = was_capped = !token;
+          }
+          if (stash.n && !capped) {
+            li = stash_li;
+            g = take_stash(&stash, &pp);
+            if (lane == 0) atomicAdd(&a.loc[li].it->pushed, 1u);
+            kind = JOB_PUSH;
+          }
+          for (uint32_t t = 0; t < a.n_local && kind == JOB_NONE && !pops_done && !reserved && !capped && !stash.n; ++t) {
             li = (blockIdx.x + t) % a.n_local;
             g = warp_pop(queue_of(a, a.loc[li]), a.k + 1, phase, 1u, &pp, &stash);
             if (lane == 0) stash_li = li;
@@ -1779,8 +1882,12 @@ __global__ void __launch_bounds__(P3_COMM_MAX_THREADS, 1) k_comm(const __grid_co
               kind = JOB_PUSH;
             }
           }
+          if (token && kind != JOB_PUSH) {  // nothing popped: give the token back
+            if (lane == 0) atomicSub(&a.loc[0].it->push_live, 1u);
+            token = false;
+          }
           // notify mode: PULLs wait behind the pushes (the baseline's per-server FIFO outbox)
-          for (uint32_t t = 0; t < a.n_local && kind == JOB_NONE && a.notify; ++t)
+          for (uint32_t t = 0; t < a.n_local && kind == JOB_NONE && a.notify == 1; ++t)
             pulled |= warp_issue_pull(a, a.loc[(blockIdx.x + t) % a.n_local]);
           if (kind == JOB_NONE && !pops_done && a.mode == P3_COMM_FINISH) {
             // FINISH runs after every publication of the iteration: once every local slice
@@ -1821,9 +1928,11 @@ __global__ void __launch_bounds__(P3_COMM_MAX_THREADS, 1) k_comm(const __grid_co
               const uint32_t own = a.plan.own_total[L.rank];
               fin = fin && ld_relaxed_gpu(&L.it->pushed) >= a.plan.total_slices &&
                     ld_relaxed_gpu(&L.it->reduced) >= own;
-              if (!ONE && a.notify)  // every NOTIFY pulled, every PULL of an owned slice answered
+              if (!ONE && a.notify == 1)  // every NOTIFY pulled, every PULL of an owned slice answered
                 fin = fin && ld_relaxed_gpu(L.pcount) >= a.plan.total_slices - own &&
                       ld_relaxed_gpu(L.pcount + 1) >= own * (a.plan.world - 1);
+              if (!ONE && a.notify == 2)  // every other owner's slice fetched
+                fin = fin && ld_relaxed_gpu(L.pcount + 1) >= a.plan.total_slices - own;
             }
             verdict = (fin || ld_relaxed_gpu(a.err) != 0) ? 1u : (globaltimer() - t0 > a.timeout_ns ? 2u : 0u);
           }
@@ -1844,7 +1953,7 @@ __global__ void __launch_bounds__(P3_COMM_MAX_THREADS, 1) k_comm(const __grid_co
         }
         verdict = __shfl_sync(FULL_MASK, verdict, 0);
         if (verdict == 0) {
-          backoff = min(2u * backoff + 64u, pops_done ? 512u : 4096u);
+          backoff = min(2u * backoff + 64u, (pops_done || was_capped) ? 512u : 4096u);
           __nanosleep(backoff);
           continue;
         }
@@ -1860,10 +1969,11 @@ __global__ void __launch_bounds__(P3_COMM_MAX_THREADS, 1) k_comm(const __grid_co
       }
       if (kind == JOB_PUSH) {
         const uint32_t how = prepare_push(a, li, g, pp.layer, pp.word, nullptr, pp.t0);
+        if (token && how != PUSH_REMOTE && lane == 0) atomicSub(&a.loc[0].it->push_live, 1u);  // (no link use)
         if (how == PUSH_DONE) continue;  // own slice, still waiting for peers: counted in place
         if (how == PUSH_REDUCE) kind = JOB_REDUCE;  // own slice completed it: reduce right away
       }
-      if (!ONE && (kind == JOB_PUSH || kind == JOB_REDUCE || kind == JOB_ANSWER) && a.ns_per_byte != 0.f &&
+      if (!ONE && (kind == JOB_PUSH || kind == JOB_REDUCE || kind == JOB_ANSWER || kind == JOB_FETCH) && a.ns_per_byte != 0.f &&
           a.plan.world > 1) {
         // egress bytes of this job on the rank's link (K7): a push, an answer to a PULL, or the
         // N-1 broadcast copies of a reduce (none in notify mode: the peers pull)
@@ -1880,8 +1990,10 @@ __global__ void __launch_bounds__(P3_COMM_MAX_THREADS, 1) k_comm(const __grid_co
         prepare_push(a, li, g, pp.layer, pp.word, &slots[b]);
       } else if (kind == JOB_ANSWER) {
         prepare_answer(a, li, g, pp.layer, ans_q, &slots[b]);
+      } else if (kind == JOB_FETCH) {
+        prepare_answer(a, li, g, pp.layer, a.loc[li].rank, &slots[b], true);
       } else if (kind == JOB_REDUCE) {
-        prepare_reduce(a, li, g, pp.layer, pp.word, &slots[b], pp.run);
+        prepare_reduce(a, li, g, pp.layer, pp.word, &slots[b], pp.run, pp.piece);
       } else {
         for (uint32_t i = 1; i < P3_SLOTS; ++i) {  // leave every barrier balanced
           const uint32_t bi = (b + i) % P3_SLOTS;
@@ -1894,7 +2006,7 @@ __global__ void __launch_bounds__(P3_COMM_MAX_THREADS, 1) k_comm(const __grid_co
       bar_arrive(BAR_FULL(b), 96);  // producer + signaler wait on it
       if (kind == JOB_EXIT) break;
       pending[b] = true;
-      last_push = kind == JOB_PUSH || kind == JOB_ANSWER;
+      last_push = kind == JOB_PUSH || kind == JOB_ANSWER || kind == JOB_FETCH;
       b = (b + 1) % P3_SLOTS;
       if (lane == 0) atomicAdd(&stats->jobs, 1u);
     }
@@ -1927,6 +2039,7 @@ __global__ void __launch_bounds__(P3_COMM_MAX_THREADS, 1) k_comm(const __grid_co
       mine.ndst = j.ndst;
       mine.answer = j.answer;
       mine.pb16 = j.pb16;
+      mine.pieces = j.pieces;
       __syncwarp();
       bar_arrive(BAR_EMPTY(b), 64);
       if (lane == 0) {

@@ -46,6 +46,10 @@ def main():
         e.record(st)
         ctx.sync_all(k + 1, 30.0)
         st.synchronize()
+        if k == 3 and os.environ.get("P3_TL_DUMP"):  # raw records of every rank (analysed offline)
+            recs = [(r.t_ns, r.t0_ns, r.event, r.layer, r.slice, r.rank) for r in ctx.trace(0) if r.iteration == k]
+            with open(os.path.join(os.environ["P3_TL_DUMP"], f"tl_{m}_rank{rank}.json"), "w") as f:
+                json.dump(recs, f)
         if rank == 0 and k == 3:
             tr_all = [r for r in ctx.trace(0) if r.iteration == k]
             tr = [r for r in tr_all if r.event in (0, 1)]
