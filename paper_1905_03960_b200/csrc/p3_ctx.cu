@@ -333,10 +333,15 @@ int p3_ctx_create(const p3_config_t* cfg, p3_ctx_t** out) {
     c->knobs.pop_relax = env_u32("P3_POP_RELAX", 0);  // 0: the config's
     c->knobs.tma_store_red = env_u32("P3_TMA_STORE_RED", 0);
     c->knobs.push_max = env_u32("P3_PUSH_MAX", 2);
-    c->knobs.push_cap = env_u32("P3_PUSH_CAP", 0);
-    c->knobs.bcast_pull = env_u32("P3_BCAST_PULL", 0);
-    c->knobs.lazy_pick = env_u32("P3_LAZY_PICK", 0);
-    c->knobs.srv_piece = env_u32("P3_SRV_PIECE", 0) & ~7u;
+    if (P3_EXP) {  // experiment switches (a -DP3_EXP=1 build)
+      c->knobs.push_cap = env_u32("P3_PUSH_CAP", 0);
+      c->knobs.bcast_pull = env_u32("P3_BCAST_PULL", 0);
+      c->knobs.lazy_pick = env_u32("P3_LAZY_PICK", 0);
+      c->knobs.srv_piece = env_u32("P3_SRV_PIECE", 0) & ~7u;
+    } else {
+      for (const char* k : {"P3_PUSH_CAP", "P3_BCAST_PULL", "P3_LAZY_PICK", "P3_SRV_PIECE"})
+        if (getenv(k)) fprintf(stderr, "p3: %s ignored (experiment switch; build with -DP3_EXP=1)\n", k);
+    }
     c->knobs.stream = env_u32("P3_STREAM", 1);  // single rank: streaming FINISH (0: slice pops)
   }
   std::string perr;

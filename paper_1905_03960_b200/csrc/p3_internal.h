@@ -8,6 +8,12 @@
 
 #include "../../include/p3.h"
 
+// P3_EXP=1 compiles the comm-kernel experiment switches in (P3_PUSH_CAP, P3_LAZY_PICK,
+// P3_SRV_PIECE, P3_BCAST_PULL; measured slower or neutral, profiles/r02_summary.md §7);
+// the default build leaves them out so they cost the scheduler nothing.
+#ifndef P3_EXP
+#define P3_EXP 0
+#endif
 #ifndef P3_COMM_MAX_THREADS
 #define P3_COMM_MAX_THREADS 512  // comm CTA size bound (launch bounds: 126 registers at 512)
 #endif

@@ -834,7 +834,7 @@ __device__ P3_COLD uint32_t warp_server_pick(const CommArgs& a, const LocalDev& 
         const uint32_t pj = lf + i0 + jj;
         uint32_t won = 0, piece = 0;
         if (lane == 0) {
-          if (a.srv_piece) {
+          if (P3_EXP && a.srv_piece) {
             // pieces: claim the next piece; the claim of the last one claims the slice
             const uint32_t np = (P.slice_len[gj] + a.srv_piece - 1) / a.srv_piece;
             piece = atomicAdd(L.piece_next + pj, 1u);
@@ -851,7 +851,7 @@ __device__ P3_COLD uint32_t warp_server_pick(const CommArgs& a, const LocalDev& 
           if (won == 1) {
             atomicAdd(L.srv_taken + l, 1u);
             atomicAdd(&L.it->reduced, 1u);
-            if (L.trace_cap && (!a.srv_piece || piece == 0))
+            if (L.trace_cap && (!(P3_EXP && a.srv_piece) || piece == 0))
               trace_append(L, k, l, gj - P.layer_first[l], o, P3_EV_PICK, t_snap);
           }
         }
@@ -1045,7 +1045,7 @@ __device__ uint32_t prepare_push(const CommArgs& a, uint32_t li, uint32_t g, uin
           // time is taken before the backlog is read.
           const uint64_t tc = L.trace_cap ? globaltimer() : 0ull;
           const uint32_t backlog = done_before + 1u - a.k * P.own_total[o] - ld_relaxed_gpu(&L.it->reduced);
-          if (!a.srv_piece && (int32_t)backlog <= 1 && atomicCAS(L.claim + opos, a.k, a.k + 1) == a.k) {
+          if (!(P3_EXP && a.srv_piece) && (int32_t)backlog <= 1 && atomicCAS(L.claim + opos, a.k, a.k + 1) == a.k) {
             atomicAdd(L.srv_taken + l, 1u);
             atomicAdd(&L.it->reduced, 1u);
             if (L.trace_cap) trace_append(L, a.k, l, g - P.layer_first[l], o, P3_EV_PICK, tc);
@@ -1093,7 +1093,7 @@ __device__ void prepare_reduce(const CommArgs& a, uint32_t li, uint32_t g, uint3
   const LocalDev& L = a.loc[li];
   // srv_piece: elements [piece * srv_piece, +srv_piece) of the slice
   const uint32_t o = L.rank, N = P.world;
-  const bool pieces = a.srv_piece && N > 1;
+  const bool pieces = P3_EXP && a.srv_piece && N > 1;
   const uint32_t pe0 = pieces ? piece * a.srv_piece : 0u;
   const uint32_t q = threadIdx.x & 31;
   // independent loads first (one round trip), then the acquire that orders the data reads
@@ -1524,7 +1524,7 @@ __device__ P3_COLD void signal_job(const CommArgs& a, const Job& j) {
     const uint32_t old = atom_add_relaxed_sys(a.peers.arrivals[j.rank] + j.opos, 1u);
     P3_CHECK(old >= a.k * P.world && old < (a.k + 1) * P.world);  // one push per rank and slice
     red_add_relaxed_sys(a.peers.tally[j.rank], 1u);
-    if (a.push_cap) atomicSub(&a.loc[0].it->push_live, 1u);
+    if (P3_EXP && a.push_cap) atomicSub(&a.loc[0].it->push_live, 1u);
     if (old + 1 == (a.k + 1) * P.world) {
       red_add_relaxed_sys(a.peers.hint[j.rank] + j.layer, 1u);
       red_add_relaxed_sys(a.peers.tally[j.rank] + 1, 1u);
@@ -1536,7 +1536,7 @@ __device__ P3_COLD void signal_job(const CommArgs& a, const Job& j) {
     atomicAdd(L.bytes + 1, (j.bf16 ? 2ull : 4ull) * j.len);
     return;
   }
-  if (j.pieces > 1) {
+  if (P3_EXP && j.pieces > 1) {
     // a piece of a slice reduced in pieces: only the last one to finish signals the slice,
     // after acquiring the other pieces' releases
     atomicAdd(L.bytes + 0, (j.bf16 || j.pb16 ? 2ull : 4ull) * j.len * (j.n - 1));
@@ -1559,14 +1559,14 @@ __device__ P3_COLD void signal_job(const CommArgs& a, const Job& j) {
         if (L.trace_cap) trace_append(L, a.k, j.layer, j.g + i - P.layer_first[j.layer], q, P3_EV_NOTIFY);
       }
     }
-    if (j.pieces <= 1) atomicAdd(L.bytes + 0, (j.bf16 || j.pb16 ? 2ull : 4ull) * j.len * (j.n - 1));  // pushes received
+    if (!P3_EXP || j.pieces <= 1) atomicAdd(L.bytes + 0, (j.bf16 || j.pb16 ? 2ull : 4ull) * j.len * (j.n - 1));  // pushes received
   } else {
     const uint32_t grp = P.layer_group[j.layer];
     for (uint32_t q = 0; q < j.n; ++q) {
       red_add_relaxed_sys(a.peers.done[q] + j.layer, j.run);
       red_add_relaxed_sys(a.peers.gdone[q] + grp, j.run);
     }
-    if (j.pieces <= 1) {
+    if (!P3_EXP || j.pieces <= 1) {
       atomicAdd(L.bytes + 0, (j.bf16 || j.pb16 ? 2ull : 4ull) * j.len * (j.n - 1));  // pushes received
       atomicAdd(L.bytes + 1, (j.pb16 ? 2ull : 4ull) * j.len * (j.n - 1));  // broadcasts sent
     }
@@ -1818,7 +1818,7 @@ __global__ void __launch_bounds__(P3_COMM_MAX_THREADS, 1) k_comm(const __grid_co
       // progress, like the reference's server and sender threads: `push_split` > 0 makes
       // every push_split-th CTA look for pushes first, the others for server work first.
       const bool push_first = a.push_split && (blockIdx.x % a.push_split) == a.push_split - 1;
-      if (!ONE && a.lazy_pick && pops_done) {
+      if (!ONE && P3_EXP && a.lazy_pick && pops_done) {
         // late binding: a job picked now would wait behind the one moving; with no pushes left,
         // leave it to an idle CTA unless this one's movers are done too
         const uint32_t pb = (b + P3_SLOTS - 1) % P3_SLOTS;
@@ -1841,7 +1841,7 @@ __global__ void __launch_bounds__(P3_COMM_MAX_THREADS, 1) k_comm(const __grid_co
             g = warp_answer_pick(a, a.loc[li], &pp.layer, &ans_q);
             if (g != P3_NONE) kind = JOB_ANSWER;
           }
-          for (uint32_t t = 0; t < a.n_local && kind == JOB_NONE && a.notify == 2; ++t) {
+          for (uint32_t t = 0; t < a.n_local && kind == JOB_NONE && P3_EXP && a.notify == 2; ++t) {
             li = (blockIdx.x + t) % a.n_local;
             g = warp_take_notify(a, a.loc[li], &pp.layer);
             if (g != P3_NONE) kind = JOB_FETCH;
@@ -1857,7 +1857,7 @@ __global__ void __launch_bounds__(P3_COMM_MAX_THREADS, 1) k_comm(const __grid_co
           // complete (and their reductions start) early instead of every CTA's pushes sharing
           // the link at once
           bool capped = false;
-          if (a.push_cap && (stash.n || (!pops_done && !reserved))) {
+          if (P3_EXP && a.push_cap && (stash.n || (!pops_done && !reserved))) {
             uint32_t ok = 0;
             if (lane == 0) {
               ok = atomicAdd(&a.loc[0].it->push_live, 1u) < a.push_cap;
@@ -1931,7 +1931,7 @@ __global__ void __launch_bounds__(P3_COMM_MAX_THREADS, 1) k_comm(const __grid_co
               if (!ONE && a.notify == 1)  // every NOTIFY pulled, every PULL of an owned slice answered
                 fin = fin && ld_relaxed_gpu(L.pcount) >= a.plan.total_slices - own &&
                       ld_relaxed_gpu(L.pcount + 1) >= own * (a.plan.world - 1);
-              if (!ONE && a.notify == 2)  // every other owner's slice fetched
+              if (!ONE && P3_EXP && a.notify == 2)  // every other owner's slice fetched
                 fin = fin && ld_relaxed_gpu(L.pcount + 1) >= a.plan.total_slices - own;
             }
             verdict = (fin || ld_relaxed_gpu(a.err) != 0) ? 1u : (globaltimer() - t0 > a.timeout_ns ? 2u : 0u);
@@ -2142,9 +2142,10 @@ __global__ void __launch_bounds__(P3_COMM_MAX_THREADS, 1) k_comm(const __grid_co
     }
   } else {
     // consumers: compute each stage from shared memory, release it, report finished jobs.
-    // A stage that leaves by TMA bulk store is released by the first consumer warp only once
-    // the engine has read it — deferred to the next bulk stage (wait for all groups but the
-    // newest), so the next tile computes while the store drains.
+    // A stage that leaves by TMA bulk store is released once the engine has read it; with
+    // P3_EXP the first consumer warp defers that wait to the next bulk stage (all groups but
+    // the newest), so the next tile computes while the store drains (measured: helps only the
+    // TMA-stored reduce variants, ~1% slower in the default configuration).
     const uint32_t tid = threadIdx.x - 96;
     const bool w0 = warp == 3;  // the first consumer warp (tid 0 issues the bulk stores)
     uint32_t pend = P3_NONE;    // (w0) stage whose release waits for its bulk store's read
@@ -2201,10 +2202,11 @@ __global__ void __launch_bounds__(P3_COMM_MAX_THREADS, 1) k_comm(const __grid_co
         consume_tile<ONE>(a, j, d, stage_mem + (size_t)sidx * P3_STAGE_BYTES, tid, ncons);
       }
       const bool last = (d.flags & ST_LAST) != 0;
+      if (!P3_EXP && bulk && !last && tid == 0) tma_store_wait_read();  // (default: release at once)
       if (last && tid == 0 && (a.tma_store || a.tma_store_red))
         tma_store_wait_all();  // every bulk store of the job complete before its signal
       __syncwarp();
-      if (w0 && bulk && !last) {  // release the previous deferred stage, defer this one
+      if (P3_EXP && w0 && bulk && !last) {  // release the previous deferred stage, defer this one
         if (pend != P3_NONE) {
           if (lane == 0) tma_store_wait_read_all_but_one();
           __syncwarp();
