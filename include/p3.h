@@ -220,8 +220,9 @@ typedef struct p3_config {
   float lr;                            /* RunConfig.lr (cli.py:69) */
   float momentum;                      /* 0 == the reference's plain SGD */
   uint32_t comm_ctas;                  /* CTAs of each DRAIN launch of the comm kernel */
-  uint32_t comm_threads;               /* threads per comm CTA (multiple of 32 in [128, 512]:
-                                          scheduler, signaler, TMA producer, consumers) */
+  uint32_t comm_threads;               /* threads per comm CTA (multiple of 32 in [128, 512],
+                                          [160, 512] when world > 1: scheduler, signaler(s),
+                                          TMA producer, consumers) */
   double timeout_s;                    /* device spin deadline (deadlock_timeout) */
   uint32_t trace_cap;                  /* trace records per local rank (0 = off) */
   uint32_t emulate_grads;              /* allocate a gradient arena for gradgen mode */

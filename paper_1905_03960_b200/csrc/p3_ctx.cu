@@ -114,7 +114,7 @@ struct p3_ctx {
   // P3_TRACE_CTA=1 (trace records carry CTA indices; CTA start / exit records)
   struct {
     uint32_t use_tma = 1, push_split = 0, srv_filter = 0, trace_cta = 0, srv_reserve = 0, tma_store = 1, tma_store_red = 0, pop_relax = 0,
-             push_max = 2, stream = 1, push_cap = 0, bcast_pull = 0, lazy_pick = 0, srv_piece = 0;
+             push_max = 2, stream = 1, push_cap = 0, bcast_pull = 0, lazy_pick = 0, srv_piece = 0, push_ctas = 0;
   } knobs;
   std::vector<uint32_t> own_total;
   std::vector<uint64_t> own_stride;
@@ -298,9 +298,12 @@ int p3_ctx_create(const p3_config_t* cfg, p3_ctx_t** out) {
   if (cfg->n_layers < 1 || !cfg->layer_counts) return fail(nullptr, P3_EUSAGE, "profile needs at least one layer");
   if (cfg->plan_mode != P3_PLAN_P3 && cfg->plan_mode != P3_PLAN_BASELINE) return fail(nullptr, P3_EUSAGE, "bad plan_mode");
   if (cfg->throttle_bps < 0) return fail(nullptr, P3_EUSAGE, "throttle rate must be >= 0 (0 disables shaping)");
-  if (cfg->comm_threads < 128 || cfg->comm_threads > P3_COMM_MAX_THREADS || cfg->comm_threads % 32)
+  // scheduler + signaler(s) + producer + at least one consumer warp (N > 1: P3_NSIG signalers)
+  const uint32_t min_thr = 32u * (3u + (cfg->world > 1 ? (uint32_t)P3_NSIG : 1u));
+  if (cfg->comm_threads < min_thr || cfg->comm_threads > P3_COMM_MAX_THREADS || cfg->comm_threads % 32)
     return fail(nullptr, P3_EUSAGE,
-                "comm_threads must be a multiple of 32 in [128, " + std::to_string(P3_COMM_MAX_THREADS) + "] (scheduler + signaler + producer + consumer warps)");
+                "comm_threads must be a multiple of 32 in [" + std::to_string(min_thr) + ", " +
+                    std::to_string(P3_COMM_MAX_THREADS) + "] (scheduler + signalers + producer + consumer warps)");
   if (cfg->comm_ctas < 1) return fail(nullptr, P3_EUSAGE, "comm_ctas must be >= 1");
   if (cfg->param_bf16 && (cfg->push_bf16 || cfg->emulate_grads))
     return fail(nullptr, P3_EUSAGE, "param_bf16 takes bf16 gradients from the model (no push_bf16, no emulate_grads)");
@@ -338,8 +341,9 @@ int p3_ctx_create(const p3_config_t* cfg, p3_ctx_t** out) {
       c->knobs.bcast_pull = env_u32("P3_BCAST_PULL", 0);
       c->knobs.lazy_pick = env_u32("P3_LAZY_PICK", 0);
       c->knobs.srv_piece = env_u32("P3_SRV_PIECE", 0) & ~7u;
+      c->knobs.push_ctas = env_u32("P3_PUSH_CTAS", 0);
     } else {
-      for (const char* k : {"P3_PUSH_CAP", "P3_BCAST_PULL", "P3_LAZY_PICK", "P3_SRV_PIECE"})
+      for (const char* k : {"P3_PUSH_CAP", "P3_BCAST_PULL", "P3_LAZY_PICK", "P3_SRV_PIECE", "P3_PUSH_CTAS"})
         if (getenv(k)) fprintf(stderr, "p3: %s ignored (experiment switch; build with -DP3_EXP=1)\n", k);
     }
     c->knobs.stream = env_u32("P3_STREAM", 1);  // single rank: streaming FINISH (0: slice pops)
@@ -713,6 +717,7 @@ static CommArgs comm_args(p3_ctx* c, uint32_t mode, uint32_t ctas) {
   a.push_cap = c->knobs.push_cap;
   a.lazy_pick = c->knobs.lazy_pick;
   a.srv_piece = c->knobs.srv_piece;
+  a.push_ctas = c->knobs.push_ctas;
   // bounded relaxation of the pop order: a pop takes one of the C most urgent slices, C =
   // the launch's concurrent consumers (its CTAs) unless configured lower
   // (measured, tools/sync_sweep.py, ResNet-50 N=1 sync-only: C=8 2.2 TB/s, C=148 3.4 TB/s —

@@ -11,6 +11,10 @@
 // P3_EXP=1 compiles the comm-kernel experiment switches in (P3_PUSH_CAP, P3_LAZY_PICK,
 // P3_SRV_PIECE, P3_BCAST_PULL; measured slower or neutral, profiles/r02_summary.md §7);
 // the default build leaves them out so they cost the scheduler nothing.
+// Signaler warps of the N > 1 comm kernel (1, or one per job slot).
+#ifndef P3_NSIG
+#define P3_NSIG 2
+#endif
 #ifndef P3_EXP
 #define P3_EXP 0
 #endif
@@ -160,7 +164,8 @@ struct CommArgs {
   uint32_t push_cap;
   uint32_t srv_piece;  // >0: a completed owned slice is reduced in pieces of this many elements
                        // (multiple of 8), each claimed by whichever CTA is free
-  uint32_t lazy_pick;  // FINISH, N > 1: once every local slice is claimed, pick the next job only
+  uint32_t lazy_pick;
+  uint32_t push_ctas;  // FINISH, N > 1: CTAs [0, push_ctas) only push, the others only reduce  // FINISH, N > 1: once every local slice is claimed, pick the next job only
                        // when the CTA's movers are idle (no job bound to a busy CTA)  // >0: at most this many remote pushes of a rank in flight (pops wait)
   uint32_t push_max;  // FINISH: 1 = a CTA keeps at most one push in flight (the other slot for reduces)
   uint32_t use_tma;   // movers stage sources through shared memory with TMA (else direct loads)

@@ -1524,7 +1524,6 @@ __device__ P3_COLD void signal_job(const CommArgs& a, const Job& j) {
     const uint32_t old = atom_add_relaxed_sys(a.peers.arrivals[j.rank] + j.opos, 1u);
     P3_CHECK(old >= a.k * P.world && old < (a.k + 1) * P.world);  // one push per rank and slice
     red_add_relaxed_sys(a.peers.tally[j.rank], 1u);
-    if (P3_EXP && a.push_cap) atomicSub(&a.loc[0].it->push_live, 1u);
     if (old + 1 == (a.k + 1) * P.world) {
       red_add_relaxed_sys(a.peers.hint[j.rank] + j.layer, 1u);
       red_add_relaxed_sys(a.peers.tally[j.rank] + 1, 1u);
@@ -1753,7 +1752,13 @@ __global__ void __launch_bounds__(P3_COMM_MAX_THREADS, 1) k_comm(const __grid_co
   extern __shared__ __align__(128) uint8_t stage_mem[];  // P3_STAGES x P3_STAGE_BYTES
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t nthr = blockDim.x;
-  const uint32_t ncons = nthr - 96;  // consumer threads (warps 3..)
+  // NSIG signaler warps: with one per job slot, slot b's jobs are signalled by their own warp
+  // (1, then 3, 4, ...), so a slow system-scope release of one job does not hold back the next
+  // job's slot (measured at N=2: ResNet-50 sync -8%)
+  constexpr uint32_t NSIG = ONE ? 1u : P3_NSIG;
+  static_assert(NSIG == 1 || NSIG == P3_SLOTS, "signalers: one, or one per job slot");
+  const uint32_t cw = 2 + NSIG;          // first consumer warp
+  const uint32_t ncons = nthr - 32 * cw;  // consumer threads
   IterState* stats = a.loc[0].it;
   if (threadIdx.x == 0) {
     for (uint32_t i = 0; i < P3_STAGES; ++i) {
@@ -1818,6 +1823,9 @@ __global__ void __launch_bounds__(P3_COMM_MAX_THREADS, 1) k_comm(const __grid_co
       // progress, like the reference's server and sender threads: `push_split` > 0 makes
       // every push_split-th CTA look for pushes first, the others for server work first.
       const bool push_first = a.push_split && (blockIdx.x % a.push_split) == a.push_split - 1;
+      // push_ctas: split roles (FINISH) — the first push_ctas CTAs only push, the rest only reduce
+      const bool split = P3_EXP && a.push_ctas && a.mode == P3_COMM_FINISH;
+      const bool push_only = split && blockIdx.x < a.push_ctas, srv_only = split && blockIdx.x >= a.push_ctas;
       if (!ONE && P3_EXP && a.lazy_pick && pops_done) {
         // late binding: a job picked now would wait behind the one moving; with no pushes left,
         // leave it to an idle CTA unless this one's movers are done too
@@ -1831,7 +1839,7 @@ __global__ void __launch_bounds__(P3_COMM_MAX_THREADS, 1) k_comm(const __grid_co
       bool pulled = false, was_capped = false, token = false;
       for (uint32_t round = 0; round < 2 && kind == JOB_NONE && !ONE && a.plan.world > 1; ++round) {
         if ((round == 0) != push_first) {
-          for (uint32_t t = 0; t < a.n_local && kind == JOB_NONE; ++t) {
+          for (uint32_t t = 0; t < a.n_local && kind == JOB_NONE && !push_only; ++t) {
             li = (blockIdx.x + t) % a.n_local;
             g = warp_server_pick(a, a.loc[li], &pp.layer, phase, &pp.piece);
             if (g != P3_NONE) kind = JOB_REDUCE;
@@ -1849,7 +1857,7 @@ __global__ void __launch_bounds__(P3_COMM_MAX_THREADS, 1) k_comm(const __grid_co
         } else {
           // server-reserved CTAs (srv_reserve > 0: every srv_reserve-th CTA) never take pushes,
           // so a completed slice is reduced while the other CTAs' pipelines hold pushes
-          const bool reserved = (a.srv_reserve && (blockIdx.x % a.srv_reserve) == 0) ||
+          const bool reserved = srv_only || (a.srv_reserve && (blockIdx.x % a.srv_reserve) == 0) ||
                                 (a.push_max == 1 && a.mode == P3_COMM_FINISH && last_push && backoff < 512u &&
                                  pending[(b + P3_SLOTS - 1) % P3_SLOTS]);  // (an idle scheduler pushes anyway)
           // push_cap: a pop takes one of push_cap tokens of the rank (returned by the push's
@@ -2004,7 +2012,15 @@ __global__ void __launch_bounds__(P3_COMM_MAX_THREADS, 1) k_comm(const __grid_co
       t_wait += stat_clock() - tw;
       __syncwarp();
       bar_arrive(BAR_FULL(b), 96);  // producer + signaler wait on it
-      if (kind == JOB_EXIT) break;
+      if (kind == JOB_EXIT) {
+        for (uint32_t i = 1; NSIG > 1 && i < P3_SLOTS; ++i) {  // every slot's signaler leaves
+          const uint32_t bi = (b + i) % P3_SLOTS;  // (empty: synced above)
+          if (lane == 0) slots[bi].kind = JOB_EXIT;
+          __syncwarp();
+          bar_arrive(BAR_FULL(bi), 96);
+        }
+        break;
+      }
       pending[b] = true;
       last_push = kind == JOB_PUSH || kind == JOB_ANSWER || kind == JOB_FETCH;
       b = (b + 1) % P3_SLOTS;
@@ -2017,10 +2033,10 @@ __global__ void __launch_bounds__(P3_COMM_MAX_THREADS, 1) k_comm(const __grid_co
     }
     if (phase) *(volatile uint32_t*)phase = (a.k << 24) | (5u << 20);
     if (a.trace_cta && lane == 0) trace_append(a.loc[0], a.k, 0, 0, blockIdx.x, 17);  // diagnostics: scheduler exit
-  } else if (warp == 1) {
+  } else if (warp == 1 || (warp >= 3 && warp < 2 + NSIG)) {
     // signaler: in job order, once the consumers are done with a job, fence and publish
     uint64_t t_sig = 0;
-    for (uint32_t b = 0;; b = (b + 1) % P3_SLOTS) {
+    for (uint32_t b = warp == 1 ? 0u : warp - 2;; b = (b + NSIG) % P3_SLOTS) {
       bar_sync(BAR_FULL(b), 96);
       const Job& j = slots[b];
       if (j.kind == JOB_EXIT) break;
@@ -2040,6 +2056,9 @@ __global__ void __launch_bounds__(P3_COMM_MAX_THREADS, 1) k_comm(const __grid_co
       mine.answer = j.answer;
       mine.pb16 = j.pb16;
       mine.pieces = j.pieces;
+      // push_cap: the token goes back once the data has moved (before the signal's fence)
+      if (P3_EXP && a.push_cap && lane == 0 && mine.kind == JOB_PUSH && !mine.answer)
+        atomicSub(&a.loc[0].it->push_live, 1u);
       __syncwarp();
       bar_arrive(BAR_EMPTY(b), 64);
       if (lane == 0) {
@@ -2138,7 +2157,10 @@ __global__ void __launch_bounds__(P3_COMM_MAX_THREADS, 1) k_comm(const __grid_co
         }
       }
       __syncwarp();
-      if (j.kind == JOB_EXIT) break;
+      if (j.kind == JOB_EXIT) {
+        for (uint32_t i = 1; NSIG > 1 && i < P3_SLOTS; ++i) bar_sync(BAR_FULL((b + i) % P3_SLOTS), 96);
+        break;
+      }
     }
   } else {
     // consumers: compute each stage from shared memory, release it, report finished jobs.
@@ -2146,15 +2168,37 @@ __global__ void __launch_bounds__(P3_COMM_MAX_THREADS, 1) k_comm(const __grid_co
     // P3_EXP the first consumer warp defers that wait to the next bulk stage (all groups but
     // the newest), so the next tile computes while the store drains (measured: helps only the
     // TMA-stored reduce variants, ~1% slower in the default configuration).
-    const uint32_t tid = threadIdx.x - 96;
-    const bool w0 = warp == 3;  // the first consumer warp (tid 0 issues the bulk stores)
+    const uint32_t tid = threadIdx.x - 32 * cw;
+    const bool w0 = warp == cw;  // the first consumer warp (tid 0 issues the bulk stores)
     uint32_t pend = P3_NONE;    // (w0) stage whose release waits for its bulk store's read
+    // (P3_EXP, w0) job slot of a push whose completion wait — and w0's DONE arrival — moved to
+    // w0's next stage, so the next job's stores start while this one's drain
+    uint32_t done_pend = P3_NONE;
     uint64_t t_move = 0;
     for (uint32_t it = 0;; ++it) {
       const uint32_t sidx = it % P3_STAGES;
+      if (P3_EXP && w0 && done_pend != P3_NONE) {
+        // no next stage soon (e.g. the scheduler waits for work that this push's signal
+        // unblocks): complete the push now
+        const uint64_t tw = globaltimer();
+        bool ready = false;
+        while (!(ready = mbar_try_wait(&full_bar[sidx], (it / P3_STAGES) & 1u)) && globaltimer() - tw < 2000) {
+        }
+        if (!ready) {
+          if (lane == 0) tma_store_wait_all();
+          __syncwarp();
+          bar_arrive(BAR_DONE(done_pend), ncons + 32);
+          done_pend = P3_NONE;
+        }
+      }
       mbar_wait_bounded(&full_bar[sidx], (it / P3_STAGES) & 1u, a);
       const StageDesc d = sdesc[sidx];
       if (d.flags & ST_EXIT) {
+        if (P3_EXP && w0 && done_pend != P3_NONE) {
+          if (lane == 0) tma_store_wait_all();
+          __syncwarp();
+          bar_arrive(BAR_DONE(done_pend), ncons + 32);
+        }
         if (w0 && pend != P3_NONE) {
           if (lane == 0) tma_store_wait_read();
           __syncwarp();
@@ -2202,10 +2246,22 @@ __global__ void __launch_bounds__(P3_COMM_MAX_THREADS, 1) k_comm(const __grid_co
         consume_tile<ONE>(a, j, d, stage_mem + (size_t)sidx * P3_STAGE_BYTES, tid, ncons);
       }
       const bool last = (d.flags & ST_LAST) != 0;
+      const bool defer_done = P3_EXP && last && bulk_push;
       if (!P3_EXP && bulk && !last && tid == 0) tma_store_wait_read();  // (default: release at once)
-      if (last && tid == 0 && (a.tma_store || a.tma_store_red))
-        tma_store_wait_all();  // every bulk store of the job complete before its signal
+      if (last && tid == 0 && (a.tma_store || a.tma_store_red)) {
+        if (defer_done) tma_store_wait_read();  // (completion: at w0's next stage)
+        else tma_store_wait_all();  // every bulk store of the job complete before its signal
+      }
       __syncwarp();
+      if (P3_EXP && w0 && done_pend != P3_NONE) {  // the previous push: complete, then DONE
+        if (lane == 0) {
+          if (bulk) asm volatile("cp.async.bulk.wait_group 1;" ::: "memory");  // all but this stage's
+          else tma_store_wait_all();
+        }
+        __syncwarp();
+        bar_arrive(BAR_DONE(done_pend), ncons + 32);
+        done_pend = P3_NONE;
+      }
       if (P3_EXP && w0 && bulk && !last) {  // release the previous deferred stage, defer this one
         if (pend != P3_NONE) {
           if (lane == 0) tma_store_wait_read_all_but_one();
@@ -2223,7 +2279,10 @@ __global__ void __launch_bounds__(P3_COMM_MAX_THREADS, 1) k_comm(const __grid_co
         if (lane == 0) mbar_arrive(&empty_bar[sidx]);
       }
       if (tid == 0) t_move += stat_clock() - tm;
-      if (d.flags & ST_LAST) bar_arrive(BAR_DONE(d.b), ncons + 32);
+      if (d.flags & ST_LAST) {
+        if (P3_EXP && w0 && defer_done) done_pend = d.b;
+        else bar_arrive(BAR_DONE(d.b), ncons + 32);
+      }
     }
     if (tid == 0) atomicAdd(&stats->t_move, (unsigned long long)t_move);
   }

@@ -115,5 +115,51 @@ int main() {
       }
     }
   }
+  // bidirectional: both GPUs push to each other at the same time (the N=2 exchange pattern)
+  {
+    uint8_t *loc1, *rem0;  // device 1's source, device 0's receive buffer
+    CK(cudaSetDevice(1));
+    CK(cudaDeviceEnablePeerAccess(0, 0));
+    CK(cudaMalloc(&loc1, bytes));
+    CK(cudaMemset(loc1, 2, bytes));
+    CK(cudaFuncSetAttribute(k_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    cudaEvent_t f0, f1;
+    CK(cudaEventCreate(&f0));
+    CK(cudaEventCreate(&f1));
+    CK(cudaSetDevice(0));
+    CK(cudaMalloc(&rem0, bytes));
+    for (int method = 0; method < 2; ++method)
+      for (int ctas : {32, 64, 148}) {
+        float best0 = 1e30f, best1 = 1e30f;
+        for (int rep = 0; rep < 4; ++rep) {
+          CK(cudaSetDevice(0));
+          CK(cudaDeviceSynchronize());
+          CK(cudaSetDevice(1));
+          CK(cudaDeviceSynchronize());
+          for (int dev = 0; dev < 2; ++dev) {
+            CK(cudaSetDevice(dev));
+            const uint8_t* src = dev == 0 ? loc : loc1;
+            uint8_t* dst = dev == 0 ? rem : rem0;
+            CK(cudaEventRecord(dev == 0 ? e0 : f0));
+            if (method == 0)
+              k_st<<<ctas, 512>>>((const float4*)src, (float4*)dst, bytes / 16);
+            else
+              k_bulk<<<ctas, 32, 65536 * 3>>>(src, dst, bytes, 65536, 3);
+            CK(cudaEventRecord(dev == 0 ? e1 : f1));
+          }
+          float m0, m1;
+          CK(cudaSetDevice(0));
+          CK(cudaEventSynchronize(e1));
+          CK(cudaEventElapsedTime(&m0, e0, e1));
+          CK(cudaSetDevice(1));
+          CK(cudaEventSynchronize(f1));
+          CK(cudaEventElapsedTime(&m1, f0, f1));
+          CK(cudaGetLastError());
+          if (rep) { best0 = std::min(best0, m0); best1 = std::min(best1, m1); }
+        }
+        printf("P2P {\"method\": \"bidir_%s\", \"ctas\": %d, \"chunk\": 65536, \"stages\": 3, \"MB\": %.0f, \"GBps\": %.1f, \"GBps_dev1\": %.1f, \"GBps_per_cta\": %.2f}\n",
+               method == 0 ? "st" : "bulk", ctas, bytes / 1e6, bytes / best0 / 1e6, bytes / best1 / 1e6, bytes / best0 / 1e6 / ctas);
+      }
+  }
   return 0;
 }
