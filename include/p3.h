@@ -270,6 +270,14 @@ typedef struct p3_config {
                                           path) and broadcasts bf16(master), round to nearest
                                           even. Call p3_master_init once the replica holds the
                                           initial parameters. */
+  uint32_t nvls;                       /* N > 1, one local rank per process, fp32 replicas, not
+                                          notify_pull: broadcasts go through an NVLS multicast
+                                          object spanning every rank's replica W (one
+                                          multimem.st per element; the NVSwitch delivers it to
+                                          all N replicas). The arena is then a VMM allocation
+                                          shared by file descriptor: bootstrap with
+                                          p3_ctx_export_fd / p3_ctx_open_peers_fd and
+                                          p3_nvls_create / _attach / _bind instead of IPC. */
 } p3_config_t;
 
 /* Builds the plan, allocates per-local-rank arenas (parameters W zero-initialised like
@@ -283,6 +291,20 @@ int p3_ctx_destroy(p3_ctx_t* ctx);
 #define P3_IPC_BYTES 64
 int p3_ctx_ipc_handle(p3_ctx_t* ctx, uint32_t local_idx, void* out);
 int p3_ctx_open_peers(p3_ctx_t* ctx, const void* handles);
+
+/* NVLS bootstrap (cfg.nvls; replaces p3_ctx_ipc_handle / p3_ctx_open_peers; the descriptors
+ * travel between processes over a Unix socket, SCM_RIGHTS):
+ *   p3_ctx_export_fd     a POSIX file descriptor of the local rank's arena (caller closes it);
+ *   p3_ctx_open_peers_fd map every other rank's arena (fds[r]; the local entry is ignored);
+ *   p3_nvls_create       one rank: create the multicast object for the replica region, fd out;
+ *   p3_nvls_attach       every rank: import it (fd >= 0; the creator passes -1) and add its GPU;
+ *   p3_nvls_bind         every rank, once all have attached: bind its replica and map the
+ *                        multicast address. */
+int p3_ctx_export_fd(p3_ctx_t* ctx, uint32_t local_idx, int* fd);
+int p3_ctx_open_peers_fd(p3_ctx_t* ctx, const int* fds);
+int p3_nvls_create(p3_ctx_t* ctx, int* fd);
+int p3_nvls_attach(p3_ctx_t* ctx, int fd);
+int p3_nvls_bind(p3_ctx_t* ctx);
 
 /* Device pointer of local rank's parameter replica and each layer's element offset in
  * it (layers are 16-byte aligned). TrainingWorker.params, worker.py:72. */

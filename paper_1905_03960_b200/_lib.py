@@ -108,6 +108,7 @@ class Config(ctypes.Structure):
         ("drain_streams", ctypes.c_uint32),
         ("notify_pull", ctypes.c_uint32),
         ("param_bf16", ctypes.c_uint32),
+        ("nvls", ctypes.c_uint32),
     ]
 
 
@@ -135,6 +136,11 @@ SIGNATURES = {
     "p3_ctx_destroy": (ctypes.c_int, [_P]),
     "p3_ctx_ipc_handle": (ctypes.c_int, [_P, _U32, _P]),
     "p3_ctx_open_peers": (ctypes.c_int, [_P, _P]),
+    "p3_ctx_export_fd": (ctypes.c_int, [_P, _U32, ctypes.POINTER(ctypes.c_int)]),
+    "p3_ctx_open_peers_fd": (ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_int)]),
+    "p3_nvls_create": (ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_int)]),
+    "p3_nvls_attach": (ctypes.c_int, [_P, ctypes.c_int]),
+    "p3_nvls_bind": (ctypes.c_int, [_P]),
     "p3_ctx_params": (ctypes.c_int, [_P, _U32, ctypes.POINTER(_P)]),
     "p3_ctx_layer_offset": (ctypes.c_int, [_P, _U32, _PU64]),
     "p3_ctx_grads": (ctypes.c_int, [_P, _U32, ctypes.POINTER(_P)]),

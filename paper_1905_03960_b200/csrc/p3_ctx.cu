@@ -24,6 +24,56 @@ void set_thread_error(const std::string& msg) { g_thread_error = msg; }
 
 // ------------------------------------------------------------ driver entry points
 
+// Virtual memory management and multicast (NVLS) entry points, resolved on first use.
+struct Vmm {
+  decltype(&cuMemCreate) create = nullptr;
+  decltype(&cuMemRelease) release = nullptr;
+  decltype(&cuMemAddressReserve) reserve = nullptr;
+  decltype(&cuMemAddressFree) addr_free = nullptr;
+  decltype(&cuMemMap) map = nullptr;
+  decltype(&cuMemUnmap) unmap = nullptr;
+  decltype(&cuMemSetAccess) set_access = nullptr;
+  decltype(&cuMemGetAllocationGranularity) alloc_gran = nullptr;
+  decltype(&cuMemExportToShareableHandle) export_h = nullptr;
+  decltype(&cuMemImportFromShareableHandle) import_h = nullptr;
+  decltype(&cuMulticastCreate) mc_create = nullptr;
+  decltype(&cuMulticastAddDevice) mc_add = nullptr;
+  decltype(&cuMulticastBindMem) mc_bind = nullptr;
+  decltype(&cuMulticastUnbind) mc_unbind = nullptr;
+  decltype(&cuMulticastGetGranularity) mc_gran = nullptr;
+  bool ok = false;
+};
+
+static Vmm& vmm() {
+  static Vmm v;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    bool ok = true;
+    auto get = [&](const char* name, void** fp) {
+      cudaDriverEntryPointQueryResult q;
+      ok &= cudaGetDriverEntryPointByVersion(name, fp, 12080, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess;
+    };
+    get("cuMemCreate", (void**)&v.create);
+    get("cuMemRelease", (void**)&v.release);
+    get("cuMemAddressReserve", (void**)&v.reserve);
+    get("cuMemAddressFree", (void**)&v.addr_free);
+    get("cuMemMap", (void**)&v.map);
+    get("cuMemUnmap", (void**)&v.unmap);
+    get("cuMemSetAccess", (void**)&v.set_access);
+    get("cuMemGetAllocationGranularity", (void**)&v.alloc_gran);
+    get("cuMemExportToShareableHandle", (void**)&v.export_h);
+    get("cuMemImportFromShareableHandle", (void**)&v.import_h);
+    get("cuMulticastCreate", (void**)&v.mc_create);
+    get("cuMulticastAddDevice", (void**)&v.mc_add);
+    get("cuMulticastBindMem", (void**)&v.mc_bind);
+    get("cuMulticastUnbind", (void**)&v.mc_unbind);
+    get("cuMulticastGetGranularity", (void**)&v.mc_gran);
+    v.ok = ok;
+  });
+  return v;
+}
+
 typedef CUresult (*PFN_wait32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
 typedef CUresult (*PFN_write32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
 typedef CUresult (*PFN_write64)(CUstream, CUdeviceptr, cuuint64_t, unsigned int);
@@ -121,6 +171,15 @@ struct p3_ctx {
   std::vector<uint64_t> bcast_in_bytes;  // per rank: broadcast payload received per iteration
   uint64_t w_elems = 0;
   int device = 0;
+  // NVLS (cfg.nvls): VMM arenas shared by fd, and the multicast object over the replicas
+  size_t alloc_gran = 0, mc_gran = 0, w_pad = 0;
+  CUmemGenericAllocationHandle arena_h = 0;
+  size_t arena_sz = 0;
+  CUmemGenericAllocationHandle peer_h[P3_MAX_RANKS]{};
+  size_t peer_sz[P3_MAX_RANKS]{};
+  CUmemGenericAllocationHandle mc_h = 0;
+  bool mc_added = false, mc_bound = false;
+  float* mcw = nullptr;
 
   void* d_plan = nullptr;
   PlanDev plan_dev{};
@@ -181,11 +240,62 @@ int cuda_fail(p3_ctx* c, cudaError_t e, const char* what) {
     if (e_ != cudaSuccess) return cuda_fail(c, e_, #call); \
   } while (0)
 
+#define CU_OK(call, what)                                                                          \
+  do {                                                                                             \
+    CUresult r_ = (call);                                                                          \
+    if (r_ != CUDA_SUCCESS) return fail(c, P3_ECUDA, std::string(what) + " failed (CUresult " + std::to_string((int)r_) + ")"); \
+  } while (0)
+
+CUmemAllocationProp vmm_prop(const p3_ctx* c) {
+  CUmemAllocationProp ap = {};
+  ap.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+  ap.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+  ap.location.id = c->device;
+  ap.requestedHandleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
+  return ap;
+}
+
+CUmemAccessDesc vmm_access(const p3_ctx* c) {
+  CUmemAccessDesc ad = {};
+  ad.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+  ad.location.id = c->device;
+  ad.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+  return ad;
+}
+
+// Map `h` (size bytes) at a fresh address aligned to the multicast granule, readable and
+// writable from this context's GPU.
+int vmm_map(p3_ctx* c, CUmemGenericAllocationHandle h, size_t size, void** out) {
+  Vmm& v = vmm();
+  CUdeviceptr va = 0;
+  CU_OK(v.reserve(&va, size, c->mc_gran, 0, 0), "cuMemAddressReserve");
+  CUresult r = v.map(va, size, 0, h, 0);
+  if (r != CUDA_SUCCESS) {
+    v.addr_free(va, size);
+    return fail(c, P3_ECUDA, "cuMemMap failed (CUresult " + std::to_string((int)r) + ")");
+  }
+  const CUmemAccessDesc ad = vmm_access(c);
+  r = v.set_access(va, size, &ad, 1);
+  if (r != CUDA_SUCCESS) {
+    v.unmap(va, size);
+    v.addr_free(va, size);
+    return fail(c, P3_ECUDA, "cuMemSetAccess failed (CUresult " + std::to_string((int)r) + ")");
+  }
+  *out = reinterpret_cast<void*>(va);
+  return P3_OK;
+}
+
+void vmm_unmap(void* va, size_t size) {
+  vmm().unmap(reinterpret_cast<CUdeviceptr>(va), size);
+  vmm().addr_free(reinterpret_cast<CUdeviceptr>(va), size);
+}
+
 PeerLayout peer_layout_of(const p3_ctx* c, uint32_t rank) {
   PeerLayout p;
   uint64_t o = 0;
   p.w = o;
-  o = align_up(o + c->w_elems * (c->cfg.param_bf16 ? 2 : 4), 256);
+  // (nvls: the replica region is bound to the multicast object in whole granules)
+  o = align_up(o + c->w_elems * (c->cfg.param_bf16 ? 2 : 4), c->cfg.nvls ? c->mc_gran : 256);
   p.r = o;
   o = align_up(o + (uint64_t)c->N * c->own_stride[rank] * 4, 256);
   p.arrivals = o;
@@ -312,6 +422,13 @@ int p3_ctx_create(const p3_config_t* cfg, p3_ctx_t** out) {
   for (uint32_t i = 0; i < cfg->n_local; ++i)
     if (cfg->local_ranks[i] >= cfg->world) return fail(nullptr, P3_EUSAGE, "local rank out of range");
   if (!driver().ok) return fail(nullptr, P3_ECUDA, "CUDA driver stream memory operations unavailable");
+  if (cfg->nvls) {
+    if (cfg->world < 2 || cfg->n_local != 1)
+      return fail(nullptr, P3_EUSAGE, "nvls needs world > 1 and one local rank per process");
+    if (cfg->notify_pull || cfg->param_bf16)
+      return fail(nullptr, P3_EUSAGE, "nvls broadcasts fp32 replicas in the P3 protocol (no notify_pull, no param_bf16)");
+    if (!vmm().ok) return fail(nullptr, P3_ECUDA, "CUDA VMM / multicast driver entry points unavailable");
+  }
   if (preload_kernels() != P3_OK) return fail(nullptr, P3_ECUDA, "loading the sm_100a kernels failed");
 
   c = new p3_ctx();
@@ -362,6 +479,27 @@ int p3_ctx_create(const p3_config_t* cfg, p3_ctx_t** out) {
   }
   c->S = (uint32_t)c->plan.size();
   cudaGetDevice(&c->device);
+  if (cfg->nvls) {  // allocation and multicast granules (the replica region is bound in whole granules)
+    int mc = 0;
+    driver().attr(&mc, CU_DEVICE_ATTRIBUTE_MULTICAST_SUPPORTED, c->device);
+    if (!mc) {
+      int r2 = fail(c, P3_EUSAGE, "nvls: this GPU does not support multicast objects (no NVSwitch / fabric manager)");
+      delete c;
+      return r2;
+    }
+    const CUmemAllocationProp ap = vmm_prop(c);
+    CUmulticastObjectProp mp = {};
+    mp.numDevices = c->N;
+    mp.size = 2ull << 20;
+    mp.handleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
+    if (vmm().alloc_gran(&c->alloc_gran, &ap, CU_MEM_ALLOC_GRANULARITY_RECOMMENDED) != CUDA_SUCCESS ||
+        vmm().mc_gran(&c->mc_gran, &mp, CU_MULTICAST_GRANULARITY_MINIMUM) != CUDA_SUCCESS) {
+      int r2 = fail(c, P3_ECUDA, "nvls: granularity query failed");
+      delete c;
+      return r2;
+    }
+    c->mc_gran = std::max(c->mc_gran, c->alloc_gran);
+  }
 
   // ---- host-side plan tables
   const uint32_t L = c->L, S = c->S, N = c->N;
@@ -501,8 +639,18 @@ int p3_ctx_create(const p3_config_t* cfg, p3_ctx_t** out) {
   for (uint32_t i = 0; i < cfg->n_local; ++i) {
     const uint32_t rank = cfg->local_ranks[i];
     const PeerLayout& pl = c->peer_layout[rank];
-    e = cudaMalloc(&c->peer_arena[i], pl.bytes);
-    if (e == cudaSuccess) e = cudaMemset(c->peer_arena[i], 0, pl.bytes);
+    if (cfg->nvls) {  // VMM allocation, shareable by file descriptor (p3_ctx_export_fd)
+      const CUmemAllocationProp ap = vmm_prop(c);
+      c->arena_sz = align_up(pl.bytes, c->mc_gran);
+      e = cudaErrorMemoryAllocation;
+      if (vmm().create(&c->arena_h, c->arena_sz, &ap, 0) == CUDA_SUCCESS &&
+          vmm_map(c, c->arena_h, c->arena_sz, &c->peer_arena[i]) == P3_OK)
+        e = cudaMemset(c->peer_arena[i], 0, c->arena_sz);
+      c->w_pad = pl.r;  // the replica region, whole multicast granules
+    } else {
+      e = cudaMalloc(&c->peer_arena[i], pl.bytes);
+      if (e == cudaSuccess) e = cudaMemset(c->peer_arena[i], 0, pl.bytes);
+    }
     const uint64_t v_elems = cfg->momentum != 0.f ? c->own_stride[rank] : 0;
     const uint64_t m_elems = cfg->param_bf16 ? c->own_stride[rank] : 0;
     LocalLayout ll = local_layout_of(c, v_elems, m_elems);
@@ -592,6 +740,23 @@ int p3_ctx_create(const p3_config_t* cfg, p3_ctx_t** out) {
 int p3_ctx_destroy(p3_ctx_t* c) {
   if (!c) return P3_OK;
   cudaDeviceSynchronize();
+  if (c->cfg.nvls) {  // multicast mapping and binding, peers' and the own VMM arena
+    Vmm& v = vmm();
+    if (c->mcw) vmm_unmap(c->mcw, c->w_pad);
+    if (c->mc_bound) v.mc_unbind(c->mc_h, (CUdevice)c->device, 0, c->w_pad);
+    if (c->mc_h) v.release(c->mc_h);
+    for (uint32_t r = 0; r < P3_MAX_RANKS; ++r)
+      if (c->peer_h[r]) {
+        if (c->opened[r]) vmm_unmap(c->opened[r], c->peer_sz[r]);
+        v.release(c->peer_h[r]);
+        c->opened[r] = nullptr;
+      }
+    if (c->arena_h) {
+      if (c->peer_arena[0]) vmm_unmap(c->peer_arena[0], c->arena_sz);
+      v.release(c->arena_h);
+      c->peer_arena[0] = nullptr;
+    }
+  }
   for (uint32_t r = 0; r < P3_MAX_RANKS; ++r)
     if (c->opened[r]) cudaIpcCloseMemHandle(c->opened[r]);
   for (uint32_t i = 0; i < P3_MAX_LOCAL; ++i) {
@@ -642,6 +807,79 @@ int p3_ctx_open_peers(p3_ctx_t* c, const void* handles) {
     c->opened[r] = p;
     set_peer_pointers(c, r, static_cast<char*>(p));
   }
+  return P3_OK;
+}
+
+int p3_ctx_export_fd(p3_ctx_t* c, uint32_t li, int* fd) {
+  int rc = check_local(c, li);
+  if (rc) return rc;
+  if (!c->cfg.nvls || !fd) return fail(c, P3_EUSAGE, "p3_ctx_export_fd needs an nvls context and an output");
+  int f = -1;
+  CU_OK(vmm().export_h(&f, c->arena_h, CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR, 0), "cuMemExportToShareableHandle");
+  *fd = f;
+  return P3_OK;
+}
+
+int p3_ctx_open_peers_fd(p3_ctx_t* c, const int* fds) {
+  if (!c || !fds) return fail(c, P3_EUSAGE, "null argument");
+  if (!c->cfg.nvls) return fail(c, P3_EUSAGE, "p3_ctx_open_peers_fd needs an nvls context (else p3_ctx_open_peers)");
+  const uint32_t me = c->cfg.local_ranks[0];
+  for (uint32_t r = 0; r < c->N; ++r) {
+    if (r == me || c->opened[r]) continue;
+    CUmemGenericAllocationHandle h = 0;
+    CU_OK(vmm().import_h(&h, reinterpret_cast<void*>((intptr_t)fds[r]), CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR),
+          "cuMemImportFromShareableHandle");
+    const size_t sz = align_up(c->peer_layout[r].bytes, c->mc_gran);
+    void* va = nullptr;
+    int rc = vmm_map(c, h, sz, &va);
+    if (rc) {
+      vmm().release(h);
+      return rc;
+    }
+    c->peer_h[r] = h;
+    c->peer_sz[r] = sz;
+    c->opened[r] = va;
+    set_peer_pointers(c, r, static_cast<char*>(va));
+  }
+  return P3_OK;
+}
+
+int p3_nvls_create(p3_ctx_t* c, int* fd) {
+  if (!c || !fd) return fail(c, P3_EUSAGE, "null argument");
+  if (!c->cfg.nvls || c->mc_h) return fail(c, P3_EUSAGE, "p3_nvls_create: not an nvls context, or it already has a multicast object");
+  CUmulticastObjectProp mp = {};
+  mp.numDevices = c->N;
+  mp.size = c->w_pad;
+  mp.handleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
+  CU_OK(vmm().mc_create(&c->mc_h, &mp), "cuMulticastCreate");
+  int f = -1;
+  CU_OK(vmm().export_h(&f, c->mc_h, CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR, 0), "cuMemExportToShareableHandle (multicast)");
+  *fd = f;
+  return P3_OK;
+}
+
+int p3_nvls_attach(p3_ctx_t* c, int fd) {
+  if (!c || !c->cfg.nvls) return fail(c, P3_EUSAGE, "p3_nvls_attach needs an nvls context");
+  if (fd >= 0) {
+    if (c->mc_h) return fail(c, P3_EUSAGE, "p3_nvls_attach: the creator passes -1");
+    CU_OK(vmm().import_h(&c->mc_h, reinterpret_cast<void*>((intptr_t)fd), CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR),
+          "cuMemImportFromShareableHandle (multicast)");
+  }
+  if (!c->mc_h) return fail(c, P3_EUSAGE, "p3_nvls_attach: no multicast object (p3_nvls_create on one rank, its fd on the others)");
+  if (!c->mc_added) CU_OK(vmm().mc_add(c->mc_h, (CUdevice)c->device), "cuMulticastAddDevice");
+  c->mc_added = true;
+  return P3_OK;
+}
+
+int p3_nvls_bind(p3_ctx_t* c) {
+  if (!c || !c->cfg.nvls || !c->mc_added) return fail(c, P3_EUSAGE, "p3_nvls_bind: attach first (every rank)");
+  if (c->mcw) return P3_OK;
+  CU_OK(vmm().mc_bind(c->mc_h, 0, c->arena_h, 0, c->w_pad, 0), "cuMulticastBindMem");
+  c->mc_bound = true;
+  void* va = nullptr;
+  int rc = vmm_map(c, c->mc_h, c->w_pad, &va);
+  if (rc) return rc;
+  c->mcw = static_cast<float*>(va);
   return P3_OK;
 }
 
@@ -712,12 +950,13 @@ static CommArgs comm_args(p3_ctx* c, uint32_t mode, uint32_t ctas) {
   a.use_tma = c->knobs.use_tma;
   a.srv_reserve = c->knobs.srv_reserve;
   a.tma_store = c->knobs.tma_store;
-  a.tma_store_red = c->knobs.tma_store_red;
+  a.tma_store_red = c->mcw ? 0u : c->knobs.tma_store_red;  // (nvls: replicas by multimem.st)
   a.push_max = c->knobs.push_max;
   a.push_cap = c->knobs.push_cap;
   a.lazy_pick = c->knobs.lazy_pick;
   a.srv_piece = c->knobs.srv_piece;
   a.push_ctas = c->knobs.push_ctas;
+  a.mcw = c->mcw;
   // bounded relaxation of the pop order: a pop takes one of the C most urgent slices, C =
   // the launch's concurrent consumers (its CTAs) unless configured lower
   // (measured, tools/sync_sweep.py, ResNet-50 N=1 sync-only: C=8 2.2 TB/s, C=148 3.4 TB/s —
@@ -769,6 +1008,7 @@ int p3_iteration_begin(p3_ctx_t* c, uint64_t k, void* stream) {
   if (c->iter_open) return fail(c, P3_EUSAGE, "previous iteration not ended (p3_iteration_end)");
   for (uint32_t r = 0; r < c->N; ++r)
     if (!c->peers.W[r]) return fail(c, P3_EUSAGE, "peer arenas not opened (call p3_ctx_open_peers)");
+  if (c->cfg.nvls && !c->mcw) return fail(c, P3_EUSAGE, "nvls multicast not bound (p3_nvls_attach + p3_nvls_bind)");
   cudaStream_t s = (cudaStream_t)stream;
   const LocalLayout& ll = c->local_layout;
   for (uint32_t i = 0; i < c->cfg.n_local; ++i) {

@@ -165,7 +165,8 @@ struct CommArgs {
   uint32_t srv_piece;  // >0: a completed owned slice is reduced in pieces of this many elements
                        // (multiple of 8), each claimed by whichever CTA is free
   uint32_t lazy_pick;
-  uint32_t push_ctas;  // FINISH, N > 1: CTAs [0, push_ctas) only push, the others only reduce  // FINISH, N > 1: once every local slice is claimed, pick the next job only
+  uint32_t push_ctas;
+  float* mcw;  // nvls: multicast address of the replica region (every rank's W); null = unicast  // FINISH, N > 1: CTAs [0, push_ctas) only push, the others only reduce  // FINISH, N > 1: once every local slice is claimed, pick the next job only
                        // when the CTA's movers are idle (no job bound to a busy CTA)  // >0: at most this many remote pushes of a rank in flight (pops wait)
   uint32_t push_max;  // FINISH: 1 = a CTA keeps at most one push in flight (the other slot for reduces)
   uint32_t use_tma;   // movers stage sources through shared memory with TMA (else direct loads)

@@ -916,6 +916,8 @@ struct Job {
   float* m;         // REDUCE, param_bf16: the owner's fp32 master of the slice
   uint32_t answer;  // PUSH-shaped copy of an updated slice to a peer that pulled it (notify mode)
   uint32_t pieces;  // REDUCE: pieces the slice is reduced in (srv_piece; 1 = whole)
+  uint32_t mc;      // REDUCE, nvls: dst[0] is the multicast address of every replica (multimem.st),
+                    // m the owner's own replica (the master p read back)
   uint32_t bf16;  // pushes travel as bf16 (declared lossy mode); own = index of the fp32 source
   const float* src[P3_MAX_RANKS];  // PUSH: src[0]; REDUCE: contributions in rank order
   float* dst[P3_MAX_RANKS];        // PUSH: dst[0]; REDUCE: replicas, dst[0] = owner's master
@@ -1152,6 +1154,17 @@ __device__ void prepare_reduce(const CommArgs& a, uint32_t li, uint32_t g, uint3
     job->bf16 = a.push_bf16 ? 1u + o : 0u;  // 1 + index of the owner's own (fp32) contribution
     job->aligned = ((al | (uintptr_t)v | (uintptr_t)m) & 15) == 0;
   }
+  __syncwarp();
+  if (q == 0) {
+    // nvls: one multicast store per element reaches every replica (the NVSwitch fans it out);
+    // the master p is read from the owner's own replica
+    job->mc = a.mcw && N > 1 ? 1u : 0u;
+    if (job->mc) {
+      job->ndst = 1;
+      job->m = a.peers.W[o] + woff;
+      job->dst[0] = a.mcw + woff;
+    }
+  }
 }
 
 // bf16 transport (declared lossy mode): each rank's contribution is rounded to bf16 (round
@@ -1286,8 +1299,23 @@ __device__ void move_range(const CommArgs& a, const Job& j, uint32_t e0, uint32_
                          : j.src[tid] + e0;
     ptrs->dst[tid] = j.dst[tid] + e0;
   }
+  if (j.mc && tid == 0) ptrs->dst[0] = j.m + e0;  // nvls: update the own replica, multicast below
   bar_sync(BAR_RANGE, nthr);
   float* v = j.v ? j.v + e0 : nullptr;
+  if (j.mc) {
+    if (bf)
+      cta_update_bf16(ptrs->dst, 1, ptrs->src, (int)j.n, own, v, n, make_coef(j.n, a.lr, a.momentum), tid, nthr);
+    else
+      cta_update_generic(ptrs->dst[0], ptrs->dst, 1, ptrs->src, (int)j.n, v, n, j.aligned != 0,
+                         make_coef(j.n, a.lr, a.momentum), tid, nthr);
+    bar_sync(BAR_RANGE, nthr);  // the range's new values (global, this CTA) before the fan-out
+    for (uint32_t i = tid; i < n; i += nthr) {
+      const float p = __ldcg(j.m + e0 + i);
+      asm volatile("multimem.st.global.f32 [%0], %1;" ::"l"(j.dst[0] + e0 + i), "f"(p) : "memory");
+    }
+    bar_sync(BAR_RANGE, nthr);
+    return;
+  }
   if (bf)
     cta_update_bf16(ptrs->dst, (int)j.ndst, ptrs->src, (int)j.n, own, v, n, make_coef(j.n, a.lr, a.momentum), tid, nthr);
   else
@@ -1337,7 +1365,7 @@ __device__ __forceinline__ bool job_tma_ok(const Job& j) {
 template <int NW, bool BF, bool MOM>
 __device__ __forceinline__ void consume_reduce(const uint8_t* st, uint32_t pitch, uint32_t n4, uint32_t e4,
                                                float* const* dstp, float* vp, int own, const UpdCoef& c,
-                                               uint32_t tid, uint32_t nthr, int tosmem, int ndst) {
+                                               uint32_t tid, uint32_t nthr, int tosmem, int ndst, bool mc = false) {
   float4* dst[NW];
 #pragma unroll
   for (int q = 0; q < NW; ++q) dst[q] = reinterpret_cast<float4*>(dstp[q]) + e4;
@@ -1372,6 +1400,12 @@ __device__ __forceinline__ void consume_reduce(const uint8_t* st, uint32_t pitch
       }
     }
     if (MOM) v[k] = vv;
+    if (mc) {  // nvls: every replica at once
+      asm volatile("multimem.st.global.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst[0] + k), "f"(r.x), "f"(r.y),
+                   "f"(r.z), "f"(r.w)
+                   : "memory");
+      continue;
+    }
 #pragma unroll
     for (int q = 0; q < NW; ++q)  // (tosmem 2: the local replica here, the remote ones by TMA)
       if (q < ndst && (tosmem != 2 || q == 0)) dst[q][k] = r;
@@ -1454,14 +1488,15 @@ __device__ void consume_tile(const CommArgs& a, const Job& j, const StageDesc& d
   const UpdCoef c = make_coef(N, a.lr, a.momentum);
   float* const* dst = j.dst;
   float* v = j.v;
+  const bool mc = !ONE && j.mc;
 #define P3_CONSUME(K)                                                                                   \
   case K:                                                                                               \
     if (bf) {                                                                                           \
-      if (mom) consume_reduce<K, true, true>(st, pitch, n4, e4, dst, v, own, c, tid, nthr, tosmem, nd);     \
-      else consume_reduce<K, true, false>(st, pitch, n4, e4, dst, v, own, c, tid, nthr, tosmem, nd);        \
+      if (mom) consume_reduce<K, true, true>(st, pitch, n4, e4, dst, v, own, c, tid, nthr, tosmem, nd, mc);     \
+      else consume_reduce<K, true, false>(st, pitch, n4, e4, dst, v, own, c, tid, nthr, tosmem, nd, mc);        \
     } else {                                                                                            \
-      if (mom) consume_reduce<K, false, true>(st, pitch, n4, e4, dst, v, own, c, tid, nthr, tosmem, nd);    \
-      else consume_reduce<K, false, false>(st, pitch, n4, e4, dst, v, own, c, tid, nthr, tosmem, nd);       \
+      if (mom) consume_reduce<K, false, true>(st, pitch, n4, e4, dst, v, own, c, tid, nthr, tosmem, nd, mc);    \
+      else consume_reduce<K, false, false>(st, pitch, n4, e4, dst, v, own, c, tid, nthr, tosmem, nd, mc);       \
     }                                                                                                   \
     return;
   if (ONE) {
@@ -1495,6 +1530,12 @@ __device__ void consume_tile(const CommArgs& a, const Job& j, const StageDesc& d
     float4 vv = mom ? reinterpret_cast<const float4*>(st + (N + 1) * pitch)[k] : make_float4(0.f, 0.f, 0.f, 0.f);
     const float4 r = sgd4(reinterpret_cast<const float4*>(st + N * pitch)[k], acc, c, mom ? &vv : nullptr);
     if (mom) reinterpret_cast<float4*>(v)[e4 + k] = vv;
+    if (mc) {
+      asm volatile("multimem.st.global.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(reinterpret_cast<float4*>(dst[0]) + e4 + k),
+                   "f"(r.x), "f"(r.y), "f"(r.z), "f"(r.w)
+                   : "memory");
+      continue;
+    }
     for (int q = 0; q < nd; ++q) reinterpret_cast<float4*>(dst[q])[e4 + k] = r;
   }
 }
@@ -2137,7 +2178,7 @@ __global__ void __launch_bounds__(P3_COMM_MAX_THREADS, 1) k_comm(const __grid_co
                 g = half ? (const void*)(reinterpret_cast<const __nv_bfloat16*>(j.src[q]) + e0)
                          : (const void*)(j.src[q] + e0);
               } else if (q == j.n) {
-                g = j.pb16 ? j.m + e0 : j.dst[0] + e0;  // master copy p
+                g = (j.pb16 || j.mc) ? j.m + e0 : j.dst[0] + e0;  // master copy p
               } else {
                 g = j.v + e0;
               }

@@ -79,9 +79,76 @@ def exchange_peer_handles(handle: bytes, fingerprint: str, group=None) -> list[b
 
 
 def connect(ctx: "SyncContext", group=None) -> None:
-    """Open every peer's arena (NVLink / CUDA IPC) for a one-rank-per-process context."""
-    if ctx.world > 1:
+    """Open every peer's arena (NVLink / CUDA IPC) for a one-rank-per-process context; with
+    ``nvls`` the arenas travel as file descriptors and the replicas join one multicast object
+    (connect_nvls)."""
+    if ctx.world > 1 and ctx.nvls:
+        connect_nvls(ctx, group)
+    elif ctx.world > 1:
         ctx.open_peers(exchange_peer_handles(ctx.ipc_handle(0), ctx.fingerprint, group))
+
+
+def connect_nvls(ctx: "SyncContext", group=None) -> None:
+    """NVLS bootstrap (include/p3.h, p3_ctx_export_fd .. p3_nvls_bind): every rank serves its
+    arena's file descriptor (rank 0 also the multicast object's) on a Unix socket, the paths
+    go around with torch.distributed, each rank receives its peers' descriptors (SCM_RIGHTS)
+    and maps their arenas; then every rank adds its GPU to the multicast object, and once all
+    have, binds its replica to it."""
+    import os
+    import socket
+    import tempfile
+    import threading
+    import uuid
+
+    import torch.distributed as dist
+
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    fd = ctx.export_fd(0)
+    mc_fd = ctx.nvls_create() if rank == 0 else -1
+    path = os.path.join(tempfile.gettempdir(), f"p3_nvls_{uuid.uuid4().hex}_{rank}.sock")
+    srv = socket.socket(socket.AF_UNIX, socket.SOCK_STREAM)
+    srv.bind(path)
+    srv.listen(world)
+    mine = [fd] + ([mc_fd] if rank == 0 else [])
+
+    def serve() -> None:
+        for _ in range(world - 1):
+            conn, _ = srv.accept()
+            with conn:
+                socket.send_fds(conn, [b"p3"], mine)
+                conn.recv(1)  # the peer holds its copies: the descriptors may close
+
+    t = threading.Thread(target=serve, daemon=True)
+    t.start()
+    rows = [None] * world
+    dist.all_gather_object(rows, (rank, ctx.fingerprint, path), group=group)
+    if len({r[1] for r in rows}) != 1:
+        from .plan import PlanError
+
+        raise PlanError("ranks built different sync plans (fingerprints differ)")
+    fds, mc = [-1] * world, -1
+    try:
+        for r in range(world):
+            if r == rank:
+                continue
+            with socket.socket(socket.AF_UNIX, socket.SOCK_STREAM) as cl:
+                cl.connect(rows[r][2])
+                _, got, _, _ = socket.recv_fds(cl, 16, 2)
+                cl.sendall(b"k")
+            fds[r] = got[0]
+            if r == 0:
+                mc = got[1]
+        t.join()
+        ctx.open_peers_fd(fds)
+        ctx.nvls_attach(mc)
+        dist.barrier(group)  # every GPU added before any bind
+        ctx.nvls_bind()
+        dist.barrier(group)
+    finally:
+        srv.close()
+        os.unlink(path)
+        for f in mine + [x for x in fds if x >= 0] + ([mc] if mc >= 0 else []):
+            os.close(f)
 
 
 class SyncContext:
@@ -118,6 +185,7 @@ class SyncContext:
         drain_streams: int = 0,
         notify_pull: bool = False,
         param_dtype: str = "fp32",
+        nvls: bool = False,
     ) -> None:
         import torch
 
@@ -176,6 +244,8 @@ class SyncContext:
             raise ValueError("param_dtype must be 'fp32' or 'bf16'")
         cfg.param_bf16 = 1 if param_dtype == "bf16" else 0
         self.param_dtype = param_dtype
+        cfg.nvls = 1 if nvls else 0
+        self.nvls = bool(nvls)
         self.strict = comm_ctas == 1 and (finish_ctas or comm_ctas) == 1 and pop_relax == 1 and drain_streams == 1
         h = ctypes.c_void_p()
         _lib.check(self.lib.p3_ctx_create(ctypes.byref(cfg), ctypes.byref(h)), what="p3_ctx_create")
@@ -232,6 +302,26 @@ class SyncContext:
         buf = ctypes.create_string_buffer(_lib.P3_IPC_BYTES)
         self._check(self.lib.p3_ctx_ipc_handle(self._h, li, buf), "p3_ctx_ipc_handle")
         return buf.raw
+
+    def export_fd(self, li: int = 0) -> int:
+        fd = ctypes.c_int(-1)
+        self._check(self.lib.p3_ctx_export_fd(self._h, li, ctypes.byref(fd)), "p3_ctx_export_fd")
+        return fd.value
+
+    def open_peers_fd(self, fds: list[int]) -> None:
+        arr = (ctypes.c_int * len(fds))(*fds)
+        self._check(self.lib.p3_ctx_open_peers_fd(self._h, arr), "p3_ctx_open_peers_fd")
+
+    def nvls_create(self) -> int:
+        fd = ctypes.c_int(-1)
+        self._check(self.lib.p3_nvls_create(self._h, ctypes.byref(fd)), "p3_nvls_create")
+        return fd.value
+
+    def nvls_attach(self, fd: int) -> None:
+        self._check(self.lib.p3_nvls_attach(self._h, fd), "p3_nvls_attach")
+
+    def nvls_bind(self) -> None:
+        self._check(self.lib.p3_nvls_bind(self._h), "p3_nvls_bind")
 
     def open_peers(self, handles: list[bytes]) -> None:
         blob = b"".join(h.ljust(_lib.P3_IPC_BYTES, b"\0") for h in handles)

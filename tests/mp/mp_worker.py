@@ -77,6 +77,39 @@ def main():
     dist.barrier()
     w.close()
 
+    # NVLS multicast broadcasts (one multimem.st per element reaches every replica; arenas
+    # shared by file descriptor): the same digests, where the GPUs support multicast objects
+    from paper_1905_03960_b200.runtime import connect
+
+    out["nvls"] = "ok"
+    for name, kind, iters, counts_, seed in (("resnet50-like", "distinct", 4, None, None),
+                                              ("vgg19-like", "same", 10, None, None),
+                                              ("resnet50-real", "distinct", 2, counts, 1905)):
+        if counts_ is None and (name, world, kind) not in want:
+            continue
+        prof = builtin_profile(name) if counts_ is None else ModelProfile(name, seed, tuple(
+            LayerSpec(i, f"t{i}", c, 0, 0) for i, c in enumerate(counts_)))
+        ctas = 148 if counts_ is not None else 16
+        cfg = WorkerConfig(rank=rank, mode="p3", world=world, iterations=iters, deadlock_timeout=60.0,
+                           emulate_compute=kind == "same", comm_ctas=ctas, rank_distinct_grads=kind == "distinct")
+        try:
+            ctx = SyncContext(prof.param_counts(), world, [rank], lr=cfg.lr, comm_ctas=ctas, timeout_s=60.0,
+                              emulate_grads=True, nvls=True)
+        except Exception as e:  # noqa: BLE001  (no multicast support on this box)
+            out["nvls"] = f"unavailable: {e}"
+            break
+        connect(ctx)
+        w = TrainingWorker(cfg, prof, ranks=[rank], ctx=ctx)
+        try:
+            w.run()
+            got = f"{w.params_digest(0):016x}"
+        except Exception as e:  # noqa: BLE001
+            got = f"error: {e}"
+        want_d = want[(name, world, kind)] if counts_ is None else ref[0]
+        out["digests"][f"{name}/{kind}/nvls"] = [got, want_d]
+        dist.barrier()
+        w.close()
+
     # the layer-wise baseline (KVStore placement + FIFO) on the same kernels across processes:
     # bit-identical to P3 (SPEC acceptance #3)
     for name in ("toy3", "vgg19-like"):

@@ -3,7 +3,7 @@ one FINISH launch per iteration; max over ranks. torchrun --nproc-per-node N too
 import os, sys, json, statistics
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch, torch.distributed as dist
-from paper_1905_03960_b200.runtime import SyncContext
+from paper_1905_03960_b200.runtime import SyncContext, connect
 from paper_1905_03960_b200.torch_models import real_counts
 
 def main():
@@ -25,7 +25,7 @@ def main():
                 ctx = SyncContext(counts, world, [rank], max_slice=ms, comm_ctas=ctas, comm_threads=threads,
                                   timeout_s=60.0, emulate_grads=True, **extra)
                 if world > 1:
-                    hs = [None] * world; dist.all_gather_object(hs, ctx.ipc_handle(0)); ctx.open_peers(hs)
+                    connect(ctx)  # (CUDA IPC, or fd + multicast with extra {"nvls": true})
                 st = torch.cuda.Stream()
                 for l in range(len(counts)): ctx.gradgen_layer(0, 7 + rank, 0, l, st)
                 st.synchronize()
