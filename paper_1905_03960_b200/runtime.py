@@ -103,13 +103,23 @@ def connect_nvls(ctx: "SyncContext", group=None) -> None:
     import torch.distributed as dist
 
     world, rank = dist.get_world_size(group), dist.get_rank(group)
-    fd = ctx.export_fd(0)
-    mc_fd = ctx.nvls_create() if rank == 0 else -1
+    mine, err = [], None
+    try:  # (a failure on one rank must not leave the others waiting in the exchange)
+        mine.append(ctx.export_fd(0))
+        if rank == 0:
+            mine.append(ctx.nvls_create())
+    except Exception as e:  # noqa: BLE001
+        err = f"rank {rank}: {e}"
+    errs = [None] * world
+    dist.all_gather_object(errs, err, group=group)
+    if any(errs):
+        for f in mine:
+            os.close(f)
+        raise RuntimeError("nvls bootstrap failed: " + "; ".join(e for e in errs if e))
     path = os.path.join(tempfile.gettempdir(), f"p3_nvls_{uuid.uuid4().hex}_{rank}.sock")
     srv = socket.socket(socket.AF_UNIX, socket.SOCK_STREAM)
     srv.bind(path)
     srv.listen(world)
-    mine = [fd] + ([mc_fd] if rank == 0 else [])
 
     def serve() -> None:
         for _ in range(world - 1):
