@@ -82,6 +82,51 @@ def main():
         results[name] = {"plan_agree": agree, "digest": f"{orc.digest(params):016x}", "iters": iters,
                          "distinct": distinct}
     out["protocol"] = results
+
+    # 4. the NVLS bootstrap (runtime.connect_nvls): arena and multicast descriptors travel over
+    # Unix sockets; a stand-in context hands out descriptors of files and records what arrives
+    import tempfile
+
+    from paper_1905_03960_b200.runtime import connect_nvls
+
+    class FdCtx:
+        fingerprint = "same-plan"
+
+        def __init__(self):
+            self.dir = tempfile.mkdtemp()
+            self.calls = []
+
+        def _fd(self, name):
+            return os.open(os.path.join(self.dir, name), os.O_CREAT | os.O_RDWR)
+
+        def export_fd(self, li):
+            fd = self._fd("arena")
+            self.arena = os.fstat(fd).st_ino
+            return fd
+
+        def nvls_create(self):
+            fd = self._fd("mc")
+            self.mc = os.fstat(fd).st_ino
+            return fd
+
+        def open_peers_fd(self, fds):
+            self.calls.append("open")
+            self.peers = [os.fstat(f).st_ino if f >= 0 else None for f in fds]
+
+        def nvls_attach(self, fd):
+            self.calls.append("attach")
+            self.mc_seen = os.fstat(fd).st_ino if fd >= 0 else getattr(self, "mc", None)
+
+        def nvls_bind(self):
+            self.calls.append("bind")
+
+    fc = FdCtx()
+    connect_nvls(fc)
+    ids = [None] * world
+    dist.all_gather_object(ids, (fc.arena, getattr(fc, "mc", None)))
+    out["nvls_bootstrap"] = (fc.calls == ["open", "attach", "bind"]
+                             and all(fc.peers[r] == (None if r == rank else ids[r][0]) for r in range(world))
+                             and fc.mc_seen == ids[0][1] and ids[0][1] is not None)
     Path(os.environ["P3_MP_OUT"], f"rank{rank}.json").write_text(json.dumps(out))
     dist.destroy_process_group()
 

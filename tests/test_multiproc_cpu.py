@@ -20,6 +20,7 @@ def test_two_rank_host_logic(golden, tmp_path):
     want = {(d[0], d[1], d[2], d[4]): d[5] for d in golden["digests"]}
     for r in res:
         assert r["exchange_order"] and r["mismatch_refused"] and r["max_over_ranks"], r
+        assert r["nvls_bootstrap"], r
         for name, v in r["protocol"].items():
             assert v["plan_agree"], (r["rank"], name)
             key = (name, 2, v["iters"], "distinct" if v["distinct"] else "same")
