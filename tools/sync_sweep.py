@@ -19,7 +19,21 @@ def main():
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     rows = []
     for m in models:
-        counts = real_counts(m); P = sum(counts)
+        if m.endswith("-notiny"):  # experiment: the model without its layers under 8K parameters
+            counts = [c for c in real_counts(m[:-7]) if c >= 8192]
+        elif m.endswith("-merged"):  # experiment: tiny layers merged into runs of >= 8K parameters
+            counts, acc = [], 0
+            for c in real_counts(m[:-7]):
+                if c >= 8192:
+                    if acc: counts.append(acc); acc = 0
+                    counts.append(c)
+                else:
+                    acc += c
+                    if acc >= 8192: counts.append(acc); acc = 0
+            if acc: counts.append(acc)
+        else:
+            counts = real_counts(m)
+        P = sum(counts)
         for ms in slices:
             for ctas in ctas_list:
                 ctx = SyncContext(counts, world, [rank], max_slice=ms, comm_ctas=ctas, comm_threads=threads,
