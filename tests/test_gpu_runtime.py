@@ -431,11 +431,11 @@ def test_nvls_config_checks(cuda):
     """cfg.nvls (multicast broadcasts) is for one local rank per process at world > 1 with fp32
     replicas; other combinations fail at creation with a usage error (the multi-process path
     itself runs in tests/test_multigpu.py)."""
-    from paper_1905_03960_b200._lib import P3Error
+    from paper_1905_03960_b200.plan import PlanError
     from paper_1905_03960_b200.runtime import SyncContext
 
     counts = [1000, 2000, 3000]
     for kw in (dict(world=1, local_ranks=[0]), dict(world=2, local_ranks=[0, 1]),
                dict(world=2, local_ranks=[0], notify_pull=True)):
-        with pytest.raises(P3Error):
+        with pytest.raises(PlanError, match="nvls"):  # (usage errors surface as PlanError)
             SyncContext(counts, kw.pop("world"), kw.pop("local_ranks"), nvls=True, **kw)

@@ -1,0 +1,6 @@
+# scheduling switches on the per-slot-signaler kernel (N=2 sync-only)
+for i in 1 2; do
+for kv in "X=0" "P3_POP_RELAX=32" "P3_POP_RELAX=64" "P3_PUSH_SPLIT=2" "P3_PUSH_SPLIT=4" "P3_SRV_RESERVE=8" "P3_SRV_RESERVE=16" "P3_SRV_FILTER=1" "P3_SRV_FILTER=2"; do
+  env $kv timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29620 \
+    tools/sync_sweep.py resnet50,seq2seq,vgg19 148 2>/dev/null | grep SWEEP | sed "s/^SWEEP /SWEEP $kv /"
+done; done
