@@ -163,7 +163,7 @@ struct p3_ctx {
   // P3_TMA=0 (direct loads instead of the TMA stage ring), P3_PUSH_SPLIT=n, P3_SRV_FILTER=n,
   // P3_TRACE_CTA=1 (trace records carry CTA indices; CTA start / exit records)
   struct {
-    uint32_t use_tma = 1, push_split = 2, srv_filter = 0, trace_cta = 0, srv_reserve = 0, tma_store = 1, tma_store_red = 0, pop_relax = 0,
+    uint32_t use_tma = 1, push_split = 0xffffffffu, srv_filter = 0, trace_cta = 0, srv_reserve = 0, tma_store = 1, tma_store_red = 0, pop_relax = 0,
              push_max = 2, stream = 1, push_cap = 0, bcast_pull = 0, lazy_pick = 0, srv_piece = 0, push_ctas = 0;
   } knobs;
   std::vector<uint32_t> own_total;
@@ -445,9 +445,8 @@ int p3_ctx_create(const p3_config_t* cfg, p3_ctx_t** out) {
       return e ? (uint32_t)atoi(e) : dflt;
     };
     c->knobs.use_tma = env_u32("P3_TMA", 1);
-    // every 2nd CTA looks for pushes before server work (measured at N=2 with one signaler per
-    // slot: sync-only ResNet-50 -3%, seq2seq -2%, VGG-19 -1%; profiles/r02_summary.md §7)
-    c->knobs.push_split = env_u32("P3_PUSH_SPLIT", 2);
+    // (unset: auto, see comm_args)
+    c->knobs.push_split = env_u32("P3_PUSH_SPLIT", 0xffffffffu);
     c->knobs.srv_filter = env_u32("P3_SRV_FILTER", 0);
     c->knobs.trace_cta = getenv("P3_TRACE_CTA") != nullptr;
     c->knobs.srv_reserve = env_u32("P3_SRV_RESERVE", 0);
@@ -947,7 +946,12 @@ static CommArgs comm_args(p3_ctx* c, uint32_t mode, uint32_t ctas) {
   a.ntf_cap = c->S;
   a.pull_cap = c->S * (c->N > 1 ? c->N - 1 : 1);
   a.trace_cta = c->knobs.trace_cta;
-  a.push_split = c->knobs.push_split;
+  // auto: every 2nd CTA of an unthrottled FINISH launch looks for pushes before server work
+  // (N=2 sync-only with one signaler per slot: ResNet-50 -3%, seq2seq -2%, VGG-19 -1%); not in
+  // DRAIN launches or under the K7 throttle, where it cost throttled P3 training 17% at N=2
+  // (profiles/r02_summary.md §7)
+  a.push_split = c->knobs.push_split != 0xffffffffu ? c->knobs.push_split
+                 : (mode == P3_COMM_FINISH && c->cfg.throttle_bps <= 0) ? 2u : 0u;
   a.srv_filter = c->knobs.srv_filter;
   a.use_tma = c->knobs.use_tma;
   a.srv_reserve = c->knobs.srv_reserve;
