@@ -238,6 +238,10 @@ def sync_only_roofline(args, world, rank, counts):
     connect(ctx)
     stream = torch.cuda.Stream()
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")  # > 126 MB L2
+    # a read sweep of another buffer after the flush write retires the flush's dirty lines
+    # before the timed region (else their write-back lands inside the kernel: ~60 MB of extra
+    # DRAM writes, ~8 us at N=1 — tools/stream_gap.py under ncu --cache-control none)
+    sweep = torch.zeros(256 << 20, dtype=torch.uint8, device="cuda")
     align = torch.zeros(1, device="cuda")
     for l in range(len(counts)):
         ctx.gradgen_layer(0, 7, 0, l, stream)
@@ -253,6 +257,7 @@ def sync_only_roofline(args, world, rank, counts):
             dev0 = ctx.counters(0)
         with torch.cuda.stream(stream):
             flush.fill_(k & 0xFF)
+            sweep.sum(dtype=torch.int32)
         for l in range(len(counts)):  # published before the iteration opens: no DRAIN launches
             ctx.layer_ready(0, l, k, None, stream)
         stream.synchronize()
@@ -538,7 +543,8 @@ def run_ours(args):
                             else "k_comm (K3 push + K4 reduce/SGD/bcast)"),
                  "algorithmic_bytes_per_launch": alg, "launch_ms": sync_ms, "ctas": ctas,
                  "measured_in": "sync-only phase: all layers' gradients in HBM and published, one launch per "
-                                "iteration over the whole GPU, L2 flushed (256 MB write) between launches"})
+                                "iteration over the whole GPU, L2 flushed between launches (256 MB write, then a 256 MB "
+                                "read of another buffer so no dirty flush lines are written back inside the kernel)"})
 
     out = None
     if rank == 0:
