@@ -17,6 +17,7 @@ def main():
     threads = int(sys.argv[4]) if len(sys.argv) > 4 else 512
     extra = json.loads(sys.argv[5]) if len(sys.argv) > 5 else {}
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    sweep = torch.zeros(256 << 20, dtype=torch.uint8, device="cuda")  # retires the flush's dirty lines (bench.py)
     rows = []
     for m in models:
         if m.endswith("-notiny"):  # experiment: the model without its layers under 8K parameters
@@ -45,7 +46,7 @@ def main():
                 st.synchronize()
                 ts = []
                 for k in range(8):
-                    with torch.cuda.stream(st): flush.fill_(k)
+                    with torch.cuda.stream(st): flush.fill_(k); sweep.sum(dtype=torch.int32)
                     for l in range(len(counts)): ctx.layer_ready(0, l, k, None, st)
                     st.synchronize()
                     if world > 1: dist.barrier()
