@@ -1766,7 +1766,8 @@ __device__ P3_COLD void prepare_answer(const CommArgs& a, uint32_t li, uint32_t 
 }
 
 // Comm kernel. Warp 0 of every CTA is the scheduler, warp 1 the signaler, warp 2 the TMA
-// producer, warps 3.. the consumers; two job slots and a 3-stage ring in shared memory.
+// producer, warps 3.. the consumers; two job slots and a 3-stage ring in shared memory. At
+// N > 1 (k_comm<false>) each job slot has its own signaler: warps 1 and 3, consumers from 4.
 //   scheduler: pick the next job — server work first (a reduced slice unblocks the next
 //   forward pass), then the most urgent published slice of the local worker queues — and
 //   prepare its pointers while the previous job is still moving;
