@@ -266,6 +266,7 @@ class P3DataParallel(_HookedDataParallel):
         order: str = "forward",
         local_world: P3LocalWorld | None = None,
         notify_pull: bool | None = None,
+        nvls: bool = False,
     ) -> None:
         super().__init__(module, order)
         dtypes = {p.dtype for p in self.params}
@@ -307,6 +308,7 @@ class P3DataParallel(_HookedDataParallel):
             finish_ctas=finish_ctas, push_dtype=push_dtype,
             notify_pull=(plan_mode == "baseline") if notify_pull is None else notify_pull,
             param_dtype=self.param_dtype,
+            nvls=nvls,  # opt-in multicast broadcasts (one process per GPU; include/p3.h cfg.nvls)
         )
         self.ctx: SyncContext | None = None
         self.comm_stream = None

@@ -171,12 +171,14 @@ def main():
     # ranks' own autograd gradients (gathered here), separately rounded (server.py:55-68)
     from paper_1905_03960_b200.torch_models import build_model, loss_fn, synthetic_batch
 
-    for name, batch in (("resnet50", 8), ("seq2seq", 8)):
+    for name, batch, nvls in (("resnet50", 8, False), ("seq2seq", 8, False), ("resnet50", 8, True)):
+        if nvls and out["nvls"] != "ok":
+            continue  # (NVLS: the same check with multicast broadcasts, where the box has them)
         torch.manual_seed(7)
         m = build_model(name).cuda()
         if name == "resnet50":
             m = m.to(memory_format=torch.channels_last)
-        d = P3DataParallel(m, lr=lr, comm_ctas=8, timeout_s=60.0)
+        d = P3DataParallel(m, lr=lr, comm_ctas=8, timeout_s=60.0, nvls=nvls)
         names = [n for n, p in m.named_parameters() if p.requires_grad]
         exact, differs = True, False
         for it in range(3):
@@ -196,7 +198,7 @@ def main():
                 want = old[n] - (acc / torch.full_like(acc, world)).mul(lr)
                 exact &= bool(torch.equal(params[n].detach(), want))
                 differs |= not torch.equal(gs[0], gs[-1])
-        out[f"torch_p3_distinct_{name}"] = exact and differs
+        out[f"torch_p3_distinct_{name}" + ("_nvls" if nvls else "")] = exact and differs
         d.close()
         del d, m
         torch.cuda.empty_cache()

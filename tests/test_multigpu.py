@@ -40,5 +40,7 @@ def test_multiprocess_parity(world, tmp_path):
         assert r["torch_p3_distinct_seq2seq"], r
         assert r["torch_p3_bf16_replicas"], r
         assert r["nvls"] == "ok" or r["nvls"].startswith("unavailable"), r["nvls"]
+        if r["nvls"] == "ok":  # torch-mode training with multicast broadcasts, bit-exact too
+            assert r["torch_p3_distinct_resnet50_nvls"], r
         if os.environ.get("P3_EXPECT_NVLS"):  # a box known to have multicast (NVSwitch)
             assert r["nvls"] == "ok" and any(k.endswith("/nvls") for k in r["digests"]), r["nvls"]
