@@ -459,7 +459,10 @@ struct QueueView {
   const LocalDev* ring;  // publication ring to ingest from (nullptr: scripted queue)
 };
 
-__device__ void ingest(const LocalDev& L, uint32_t sched);
+#ifndef P3_INGEST_U
+#define P3_INGEST_U 8  // publication-ring entries per lane loaded before use (ingest)
+#endif
+__device__ __noinline__ void ingest(const LocalDev& L, uint32_t sched);
 __device__ __forceinline__ uint64_t globaltimer_lane0() {
   uint64_t t = (threadIdx.x & 31) == 0 ? globaltimer() : 0ull;
   return __shfl_sync(0xffffffffu, (unsigned long long)t, 0);
@@ -968,7 +971,7 @@ __device__ P3_COLD void pace(const CommArgs& a, const LocalDev& L, uint64_t byte
 // advanced by a stream memory write ordered after the kernels that produced the gradients,
 // so entries below it are safe to expose; the first warp to move `ingested` forward copies
 // them, the others see the layers on a later pick.
-__device__ void ingest(const LocalDev& L, uint32_t sched) {
+__device__ __noinline__ void ingest(const LocalDev& L, uint32_t sched) {
   const uint32_t lane = threadIdx.x & 31;
   uint32_t lo = 0, hi = 0, won = 0;
   if (lane == 0) {
@@ -984,20 +987,39 @@ __device__ void ingest(const LocalDev& L, uint32_t sched) {
   // pattern) sees the gradients the memory write of pubseq was ordered after
   __syncwarp();
   fence_acq_rel_gpu();
-  for (uint32_t i = lo + lane; (int32_t)(hi - i) > 0; i += 32) {
-    const volatile PubEntry* e = L.ring + (i % L.ring_cap);
-    const uint32_t layer = e->layer;
-    const uint32_t key = e->key;
-    const unsigned long long word = e->word;
-    if (sched == P3_SCHED_FIFO) {
-      // the publish sequence is visible before the word (FIFO pops load the word with acquire)
-      *(volatile uint32_t*)(L.fifo_key + layer) = key;
-      __threadfence();
+  // The ring is in pinned host memory: every read is a PCIe round trip, so each lane issues
+  // the 16-byte loads of up to P3_INGEST_U entries before using any (a whole iteration's
+  // publications — 161 for ResNet-50 — in one or two round trips instead of one per 32).
+  constexpr uint32_t U = P3_INGEST_U;
+  for (uint32_t base = lo; (int32_t)(hi - base) > 0; base += 32 * U) {
+    uint4 ent[U];
+#pragma unroll
+    for (uint32_t u = 0; u < U; ++u) {
+      const uint32_t i = base + 32 * u + lane;
+      if ((int32_t)(hi - i) > 0) {
+        const PubEntry* e = L.ring + (i % L.ring_cap);
+        asm volatile("ld.volatile.global.v4.u32 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(ent[u].x), "=r"(ent[u].y), "=r"(ent[u].z), "=r"(ent[u].w)
+                     : "l"(e));
+      }
     }
-    *(volatile unsigned long long*)(L.pub + layer) = word;
-    if (L.trace_cap) {  // PUBLISH (put_batch) once the word is visible to every pop
-      __threadfence();
-      trace_append(L, (uint32_t)(word >> 48) - 1u, layer, key, L.rank, P3_EV_PUBLISH);
+#pragma unroll
+    for (uint32_t u = 0; u < U; ++u) {
+      const uint32_t i = base + 32 * u + lane;
+      if ((int32_t)(hi - i) <= 0) continue;
+      const uint32_t layer = ent[u].x;
+      const uint32_t key = ent[u].y;
+      const unsigned long long word = (unsigned long long)ent[u].z | ((unsigned long long)ent[u].w << 32);
+      if (sched == P3_SCHED_FIFO) {
+        // the publish sequence is visible before the word (FIFO pops load the word with acquire)
+        *(volatile uint32_t*)(L.fifo_key + layer) = key;
+        __threadfence();
+      }
+      *(volatile unsigned long long*)(L.pub + layer) = word;
+      if (L.trace_cap) {  // PUBLISH (put_batch) once the word is visible to every pop
+        __threadfence();
+        trace_append(L, (uint32_t)(word >> 48) - 1u, layer, key, L.rank, P3_EV_PUBLISH);
+      }
     }
   }
   __syncwarp();
@@ -2003,7 +2025,10 @@ __global__ void __launch_bounds__(P3_COMM_MAX_THREADS, 1) k_comm(const __grid_co
         }
         verdict = __shfl_sync(FULL_MASK, verdict, 0);
         if (verdict == 0) {
-          backoff = min(2u * backoff + 64u, (pops_done || was_capped) ? 512u : 4096u);
+          // FINISH runs after the iteration's last publication: what it waits for is near
+          // (the ingest of the ring, a peer's push), so it polls at most every 0.5 us; a DRAIN
+          // launch may wait for the backward pass and backs off up to 4 us
+          backoff = min(2u * backoff + 64u, (a.mode == P3_COMM_FINISH || pops_done || was_capped) ? 512u : 4096u);
           __nanosleep(backoff);
           continue;
         }
@@ -2251,6 +2276,8 @@ __global__ void __launch_bounds__(P3_COMM_MAX_THREADS, 1) k_comm(const __grid_co
       P3_CHECK(d.b < P3_SLOTS);
       const uint64_t tm = tid == 0 ? stat_clock() : 0;
       const Job& j = slots[d.b];
+      if (P3_TRACE && a.trace_cta && tid == 0 && d.e0 == 0)  // diagnostics: a job's first stage (18)
+        trace_append(a.loc[j.li], a.k, j.layer, j.g - a.plan.layer_first[j.layer], blockIdx.x, 18, j.kind);
       const bool bulk_push = a.tma_store && j.kind == JOB_PUSH && j.bf16 != 1 && !(d.flags & ST_DIRECT);
       bool bulk = false;  // this stage leaves by TMA bulk store (one group)
       if (bulk_push) {
@@ -2321,6 +2348,8 @@ __global__ void __launch_bounds__(P3_COMM_MAX_THREADS, 1) k_comm(const __grid_co
         if (lane == 0) mbar_arrive(&empty_bar[sidx]);
       }
       if (tid == 0) t_move += stat_clock() - tm;
+      if (P3_TRACE && a.trace_cta && tid == 0 && (d.flags & ST_LAST))  // ... and its last one done (19)
+        trace_append(a.loc[j.li], a.k, j.layer, j.g - a.plan.layer_first[j.layer], blockIdx.x, 19, j.kind);
       if (d.flags & ST_LAST) {
         if (P3_EXP && w0 && defer_done) done_pend = d.b;
         else bar_arrive(BAR_DONE(d.b), ncons + 32);
