@@ -971,6 +971,36 @@ __device__ P3_COLD void pace(const CommArgs& a, const LocalDev& L, uint64_t byte
 // advanced by a stream memory write ordered after the kernels that produced the gradients,
 // so entries below it are safe to expose; the first warp to move `ingested` forward copies
 // them, the others see the layers on a later pick.
+// The single-rank streaming kernel keeps the one-entry-per-lane ingest inline: the batched,
+// out-of-line one changed its register allocation (111 -> 128) and cost ~0.8% there.
+__device__ __forceinline__ void ingest_lanes(const LocalDev& L) {
+  const uint32_t lane = threadIdx.x & 31;
+  uint32_t lo = 0, hi = 0, won = 0;
+  if (lane == 0) {
+    lo = ld_relaxed_gpu(L.ingested);
+    hi = ld_acquire_gpu(L.pubseq);
+    if ((int32_t)(hi - lo) > 0) won = atomicCAS(L.ingested, lo, hi) == lo;
+  }
+  won = __shfl_sync(FULL_MASK, won, 0);
+  if (!won) return;
+  lo = __shfl_sync(FULL_MASK, lo, 0);
+  hi = __shfl_sync(FULL_MASK, hi, 0);
+  __syncwarp();
+  fence_acq_rel_gpu();
+  for (uint32_t i = lo + lane; (int32_t)(hi - i) > 0; i += 32) {
+    const volatile PubEntry* e = L.ring + (i % L.ring_cap);
+    const uint32_t layer = e->layer;
+    const unsigned long long word = e->word;
+    *(volatile unsigned long long*)(L.pub + layer) = word;
+    if (L.trace_cap) {
+      __threadfence();
+      trace_append(L, (uint32_t)(word >> 48) - 1u, layer, e->key, L.rank, P3_EV_PUBLISH);
+    }
+  }
+  __syncwarp();
+  if (lane == 0) *(volatile uint32_t*)L.ingested_host = hi;
+}
+
 __device__ __noinline__ void ingest(const LocalDev& L, uint32_t sched) {
   const uint32_t lane = threadIdx.x & 31;
   uint32_t lo = 0, hi = 0, won = 0;
@@ -2536,7 +2566,7 @@ __global__ void __launch_bounds__(P3_STREAM_THREADS, P3_STREAM_CTAS_PER_SM)
         if (!pub_ready(word, a.k + 1)) {  // published before this launch; maybe not yet ingested
           const uint64_t t0 = globaltimer();
           while (!pub_ready(word, a.k + 1)) {
-            ingest(L, a.sched);
+            ingest_lanes(L);  // (single rank: priority discipline, no FIFO keys)
             __nanosleep(128);
             word = ld_relaxed_gpu64(L.pub + lc);
             if (globaltimer() - t0 > a.timeout_ns) {
